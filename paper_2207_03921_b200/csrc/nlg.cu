@@ -1,0 +1,1673 @@
+// nlg.cu -- B200 (sm_100a) nonlocal stiffness assembly: kernels, the
+// per-batch pipeline and the C ABI declared in include/nlg.h.
+//
+// Pipeline of one nlg_assemble call (rows [row_lo, row_hi)):
+//   prep      k_bounds (barycentre/radius, assembly.py:130-134), k_bbox,
+//             k_cell + radix sort + k_cell_ranges: uniform grid of
+//             barycentres with cell >= prer + 2 r_max (replaces the BFS of
+//             _engine.py:530-599 with the exhaustive "brute" semantics,
+//             _engine.py:486-529, which the reference equals bitwise under
+//             its Assumption 4)
+//   batch     k_mark_*: owner-computes root selection for the row range
+//             k_count / k_fill: candidate pairs per root, split into full,
+//             clipped and singular (identical / edge / vertex) lists
+//             k_full, k_partial: one thread per visit (nlg_eval.cuh)
+//             k_singular<U>: one CTA per touching pair, tensor rules
+//             k_kk_reduce: per-root, fixed-order sum of the root's own block
+//             radix sort of (row, col) keys + k_seg_* : deterministic
+//             segmented sum -> CSR (replaces _merge_triplets)
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nlg.h"
+#include "nlg_eval.cuh"
+
+using namespace nlg;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+void set_err(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      set_err("%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_));             \
+      return NLG_ERR_CUDA;                                                                 \
+    }                                                                                      \
+  } while (0)
+
+#define LAUNCHED()                                                                         \
+  do {                                                                                     \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                    \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess) {                                                               \
+      set_err("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_));             \
+      return NLG_ERR_CUDA;                                                                 \
+    }                                                                                      \
+  } while (0)
+
+constexpr unsigned long long kSentinel = ~0ull;
+constexpr int kCnt = 7;  // per-root counters: full, partial, sing id/edge/vertex, epi, emit-kk
+enum { C_FULL = 0, C_PART = 1, C_SID = 2, C_SED = 3, C_SVX = 4, C_EPI = 5, C_KK = 6 };
+
+// device counters (FLOP accounting), indices
+enum {
+  K_EVAL_FULL0 = 0,  // inner evals the reference makes for full pairs: mode0 + mode1 (2 x 49)
+  K_EVAL_FULL2,      // identical full pairs, mode 2
+  K_OUT_FULL0,       // outer points (7 per sweep)
+  K_OUT_FULL2,
+  K_EVAL_M0, K_EVAL_M1, K_EVAL_M2,
+  K_OUT_M0, K_OUT_M1, K_OUT_M2,
+  K_SPTS3, K_SPTS4, K_SPTS5, K_SPTS6,
+  K_NCOUNTERS
+};
+
+__device__ __forceinline__ unsigned long long d2ord(double v) {
+  unsigned long long b = __double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double ord2d(unsigned long long o) {
+  unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  double v;
+  memcpy(&v, &b, 8);
+  return v;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// ---------------------------------------------------------------- prep
+__global__ void k_convert(const double* __restrict__ vin, const long long* __restrict__ ein,
+                          const long long* __restrict__ lab, const long long* __restrict__ outer,
+                          const long long* __restrict__ dof, int V, int K, double2* vtx, int4* elem,
+                          int4* dofs) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < V) vtx[i] = make_double2(vin[2 * i], vin[2 * i + 1]);
+  if (i < K) {
+    const int flags = (int)lab[i] | ((outer[i] != 0) << 4);
+    elem[i] = make_int4((int)ein[3 * i], (int)ein[3 * i + 1], (int)ein[3 * i + 2], flags);
+    dofs[i] = make_int4((int)dof[3 * i], (int)dof[3 * i + 1], (int)dof[3 * i + 2], 0);
+  }
+}
+
+// barycentre ((v0 + v1) + v2) / 3 and bounding radius, numpy's order
+// (assembly.py:130-134); bbox/rmax over active elements via ordered atomics
+__global__ void k_bounds(Params P, double2* ctr, double* rad, unsigned long long* ext) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.K) return;
+  const int4 e = P.elem[k];
+  const double2 a = P.vtx[e.x], b = P.vtx[e.y], c = P.vtx[e.z];
+  const double cx = __dadd_rn(__dadd_rn(a.x, b.x), c.x) / 3.0;
+  const double cy = __dadd_rn(__dadd_rn(a.y, b.y), c.y) / 3.0;
+  const double ra = sqrt(sumsq(a.x - cx, a.y - cy));
+  const double rb = sqrt(sumsq(b.x - cx, b.y - cy));
+  const double rc = sqrt(sumsq(c.x - cx, c.y - cy));
+  const double r = fmax(fmax(ra, rb), rc);
+  ctr[k] = make_double2(cx, cy);
+  rad[k] = r;
+  if ((e.w & 15) != 0) {
+    atomicMin(&ext[0], d2ord(cx));
+    atomicMin(&ext[1], d2ord(cy));
+    atomicMax(&ext[2], d2ord(cx));
+    atomicMax(&ext[3], d2ord(cy));
+    atomicMax(&ext[4], d2ord(r));
+  }
+}
+
+struct Grid {
+  double ox, oy, cs;
+  int nx, ny;
+  const int* __restrict__ start;  // [ncell + 1]
+  const int* __restrict__ items;  // active element ids sorted by cell
+};
+
+__global__ void k_cell(Params P, Grid G, unsigned* key, int* val) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.K) return;
+  const int4 e = P.elem[k];
+  unsigned cell = (unsigned)(G.nx * G.ny);
+  if ((e.w & 15) != 0) {
+    const double2 c = P.ctr[k];
+    int ix = (int)floor((c.x - G.ox) / G.cs), iy = (int)floor((c.y - G.oy) / G.cs);
+    ix = min(max(ix, 0), G.nx - 1);
+    iy = min(max(iy, 0), G.ny - 1);
+    cell = (unsigned)(iy * G.nx + ix);
+  }
+  key[k] = cell;
+  val[k] = k;
+}
+
+__global__ void k_cell_ranges(const unsigned* __restrict__ skey, int K, int ncell, int* start) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > ncell) return;
+  int lo = 0, hi = K;  // lower_bound
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (skey[mid] < (unsigned)c) lo = mid + 1; else hi = mid;
+  }
+  start[c] = lo;
+}
+
+// ---------------------------------------------------------------- batch marking
+__device__ __forceinline__ bool row_in(const Params& P, long long base) {
+  // any component row nc*base + c in [row_lo, row_hi)
+  const long long r0 = (long long)P.nc * base;
+  return r0 + P.nc - 1 >= P.row_lo && r0 < P.row_hi;
+}
+
+__global__ void k_mark_a(Params P, unsigned char* needA) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.K) return;
+  const int4 d = P.dofs[k];
+  needA[k] = row_in(P, d.x) || row_in(P, d.y) || row_in(P, d.z);
+}
+
+__global__ void k_mark_vertices(Params P, const unsigned char* needA, unsigned char* vmark) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.K || !needA[k]) return;
+  const int4 e = P.elem[k];
+  vmark[e.x] = 1;
+  vmark[e.y] = 1;
+  vmark[e.z] = 1;
+}
+
+// root flag: outer element that emits its own rows (A) or may own a singular
+// pair reaching the range (touches an A element, path 2 only)
+__global__ void k_mark_roots(Params P, const unsigned char* needA, const unsigned char* vmark,
+                             int* flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.K) return;
+  const int4 e = P.elem[k];
+  bool f = false;
+  if (e.w & 16) {
+    f = needA[k];
+    if (!f && P.path == 2 && vmark) f = vmark[e.x] || vmark[e.y] || vmark[e.z];
+  }
+  flag[k] = f;
+}
+
+// ---------------------------------------------------------------- candidates
+// category of the ordered pair (k, l) as root k sees it:
+//  -1 rejected / not emitted here, 0 full, 1 clipped, 2/3/4 singular id/edge/vertex.
+// *visited is set when the reference would count the visit (EPI).
+__device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2 ck, double rk,
+                                        bool needAk, const unsigned char* __restrict__ needA, int l,
+                                        bool& visited) {
+  visited = false;
+  const int4 el = __ldg(&P.elem[l]);
+  const int ns = (ek.x == el.x) + (ek.x == el.y) + (ek.x == el.z) + (ek.y == el.x) + (ek.y == el.y) +
+                 (ek.y == el.z) + (ek.z == el.x) + (ek.z == el.y) + (ek.z == el.z);
+  const bool touching = (k == l) || ns > 0;
+  const double2 cl = __ldg(&P.ctr[l]);
+  const double rl = __ldg(&P.rad[l]);
+  const double dist = sqrt(sumsq(ck.x - cl.x, ck.y - cl.y));
+  if (!touching && __dsub_rn(__dsub_rn(dist, rk), rl) > P.prer) return -1;
+  visited = true;
+  if (touching && P.path == 2) {
+    if (l != k && (el.w & 16) && l < k) return -1;  // owned by the smaller root (_engine.py:233)
+    if (!(needAk || needA[l])) return -1;
+    return k == l ? 2 : (ns == 2 ? 3 : 4);
+  }
+  if (!needAk) return -1;
+  return __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta ? 0 : 1;
+}
+
+template <bool FILL>
+__global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
+                             const unsigned char* __restrict__ needA, int* __restrict__ cnt,
+                             const long long* __restrict__ off, int2* __restrict__ lf,
+                             int2* __restrict__ lp, int2* __restrict__ ls0, int2* __restrict__ ls1,
+                             int2* __restrict__ ls2) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int i = warp; i < nR; i += nwarps) {
+    const int k = roots[i];
+    const int4 ek = P.elem[k];
+    const double2 ck = P.ctr[k];
+    const double rk = P.rad[k];
+    const bool needAk = needA[k];
+    int ix = (int)floor((ck.x - G.ox) / G.cs), iy = (int)floor((ck.y - G.oy) / G.cs);
+    ix = min(max(ix, 0), G.nx - 1);
+    iy = min(max(iy, 0), G.ny - 1);
+    int c[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long base[5];
+    int2* lists[5] = {lf, lp, ls0, ls1, ls2};
+    if (FILL)
+      for (int j = 0; j < 5; ++j) base[j] = off[(long long)j * (nR + 1) + i];
+    for (int yy = max(iy - 1, 0); yy <= min(iy + 1, G.ny - 1); ++yy) {
+      const int c0 = G.start[yy * G.nx + max(ix - 1, 0)];
+      const int c1 = G.start[yy * G.nx + min(ix + 1, G.nx - 1) + 1];
+      for (int j0 = c0; j0 < c1; j0 += 32) {
+        const int j = j0 + lane;
+        int cat = -1;
+        bool vis = false;
+        if (j < c1) cat = classify(P, k, ek, ck, rk, needAk, needA, G.items[j], vis);
+        if (!FILL) {
+          c[C_EPI] += vis;
+          if (cat >= 0) c[cat]++;
+        } else {
+          const int l = j < c1 ? G.items[j] : 0;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            const unsigned m = __ballot_sync(0xffffffffu, cat == q);
+            if (cat == q) lists[q][base[q] + __popc(m & lt)] = make_int2(k, l);
+            base[q] += __popc(m);
+          }
+        }
+      }
+    }
+    if (!FILL) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        int v = c[q];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        c[q] = v;
+      }
+      if (lane == 0) {
+        for (int q = 0; q < 6; ++q) cnt[(long long)q * nR + i] = c[q];
+        // does this root own the batch's count of its pairs (EPI home rule)?
+        const int4 d = P.dofs[k];
+        const long long rmin = (long long)P.nc * min(d.x, min(d.y, d.z));
+        cnt[(long long)C_KK * nR + i] = needAk ? ((rmin >= P.row_lo && rmin < P.row_hi) ? 2 : 1) : 0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- visits
+__device__ __forceinline__ unsigned long long coo_key(const Params& P, long long row, long long col) {
+  if (row < P.row_lo || row >= P.row_hi) return kSentinel;
+  return (unsigned long long)(row - P.row_lo) * (unsigned long long)P.J + (unsigned long long)col;
+}
+// reference emits a triplet iff v != 0 (_engine.py:410-424); an absent
+// entry is stored as +0.0, a present one that is exactly zero as -0.0
+__device__ __forceinline__ double emit_val(double v) { return v != 0.0 ? v : 0.0; }
+
+__device__ __forceinline__ void note_nonfinite(double v, int k, int l, int K,
+                                               unsigned long long* errpair) {
+  if (!isfinite(v)) atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
+}
+
+template <typename T>
+__device__ __forceinline__ void warp_add_ll(T v, unsigned long long* dst) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane_id() == 0 && v) atomicAdd(dst, (unsigned long long)v);
+}
+
+struct VisitOut {
+  double* kkv;              // [E][nvis] kk block values (entry-major)
+  unsigned long long* kkf;  // [nvis] presence bits of the kk block
+  long long nvis;           // n_full + n_partial
+  long long vofs;           // this list's first visit index
+  unsigned long long* keys;  // COO
+  double* vals;
+  long long cbase;  // this list's COO slot base (entry-major over the list)
+  long long nlist;
+  unsigned long long* counters;
+  unsigned long long* errpair;
+};
+
+template <int KID, bool FULL>
+__global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict__ list, VisitOut O) {
+  using T = KTraits<KID>;
+  constexpr int E = T::E, NC = T::NC;
+  long long ev0 = 0, ev2 = 0, out0 = 0, out2 = 0, e_m1 = 0, o_m1 = 0;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < O.nlist;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int2 pr = list[v];
+    const int k = pr.x, l = pr.y;
+    double kx[3], ky[3], lx[3], ly[3];
+    load_tri(P, k, kx, ky);
+    const int4 ek = __ldg(&P.elem[k]);
+    const int4 el = __ldg(&P.elem[l]);
+    const bool touching = (k == l) || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
+                          ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
+    const double rs2 = (touching && P.path == 1) ? P.rskip2 : 0.0;
+    double kk[E], kl[E];
+    unsigned long long flags = 0;
+    if (k == l) {
+      if (FULL) {
+        full_identical<KID>(P, kx, ky, rs2, kk, kl, ev2);
+        out2 += 7;
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) kk[e] = kl[e] = 0.0;
+        sweep<KID, 2>(P, kx, ky, kx, ky, rs2, kk, kl, e_m1, o_m1);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (kk[e] != 0.0 || kl[e] != 0.0) flags |= 1ull << e;
+        kk[e] += kl[e];
+        kl[e] = 0.0;
+      }
+    } else {
+      load_tri(P, l, lx, ly);
+      if (FULL) {
+        full_pair<KID>(P, kx, ky, lx, ly, rs2, kk, kl, ev0);
+        out0 += 14;
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) kk[e] = kl[e] = 0.0;
+        sweep<KID, 0>(P, kx, ky, lx, ly, rs2, kk, kl, ev0, out0);
+        sweep<KID, 1>(P, lx, ly, kx, ky, rs2, kk, kl, ev2, out2);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (kk[e] != 0.0) flags |= 1ull << e;
+    }
+    // root block -> per-visit scratch; neighbour block -> COO
+    const long long vi = O.vofs + v;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      note_nonfinite(kk[e], k, l, P.K, O.errpair);
+      O.kkv[(long long)e * O.nvis + vi] = kk[e];
+    }
+    O.kkf[vi] = flags;
+    const int4 dk = __ldg(&P.dofs[k]);
+    const int4 dl = __ldg(&P.dofs[l]);
+    const int dka[3] = {dk.x, dk.y, dk.z}, dla[3] = {dl.x, dl.y, dl.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int d = 0; d < NC; ++d) {
+            const int e = ((a * NC + c) * 3 + b) * NC + d;
+            const long long slot = O.cbase + (long long)e * O.nlist + v;
+            if (k == l) {
+              O.keys[slot] = kSentinel;
+              O.vals[slot] = 0.0;
+            } else {
+              note_nonfinite(kl[e], k, l, P.K, O.errpair);
+              O.keys[slot] = coo_key(P, (long long)NC * dka[a] + c, (long long)NC * dla[b] + d);
+              O.vals[slot] = emit_val(kl[e]);
+            }
+          }
+  }
+  if (FULL) {
+    warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
+    warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
+    warp_add_ll(out0, &O.counters[K_OUT_FULL0]);
+    warp_add_ll(out2, &O.counters[K_OUT_FULL2]);
+  } else {
+    // mode-0 evals in ev0/out0, mode-1 in ev2/out2, mode-2 (identical) in e_m1/o_m1
+    warp_add_ll(ev0, &O.counters[K_EVAL_M0]);
+    warp_add_ll(out0, &O.counters[K_OUT_M0]);
+    warp_add_ll(ev2, &O.counters[K_EVAL_M1]);
+    warp_add_ll(out2, &O.counters[K_OUT_M1]);
+    warp_add_ll(e_m1, &O.counters[K_EVAL_M2]);
+    warp_add_ll(o_m1, &O.counters[K_OUT_M2]);
+  }
+}
+
+// per-root sum of the root's own block over all its visits, fixed order
+template <int E>
+__global__ void k_kk_reduce(Params P, const int* __restrict__ roots, int nR,
+                            const int* __restrict__ cnt, const long long* __restrict__ off,
+                            long long nF, const double* __restrict__ kkv,
+                            const unsigned long long* __restrict__ kkf, long long nvis,
+                            unsigned long long* keys, double* vals, long long cbase) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int NC = E == 36 ? 2 : 1;
+  for (int i = warp; i < nR; i += nwarps) {
+    const int k = roots[i];
+    const bool emit = cnt[(long long)C_KK * nR + i] != 0;
+    const long long f0 = off[0 * (long long)(nR + 1) + i], fn = cnt[(long long)C_FULL * nR + i];
+    const long long p0 = nF + off[1 * (long long)(nR + 1) + i], pn = cnt[(long long)C_PART * nR + i];
+    unsigned long long fl = 0;
+    for (long long j = lane; j < fn; j += 32) fl |= kkf[f0 + j];
+    for (long long j = lane; j < pn; j += 32) fl |= kkf[p0 + j];
+    for (int o = 16; o; o >>= 1) fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    const int4 dk = P.dofs[k];
+    const int dka[3] = {dk.x, dk.y, dk.z};
+    for (int e = 0; e < E; ++e) {
+      double s = 0.0;
+      for (long long j = lane; j < fn; j += 32) s += kkv[(long long)e * nvis + f0 + j];
+      for (long long j = lane; j < pn; j += 32) s += kkv[(long long)e * nvis + p0 + j];
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        const int rr = e / (3 * NC), cc = e % (3 * NC);
+        const int a = rr / NC, c = rr % NC, b = cc / NC, d = cc % NC;
+        const long long slot = cbase + (long long)e * nR + i;
+        const bool present = emit && ((fl >> e) & 1ull);
+        keys[slot] = present ? coo_key(P, (long long)NC * dka[a] + c, (long long)NC * dka[b] + d)
+                             : kSentinel;
+        vals[slot] = present ? (s != 0.0 ? s : -0.0) : 0.0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- singular pairs
+struct SingRule {
+  const double* __restrict__ xs;
+  const double* __restrict__ ys;
+  const double* __restrict__ w;
+  const double* __restrict__ hx;
+  const double* __restrict__ hy;
+  int n;
+};
+
+template <int U, int NC, bool SYM>
+struct SingAcc {
+  static constexpr int UN = U * NC;
+  static constexpr int N = SYM ? UN * (UN + 1) / 2 : UN * UN;
+  __device__ static constexpr int idx(int i, int j) {
+    return SYM ? (i <= j ? i * UN - i * (i - 1) / 2 + (j - i) : j * UN - j * (j - 1) / 2 + (i - j))
+               : i * UN + j;
+  }
+};
+
+// FAM 0 identical (U = 3), 1 edge (U = 4, DG 6), 2 vertex (U = 5, DG 6);
+// frames and union tables follow _engine._visit_pair :230-308.
+template <int KID, int FAM, int U>
+__global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restrict__ list,
+                                                  long long n, SingRule R,
+                                                  unsigned long long* keys, double* vals,
+                                                  long long cbase, unsigned long long* counters,
+                                                  unsigned long long* errpair) {
+  using T = KTraits<KID>;
+  constexpr int NC = T::NC, UN = U * NC;
+  using A = SingAcc<U, NC, T::SYM>;
+  constexpr int SLOTS = 36 * NC * NC;
+  __shared__ double sTA[3][2], sTB[3][2], sScale;
+  __shared__ int sMk[6], sMl[6], sUb[6];
+  __shared__ double red[4][A::N];
+  long long npts = 0;
+  for (long long pi = blockIdx.x; pi < n; pi += gridDim.x) {
+    const int k = list[pi].x, l = list[pi].y;
+    if (threadIdx.x == 0) {
+      const int4 ek = P.elem[k], el = P.elem[l];
+      const int4 dk = P.dofs[k], dl = P.dofs[l];
+      const int ea[3] = {ek.x, ek.y, ek.z}, eb[3] = {el.x, el.y, el.z};
+      const int da[3] = {dk.x, dk.y, dk.z}, db[3] = {dl.x, dl.y, dl.z};
+      int permk[3] = {0, 1, 2}, perml[3] = {0, 1, 2};
+      int a0 = -1, a1 = -1, b0 = -1, b1 = -1, ns = 0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          if (ea[a] == eb[b]) {
+            if (ns == 0) { a0 = a; b0 = b; } else if (ns == 1) { a1 = a; b1 = b; }
+            ++ns;
+          }
+      if (FAM == 0) {
+        for (int m = 0; m < 3; ++m) { sMk[m] = m; sMl[m] = m; sUb[m] = da[m]; }
+      } else if (FAM == 1) {
+        if (ea[a0] > ea[a1]) { int t = a0; a0 = a1; a1 = t; t = b0; b0 = b1; b1 = t; }
+        permk[0] = a0; permk[1] = a1; permk[2] = 3 - a0 - a1;
+        perml[0] = b0; perml[1] = b1; perml[2] = 3 - b0 - b1;
+        const int mk[4] = {0, 1, 2, -1}, ml[4] = {0, 1, -1, 2};
+        for (int m = 0; m < 4; ++m) { sMk[m] = mk[m]; sMl[m] = ml[m]; }
+        sUb[0] = da[permk[0]]; sUb[1] = da[permk[1]]; sUb[2] = da[permk[2]]; sUb[3] = db[perml[2]];
+      } else {
+        permk[0] = a0; permk[1] = (a0 + 1) % 3; permk[2] = (a0 + 2) % 3;
+        perml[0] = b0; perml[1] = (b0 + 1) % 3; perml[2] = (b0 + 2) % 3;
+        const int mk[5] = {0, 1, 2, -1, -1}, ml[5] = {0, -1, -1, 1, 2};
+        for (int m = 0; m < 5; ++m) { sMk[m] = mk[m]; sMl[m] = ml[m]; }
+        sUb[0] = da[permk[0]]; sUb[1] = da[permk[1]]; sUb[2] = da[permk[2]];
+        sUb[3] = db[perml[1]]; sUb[4] = db[perml[2]];
+      }
+      if (FAM != 0 && U == 6) {  // DG union: all six local hats
+        for (int m = 0; m < 3; ++m) {
+          sMk[m] = m; sMk[3 + m] = -1; sMl[m] = -1; sMl[3 + m] = m;
+          sUb[m] = da[permk[m]]; sUb[3 + m] = db[perml[m]];
+        }
+      }
+      for (int m = 0; m < 3; ++m) {
+        const double2 va = P.vtx[ea[permk[m]]], vb = P.vtx[eb[perml[m]]];
+        sTA[m][0] = va.x; sTA[m][1] = va.y;
+        sTB[m][0] = vb.x; sTB[m][1] = vb.y;
+      }
+      const double ck = cross2(sTA[1][0] - sTA[0][0], sTA[2][1] - sTA[0][1], sTA[1][1] - sTA[0][1], sTA[2][0] - sTA[0][0]);
+      const double cl = cross2(sTB[1][0] - sTB[0][0], sTB[2][1] - sTB[0][1], sTB[1][1] - sTB[0][1], sTB[2][0] - sTB[0][0]);
+      double sc = fabs(ck) * fabs(cl);
+      if (k != l) sc *= 2.0;
+      sScale = sc;
+    }
+    __syncthreads();
+    double acc[A::N];
+#pragma unroll
+    for (int i = 0; i < A::N; ++i) acc[i] = 0.0;
+    const double t0x = sTA[0][0], t0y = sTA[0][1], u0x = sTB[0][0], u0y = sTB[0][1];
+    const double e1kx = sTA[1][0] - t0x, e1ky = sTA[1][1] - t0y, e2kx = sTA[2][0] - t0x, e2ky = sTA[2][1] - t0y;
+    const double e1lx = sTB[1][0] - u0x, e1ly = sTB[1][1] - u0y, e2lx = sTB[2][0] - u0x, e2ly = sTB[2][1] - u0y;
+    int mk[U], ml[U];
+#pragma unroll
+    for (int m = 0; m < U; ++m) { mk[m] = sMk[m]; ml[m] = sMl[m]; }
+    for (int i = threadIdx.x; i < R.n; i += blockDim.x) {
+      const double xs0 = __ldg(&R.xs[2 * i]), xs1 = __ldg(&R.xs[2 * i + 1]);
+      const double ys0 = __ldg(&R.ys[2 * i]), ys1 = __ldg(&R.ys[2 * i + 1]);
+      const double x0 = __dadd_rn(__dadd_rn(t0x, mul(e1kx, xs0)), mul(e2kx, xs1));
+      const double x1 = __dadd_rn(__dadd_rn(t0y, mul(e1ky, xs0)), mul(e2ky, xs1));
+      const double y0 = __dadd_rn(__dadd_rn(u0x, mul(e1lx, ys0)), mul(e2lx, ys1));
+      const double y1 = __dadd_rn(__dadd_rn(u0y, mul(e1ly, ys0)), mul(e2ly, ys1));
+      const double d0 = x0 - y0, d1 = x1 - y1;
+      const double r2 = sumsq(d0, d1);
+      if (r2 <= 0.0) continue;
+      double pv[NC * NC], qv[NC * NC];
+      kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
+      ++npts;
+      double phx[U], phy[U], tm[U];
+#pragma unroll
+      for (int m = 0; m < U; ++m) {
+        phx[m] = mk[m] >= 0 ? __ldg(&R.hx[3 * i + mk[m]]) : 0.0;
+        phy[m] = ml[m] >= 0 ? __ldg(&R.hy[3 * i + ml[m]]) : 0.0;
+        tm[m] = phx[m] - phy[m];
+      }
+      const double wi = __ldg(&R.w[i]);
+#pragma unroll
+      for (int m = 0; m < U; ++m)
+#pragma unroll
+        for (int mp = 0; mp < U; ++mp) {
+          if (T::SYM && mp < m) continue;
+          const double cf = wi * (tm[m] * tm[mp]);
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int d = 0; d < NC; ++d) {
+              const int ii = m * NC + c, jj = mp * NC + d;
+              if (T::SYM && m == mp && jj < ii) continue;
+              if (T::SYM)
+                acc[A::idx(ii, jj)] = fma(cf, pv[c * NC + d], acc[A::idx(ii, jj)]);
+              else
+                acc[A::idx(ii, jj)] += (wi * tm[m]) * (pv[c * NC + d] * phx[mp] - qv[c * NC + d] * phy[mp]);
+            }
+        }
+    }
+    // deterministic block reduction
+#pragma unroll
+    for (int i = 0; i < A::N; ++i) {
+      double v = acc[i];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane_id() == 0) red[threadIdx.x >> 5][i] = v;
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < SLOTS; s += blockDim.x) {
+      const long long slot = cbase + pi * SLOTS + s;
+      const int ii = s / (6 * NC), jj = s % (6 * NC);
+      if (ii >= UN || jj >= UN) {
+        keys[slot] = kSentinel;
+        vals[slot] = 0.0;
+        continue;
+      }
+      const int ai = A::idx(ii, jj);
+      const double v = (((red[0][ai] + red[1][ai]) + red[2][ai]) + red[3][ai]) * sScale;
+      note_nonfinite(v, k, l, P.K, errpair);
+      const int m = ii / NC, c = ii % NC, mp = jj / NC, d = jj % NC;
+      keys[slot] = coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d);
+      vals[slot] = emit_val(v);
+    }
+    __syncthreads();
+  }
+  warp_add_ll(npts, &counters[K_SPTS3 + (U - 3)]);
+}
+
+// ---------------------------------------------------------------- merge
+__global__ void k_seg_heads(const unsigned long long* __restrict__ key, long long n, int* head) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long k = key[i];
+  head[i] = k != kSentinel && (i == 0 || key[i - 1] != k);
+}
+
+__global__ void k_seg_starts(const unsigned long long* __restrict__ key, long long n,
+                             const int* __restrict__ head, const long long* __restrict__ sid,
+                             long long* start) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (head[i]) start[sid[i]] = i;
+  const bool valid = key[i] != kSentinel;
+  if (valid && (i + 1 == n || key[i + 1] == kSentinel)) start[sid[i] + head[i]] = i + 1;
+}
+
+// one thread per (row, col): left-to-right sum in COO position order
+__global__ void k_seg_sum(const unsigned long long* __restrict__ key, const double* __restrict__ val,
+                          const long long* __restrict__ start, long long nseg, long long J,
+                          int* present, int* rowcnt, int* col, double* sum) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const long long a = start[s], b = start[s + 1];
+  double acc = 0.0;
+  bool pres = false;
+  for (long long i = a; i < b; ++i) {
+    const double v = val[i];
+    acc += v;
+    pres |= __double_as_longlong(v) != 0;
+  }
+  const unsigned long long kk = key[a];
+  present[s] = pres;
+  col[s] = (int)(kk % (unsigned long long)J);
+  sum[s] = acc;
+  if (pres) atomicAdd(&rowcnt[kk / (unsigned long long)J], 1);
+}
+
+__global__ void k_seg_scatter(const int* __restrict__ present, const long long* __restrict__ pos,
+                              const int* __restrict__ col, const double* __restrict__ sum,
+                              long long nseg, int* indices, double* data) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= nseg || !present[s]) return;
+  indices[pos[s]] = col[s];
+  data[pos[s]] = sum[s];
+}
+
+__global__ void k_add_offset(long long* p, long long n, long long off) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) p[i] += off;
+}
+
+// ---------------------------------------------------------------- load vector
+__global__ void k_load_points(Params P, const int* __restrict__ act, int nact, double* pts) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)nact * 7) return;
+  const int m = (int)(t / 7), p = (int)(t % 7);
+  double tx[3], ty[3];
+  load_tri(P, act[m], tx, ty);
+  const double e1x = tx[1] - tx[0], e1y = ty[1] - ty[0], e2x = tx[2] - tx[0], e2y = ty[2] - ty[0];
+  // coords[:, 0] + e1 * op0 + e2 * op1 (assembly.py:468-469)
+  pts[2 * t] = __dadd_rn(__dadd_rn(tx[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+  pts[2 * t + 1] = __dadd_rn(__dadd_rn(ty[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+}
+
+// per active element: contrib[a][c] = 2A sum_p ow_p oh_pa f(x_p)_c
+__global__ void k_load_contrib(Params P, const int* __restrict__ act, int nact,
+                               const double* __restrict__ fx, int fconst, double* contrib) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= nact) return;
+  double tx[3], ty[3];
+  load_tri(P, act[m], tx, ty);
+  const double twoA = twice_area(tx, ty);
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < P.nc; ++c) {
+      double s = 0.0;
+      for (int p = 0; p < 7; ++p) {
+        const double f = fconst ? fx[c] : fx[((long long)m * 7 + p) * P.nc + c];
+        s += (c_rule.ow[p] * c_rule.oh[p][a]) * f;
+      }
+      contrib[((long long)m * 3 + a) * P.nc + c] = s * twoA;
+    }
+}
+
+// b[nc*dof + c]: sum over the (element, local hat) incidences of the dof in
+// element order (the np.add.at scatter order, assembly.py:477-480)
+__global__ void k_load_gather(const int* __restrict__ inc_start, const int* __restrict__ inc_item,
+                              const double* __restrict__ contrib, int nbase, int nc, double* b) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nbase) return;
+  for (int c = 0; c < nc; ++c) {
+    double s = 0.0;
+    for (int j = inc_start[v]; j < inc_start[v + 1]; ++j) s += contrib[(long long)inc_item[j] * nc + c];
+    b[(long long)nc * v + c] = s;
+  }
+}
+
+__global__ void k_load_inc(Params P, const int* __restrict__ act, int nact, unsigned* key, int* item) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)nact * 3) return;
+  const int m = (int)(t / 3), a = (int)(t % 3);
+  const int4 d = P.dofs[act[m]];
+  key[t] = (unsigned)(a == 0 ? d.x : a == 1 ? d.y : d.z);
+  item[t] = (int)t;  // m * 3 + a, element-major
+}
+
+__global__ void k_active(Params P, int* flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < P.K) flag[k] = (P.elem[k].w & 15) != 0;
+}
+
+// ---------------------------------------------------------------- fp64 peak
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+  for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-9 + j;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+  double s = 0;
+  for (int j = 0; j < 8; ++j) s += x[j];
+  if (s == 1234.5) out[0] = s;
+}
+
+__global__ void k_iota(int* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+
+inline unsigned grid_for(long long n, int bs) {
+  long long g = (n + bs - 1) / bs;
+  return (unsigned)std::max(1LL, std::min(g, 2147483647LL));
+}
+
+}  // namespace
+
+// ===================================================================== plan
+struct nlg_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Params P{};
+  // owned device arrays
+  double2* vtx = nullptr;
+  int4* elem = nullptr;
+  int4* dofs = nullptr;
+  double2* ctr = nullptr;
+  double* rad = nullptr;
+  double* sing_tab[3][5] = {};
+  int sing_n[3] = {0, 0, 0};
+  bool prepped = false;
+  Grid G{};
+  int* grid_start = nullptr;
+  int* grid_items = nullptr;
+  // load vector support
+  int* act = nullptr;
+  int nact = -1;
+  int nbase = 0;
+};
+
+namespace {
+
+struct DevBuf {  // stream-ordered scratch
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t n, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(&p, std::max<size_t>(n, 16), st);
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+nlg_status prep(nlg_plan* pl) {
+  if (pl->prepped) return NLG_OK;
+  Params& P = pl->P;
+  cudaStream_t st = pl->stream;
+  const int K = P.K;
+  DevBuf ext;
+  CK(ext.alloc(5 * sizeof(unsigned long long), st));
+  unsigned long long init[5] = {~0ull, ~0ull, 0ull, 0ull, 0ull};
+  CK(cudaMemcpyAsync(ext.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+  k_bounds<<<grid_for(K, 256), 256, 0, st>>>(P, pl->ctr, pl->rad, ext.as<unsigned long long>());
+  LAUNCHED();
+  unsigned long long h[5];
+  CK(cudaMemcpyAsync(h, ext.p, sizeof h, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double ox = ord2d(h[0]), oy = ord2d(h[1]), mx = ord2d(h[2]), my = ord2d(h[3]), rmax = ord2d(h[4]);
+  if (h[2] == 0ull) { ox = oy = mx = my = 0.0; rmax = 0.0; }  // no active element
+  double cs = (P.prer + 2.0 * rmax) * (1.0 + 1e-9) + 1e-300;
+  // keep the cell count bounded (tiny horizons on huge meshes)
+  const double ext_x = mx - ox, ext_y = my - oy;
+  while ((ext_x / cs + 1.0) * (ext_y / cs + 1.0) > 6.0e7) cs *= 2.0;
+  Grid G;
+  G.ox = ox; G.oy = oy; G.cs = cs;
+  G.nx = (int)floor(ext_x / cs) + 1;
+  G.ny = (int)floor(ext_y / cs) + 1;
+  const int ncell = G.nx * G.ny;
+  DevBuf key, val, key2;
+  CK(key.alloc(sizeof(unsigned) * K, st));
+  CK(val.alloc(sizeof(int) * K, st));
+  CK(key2.alloc(sizeof(unsigned) * K, st));
+  if (pl->grid_items) cudaFreeAsync(pl->grid_items, st);
+  if (pl->grid_start) cudaFreeAsync(pl->grid_start, st);
+  CK(cudaMallocAsync(&pl->grid_items, sizeof(int) * std::max(K, 1), st));
+  CK(cudaMallocAsync(&pl->grid_start, sizeof(int) * (ncell + 1), st));
+  k_cell<<<grid_for(K, 256), 256, 0, st>>>(P, G, key.as<unsigned>(), val.as<int>());
+  LAUNCHED();
+  int bits = 1;
+  while ((1ll << bits) <= ncell) ++bits;
+  size_t tmpb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmpb, key.as<unsigned>(), key2.as<unsigned>(), val.as<int>(),
+                                     pl->grid_items, K, 0, bits, st));
+  DevBuf tmp;
+  CK(tmp.alloc(tmpb, st));
+  CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmpb, key.as<unsigned>(), key2.as<unsigned>(), val.as<int>(),
+                                     pl->grid_items, K, 0, bits, st));
+  g_launches += 4;
+  k_cell_ranges<<<grid_for(ncell + 1, 256), 256, 0, st>>>(key2.as<unsigned>(), K, ncell, pl->grid_start);
+  LAUNCHED();
+  G.start = pl->grid_start;
+  G.items = pl->grid_items;
+  pl->G = G;
+  pl->prepped = true;
+  return NLG_OK;
+}
+
+struct Csr {  // one batch's rows
+  long long row_lo, row_hi, nnz;
+  long long* indptr;
+  int* indices;
+  double* data;
+};
+
+struct Counters {
+  unsigned long long c[K_NCOUNTERS];
+};
+
+// algorithmic FP64 flops of the reference for the counted work
+long long alg_flops(const Params& P, const unsigned long long* c) {
+  const long long nc = P.nc, nc2 = nc * nc;
+  const bool ns = !P.sym;
+  const long long kf = P.kid == 0 ? 2 : P.kid == 1 ? 9 : P.kid == 3 ? 4 : 0;
+  const long long a0 = ns ? 9 * nc2 : 8 * nc2, a1 = ns ? 35 * nc2 : 34 * nc2, a2 = 35 * nc2;
+  const long long f0 = 9 * nc * (3 + 4 * nc) + 9, f1 = 9 * nc * (1 + 4 * nc) + 9, f2 = 9 * nc * (4 + 8 * nc) + 9;
+  long long fl = 0;
+  // full pairs: K_EVAL_FULL0 counts the 7x7 point pairs once; the reference
+  // evaluates each in mode 0 and again in mode 1
+  fl += (long long)c[K_EVAL_FULL0] * ((26 + kf + a0) + (26 + kf + a1));
+  fl += (long long)c[K_OUT_FULL0] / 2 * (f0 + f1);
+  fl += (long long)c[K_EVAL_FULL2] * (26 + kf + a2) + (long long)c[K_OUT_FULL2] * f2;
+  fl += (long long)c[K_EVAL_M0] * (26 + kf + a0) + (long long)c[K_OUT_M0] * f0;
+  fl += (long long)c[K_EVAL_M1] * (26 + kf + a1) + (long long)c[K_OUT_M1] * f1;
+  fl += (long long)c[K_EVAL_M2] * (26 + kf + a2) + (long long)c[K_OUT_M2] * f2;
+  for (int u = 3; u <= 6; ++u)
+    fl += (long long)c[K_SPTS3 + u - 3] * (16 + 5 + kf + u + u * u * (2 + 2 * nc2));
+  return fl;
+}
+
+template <int KID>
+nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long nF, const int2* lp,
+                      long long nP, VisitOut O, cudaEvent_t ev_mid) {
+  O.vofs = 0;
+  O.nlist = nF;
+  if (nF) {
+    k_visits<KID, true><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, O);
+    LAUNCHED();
+  }
+  CK(cudaEventRecord(ev_mid, pl->stream));
+  O.vofs = nF;
+  O.cbase += 9LL * KTraits<KID>::NC2 * nF;
+  O.nlist = nP;
+  if (nP) {
+    k_visits<KID, false><<<grid_for(nP, 128), 128, 0, pl->stream>>>(P, lp, O);
+    LAUNCHED();
+  }
+  return NLG_OK;
+}
+
+template <int KID>
+nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const long long* nS,
+                        unsigned long long* keys, double* vals, long long cbase,
+                        unsigned long long* counters, unsigned long long* errpair) {
+  constexpr int NC = KTraits<KID>::NC;
+  const long long slots = 36LL * NC * NC;
+  for (int f = 0; f < 3; ++f) {
+    if (!nS[f]) continue;
+    SingRule R{pl->sing_tab[f][0], pl->sing_tab[f][1], pl->sing_tab[f][2], pl->sing_tab[f][3],
+               pl->sing_tab[f][4], pl->sing_n[f]};
+    const unsigned g = (unsigned)std::min<long long>(nS[f], 1 << 20);
+    if (f == 0)
+      k_singular<KID, 0, 3><<<g, 128, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair);
+    else if (P.is_dg)
+      (f == 1 ? k_singular<KID, 1, 6> : k_singular<KID, 2, 6>)<<<g, 128, 0, pl->stream>>>(
+          P, ls[f], nS[f], R, keys, vals, cbase, counters, errpair);
+    else if (f == 1)
+      k_singular<KID, 1, 4><<<g, 128, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair);
+    else
+      k_singular<KID, 2, 5><<<g, 128, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair);
+    LAUNCHED();
+    cbase += nS[f] * slots;
+  }
+  return NLG_OK;
+}
+
+struct Timing {
+  double prep = 0, cand = 0, full = 0, part = 0, sing = 0, merge = 0;
+};
+
+// one row batch: returns NLG_OK and appends to `out`, or asks for a split
+nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget,
+                     std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
+                     unsigned long long* d_counters, unsigned long long* d_err, bool* need_split) {
+  *need_split = false;
+  Params P = pl->P;
+  P.row_lo = row_lo;
+  P.row_hi = row_hi;
+  cudaStream_t s = pl->stream;
+  const int K = P.K;
+  cudaEvent_t ev[8];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); }
+  } evg{ev};
+  CK(cudaEventRecord(ev[0], s));
+  // ---- root selection
+  DevBuf needA, vmark, rflag, roots, nroots;
+  CK(needA.alloc(K, s));
+  CK(rflag.alloc(sizeof(int) * K, s));
+  CK(roots.alloc(sizeof(int) * K, s));
+  CK(nroots.alloc(sizeof(int), s));
+  k_mark_a<<<grid_for(K, 256), 256, 0, s>>>(P, needA.as<unsigned char>());
+  LAUNCHED();
+  if (P.path == 2) {
+    CK(vmark.alloc(P.V, s));
+    CK(cudaMemsetAsync(vmark.p, 0, P.V, s));
+    k_mark_vertices<<<grid_for(K, 256), 256, 0, s>>>(P, needA.as<unsigned char>(), vmark.as<unsigned char>());
+    LAUNCHED();
+  }
+  k_mark_roots<<<grid_for(K, 256), 256, 0, s>>>(P, needA.as<unsigned char>(), vmark.as<unsigned char>(),
+                                                 rflag.as<int>());
+  LAUNCHED();
+  {
+    DevBuf idx;
+    CK(idx.alloc(sizeof(int) * K, s));
+    k_iota<<<grid_for(K, 256), 256, 0, s>>>(idx.as<int>(), K);
+    LAUNCHED();
+    size_t tb = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, idx.as<int>(), rflag.as<int>(), roots.as<int>(),
+                                  nroots.as<int>(), K, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceSelect::Flagged(tmp.p, tb, idx.as<int>(), rflag.as<int>(), roots.as<int>(),
+                                  nroots.as<int>(), K, s));
+    g_launches += 1;
+  }
+  int nR = 0;
+  CK(cudaMemcpyAsync(&nR, nroots.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // ---- candidate counts
+  DevBuf cnt, off;
+  CK(cnt.alloc(sizeof(int) * (size_t)kCnt * std::max(nR, 1), s));
+  CK(off.alloc(sizeof(long long) * 6 * (size_t)(nR + 1), s));
+  const int cand_blocks = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
+  if (nR) {
+    k_candidates<false><<<std::max(cand_blocks, 1), 256, 0, s>>>(
+        P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), cnt.as<int>(), nullptr, nullptr,
+        nullptr, nullptr, nullptr, nullptr);
+    LAUNCHED();
+  }
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int>(), off.as<long long>(), nR + 1, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    for (int q = 0; q < 6; ++q) {
+      // off[q] = exclusive scan of cnt[q] over nR+1 entries (last = total);
+      // the (nR+1)-th input reads the next column's first entry, so scan nR
+      // entries and write the total separately
+      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
+                                       off.as<long long>() + (size_t)q * (nR + 1), nR, s));
+      g_launches += 1;
+    }
+  }
+  // totals: off[q][nR-1] + cnt[q][nR-1]
+  long long tot[6] = {0, 0, 0, 0, 0, 0};
+  if (nR) {
+    long long lastoff[6];
+    int lastcnt[6];
+    for (int q = 0; q < 6; ++q) {
+      CK(cudaMemcpyAsync(&lastoff[q], off.as<long long>() + (size_t)q * (nR + 1) + nR - 1, sizeof(long long),
+                         cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&lastcnt[q], cnt.as<int>() + (size_t)q * nR + nR - 1, sizeof(int),
+                         cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int q = 0; q < 6; ++q) {
+      tot[q] = lastoff[q] + lastcnt[q];
+      CK(cudaMemcpyAsync(off.as<long long>() + (size_t)q * (nR + 1) + nR, &tot[q], sizeof(long long),
+                         cudaMemcpyHostToDevice, s));
+    }
+  }
+  const long long nF = tot[C_FULL], nPt = tot[C_PART];
+  const long long nS[3] = {tot[C_SID], tot[C_SED], tot[C_SVX]};
+  const int NC = P.nc;
+  const long long E = 9LL * NC * NC;
+  const long long nvis = nF + nPt;
+  const long long coo = (long long)nR * E + nvis * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
+  // bytes: keys+vals twice (sort double buffer) + kk scratch + lists + merge arrays
+  const long long bytes = coo * 16 * 2 + nvis * (E * 8 + 8) + (nvis + nS[0] + nS[1] + nS[2]) * 8 +
+                          coo * 8 * 3;
+  if (budget > 0 && bytes > budget && row_hi - row_lo > 1) {
+    *need_split = true;
+    return NLG_OK;
+  }
+  if (coo >= (1LL << 31)) {
+    if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
+    set_err("a single row needs %lld COO slots", coo);
+    return NLG_ERR_CUDA;
+  }
+  // EPI of the roots whose home is this batch: sum cnt[EPI] where cnt[KK] == 2
+  {
+    std::vector<int> hc((size_t)2 * nR);
+    if (nR) {
+      CK(cudaMemcpyAsync(hc.data(), cnt.as<int>() + (size_t)C_EPI * nR, sizeof(int) * nR, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hc.data() + nR, cnt.as<int>() + (size_t)C_KK * nR, sizeof(int) * nR, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    for (int i = 0; i < nR; ++i)
+      if (hc[nR + i] == 2) { st->epi += hc[i]; st->n_roots += 1; }
+  }
+  // ---- candidate lists
+  DevBuf lists;
+  CK(lists.alloc(sizeof(int2) * (size_t)std::max(1LL, nvis + nS[0] + nS[1] + nS[2]), s));
+  int2* lf = lists.as<int2>();
+  int2* lp = lf + nF;
+  int2* ls[3] = {lp + nPt, lp + nPt + nS[0], lp + nPt + nS[0] + nS[1]};
+  if (nR) {
+    k_candidates<true><<<std::max(cand_blocks, 1), 256, 0, s>>>(
+        P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), cnt.as<int>(), off.as<long long>(), lf,
+        lp, ls[0], ls[1], ls[2]);
+    LAUNCHED();
+  }
+  CK(cudaEventRecord(ev[1], s));
+  // ---- integrate
+  DevBuf keys, vals, keys2, vals2, kkv, kkf;
+  CK(keys.alloc(sizeof(unsigned long long) * coo, s));
+  CK(vals.alloc(sizeof(double) * coo, s));
+  CK(kkv.alloc(sizeof(double) * E * std::max(nvis, 1LL), s));
+  CK(kkf.alloc(sizeof(unsigned long long) * std::max(nvis, 1LL), s));
+  VisitOut O;
+  O.kkv = kkv.as<double>();
+  O.kkf = kkf.as<unsigned long long>();
+  O.nvis = nvis;
+  O.keys = keys.as<unsigned long long>();
+  O.vals = vals.as<double>();
+  O.cbase = (long long)nR * E;
+  O.counters = d_counters;
+  O.errpair = d_err;
+  nlg_status rc = NLG_OK;
+  switch (P.kid) {
+    case 0: rc = run_visits<0>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
+    case 1: rc = run_visits<1>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
+    case 2: rc = run_visits<2>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
+    default: rc = run_visits<3>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
+  }
+  if (rc) return rc;
+  CK(cudaEventRecord(ev[3], s));
+  const long long sbase = (long long)nR * E + nvis * E;
+  switch (P.kid) {
+    case 0: rc = run_singular<0>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
+    case 1: rc = run_singular<1>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
+    case 2: rc = run_singular<2>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
+    default: rc = run_singular<3>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
+  }
+  if (rc) return rc;
+  CK(cudaEventRecord(ev[4], s));
+  if (nR) {
+    const int g = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
+    if (NC == 1)
+      k_kk_reduce<9><<<std::max(g, 1), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), off.as<long long>(), nF,
+                                                     O.kkv, O.kkf, nvis, O.keys, O.vals, 0);
+    else
+      k_kk_reduce<36><<<std::max(g, 1), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), off.as<long long>(), nF,
+                                                      O.kkv, O.kkf, nvis, O.keys, O.vals, 0);
+    LAUNCHED();
+  }
+  // ---- sort (row, col) keys; stable, so equal keys keep COO position order
+  const long long nrows = row_hi - row_lo;
+  int bits = 1;
+  {
+    const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
+    while (bits < 64 && (1ull << bits) <= maxkey) ++bits;
+  }
+  CK(keys2.alloc(sizeof(unsigned long long) * coo, s));
+  CK(vals2.alloc(sizeof(double) * coo, s));
+  cub::DoubleBuffer<unsigned long long> dk(keys.as<unsigned long long>(), keys2.as<unsigned long long>());
+  cub::DoubleBuffer<double> dv(vals.as<double>(), vals2.as<double>());
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)coo, 0, bits, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, (int)coo, 0, bits, s));
+    g_launches += (bits + 7) / 8 + 1;
+  }
+  // the sentinel's low `bits` bits are all ones, above every valid key
+  const unsigned long long* sk = dk.Current();
+  const double* sv = dv.Current();
+  // ---- segmented reduction to CSR
+  DevBuf head, sid, start, present, rowcnt, col, sum, pos;
+  CK(head.alloc(sizeof(int) * coo, s));
+  CK(sid.alloc(sizeof(long long) * (coo + 1), s));
+  k_seg_heads<<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>());
+  LAUNCHED();
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
+    g_launches += 1;
+  }
+  long long nseg = 0;
+  if (coo) {
+    long long lsid;
+    int lhead;
+    CK(cudaMemcpyAsync(&lsid, sid.as<long long>() + coo - 1, sizeof lsid, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lhead, head.as<int>() + coo - 1, sizeof lhead, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nseg = lsid + lhead;
+  }
+  CK(start.alloc(sizeof(long long) * (nseg + 1), s));
+  CK(present.alloc(sizeof(int) * std::max(nseg, 1LL), s));
+  CK(col.alloc(sizeof(int) * std::max(nseg, 1LL), s));
+  CK(sum.alloc(sizeof(double) * std::max(nseg, 1LL), s));
+  CK(pos.alloc(sizeof(long long) * (nseg + 1), s));
+  CK(rowcnt.alloc(sizeof(int) * (nrows + 1), s));
+  CK(cudaMemsetAsync(rowcnt.p, 0, sizeof(int) * (nrows + 1), s));
+  long long nnz = 0;
+  Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
+  CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
+  if (nseg) {
+    k_seg_starts<<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>(), sid.as<long long>(),
+                                                    start.as<long long>());
+    LAUNCHED();
+    k_seg_sum<<<grid_for(nseg, 256), 256, 0, s>>>(sk, sv, start.as<long long>(), nseg, P.J, present.as<int>(),
+                                                  rowcnt.as<int>(), col.as<int>(), sum.as<double>());
+    LAUNCHED();
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
+    long long lpos;
+    int lpres;
+    CK(cudaMemcpyAsync(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lpres, present.as<int>() + nseg - 1, sizeof lpres, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nnz = lpos + lpres;
+    CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
+    CK(cudaMallocAsync(&piece.data, sizeof(double) * std::max(nnz, 1LL), s));
+    k_seg_scatter<<<grid_for(nseg, 256), 256, 0, s>>>(present.as<int>(), pos.as<long long>(), col.as<int>(),
+                                                      sum.as<double>(), nseg, piece.indices, piece.data);
+    LAUNCHED();
+  } else {
+    CK(cudaMallocAsync(&piece.indices, sizeof(int), s));
+    CK(cudaMallocAsync(&piece.data, sizeof(double), s));
+  }
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    g_launches += 2;
+  }
+  piece.nnz = nnz;
+  out.push_back(piece);
+  CK(cudaEventRecord(ev[5], s));
+  CK(cudaStreamSynchronize(s));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); tm.cand += ms;
+  CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); tm.full += ms;
+  CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); tm.part += ms;
+  CK(cudaEventElapsedTime(&ms, ev[3], ev[4])); tm.sing += ms;
+  CK(cudaEventElapsedTime(&ms, ev[4], ev[5])); tm.merge += ms;
+  st->n_full += nF;
+  st->n_partial += nPt;
+  st->n_singular += nS[0] + nS[1] + nS[2];
+  st->coo_entries += coo;
+  st->n_batches += 1;
+  (void)ctr;
+  return NLG_OK;
+}
+
+nlg_status upload_table(const double* h, size_t n, double** d, cudaStream_t s) {
+  CK(cudaMallocAsync(d, sizeof(double) * std::max<size_t>(n, 1), s));
+  if (n) CK(cudaMemcpyAsync(*d, h, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  return NLG_OK;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int32_t nlg_abi_version(void) { return NLG_ABI_VERSION; }
+const char* nlg_last_error(void) { return g_err.c_str(); }
+int64_t nlg_launch_count(void) { return g_launches.load(); }
+
+nlg_status nlg_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    set_err("cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    return NLG_ERR_CUDA;
+  }
+  *count = n;
+  return NLG_OK;
+}
+
+nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, nlg_plan** out) {
+  *out = nullptr;
+  if (!pb) { set_err("null problem"); return NLG_ERR_CONFIG; }
+  if (pb->n_outer != 7 || pb->n_inner != 7) { set_err("only the 7-point triangle rule is supported"); return NLG_ERR_CONFIG; }
+  if (pb->kernel_id < 0 || pb->kernel_id > 3) { set_err("unknown kernel id %d", pb->kernel_id); return NLG_ERR_CONFIG; }
+  const int want_nc = pb->kernel_id == 1 ? 2 : 1;
+  if (pb->nc != want_nc) { set_err("kernel id %d needs nc=%d, got %d", pb->kernel_id, want_nc, pb->nc); return NLG_ERR_CONFIG; }
+  if ((pb->kernel_id == 3) == (pb->symmetric != 0)) { set_err("kernel id %d has the wrong symmetry flag", pb->kernel_id); return NLG_ERR_CONFIG; }
+  if (pb->ball_id < 0 || pb->ball_id > 2 || pb->path_touch < 0 || pb->path_touch > 2) { set_err("bad ball/path id"); return NLG_ERR_CONFIG; }
+  if (pb->n_elements < 0 || pb->n_vertices < 0 || pb->n_elements >= (1LL << 31) || pb->n_vertices >= (1LL << 31)) {
+    set_err("mesh size out of range"); return NLG_ERR_CONFIG;
+  }
+  if (pb->n_dofs <= 0 || pb->n_dofs >= (1LL << 31)) { set_err("dof count out of range"); return NLG_ERR_CONFIG; }
+  CK(cudaSetDevice(device));
+  nlg_plan* pl = new nlg_plan();
+  pl->device = device;
+  pl->stream = (cudaStream_t)stream;
+  cudaStream_t s = pl->stream;
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  Params& P = pl->P;
+  P.K = (int)pb->n_elements;
+  P.V = (int)pb->n_vertices;
+  P.nc = pb->nc;
+  P.kid = pb->kernel_id;
+  P.ball = pb->ball_id;
+  P.path = pb->path_touch;
+  P.sym = pb->symmetric;
+  P.is_dg = pb->is_dg;
+  P.s = pb->s;
+  P.kexp = -1.0 - pb->s;
+  P.cst = pb->scale;
+  P.delta = pb->delta;
+  P.prer = pb->ball_id == 2 ? pb->delta * sqrt(2.0) : pb->delta;  // _engine.py:445
+  P.rskip2 = pb->rskip2;
+  P.drop2 = pb->drop2;
+  P.kp0 = pb->kp0;
+  P.kp1 = pb->kp1;
+  P.J = pb->n_dofs;
+  Rule7 hr;
+  for (int p = 0; p < 7; ++p) {
+    hr.op[p][0] = pb->op[2 * p]; hr.op[p][1] = pb->op[2 * p + 1];
+    hr.ip[p][0] = pb->ip[2 * p]; hr.ip[p][1] = pb->ip[2 * p + 1];
+    hr.ow[p] = pb->ow[p]; hr.iw[p] = pb->iw[p];
+    for (int a = 0; a < 3; ++a) hr.oh[p][a] = pb->oh[3 * p + a];
+  }
+  // fast-path tables use the outer rule for both sides: they must agree
+  for (int p = 0; p < 7; ++p)
+    if (hr.op[p][0] != hr.ip[p][0] || hr.op[p][1] != hr.ip[p][1] || hr.ow[p] != hr.iw[p]) {
+      set_err("outer and inner rules differ");
+      delete pl;
+      return NLG_ERR_CONFIG;
+    }
+  for (int p = 0; p < 7; ++p)
+    for (int a = 0; a < 3; ++a) {
+      hr.wh[p][a] = hr.ow[p] * hr.oh[p][a];
+      for (int b = 0; b < 3; ++b) hr.whh[p][a * 3 + b] = hr.ow[p] * hr.oh[p][a] * hr.oh[p][b];
+    }
+  if (cudaMemcpyToSymbolAsync(c_rule, &hr, sizeof hr, 0, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    set_err("rule upload failed");
+    delete pl;
+    return NLG_ERR_CUDA;
+  }
+  const long long V = pb->n_vertices, K = pb->n_elements;
+  nlg_status rc = NLG_OK;
+  auto fail = [&](nlg_status r) { nlg_plan_destroy(pl); return r; };
+  if (cudaMallocAsync(&pl->vtx, sizeof(double2) * std::max(V, 1LL), s) ||
+      cudaMallocAsync(&pl->elem, sizeof(int4) * std::max(K, 1LL), s) ||
+      cudaMallocAsync(&pl->dofs, sizeof(int4) * std::max(K, 1LL), s) ||
+      cudaMallocAsync(&pl->ctr, sizeof(double2) * std::max(K, 1LL), s) ||
+      cudaMallocAsync(&pl->rad, sizeof(double) * std::max(K, 1LL), s)) {
+    set_err("device allocation failed");
+    return fail(NLG_ERR_CUDA);
+  }
+  {
+    // stage inputs on the device (copy when they are host arrays)
+    const double* dv = pb->vertices;
+    const long long *de = (const long long*)pb->elements, *dl = (const long long*)pb->labels,
+                    *dou = (const long long*)pb->outer_mask, *dd = (const long long*)pb->dof_map;
+    DevBuf sv, se, sl, so, sd;
+    if (!pb->inputs_on_device) {
+      if (sv.alloc(sizeof(double) * 2 * V, s) || se.alloc(sizeof(long long) * 3 * K, s) ||
+          sl.alloc(sizeof(long long) * K, s) || so.alloc(sizeof(long long) * K, s) ||
+          sd.alloc(sizeof(long long) * 3 * K, s)) {
+        set_err("device allocation failed");
+        return fail(NLG_ERR_CUDA);
+      }
+      if (V) cudaMemcpyAsync(sv.p, pb->vertices, sizeof(double) * 2 * V, cudaMemcpyHostToDevice, s);
+      if (K) {
+        cudaMemcpyAsync(se.p, pb->elements, sizeof(long long) * 3 * K, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(sl.p, pb->labels, sizeof(long long) * K, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(so.p, pb->outer_mask, sizeof(long long) * K, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(sd.p, pb->dof_map, sizeof(long long) * 3 * K, cudaMemcpyHostToDevice, s);
+      }
+      dv = sv.as<double>();
+      de = se.as<long long>();
+      dl = sl.as<long long>();
+      dou = so.as<long long>();
+      dd = sd.as<long long>();
+    }
+    const long long n = std::max(V, K);
+    if (n) {
+      k_convert<<<grid_for(n, 256), 256, 0, s>>>(dv, (const long long*)de, (const long long*)dl,
+                                                 (const long long*)dou, (const long long*)dd, (int)V, (int)K,
+                                                 pl->vtx, pl->elem, pl->dofs);
+      g_launches += 1;
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) { set_err("convert: %s", cudaGetErrorString(e)); return fail(NLG_ERR_CUDA); }
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { set_err("staging inputs: %s", cudaGetErrorString(e)); return fail(NLG_ERR_CUDA); }
+  }
+  for (int f = 0; f < 3; ++f) {
+    const size_t n = (size_t)pb->n_sing[f];
+    pl->sing_n[f] = pb->n_sing[f];
+    const double* src[5] = {pb->sxs[f], pb->sys[f], pb->sw[f], pb->shx[f], pb->shy[f]};
+    const size_t len[5] = {2 * n, 2 * n, n, 3 * n, 3 * n};
+    for (int t = 0; t < 5; ++t) {
+      if (n && !src[t]) { set_err("missing singular table"); return fail(NLG_ERR_CONFIG); }
+      rc = upload_table(src[t], n ? len[t] : 0, &pl->sing_tab[f][t], s);
+      if (rc) return fail(rc);
+    }
+  }
+  P.vtx = pl->vtx;
+  P.elem = pl->elem;
+  P.dofs = pl->dofs;
+  P.ctr = pl->ctr;
+  P.rad = pl->rad;
+  *out = pl;
+  return NLG_OK;
+}
+
+void nlg_plan_destroy(nlg_plan* pl) {
+  if (!pl) return;
+  cudaSetDevice(pl->device);
+  cudaStream_t s = pl->stream;
+  void* ptrs[] = {pl->vtx, pl->elem, pl->dofs, pl->ctr, pl->rad, pl->grid_start, pl->grid_items, pl->act};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, s);
+  for (auto& f : pl->sing_tab)
+    for (double* p : f)
+      if (p) cudaFreeAsync(p, s);
+  cudaStreamSynchronize(s);
+  delete pl;
+}
+
+nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t out_on_host,
+                        nlg_alloc_fn alloc, void* user, int64_t budget, nlg_stats* stats) {
+  if (!pl || !alloc) { set_err("null plan or allocator"); return NLG_ERR_CONFIG; }
+  if (row_lo < 0 || row_hi > pl->P.J || row_lo > row_hi) { set_err("row range out of bounds"); return NLG_ERR_CONFIG; }
+  CK(cudaSetDevice(pl->device));
+  cudaStream_t s = pl->stream;
+  nlg_stats st;
+  memset(&st, 0, sizeof st);
+  st.err_k = st.err_l = -1;
+  if (budget <= 0) {
+    size_t fr = 0, totm = 0;
+    CK(cudaMemGetInfo(&fr, &totm));
+    budget = (long long)(0.6 * (double)totm);
+  }
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  CK(cudaEventRecord(e0, s));
+  pl->prepped = false;  // bounds and grid are part of every assembly
+  nlg_status rc = prep(pl);
+  if (rc) return rc;
+  CK(cudaEventRecord(e1, s));
+  DevBuf dctr, derr;
+  CK(dctr.alloc(sizeof(unsigned long long) * K_NCOUNTERS, s));
+  CK(derr.alloc(sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(dctr.p, 0, sizeof(unsigned long long) * K_NCOUNTERS, s));
+  CK(cudaMemsetAsync(derr.p, 0xff, sizeof(unsigned long long), s));
+  std::vector<Csr> pieces;
+  Counters ctr{};
+  Timing tm;
+  // row batches: a work list of ranges, split in halves when over budget
+  std::vector<std::pair<long long, long long>> todo;
+  if (row_hi > row_lo) todo.push_back({row_lo, row_hi});
+  while (!todo.empty()) {
+    auto rg = todo.back();
+    todo.pop_back();
+    bool split = false;
+    rc = run_batch(pl, rg.first, rg.second, budget, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
+                   derr.as<unsigned long long>(), &split);
+    if (rc) break;
+    if (split) {
+      const long long mid = rg.first + (rg.second - rg.first) / 2;
+      todo.push_back({mid, rg.second});
+      todo.push_back({rg.first, mid});
+    }
+  }
+  if (rc) {
+    for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
+    return rc;
+  }
+  // pieces are produced in ascending row order (ranges are popped low-first)
+  long long nnz = 0;
+  for (auto& p : pieces) nnz += p.nnz;
+  const long long nrows = row_hi - row_lo;
+  long long* o_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
+  int* o_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
+  double* o_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
+  if (!o_ptr || !o_idx || !o_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  DevBuf ptrbuf;
+  CK(ptrbuf.alloc(sizeof(long long) * (nrows + 1), s));
+  long long run = 0;
+  for (auto& p : pieces) {
+    const long long nr = p.row_hi - p.row_lo;
+    if (run) {
+      k_add_offset<<<grid_for(nr + 1, 256), 256, 0, s>>>(p.indptr, nr + 1, run);
+      LAUNCHED();
+    }
+    CK(cudaMemcpyAsync(ptrbuf.as<long long>() + (p.row_lo - row_lo), p.indptr, sizeof(long long) * (nr + 1),
+                       cudaMemcpyDeviceToDevice, s));
+    if (p.nnz) {
+      CK(cudaMemcpyAsync(o_idx + run, p.indices, sizeof(int) * p.nnz, cudaMemcpyDefault, s));
+      CK(cudaMemcpyAsync(o_dat + run, p.data, sizeof(double) * p.nnz, cudaMemcpyDefault, s));
+    }
+    run += p.nnz;
+  }
+  if (nrows == 0) CK(cudaMemsetAsync(ptrbuf.p, 0, sizeof(long long), s));
+  CK(cudaMemcpyAsync(o_ptr, ptrbuf.p, sizeof(long long) * (nrows + 1), cudaMemcpyDefault, s));
+  CK(cudaEventRecord(e2, s));
+  unsigned long long hc[K_NCOUNTERS], herr;
+  CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&herr, derr.p, sizeof herr, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  st.ms_prep = ms;
+  CK(cudaEventElapsedTime(&ms, e0, e2));
+  st.ms_total = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  st.ms_candidates = tm.cand;
+  st.ms_full = tm.full;
+  st.ms_partial = tm.part;
+  st.ms_singular = tm.sing;
+  st.ms_merge = tm.merge;
+  st.ms_integrate_kernels = tm.full + tm.part + tm.sing;
+  st.nnz = nnz;
+  st.inner_evals = (long long)(hc[K_EVAL_M0] + hc[K_EVAL_M1] + hc[K_EVAL_M2]);
+  st.outer_nonempty = (long long)(hc[K_OUT_M0] + hc[K_OUT_M1] + hc[K_OUT_M2]);
+  st.sing_points = (long long)(hc[K_SPTS3] + hc[K_SPTS4] + hc[K_SPTS5] + hc[K_SPTS6]);
+  st.alg_flops = alg_flops(pl->P, hc);
+  if (herr != ~0ull) {
+    st.err_k = (long long)(herr / (unsigned long long)pl->P.K);
+    st.err_l = (long long)(herr % (unsigned long long)pl->P.K);
+  }
+  if (stats) *stats = st;
+  if (herr != ~0ull) {
+    set_err("nonfinite local contribution for element pair (%lld, %lld)", st.err_k, st.err_l);
+    return NLG_ERR_NUMERICAL;
+  }
+  return NLG_OK;
+}
+
+static nlg_status ensure_active(nlg_plan* pl) {
+  if (pl->nact >= 0) return NLG_OK;
+  cudaStream_t s = pl->stream;
+  const int K = pl->P.K;
+  DevBuf flag, idx, n;
+  CK(flag.alloc(sizeof(int) * K, s));
+  CK(idx.alloc(sizeof(int) * K, s));
+  CK(n.alloc(sizeof(int), s));
+  CK(cudaMallocAsync(&pl->act, sizeof(int) * std::max(K, 1), s));
+  k_active<<<grid_for(K, 256), 256, 0, s>>>(pl->P, flag.as<int>());
+  LAUNCHED();
+  k_iota<<<grid_for(K, 256), 256, 0, s>>>(idx.as<int>(), K);
+  LAUNCHED();
+  size_t tb = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, tb, idx.as<int>(), flag.as<int>(), pl->act, n.as<int>(), K, s));
+  DevBuf tmp;
+  CK(tmp.alloc(tb, s));
+  CK(cub::DeviceSelect::Flagged(tmp.p, tb, idx.as<int>(), flag.as<int>(), pl->act, n.as<int>(), K, s));
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, n.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  pl->nact = h;
+  pl->nbase = (int)(pl->P.J / pl->P.nc);
+  return NLG_OK;
+}
+
+nlg_status nlg_load_points(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc, void* user, int64_t* n_points) {
+  if (!pl || !alloc) { set_err("null plan or allocator"); return NLG_ERR_CONFIG; }
+  CK(cudaSetDevice(pl->device));
+  nlg_status rc = ensure_active(pl);
+  if (rc) return rc;
+  cudaStream_t s = pl->stream;
+  const long long np = (long long)pl->nact * 7;
+  *n_points = np;
+  double* out = (double*)alloc(user, sizeof(double) * 2 * std::max(np, 1LL), 4);
+  if (!out) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  DevBuf tmp;
+  double* dst = out;
+  if (out_on_host) {
+    CK(tmp.alloc(sizeof(double) * 2 * std::max(np, 1LL), s));
+    dst = tmp.as<double>();
+  }
+  if (np) {
+    k_load_points<<<grid_for(np, 256), 256, 0, s>>>(pl->P, pl->act, pl->nact, dst);
+    LAUNCHED();
+  }
+  if (out_on_host && np) CK(cudaMemcpyAsync(out, dst, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  (void)out_on_host;
+  return NLG_OK;
+}
+
+static nlg_status load_impl(nlg_plan* pl, const double* fx, int fx_on_device, int fconst, int32_t out_on_host,
+                            nlg_alloc_fn alloc, void* user) {
+  if (!pl || !alloc) { set_err("null plan or allocator"); return NLG_ERR_CONFIG; }
+  CK(cudaSetDevice(pl->device));
+  nlg_status rc = ensure_active(pl);
+  if (rc) return rc;
+  cudaStream_t s = pl->stream;
+  const int nact = pl->nact, nc = pl->P.nc;
+  const long long J = pl->P.J;
+  DevBuf dfx, contrib, key, item, key2, item2, start, bdev;
+  const long long nfx = fconst ? nc : (long long)nact * 7 * nc;
+  const double* dptr = fx;
+  if (!fx_on_device) {
+    CK(dfx.alloc(sizeof(double) * std::max(nfx, 1LL), s));
+    CK(cudaMemcpyAsync(dfx.p, fx, sizeof(double) * nfx, cudaMemcpyHostToDevice, s));
+    dptr = dfx.as<double>();
+  }
+  CK(contrib.alloc(sizeof(double) * std::max(3LL * nact * nc, 1LL), s));
+  if (nact) {
+    k_load_contrib<<<grid_for(nact, 128), 128, 0, s>>>(pl->P, pl->act, nact, dptr, fconst, contrib.as<double>());
+    LAUNCHED();
+  }
+  const long long ni = 3LL * nact;
+  CK(key.alloc(sizeof(unsigned) * std::max(ni, 1LL), s));
+  CK(item.alloc(sizeof(int) * std::max(ni, 1LL), s));
+  CK(key2.alloc(sizeof(unsigned) * std::max(ni, 1LL), s));
+  CK(item2.alloc(sizeof(int) * std::max(ni, 1LL), s));
+  CK(start.alloc(sizeof(int) * (pl->nbase + 1), s));
+  if (ni) {
+    k_load_inc<<<grid_for(ni, 256), 256, 0, s>>>(pl->P, pl->act, nact, key.as<unsigned>(), item.as<int>());
+    LAUNCHED();
+    int bits = 1;
+    while ((1ll << bits) <= pl->nbase) ++bits;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<unsigned>(), key2.as<unsigned>(), item.as<int>(),
+                                       item2.as<int>(), (int)ni, 0, bits, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.as<unsigned>(), key2.as<unsigned>(), item.as<int>(),
+                                       item2.as<int>(), (int)ni, 0, bits, s));
+    g_launches += 3;
+  }
+  k_cell_ranges<<<grid_for(pl->nbase + 1, 256), 256, 0, s>>>(key2.as<unsigned>(), (int)ni, pl->nbase,
+                                                             start.as<int>());
+  LAUNCHED();
+  double* out = (double*)alloc(user, sizeof(double) * std::max(J, 1LL), 3);
+  if (!out) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  double* dst = out;
+  if (out_on_host) {
+    CK(bdev.alloc(sizeof(double) * J, s));
+    dst = bdev.as<double>();
+  }
+  k_load_gather<<<grid_for(pl->nbase, 256), 256, 0, s>>>(start.as<int>(), item2.as<int>(), contrib.as<double>(),
+                                                         pl->nbase, nc, dst);
+  LAUNCHED();
+  if (out_on_host) CK(cudaMemcpyAsync(out, dst, sizeof(double) * J, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return NLG_OK;
+}
+
+nlg_status nlg_load(nlg_plan* pl, const double* fx, int32_t fx_on_device, int32_t out_on_host, nlg_alloc_fn alloc,
+                    void* user) {
+  return load_impl(pl, fx, fx_on_device, 0, out_on_host, alloc, user);
+}
+
+nlg_status nlg_load_const(nlg_plan* pl, const double* fconst, int32_t out_on_host, nlg_alloc_fn alloc, void* user) {
+  return load_impl(pl, fconst, 0, 1, out_on_host, alloc, user);
+}
+
+nlg_status nlg_fp64_peak(int32_t device, double* tflops) {
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* d;
+  CK(cudaMalloc(&d, 8));
+  const int bs = 512, grid = sms * 4, iters = 2048;
+  k_dfma_peak<<<grid, bs>>>(d, 8, 0.999999, 1e-7);
+  LAUNCHED();
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    CK(cudaEventRecord(a));
+    k_dfma_peak<<<grid, bs>>>(d, iters, 0.999999, 1e-7);
+    LAUNCHED();
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d);
+  *tflops = 2.0 * 8 * 16 * (double)iters * grid * bs / (best * 1e-3) / 1e12;
+  return NLG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+// nlg_eval.cuh -- per element-pair integrals on the device (FP64, CUDA cores).
+//
+// One ordered visit (k, l) of root k produces the reference's B block of
+// _engine._visit_pair (:374-425): rows on k's local hats, column half 0 on
+// k's hats ("kk") and half 1 on l's hats ("kl"), from an outer-on-k sweep
+// (mode 0) and an outer-on-l sweep (mode 1); an identical pair runs mode 2
+// (_engine._sweep :46-185, _pyengine._sweep :48-152 for P != Q).
+//
+// Two device paths compute it:
+//  * full pairs (dist + r_k + r_l <= delta, no truncation): the reference
+//    integrates the same 7x7 point pairs (x_p on k, y_q on l) in both
+//    sweeps, so one 7x7 matrix of kernel values gives the whole block:
+//        kk[a,b] = 2 c sum_p w_p H_pa H_pb sum_q w_q P_pq
+//        kl[a,b] = -2 c sum_{p,q} w_p w_q Q_pq H_pa H_qb,   c = 2A_k 2A_l
+//    (P = kernel(x_p, y_q), Q = kernel(y_q, x_p)); half the kernel
+//    evaluations of the reference and ~1/8 of its flops;
+//  * clipped pairs: the reference's two truncated sweeps, with the clip /
+//    fan / drop predicates in exact reference arithmetic (nlg_geom.cuh)
+//    and FMA-contracted accumulation.
+#pragma once
+#include <cstdint>
+
+#include "nlg_geom.cuh"
+
+namespace nlg {
+
+struct Rule7 {
+  double op[7][2], ow[7], oh[7][3], ip[7][2], iw[7];
+  double wh[7][3];   // w_p * H_pa
+  double whh[7][9];  // w_p * H_pa * H_pb
+};
+
+struct Params {
+  // mesh (device)
+  const double2* __restrict__ vtx;
+  const int4* __restrict__ elem;  // x, y, z vertex ids; w = label | outer << 4
+  const int4* __restrict__ dofs;  // x, y, z scalar dof bases
+  const double2* __restrict__ ctr;
+  const double* __restrict__ rad;
+  int K, V;
+  int nc, kid, ball, path, sym, is_dg;
+  double s, kexp, cst, delta, prer, rskip2, drop2, kp0, kp1;
+  long long J, row_lo, row_hi;
+};
+
+// the 7-point rule and its weighted hat products (identical for every plan:
+// QuadratureConfig only accepts "7point", quadrature.py:20)
+__constant__ Rule7 c_rule;
+
+template <int KID> struct KTraits {
+  static constexpr int NC = KID == 1 ? 2 : 1;
+  static constexpr bool SYM = KID != 3;
+  static constexpr int NC2 = NC * NC;
+  static constexpr int E = 9 * NC2;  // entries of one 3nc x 3nc block
+};
+
+// kernel matrix at offset d = x - y (r2 = |d|^2): _engine._kernel_mat :30-43;
+// id 3 returns P = value(x, y) and Q = value(y, x) (_pyengine._pq :38-45).
+template <int KID>
+__device__ __forceinline__ void kval(const Params& P, double x0, double y0, double d0, double d1,
+                                     double r2, double* p, double* q) {
+  if constexpr (KID == 0) {
+    p[0] = P.cst * pow(r2, P.kexp);
+  } else if constexpr (KID == 1) {
+    const double f = P.cst / (r2 * sqrt(r2));
+    const double v01 = f * d0 * d1;
+    p[0] = f * d0 * d0;
+    p[1] = v01;
+    p[2] = v01;
+    p[3] = f * d1 * d1;
+  } else if constexpr (KID == 2) {
+    p[0] = P.cst;
+  } else {
+    p[0] = (1.0 + P.kp0 * x0) * P.kp1;
+    q[0] = (1.0 + P.kp0 * y0) * P.kp1;
+  }
+}
+
+__device__ __forceinline__ void load_tri(const Params& P, int e, double* tx, double* ty) {
+  const int4 el = __ldg(&P.elem[e]);
+  const double2 a = __ldg(&P.vtx[el.x]), b = __ldg(&P.vtx[el.y]), c = __ldg(&P.vtx[el.z]);
+  tx[0] = a.x; ty[0] = a.y;
+  tx[1] = b.x; ty[1] = b.y;
+  tx[2] = c.x; ty[2] = c.y;
+}
+
+// twice the signed area, reference order (_engine.py:58)
+__device__ __forceinline__ double twice_area(const double* tx, const double* ty) {
+  return cross2(tx[1] - tx[0], ty[2] - ty[0], ty[1] - ty[0], tx[2] - tx[0]);
+}
+
+// physical 7-point positions on a triangle in the reference's order
+// (_engine.py:68-69): T0 + (T1 - T0) * xi0 + (T2 - T0) * xi1, unfused.
+__device__ __forceinline__ void rule_points(const Params& P, const double* tx, const double* ty,
+                                            double* px, double* py) {
+  const double e1x = tx[1] - tx[0], e2x = tx[2] - tx[0];
+  const double e1y = ty[1] - ty[0], e2y = ty[2] - ty[0];
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    px[p] = __dadd_rn(__dadd_rn(tx[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+    py[p] = __dadd_rn(__dadd_rn(ty[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+  }
+}
+
+// ---------------------------------------------------------------------
+// full (untruncated) non-identical pair: kk and kl blocks in one 7x7 pass
+// ---------------------------------------------------------------------
+template <int KID>
+__device__ __forceinline__ void full_pair(const Params& P, const double* kx, const double* ky,
+                                          const double* lx, const double* ly, double rs2,
+                                          double* kk, double* kl, long long& n_eval) {
+  using T = KTraits<KID>;
+  constexpr int NC2 = T::NC2;
+  double xk[7], yk[7], xl[7], yl[7];
+  rule_points(P, kx, ky, xk, yk);
+  rule_points(P, lx, ly, xl, yl);
+  const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+#pragma unroll
+  for (int e = 0; e < 9 * NC2; ++e) { kk[e] = 0.0; kl[e] = 0.0; }
+#pragma unroll 1
+  for (int p = 0; p < 7; ++p) {
+    double rp[NC2], g[3][NC2];
+#pragma unroll
+    for (int i = 0; i < NC2; ++i) { rp[i] = 0.0; g[0][i] = g[1][i] = g[2][i] = 0.0; }
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const double d0 = xk[p] - xl[q], d1 = yk[p] - yl[q];
+      const double r2 = sumsq(d0, d1);
+      if (rs2 > 0.0 && r2 < rs2) continue;
+      double pv[NC2], qv[NC2];
+      kval<KID>(P, xk[p], xl[q], d0, d1, r2, pv, qv);
+      ++n_eval;
+      const double wq = c_rule.iw[q];
+#pragma unroll
+      for (int i = 0; i < NC2; ++i) {
+        rp[i] = fma(wq, pv[i], rp[i]);
+        const double qq = T::SYM ? pv[i] : qv[i];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) g[b][i] = fma(c_rule.wh[q][b], qq, g[b][i]);
+      }
+    }
+    // fold: kk[(a,c),(b,d)] += w H_a H_b r[c,d];  kl[(a,c),(b,d)] += w H_a g_b[c,d]
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < T::NC; ++c)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int d = 0; d < T::NC; ++d) {
+            const int e = ((a * T::NC + c) * 3 + b) * T::NC + d;
+            kk[e] = fma(c_rule.whh[p][a * 3 + b], rp[c * T::NC + d], kk[e]);
+            kl[e] = fma(c_rule.wh[p][a], g[b][c * T::NC + d], kl[e]);
+          }
+  }
+#pragma unroll
+  for (int e = 0; e < 9 * NC2; ++e) { kk[e] *= c2; kl[e] *= -c2; }
+}
+
+// full identical pair (k == l, mode 2): both column halves land on k's dofs;
+// returned as the two halves so the presence test matches the reference's
+// per-triplet `v != 0` (_engine.py:403-424).
+template <int KID>
+__device__ __forceinline__ void full_identical(const Params& P, const double* kx, const double* ky,
+                                               double rs2, double* h0, double* h1, long long& n_eval) {
+  using T = KTraits<KID>;
+  constexpr int NC = T::NC, NC2 = T::NC2;
+  double xk[7], yk[7];
+  rule_points(P, kx, ky, xk, yk);
+  const double ta = twice_area(kx, ky);
+  const double c = ta * ta;
+  double colq[7][NC2];
+#pragma unroll
+  for (int e = 0; e < 9 * NC2; ++e) { h0[e] = 0.0; h1[e] = 0.0; }
+  for (int q = 0; q < 7; ++q)
+    for (int i = 0; i < NC2; ++i) colq[q][i] = 0.0;
+  for (int p = 0; p < 7; ++p) {
+    double rp[NC2], gq[3][NC2], gp[3][NC2];
+    for (int i = 0; i < NC2; ++i) { rp[i] = 0.0; for (int b = 0; b < 3; ++b) gq[b][i] = gp[b][i] = 0.0; }
+    for (int q = 0; q < 7; ++q) {
+      const double d0 = xk[p] - xk[q], d1 = yk[p] - yk[q];
+      const double r2 = sumsq(d0, d1);
+      if (rs2 > 0.0 && r2 < rs2) continue;
+      double pv[NC2], qv[NC2];
+      kval<KID>(P, xk[p], xk[q], d0, d1, r2, pv, qv);
+      ++n_eval;
+      for (int i = 0; i < NC2; ++i) {
+        const double qq = T::SYM ? pv[i] : qv[i];
+        rp[i] += c_rule.iw[q] * pv[i];
+        colq[q][i] += c_rule.ow[p] * qq;
+        for (int b = 0; b < 3; ++b) {
+          gq[b][i] += c_rule.wh[q][b] * qq;
+          gp[b][i] += c_rule.wh[q][b] * pv[i];
+        }
+      }
+    }
+    for (int a = 0; a < 3; ++a)
+      for (int cc = 0; cc < NC; ++cc)
+        for (int b = 0; b < 3; ++b)
+          for (int d = 0; d < NC; ++d) {
+            const int e = ((a * NC + cc) * 3 + b) * NC + d;
+            const int i = cc * NC + d;
+            h0[e] += c_rule.whh[p][a * 3 + b] * rp[i];
+            h1[e] -= c_rule.wh[p][a] * gq[b][i] + c_rule.wh[p][b] * gp[a][i];
+          }
+  }
+  for (int q = 0; q < 7; ++q)
+    for (int a = 0; a < 3; ++a)
+      for (int cc = 0; cc < NC; ++cc)
+        for (int b = 0; b < 3; ++b)
+          for (int d = 0; d < NC; ++d) {
+            const int e = ((a * NC + cc) * 3 + b) * NC + d;
+            h0[e] += c_rule.whh[q][a * 3 + b] * colq[q][cc * NC + d];
+          }
+  for (int e = 0; e < 9 * NC2; ++e) { h0[e] *= c; h1[e] *= c; }
+}
+
+// ---------------------------------------------------------------------
+// truncated sweep (_engine._sweep :46-185 / _pyengine._sweep :48-152)
+//   MODE 0: outer = root k (to*), inner = l (ti*): kk += W oh_a oh_b S0,
+//           kl -= W oh_a SyQ_b
+//   MODE 1: outer = l, inner = root k: kl -= W oh_b SyP_a, kk += W Syy_ab
+//   MODE 2: identical pair: h0 = kk-half, h1 = second half
+// Returns true if any outer point saw a nonempty truncated region.
+// ---------------------------------------------------------------------
+template <int KID, int MODE>
+__device__ __forceinline__ bool sweep(const Params& P, const double* tox, const double* toy,
+                                      const double* tix, const double* tiy, double rs2, double* kk,
+                                      double* kl, long long& n_eval, long long& n_outer) {
+  using T = KTraits<KID>;
+  constexpr int NC = T::NC, NC2 = T::NC2;
+  const double twoA = twice_area(tox, toy);
+  const double o0 = tix[0], o1 = tiy[0];
+  const double e1x = tix[1] - o0, e1y = tiy[1] - o1, e2x = tix[2] - o0, e2y = tiy[2] - o1;
+  const double idet = 1.0 / cross2(e1x, e2y, e1y, e2x);
+  double px[7], py[7];
+  rule_points(P, tox, toy, px, py);
+  bool nonzero = false;
+#pragma unroll 1
+  for (int p = 0; p < 7; ++p) {
+    const double x0 = px[p], x1 = py[p];
+    Poly poly;
+    truncate_inner(tix, tiy, x0, x1, P.delta, P.ball, poly);
+    const int nv = poly.n;
+    if (nv < 3) continue;
+    nonzero = true;
+    ++n_outer;
+    const double W = c_rule.ow[p] * twoA;
+    double S0[NC2], SyP[3][NC2], SyQ[3][NC2], Syy[3][3][NC2];
+#pragma unroll
+    for (int i = 0; i < NC2; ++i) {
+      S0[i] = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        SyP[a][i] = SyQ[a][i] = 0.0;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) Syy[a][b][i] = 0.0;
+      }
+    }
+#pragma unroll 1
+    for (int t = 1; t < nv - 1; ++t) {
+      const double q0x = poly.x[0], q0y = poly.y[0];
+      const double ax = poly.x[t] - q0x, ay = poly.y[t] - q0y;
+      const double bx = poly.x[t + 1] - q0x, by = poly.y[t + 1] - q0y;
+      const double jac2 = cross2(ax, by, ay, bx);
+      if (jac2 <= P.drop2) continue;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        double y0, y1, d0, d1, r2;
+        if (rs2 > 0.0) {  // the diagonal-skip predicate needs the reference's rounding
+          y0 = __dadd_rn(__dadd_rn(q0x, mul(ax, c_rule.ip[q][0])), mul(bx, c_rule.ip[q][1]));
+          y1 = __dadd_rn(__dadd_rn(q0y, mul(ay, c_rule.ip[q][0])), mul(by, c_rule.ip[q][1]));
+          d0 = x0 - y0;
+          d1 = x1 - y1;
+          r2 = sumsq(d0, d1);
+          if (r2 < rs2) continue;
+        } else {
+          y0 = fma(bx, c_rule.ip[q][1], fma(ax, c_rule.ip[q][0], q0x));
+          y1 = fma(by, c_rule.ip[q][1], fma(ay, c_rule.ip[q][0], q0y));
+          d0 = x0 - y0;
+          d1 = x1 - y1;
+          r2 = fma(d0, d0, d1 * d1);
+        }
+        double pv[NC2], qv[NC2];
+        kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
+        ++n_eval;
+        const double wq = c_rule.iw[q] * jac2;
+        const double u0 = y0 - o0, u1 = y1 - o1;
+        const double xi1 = (u0 * e2y - u1 * e2x) * idet;
+        const double xi2 = (e1x * u1 - e1y * u0) * idet;
+        const double h[3] = {1.0 - xi1 - xi2, xi1, xi2};
+#pragma unroll
+        for (int i = 0; i < NC2; ++i) {
+          const double tp = wq * pv[i];
+          const double tq = T::SYM ? tp : wq * qv[i];
+          if (MODE != 1) S0[i] += tp;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (MODE != 1) SyQ[a][i] = fma(tq, h[a], SyQ[a][i]);
+            if (MODE != 0) {
+              SyP[a][i] = fma(tp, h[a], SyP[a][i]);
+#pragma unroll
+              for (int b = 0; b < 3; ++b) Syy[a][b][i] = fma(tq, h[a] * h[b], Syy[a][b][i]);
+            }
+          }
+        }
+      }
+    }
+    const double* oh = c_rule.oh[p];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int d = 0; d < NC; ++d) {
+            const int e = ((a * NC + c) * 3 + b) * NC + d;
+            const int i = c * NC + d;
+            if (MODE == 0) {
+              kk[e] += (W * (oh[a] * oh[b])) * S0[i];
+              kl[e] -= (W * oh[a]) * SyQ[b][i];
+            } else if (MODE == 1) {
+              kl[e] -= (W * oh[b]) * SyP[a][i];
+              kk[e] += W * Syy[a][b][i];
+            } else {
+              kk[e] += (W * (oh[a] * oh[b])) * S0[i] + W * Syy[a][b][i];
+              kl[e] -= (W * oh[a]) * SyQ[b][i] + (W * oh[b]) * SyP[a][i];
+            }
+          }
+  }
+  return nonzero;
+}
+
+}  // namespace nlg

@@ -1,0 +1,73 @@
+"""Load tests/golden/*.npz fixtures (made by make_golden.py from the
+reference) into this package's host types."""
+
+import glob
+import json
+import os
+
+import numpy as np
+from scipy import sparse
+
+from paper_2207_03921_b200 import kernels as KR
+from paper_2207_03921_b200.assembly import build_ansatz
+from paper_2207_03921_b200.mesh import Mesh, build_adjacency_graph
+from paper_2207_03921_b200.quadrature import QuadratureConfig
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+FUNCS = {
+    "one": lambda x: np.ones(x.shape[0]),
+    "x": lambda x: x[:, 0] * x[:, 1] + 1.0,
+    "body": lambda x: np.column_stack([np.zeros(x.shape[0]), -np.ones(x.shape[0])]),
+}
+
+
+def names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def kernel_from_spec(k):
+    kid, ball, delta = k["id"], k["ball"], k["delta"]
+    if kid == 0:
+        return KR.fractional_kernel(k["s"], delta, ball)
+    if kid == 1:
+        return KR.peridynamic_kernel(delta, ball)
+    if kid == 2:
+        return KR.constant_kernel(delta, ball, scale=k["scale"])
+    return KR.affine_kernel(delta, k["alpha"], k["scale"], ball)
+
+
+class Case:
+    def __init__(self, name):
+        z = np.load(os.path.join(GOLDEN, name + ".npz"))
+        self.name = name
+        self.spec = json.loads(str(z["spec"]))
+        self.mesh = Mesh(z["vertices"], z["elements"], z["labels"])
+        self.adjacency = build_adjacency_graph(self.mesh)
+        self.kernel = kernel_from_spec(self.spec["kernel"])
+        self.ansatz = build_ansatz(self.mesh, self.spec["ansatz"], self.spec["n"])
+        self.quad = QuadratureConfig(**self.spec["quad"])
+        self.rows = self.spec["rows"]
+        self.f = FUNCS[self.spec["f"]]
+        J = self.ansatz.dof_count
+        self.matrix = sparse.csr_matrix((z["data"], z["indices"], z["indptr"]), shape=(J, J))
+        self.b = z["b"]
+        self.free_mask = z["free_mask"]
+
+    def args(self):
+        return (self.mesh, self.adjacency, self.kernel, self.ansatz, self.quad)
+
+
+def rel_fro(a, b):
+    """||A - B||_F / ||B||_F over the union pattern."""
+    d = (a - b).tocsr()
+    nb = np.linalg.norm(b.data) if b.nnz else 1.0
+    return np.linalg.norm(d.data) / (nb if nb else 1.0)
+
+
+def same_pattern(a, b):
+    a = a.tocsr()
+    b = b.tocsr()
+    a.sort_indices()
+    b.sort_indices()
+    return np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
