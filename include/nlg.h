@@ -88,7 +88,8 @@ typedef struct nlg_stats {
   int64_t inner_evals;  /* inner-point kernel evaluations on the clipped path */
   int64_t outer_nonempty; /* outer points with a nonempty truncated region (clipped path) */
   int64_t sing_points;  /* singular-rule points evaluated */
-  int64_t alg_flops;    /* reference-algorithmic FP64 flops */
+  int64_t alg_flops;    /* reference-algorithmic FP64 flops, all phases */
+  int64_t alg_flops_full, alg_flops_partial, alg_flops_singular; /* per integration kernel */
   int64_t coo_entries;  /* COO slots sorted */
   int64_t nnz;
   int64_t n_batches;

@@ -867,24 +867,29 @@ struct Counters {
   unsigned long long c[K_NCOUNTERS];
 };
 
-// algorithmic FP64 flops of the reference for the counted work
-long long alg_flops(const Params& P, const unsigned long long* c) {
+// algorithmic FP64 flops of the reference for the counted work;
+// part: 0 full-pair kernel, 1 clipped-pair kernel, 2 singular kernel
+long long alg_flops(const Params& P, const unsigned long long* c, int part) {
   const long long nc = P.nc, nc2 = nc * nc;
   const bool ns = !P.sym;
   const long long kf = P.kid == 0 ? 2 : P.kid == 1 ? 9 : P.kid == 3 ? 4 : 0;
   const long long a0 = ns ? 9 * nc2 : 8 * nc2, a1 = ns ? 35 * nc2 : 34 * nc2, a2 = 35 * nc2;
   const long long f0 = 9 * nc * (3 + 4 * nc) + 9, f1 = 9 * nc * (1 + 4 * nc) + 9, f2 = 9 * nc * (4 + 8 * nc) + 9;
   long long fl = 0;
-  // full pairs: K_EVAL_FULL0 counts the 7x7 point pairs once; the reference
-  // evaluates each in mode 0 and again in mode 1
-  fl += (long long)c[K_EVAL_FULL0] * ((26 + kf + a0) + (26 + kf + a1));
-  fl += (long long)c[K_OUT_FULL0] / 2 * (f0 + f1);
-  fl += (long long)c[K_EVAL_FULL2] * (26 + kf + a2) + (long long)c[K_OUT_FULL2] * f2;
-  fl += (long long)c[K_EVAL_M0] * (26 + kf + a0) + (long long)c[K_OUT_M0] * f0;
-  fl += (long long)c[K_EVAL_M1] * (26 + kf + a1) + (long long)c[K_OUT_M1] * f1;
-  fl += (long long)c[K_EVAL_M2] * (26 + kf + a2) + (long long)c[K_OUT_M2] * f2;
-  for (int u = 3; u <= 6; ++u)
-    fl += (long long)c[K_SPTS3 + u - 3] * (16 + 5 + kf + u + u * u * (2 + 2 * nc2));
+  if (part == 0) {
+    // K_EVAL_FULL0 counts each 7x7 point pair once; the reference evaluates
+    // it in mode 0 and again in mode 1
+    fl += (long long)c[K_EVAL_FULL0] * ((26 + kf + a0) + (26 + kf + a1));
+    fl += (long long)c[K_OUT_FULL0] / 2 * (f0 + f1);
+    fl += (long long)c[K_EVAL_FULL2] * (26 + kf + a2) + (long long)c[K_OUT_FULL2] * f2;
+  } else if (part == 1) {
+    fl += (long long)c[K_EVAL_M0] * (26 + kf + a0) + (long long)c[K_OUT_M0] * f0;
+    fl += (long long)c[K_EVAL_M1] * (26 + kf + a1) + (long long)c[K_OUT_M1] * f1;
+    fl += (long long)c[K_EVAL_M2] * (26 + kf + a2) + (long long)c[K_OUT_M2] * f2;
+  } else {
+    for (int u = 3; u <= 6; ++u)
+      fl += (long long)c[K_SPTS3 + u - 3] * (16 + 5 + kf + u + u * u * (2 + 2 * nc2));
+  }
   return fl;
 }
 
@@ -1506,7 +1511,10 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   st.inner_evals = (long long)(hc[K_EVAL_M0] + hc[K_EVAL_M1] + hc[K_EVAL_M2]);
   st.outer_nonempty = (long long)(hc[K_OUT_M0] + hc[K_OUT_M1] + hc[K_OUT_M2]);
   st.sing_points = (long long)(hc[K_SPTS3] + hc[K_SPTS4] + hc[K_SPTS5] + hc[K_SPTS6]);
-  st.alg_flops = alg_flops(pl->P, hc);
+  st.alg_flops_full = alg_flops(pl->P, hc, 0);
+  st.alg_flops_partial = alg_flops(pl->P, hc, 1);
+  st.alg_flops_singular = alg_flops(pl->P, hc, 2);
+  st.alg_flops = st.alg_flops_full + st.alg_flops_partial + st.alg_flops_singular;
   if (herr != ~0ull) {
     st.err_k = (long long)(herr / (unsigned long long)pl->P.K);
     st.err_l = (long long)(herr % (unsigned long long)pl->P.K);
