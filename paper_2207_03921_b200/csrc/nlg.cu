@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict
     double kk[E], kl[E];
     unsigned long long flags = 0;
     if (k == l) {
-      if (FULL) {
+      if constexpr (FULL) {
         full_identical<KID>(P, kx, ky, rs2, kk, kl, ev2);
         out2 += 7;
       } else {
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict
       }
     } else {
       load_tri(P, l, lx, ly);
-      if (FULL) {
+      if constexpr (FULL) {
         full_pair<KID>(P, kx, ky, lx, ly, rs2, kk, kl, ev0);
         out0 += 14;
       } else {
@@ -421,6 +421,314 @@ __global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict
     warp_add_ll(e_m1, &O.counters[K_EVAL_M2]);
     warp_add_ll(o_m1, &O.counters[K_OUT_M2]);
   }
+}
+
+// ---------------------------------------------------------------------
+// clipped (truncated) visits, warp-cooperative.
+// A warp takes VPC visits at a time; lane = item (visit slot, sweep m, outer
+// point p), m = 0: outer k / inner l, m = 1: outer l / inner k, m = 2:
+// identical pair (mode 2).  Phase 1 clips in parallel (exact reference
+// predicates) and stores the fan in shared memory; phase 2 spreads the
+// flattened (sub-triangle, inner point) units evenly over the 32 lanes and
+// folds each unit straight into the lane's partial B block; phase 3 sums the
+// partial blocks with a reduce-scatter (lane i ends with value i) and emits.
+// The unit -> lane mapping and the reduction tree are fixed, so results are
+// run-to-run deterministic.
+// ---------------------------------------------------------------------
+template <int KID> struct ClipCfg {
+  static constexpr int NC = KTraits<KID>::NC;
+  static constexpr int NC2 = NC * NC;
+  static constexpr int VPC = NC == 1 ? 2 : 1;           // visits per warp chunk
+  static constexpr int NKK = 3 * NC * (3 * NC + 1) / 2;  // symmetric root block, unique
+  static constexpr int NKL = 9 * NC * NC;
+  static constexpr int NV = VPC * (NKK + NKL);
+  static constexpr int NP = NV <= 32 ? 32 : 64;          // padded for the reduce-scatter
+  static constexpr int PER_LANE = NP / 32;
+  static constexpr int QCAP = 32 * 7;                    // <= 7 kept sub-triangles per item
+};
+
+struct ClipWarp {
+  double px[32][kMaxPoly], py[32][kMaxPoly];
+  double sx[32][kMaxPoly], sy[32][kMaxPoly];  // clip scratch
+  double xo[32][2];
+  double W[32];
+  double tri[2][2][8];  // [visit slot][side]: o.x o.y e1x e1y e2x e2y idet
+  double rs2[2];
+  unsigned short queue[32 * 7];  // (item << 4) | t of every kept sub-triangle, item-major
+  unsigned char pm[32];
+};
+
+// (I, J) of the u-th unique entry of a symmetric n x n block, I <= J
+__device__ __forceinline__ void sym_ij(int u, int n, int& I, int& J) {
+  I = 0;
+  while (u >= n - I) { u -= n - I; ++I; }
+  J = I + u;
+}
+
+// sums of one sub-triangle: S0 = sum tp, SyP_a = sum tp h_a, SyQ_a = sum tq h_a,
+// Syy_ab = sum tq h_a h_b (a <= b), tp = wq P, tq = wq Q (_engine.py:113-153)
+template <int KID> struct SubSums {
+  static constexpr int NC2 = KTraits<KID>::NC2;
+  static constexpr bool SYM = KTraits<KID>::SYM;
+  double S0[NC2], SyP[3][NC2], SyQ[SYM ? 1 : 3][NC2], Syy[6][NC2];
+  __device__ __forceinline__ const double* syq(int a) const { return SYM ? SyP[a] : SyQ[SYM ? 0 : a]; }
+};
+
+__device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 00 01 02 11 12 22
+  const int i = a < b ? a : b, j = a < b ? b : a;
+  return i == 0 ? j : (i == 1 ? 2 + j : 5);
+}
+
+template <int KID>
+__global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
+  using T = KTraits<KID>;
+  using C = ClipCfg<KID>;
+  constexpr int NC = T::NC, NC2 = T::NC2, N3 = 3 * NC;
+  __shared__ ClipWarp smw[4];
+  ClipWarp& S = smw[threadIdx.x >> 5];
+  const int lane = lane_id();
+  const long long nchunks = (O.nlist + C::VPC - 1) / C::VPC;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  long long n_eval[3] = {0, 0, 0}, n_out[3] = {0, 0, 0};
+  for (long long ch = w0; ch < nchunks; ch += nw) {
+    // ---------------- phase 1: clip one item (visit slot, sweep, outer point) per lane
+    const int vs = lane >> 4, r = lane & 15;
+    const long long v = ch * C::VPC + vs;
+    bool valid = vs < C::VPC && r < 14 && v < O.nlist;
+    int k = 0, l = 0, m = r >= 7 ? 1 : 0;
+    const int p = r % 7;
+    if (valid) {
+      const int2 pr = list[v];
+      k = pr.x;
+      l = pr.y;
+      if (k == l) {
+        if (m == 1) valid = false;
+        m = 2;
+      }
+    }
+    unsigned mask = 0;
+    if (valid) {
+      double ox[3], oy[3], ix[3], iy[3];
+      load_tri(P, m == 1 ? l : k, ox, oy);
+      load_tri(P, m == 1 ? k : l, ix, iy);
+      const double e1x = ox[1] - ox[0], e2x = ox[2] - ox[0], e1y = oy[1] - oy[0], e2y = oy[2] - oy[0];
+      const double x0 = __dadd_rn(__dadd_rn(ox[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+      const double x1 = __dadd_rn(__dadd_rn(oy[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+      double* qx = S.px[lane];
+      double* qy = S.py[lane];
+      const int nv = truncate_inner(ix, iy, x0, x1, P.delta, P.ball, S.sx[lane], S.sy[lane], qx, qy);
+      if (nv >= 3) {
+        ++n_out[m];
+#pragma unroll 1
+        for (int t = 1; t < nv - 1; ++t) {
+          const double ax = qx[t] - qx[0], ay = qy[t] - qy[0];
+          const double bx = qx[t + 1] - qx[0], by = qy[t + 1] - qy[0];
+          if (cross2(ax, by, ay, bx) > P.drop2) mask |= 1u << t;
+        }
+      }
+      S.xo[lane][0] = x0;
+      S.xo[lane][1] = x1;
+      S.W[lane] = c_rule.ow[p] * twice_area(ox, oy);
+      if (p == 0) {  // the visit's inner triangle of this side, for the hat functions
+        double* tr = S.tri[vs][m == 1];
+        tr[0] = ix[0]; tr[1] = iy[0];
+        tr[2] = ix[1] - ix[0]; tr[3] = iy[1] - iy[0];
+        tr[4] = ix[2] - ix[0]; tr[5] = iy[2] - iy[0];
+        tr[6] = 1.0 / cross2(tr[2], tr[5], tr[3], tr[4]);
+        if (m != 1) {
+          const int4 ek = __ldg(&P.elem[k]), el = __ldg(&P.elem[l]);
+          const bool touching = k == l || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
+                                ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
+          S.rs2[vs] = (touching && P.path == 1) ? P.rskip2 : 0.0;
+        }
+      }
+    }
+    S.pm[lane] = (unsigned char)(p | (m << 4));
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    {
+      int pos = incl - cnt;
+      for (unsigned mm = mask; mm; mm &= mm - 1) S.queue[pos++] = (unsigned short)((lane << 4) | (__ffs(mm) - 1));
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    // ---------------- phase 2: one kept sub-triangle per lane, its 7 inner points
+    double acc[C::VPC][C::NKK + C::NKL];
+#pragma unroll
+    for (int a = 0; a < C::VPC; ++a)
+#pragma unroll
+      for (int i = 0; i < C::NKK + C::NKL; ++i) acc[a][i] = 0.0;
+    for (int u = lane; u < total; u += 32) {
+      const int ent = S.queue[u];
+      const int j = ent >> 4, t = ent & 15;
+      const int pmj = S.pm[j], pj = pmj & 15, mj = pmj >> 4, vsj = j >> 4;
+      const double q0x = S.px[j][0], q0y = S.py[j][0];
+      const double ax = S.px[j][t] - q0x, ay = S.py[j][t] - q0y;
+      const double bx = S.px[j][t + 1] - q0x, by = S.py[j][t + 1] - q0y;
+      const double jac2 = cross2(ax, by, ay, bx);
+      const double x0 = S.xo[j][0], x1 = S.xo[j][1];
+      const double rs2 = S.rs2[vsj];
+      const double* tr = S.tri[vsj][mj == 1];
+      const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
+      // barycentric coordinates of the inner triangle are affine along the
+      // sub-triangle: xi(q) = xi(q0) + ip0 dxi(a) + ip1 dxi(b)
+      const double u0 = q0x - o0, u1 = q0y - o1;
+      const double z1 = (u0 * e2y - u1 * e2x) * idet, z2 = (e1x * u1 - e1y * u0) * idet;
+      const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
+      const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
+      SubSums<KID> ss;
+#pragma unroll
+      for (int i = 0; i < NC2; ++i) {
+        ss.S0[i] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { ss.SyP[a][i] = 0.0; if (!T::SYM) ss.SyQ[T::SYM ? 0 : a][i] = 0.0; }
+#pragma unroll
+        for (int a = 0; a < 6; ++a) ss.Syy[a][i] = 0.0;
+      }
+      int ne = 0;
+#pragma unroll 1
+      for (int q = 0; q < 7; ++q) {
+        const double i0 = c_rule.ip[q][0], i1 = c_rule.ip[q][1];
+        const double y0 = fma(bx, i1, fma(ax, i0, q0x));
+        const double y1 = fma(by, i1, fma(ay, i0, q0y));
+        double d0 = x0 - y0, d1 = x1 - y1;
+        double r2 = fma(d0, d0, d1 * d1);
+        if (rs2 > 0.0) {  // the diagonal-skip predicate needs the reference's rounding
+          const double ey0 = __dadd_rn(__dadd_rn(q0x, mul(ax, i0)), mul(bx, i1));
+          const double ey1 = __dadd_rn(__dadd_rn(q0y, mul(ay, i0)), mul(by, i1));
+          if (sumsq(x0 - ey0, x1 - ey1) < rs2) continue;
+        }
+        double pv[NC2], qv[NC2];
+        kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
+        ++ne;
+        const double wq = c_rule.iw[q] * jac2;
+        const double xi1 = fma(i1, z1b, fma(i0, z1a, z1));
+        const double xi2 = fma(i1, z2b, fma(i0, z2a, z2));
+        const double h[3] = {1.0 - xi1 - xi2, xi1, xi2};
+#pragma unroll
+        for (int i = 0; i < NC2; ++i) {
+          const double tp = wq * pv[i];
+          const double tq = T::SYM ? tp : wq * qv[i];
+          ss.S0[i] += tp;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            ss.SyP[a][i] = fma(tp, h[a], ss.SyP[a][i]);
+            if (!T::SYM) ss.SyQ[T::SYM ? 0 : a][i] = fma(tq, h[a], ss.SyQ[T::SYM ? 0 : a][i]);
+            const double g = tq * h[a];
+#pragma unroll
+            for (int b = a; b < 3; ++b) ss.Syy[sym3(a, b)][i] = fma(g, h[b], ss.Syy[sym3(a, b)][i]);
+          }
+        }
+      }
+      n_eval[mj] += ne;
+      // fold the sub-triangle into its visit's partial block (_engine.py:154-184)
+      const double W = S.W[j];
+      const double* oh = c_rule.oh[pj];
+      double ckk[C::NKK], ckl[C::NKL];
+      {
+        int uu = 0;
+#pragma unroll
+        for (int I = 0; I < N3; ++I)
+#pragma unroll
+          for (int J = I; J < N3; ++J) {
+            const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
+            double vkk = 0.0;
+            if (mj != 1) vkk += (W * (oh[a] * oh[b])) * ss.S0[cd];
+            if (mj != 0) vkk += W * ss.Syy[sym3(a, b)][cd];
+            ckk[uu++] = vkk;
+          }
+#pragma unroll
+        for (int I = 0; I < N3; ++I)
+#pragma unroll
+          for (int J = 0; J < N3; ++J) {
+            const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
+            double vkl = 0.0;
+            if (mj != 1) vkl += (W * oh[a]) * ss.syq(b)[cd];
+            if (mj != 0) vkl += (W * oh[b]) * ss.SyP[a][cd];
+            ckl[I * N3 + J] = -vkl;
+          }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < C::VPC; ++s2)
+        if (vsj == s2) {
+#pragma unroll
+          for (int i = 0; i < C::NKK; ++i) acc[s2][i] += ckk[i];
+#pragma unroll
+          for (int i = 0; i < C::NKL; ++i) acc[s2][C::NKK + i] += ckl[i];
+        }
+    }
+    // ---------------- phase 3: reduce-scatter, lane L ends with values [L*PER_LANE, ...)
+    double vals[C::NP];
+#pragma unroll
+    for (int i = 0; i < C::NP; ++i) vals[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < C::VPC; ++a)
+#pragma unroll
+      for (int i = 0; i < C::NKK + C::NKL; ++i) vals[a * (C::NKK + C::NKL) + i] = acc[a][i];
+#pragma unroll
+    for (int off = 16, half = C::NP / 2; off >= 1; off >>= 1, half >>= 1) {
+      const bool upper = lane & off;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double send = upper ? vals[i] : vals[i + half];
+        const double keep = upper ? vals[i + half] : vals[i];
+        vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    unsigned long long fl[C::VPC];
+#pragma unroll
+    for (int a = 0; a < C::VPC; ++a) fl[a] = 0;
+#pragma unroll
+    for (int h2 = 0; h2 < C::PER_LANE; ++h2) {
+      const int gi = lane * C::PER_LANE + h2;
+      const int vsl = gi / (C::NKK + C::NKL), wi = gi % (C::NKK + C::NKL);
+      const long long vv = ch * C::VPC + vsl;
+      if (vsl >= C::VPC || vv >= O.nlist) continue;
+      const double val = vals[h2];
+      const int2 pr = list[vv];
+      note_nonfinite(val, pr.x, pr.y, P.K, O.errpair);
+      const long long vi = O.vofs + vv;
+      if (wi < C::NKK) {
+        int I, J;
+        sym_ij(wi, N3, I, J);
+        O.kkv[(long long)(I * N3 + J) * O.nvis + vi] = val;
+        O.kkv[(long long)(J * N3 + I) * O.nvis + vi] = val;
+        if (val != 0.0) {
+#pragma unroll
+          for (int a = 0; a < C::VPC; ++a)
+            if (a == vsl) fl[a] |= (1ull << (I * N3 + J)) | (1ull << (J * N3 + I));
+        }
+      } else {
+        const int e = wi - C::NKK, I = e / N3, J = e % N3;
+        const int4 dk = __ldg(&P.dofs[pr.x]), dl = __ldg(&P.dofs[pr.y]);
+        const int dka[3] = {dk.x, dk.y, dk.z}, dla[3] = {dl.x, dl.y, dl.z};
+        const long long slot = O.cbase + (long long)e * O.nlist + vv;
+        O.keys[slot] = coo_key(P, (long long)NC * dka[I / NC] + I % NC, (long long)NC * dla[J / NC] + J % NC);
+        O.vals[slot] = emit_val(val);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < C::VPC; ++a) {
+      unsigned long long f = fl[a];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+      const long long vv = ch * C::VPC + a;
+      if (lane == 0 && vv < O.nlist) O.kkf[O.vofs + vv] = f;
+    }
+    __syncwarp();
+  }
+  warp_add_ll(n_eval[0], &O.counters[K_EVAL_M0]);
+  warp_add_ll(n_out[0], &O.counters[K_OUT_M0]);
+  warp_add_ll(n_eval[1], &O.counters[K_EVAL_M1]);
+  warp_add_ll(n_out[1], &O.counters[K_OUT_M1]);
+  warp_add_ll(n_eval[2], &O.counters[K_EVAL_M2]);
+  warp_add_ll(n_out[2], &O.counters[K_OUT_M2]);
 }
 
 // per-root sum of the root's own block over all its visits, fixed order
@@ -907,7 +1215,9 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long n
   O.cbase += 9LL * KTraits<KID>::NC2 * nF;
   O.nlist = nP;
   if (nP) {
-    k_visits<KID, false><<<grid_for(nP, 128), 128, 0, pl->stream>>>(P, lp, O);
+    const long long chunks = (nP + ClipCfg<KID>::VPC - 1) / ClipCfg<KID>::VPC;
+    const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
+    k_clipped<KID><<<g, 128, 0, pl->stream>>>(P, lp, O);
     LAUNCHED();
   }
   return NLG_OK;

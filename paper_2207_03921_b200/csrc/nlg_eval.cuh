@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "nlg_geom.cuh"
+#include "nlg_math.cuh"
 
 namespace nlg {
 
@@ -60,7 +61,7 @@ template <int KID>
 __device__ __forceinline__ void kval(const Params& P, double x0, double y0, double d0, double d1,
                                      double r2, double* p, double* q) {
   if constexpr (KID == 0) {
-    p[0] = P.cst * pow(r2, P.kexp);
+    p[0] = P.cst * fast_pow_pos(r2, P.kexp);
   } else if constexpr (KID == 1) {
     const double f = P.cst / (r2 * sqrt(r2));
     const double v01 = f * d0 * d1;
