@@ -25,6 +25,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       note_nonfinite(kk[e], k, l, P.K, O.errpair);
-      O.kkv[(long long)e * O.nvis + vi] = kk[e];
+      O.kkv[vi * E + e] = kk[e];
     }
     O.kkf[vi] = flags;
     const int4 dk = __ldg(&P.dofs[k]);
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict
 #pragma unroll
           for (int d = 0; d < NC; ++d) {
             const int e = ((a * NC + c) * 3 + b) * NC + d;
-            const long long slot = O.cbase + (long long)e * O.nlist + v;
+            const long long slot = O.cbase + v * E + e;
             if (k == l) {
               O.keys[slot] = kSentinel;
               O.vals[slot] = 0.0;
@@ -456,6 +457,7 @@ struct ClipWarp {
   double rs2[2];
   unsigned short queue[32 * 7];  // (item << 4) | t of every kept sub-triangle, item-major
   unsigned char pm[32];
+  int vk[2], vl[2], dk[2][3], dl[2][3];  // per visit slot: elements and their dof bases
 };
 
 // (I, J) of the u-th unique entry of a symmetric n x n block, I <= J
@@ -490,36 +492,70 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
   const long long nchunks = (O.nlist + C::VPC - 1) / C::VPC;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  long long n_eval[3] = {0, 0, 0}, n_out[3] = {0, 0, 0};
+  long long n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;
+  // software pipeline: the next chunk's visit pair and element records are
+  // fetched while the current chunk computes
+  const int vs = lane >> 4, r = lane & 15;
+  int2 pr = make_int2(0, 0);
+  int4 ek = make_int4(0, 0, 0, 0), el = ek;
+  {
+    const long long v0 = w0 * C::VPC + vs;
+    if (vs < C::VPC && v0 < O.nlist) {
+      pr = list[v0];
+      ek = __ldg(&P.elem[pr.x]);
+      el = __ldg(&P.elem[pr.y]);
+    }
+  }
   for (long long ch = w0; ch < nchunks; ch += nw) {
     // ---------------- phase 1: clip one item (visit slot, sweep, outer point) per lane
-    const int vs = lane >> 4, r = lane & 15;
     const long long v = ch * C::VPC + vs;
     bool valid = vs < C::VPC && r < 14 && v < O.nlist;
-    int k = 0, l = 0, m = r >= 7 ? 1 : 0;
+    const int k = pr.x, l = pr.y;
+    int m = r >= 7 ? 1 : 0;
     const int p = r % 7;
-    if (valid) {
-      const int2 pr = list[v];
-      k = pr.x;
-      l = pr.y;
-      if (k == l) {
-        if (m == 1) valid = false;
-        m = 2;
-      }
+    if (valid && k == l) {
+      if (m == 1) valid = false;
+      m = 2;
+    }
+    const long long vn = (ch + nw) * C::VPC + vs;
+    const bool next_ok = vs < C::VPC && vn < O.nlist;
+    int2 prn = make_int2(0, 0);
+    if (next_ok) prn = list[vn];
+    if (r == 0 && vs < C::VPC && v < O.nlist) {
+      const int4 dk4 = __ldg(&P.dofs[k]), dl4 = __ldg(&P.dofs[l]);
+      S.vk[vs] = k;
+      S.vl[vs] = l;
+      S.dk[vs][0] = dk4.x; S.dk[vs][1] = dk4.y; S.dk[vs][2] = dk4.z;
+      S.dl[vs][0] = dl4.x; S.dl[vs][1] = dl4.y; S.dl[vs][2] = dl4.z;
     }
     unsigned mask = 0;
     if (valid) {
       double ox[3], oy[3], ix[3], iy[3];
-      load_tri(P, m == 1 ? l : k, ox, oy);
-      load_tri(P, m == 1 ? k : l, ix, iy);
+      {
+        const int4 eo = m == 1 ? el : ek, ei = m == 1 ? ek : el;
+        const double2 a0 = __ldg(&P.vtx[eo.x]), a1 = __ldg(&P.vtx[eo.y]), a2 = __ldg(&P.vtx[eo.z]);
+        const double2 b0 = __ldg(&P.vtx[ei.x]), b1 = __ldg(&P.vtx[ei.y]), b2 = __ldg(&P.vtx[ei.z]);
+        ox[0] = a0.x; oy[0] = a0.y; ox[1] = a1.x; oy[1] = a1.y; ox[2] = a2.x; oy[2] = a2.y;
+        ix[0] = b0.x; iy[0] = b0.y; ix[1] = b1.x; iy[1] = b1.y; ix[2] = b2.x; iy[2] = b2.y;
+      }
       const double e1x = ox[1] - ox[0], e2x = ox[2] - ox[0], e1y = oy[1] - oy[0], e2y = oy[2] - oy[0];
       const double x0 = __dadd_rn(__dadd_rn(ox[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
       const double x1 = __dadd_rn(__dadd_rn(oy[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
       double* qx = S.px[lane];
       double* qy = S.py[lane];
-      const int nv = truncate_inner(ix, iy, x0, x1, P.delta, P.ball, S.sx[lane], S.sy[lane], qx, qy);
+      // exact early-out: the inner triangle lies in disk(c, r); if that disk is
+      // farther than the (widened) ball by a margin no rounding can bridge,
+      // the reference's clip finds no vertex inside and no root in (0, 1)
+      const int inner_el = m == 1 ? k : l;
+      const double2 ci = __ldg(&P.ctr[inner_el]);
+      const double reach = P.delta * (1.0 + 1e-6) + __ldg(&P.rad[inner_el]);
+      const double dcx = ci.x - x0, dcy = ci.y - x1;
+      const bool far = (P.dbg & 2) || (P.ball != 2 && dcx * dcx + dcy * dcy > reach * reach);
+      const int nv = far ? 0 : truncate_inner(ix, iy, x0, x1, P.delta, P.ball, S.sx[lane], S.sy[lane], qx, qy);
       if (nv >= 3) {
-        ++n_out[m];
+        n_out0 += m == 0;
+        n_out1 += m == 1;
+        n_out2 += m == 2;
 #pragma unroll 1
         for (int t = 1; t < nv - 1; ++t) {
           const double ax = qx[t] - qx[0], ay = qy[t] - qy[0];
@@ -537,7 +573,6 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         tr[4] = ix[2] - ix[0]; tr[5] = iy[2] - iy[0];
         tr[6] = 1.0 / cross2(tr[2], tr[5], tr[3], tr[4]);
         if (m != 1) {
-          const int4 ek = __ldg(&P.elem[k]), el = __ldg(&P.elem[l]);
           const bool touching = k == l || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
                                 ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
           S.rs2[vs] = (touching && P.path == 1) ? P.rskip2 : 0.0;
@@ -564,7 +599,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     for (int a = 0; a < C::VPC; ++a)
 #pragma unroll
       for (int i = 0; i < C::NKK + C::NKL; ++i) acc[a][i] = 0.0;
-    for (int u = lane; u < total; u += 32) {
+    for (int u = lane; u < ((P.dbg & 1) ? 0 : total); u += 32) {
       const int ent = S.queue[u];
       const int j = ent >> 4, t = ent & 15;
       const int pmj = S.pm[j], pj = pmj & 15, mj = pmj >> 4, vsj = j >> 4;
@@ -626,7 +661,9 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
           }
         }
       }
-      n_eval[mj] += ne;
+      n_eval0 += mj == 0 ? ne : 0;
+      n_eval1 += mj == 1 ? ne : 0;
+      n_eval2 += mj == 2 ? ne : 0;
       // fold the sub-triangle into its visit's partial block (_engine.py:154-184)
       const double W = S.W[j];
       const double* oh = c_rule.oh[pj];
@@ -663,6 +700,11 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
           for (int i = 0; i < C::NKL; ++i) acc[s2][C::NKK + i] += ckl[i];
         }
     }
+    if (next_ok) {
+      ek = __ldg(&P.elem[prn.x]);
+      el = __ldg(&P.elem[prn.y]);
+    }
+    pr = prn;
     // ---------------- phase 3: reduce-scatter, lane L ends with values [L*PER_LANE, ...)
     double vals[C::NP];
 #pragma unroll
@@ -691,14 +733,13 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       const long long vv = ch * C::VPC + vsl;
       if (vsl >= C::VPC || vv >= O.nlist) continue;
       const double val = vals[h2];
-      const int2 pr = list[vv];
-      note_nonfinite(val, pr.x, pr.y, P.K, O.errpair);
+      note_nonfinite(val, S.vk[vsl], S.vl[vsl], P.K, O.errpair);
       const long long vi = O.vofs + vv;
       if (wi < C::NKK) {
         int I, J;
         sym_ij(wi, N3, I, J);
-        O.kkv[(long long)(I * N3 + J) * O.nvis + vi] = val;
-        O.kkv[(long long)(J * N3 + I) * O.nvis + vi] = val;
+        O.kkv[vi * (9 * NC2) + I * N3 + J] = val;
+        O.kkv[vi * (9 * NC2) + J * N3 + I] = val;
         if (val != 0.0) {
 #pragma unroll
           for (int a = 0; a < C::VPC; ++a)
@@ -706,10 +747,8 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         }
       } else {
         const int e = wi - C::NKK, I = e / N3, J = e % N3;
-        const int4 dk = __ldg(&P.dofs[pr.x]), dl = __ldg(&P.dofs[pr.y]);
-        const int dka[3] = {dk.x, dk.y, dk.z}, dla[3] = {dl.x, dl.y, dl.z};
-        const long long slot = O.cbase + (long long)e * O.nlist + vv;
-        O.keys[slot] = coo_key(P, (long long)NC * dka[I / NC] + I % NC, (long long)NC * dla[J / NC] + J % NC);
+        const long long slot = O.cbase + vv * C::NKL + e;
+        O.keys[slot] = coo_key(P, (long long)NC * S.dk[vsl][I / NC] + I % NC, (long long)NC * S.dl[vsl][J / NC] + J % NC);
         O.vals[slot] = emit_val(val);
       }
     }
@@ -723,15 +762,16 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     }
     __syncwarp();
   }
-  warp_add_ll(n_eval[0], &O.counters[K_EVAL_M0]);
-  warp_add_ll(n_out[0], &O.counters[K_OUT_M0]);
-  warp_add_ll(n_eval[1], &O.counters[K_EVAL_M1]);
-  warp_add_ll(n_out[1], &O.counters[K_OUT_M1]);
-  warp_add_ll(n_eval[2], &O.counters[K_EVAL_M2]);
-  warp_add_ll(n_out[2], &O.counters[K_OUT_M2]);
+  warp_add_ll(n_eval0, &O.counters[K_EVAL_M0]);
+  warp_add_ll(n_out0, &O.counters[K_OUT_M0]);
+  warp_add_ll(n_eval1, &O.counters[K_EVAL_M1]);
+  warp_add_ll(n_out1, &O.counters[K_OUT_M1]);
+  warp_add_ll(n_eval2, &O.counters[K_EVAL_M2]);
+  warp_add_ll(n_out2, &O.counters[K_OUT_M2]);
 }
 
 // per-root sum of the root's own block over all its visits, fixed order
+// (kkv is visit-major: [visit][E])
 template <int E>
 __global__ void k_kk_reduce(Params P, const int* __restrict__ roots, int nR,
                             const int* __restrict__ cnt, const long long* __restrict__ off,
@@ -741,32 +781,37 @@ __global__ void k_kk_reduce(Params P, const int* __restrict__ roots, int nR,
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
-  const int NC = E == 36 ? 2 : 1;
+  constexpr int NC = E == 36 ? 2 : 1;
   for (int i = warp; i < nR; i += nwarps) {
     const int k = roots[i];
     const bool emit = cnt[(long long)C_KK * nR + i] != 0;
     const long long f0 = off[0 * (long long)(nR + 1) + i], fn = cnt[(long long)C_FULL * nR + i];
     const long long p0 = nF + off[1 * (long long)(nR + 1) + i], pn = cnt[(long long)C_PART * nR + i];
     unsigned long long fl = 0;
-    for (long long j = lane; j < fn; j += 32) fl |= kkf[f0 + j];
-    for (long long j = lane; j < pn; j += 32) fl |= kkf[p0 + j];
+    double s[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) s[e] = 0.0;
+    for (long long j = lane; j < fn + pn; j += 32) {
+      const long long vi = j < fn ? f0 + j : p0 + (j - fn);
+      fl |= kkf[vi];
+#pragma unroll
+      for (int e = 0; e < E; ++e) s[e] += kkv[vi * E + e];
+    }
     for (int o = 16; o; o >>= 1) fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      for (int o = 16; o; o >>= 1) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
     const int4 dk = P.dofs[k];
     const int dka[3] = {dk.x, dk.y, dk.z};
+#pragma unroll
     for (int e = 0; e < E; ++e) {
-      double s = 0.0;
-      for (long long j = lane; j < fn; j += 32) s += kkv[(long long)e * nvis + f0 + j];
-      for (long long j = lane; j < pn; j += 32) s += kkv[(long long)e * nvis + p0 + j];
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) {
-        const int rr = e / (3 * NC), cc = e % (3 * NC);
-        const int a = rr / NC, c = rr % NC, b = cc / NC, d = cc % NC;
-        const long long slot = cbase + (long long)e * nR + i;
-        const bool present = emit && ((fl >> e) & 1ull);
-        keys[slot] = present ? coo_key(P, (long long)NC * dka[a] + c, (long long)NC * dka[b] + d)
-                             : kSentinel;
-        vals[slot] = present ? (s != 0.0 ? s : -0.0) : 0.0;
-      }
+      if (lane != e % 32) continue;
+      const int rr = e / (3 * NC), cc = e % (3 * NC);
+      const int a = rr / NC, c = rr % NC, b = cc / NC, d = cc % NC;
+      const long long slot = cbase + (long long)i * E + e;
+      const bool present = emit && ((fl >> e) & 1ull);
+      keys[slot] = present ? coo_key(P, (long long)NC * dka[a] + c, (long long)NC * dka[b] + d) : kSentinel;
+      vals[slot] = present ? (s[e] != 0.0 ? s[e] : -0.0) : 0.0;
     }
   }
 }
@@ -1612,6 +1657,7 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   P.kp0 = pb->kp0;
   P.kp1 = pb->kp1;
   P.J = pb->n_dofs;
+  P.dbg = getenv("NLG_DEBUG") ? atoi(getenv("NLG_DEBUG")) : 0;
   Rule7 hr;
   for (int p = 0; p < 7; ++p) {
     hr.op[p][0] = pb->op[2 * p]; hr.op[p][1] = pb->op[2 * p + 1];

@@ -31,6 +31,18 @@ __device__ __forceinline__ double cross2(double a, double b, double c, double d)
   return __dsub_rn(__dmul_rn(a, b), __dmul_rn(c, d));
 }
 
+// A triangle passed by value so it stays in registers across the
+// (non-inlined) clip calls; vertex i is selected without local memory.
+struct Tri {
+  double x0, x1, x2, y0, y1, y2;
+  __device__ __forceinline__ double x(int i) const { return i == 0 ? x0 : (i == 1 ? x1 : x2); }
+  __device__ __forceinline__ double y(int i) const { return i == 0 ? y0 : (i == 1 ? y1 : y2); }
+};
+
+__device__ __forceinline__ Tri make_tri(const double* tx, const double* ty) {
+  return Tri{tx[0], tx[1], tx[2], ty[0], ty[1], ty[2]};
+}
+
 // append (px, py) unless it repeats the previous row within dtol
 __device__ __forceinline__ void push_dedup(double* ox, double* oy, unsigned& flags, int& n, double px,
                                            double py, bool crossing, double dtol, bool first_ok) {
@@ -42,30 +54,32 @@ __device__ __forceinline__ void push_dedup(double* ox, double* oy, unsigned& fla
   }
 }
 
-// clip_circle: vertices of the convex CCW triangle (tx, ty) inside the
-// closed disk around (cx, cy) plus edge/circle crossings; bit i of *flags
-// marks row i as a crossing.  Returns the row count (< 3: empty/degenerate).
-__device__ __noinline__ int clip_circle(const double* tx, const double* ty, double cx, double cy,
-                                        double delta, double* ox, double* oy, unsigned* flags_out) {
+// clip_circle: vertices of the convex CCW triangle T inside the closed disk
+// around (cx, cy) plus edge/circle crossings; bit i of *flags_out marks row i
+// as a crossing.  Returns the row count (< 3: empty/degenerate).
+__device__ __noinline__ int clip_circle(Tri T, double cx, double cy, double delta, double* ox, double* oy,
+                                        unsigned* flags_out) {
   const double rad = mul(delta, 1.0 + kBallTieRel);
   const double r2 = mul(rad, rad);
   const double dtol = mul(kDedupRel, delta);
-  double q[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) q[i] = __dsub_rn(sumsq(tx[i] - cx, ty[i] - cy), r2);
+  const double q0 = __dsub_rn(sumsq(T.x0 - cx, T.y0 - cy), r2);
+  const double q1 = __dsub_rn(sumsq(T.x1 - cx, T.y1 - cy), r2);
+  const double q2 = __dsub_rn(sumsq(T.x2 - cx, T.y2 - cy), r2);
   int n = 0;
   unsigned flags = 0;
-  if (q[0] <= 0.0 && q[1] <= 0.0 && q[2] <= 0.0) {
-    // every edge runs inside: the loop below would only append the vertices
-#pragma unroll 1
-    for (int i = 0; i < 3; ++i) push_dedup(ox, oy, flags, n, tx[i], ty[i], false, dtol, true);
+  if (q0 <= 0.0 && q1 <= 0.0 && q2 <= 0.0) {
+    // every edge runs inside: the general loop would only append the vertices
+    push_dedup(ox, oy, flags, n, T.x0, T.y0, false, dtol, true);
+    push_dedup(ox, oy, flags, n, T.x1, T.y1, false, dtol, true);
+    push_dedup(ox, oy, flags, n, T.x2, T.y2, false, dtol, true);
   } else {
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
       const int j = i == 2 ? 0 : i + 1;
-      const double ax = tx[i], ay = ty[i], bx = tx[j], by = ty[j];
+      const double ax = T.x(i), ay = T.y(i), bx = T.x(j), by = T.y(j);
+      const double qa = i == 0 ? q0 : (i == 1 ? q1 : q2);
+      const double qb = j == 0 ? q0 : (j == 1 ? q1 : q2);
       const double dax = ax - cx, day = ay - cy;
-      const double qa = q[i], qb = q[j];
       if (qa <= 0.0) push_dedup(ox, oy, flags, n, ax, ay, false, dtol, true);
       const double ex = bx - ax, ey = by - ay;
       const double aa = sumsq(ex, ey);
@@ -101,26 +115,23 @@ __device__ __noinline__ int clip_circle(const double* tx, const double* ty, doub
 
 // insert_caps: copy the clip rows to (px, py), adding the arc midpoint behind
 // every chord between consecutive crossings when it lies inside the triangle.
-__device__ __noinline__ int insert_caps(const double* tx, const double* ty, const double* bx, const double* by,
-                                        unsigned bflag, int nb, double cx, double cy, double delta, double* px,
-                                        double* py) {
+__device__ __noinline__ int insert_caps(Tri T, const double* bx, const double* by, unsigned bflag, int nb,
+                                        double cx, double cy, double delta, double* px, double* py) {
   if (nb < 2) {
     for (int i = 0; i < nb; ++i) { px[i] = bx[i]; py[i] = by[i]; }
     return nb;
   }
   const double rad = mul(delta, 1.0 + kBallTieRel);
-  // crossing followed by crossing (cyclically): only then can a cap exist
-  const unsigned next = ((bflag >> 1) | ((bflag & 1u) << (nb - 1)));
-  const bool any_cap = (bflag & next) != 0;
-  double el[3];
-  double href = 0.0;
-  if (any_cap) {
-#pragma unroll 1
-    for (int i = 0; i < 3; ++i) {
-      const int j = i == 2 ? 0 : i + 1;
-      el[i] = sqrt(sumsq(tx[j] - tx[i], ty[j] - ty[i]));
-      if (el[i] > href) href = el[i];
-    }
+  // a cap needs a crossing followed (cyclically) by a crossing
+  const unsigned next = (bflag >> 1) | ((bflag & 1u) << (nb - 1));
+  double el0 = 0.0, el1 = 0.0, el2 = 0.0, href = 0.0;
+  if (bflag & next) {
+    el0 = sqrt(sumsq(T.x1 - T.x0, T.y1 - T.y0));
+    el1 = sqrt(sumsq(T.x2 - T.x1, T.y2 - T.y1));
+    el2 = sqrt(sumsq(T.x0 - T.x2, T.y0 - T.y2));
+    href = el0;
+    if (el1 > href) href = el1;
+    if (el2 > href) href = el2;
   }
   int n = 0;
 #pragma unroll 1
@@ -139,14 +150,11 @@ __device__ __noinline__ int insert_caps(const double* tx, const double* ty, cons
     if (nd < mul(1e-14, delta)) continue;
     const double capx = __dadd_rn(cx, mul(rad, mx) / nd);
     const double capy = __dadd_rn(cy, mul(rad, my) / nd);
-    bool inside = true;
-#pragma unroll 1
-    for (int e = 0; e < 3; ++e) {
-      const int f = e == 2 ? 0 : e + 1;
-      const double ex = tx[f] - tx[e], ey = ty[f] - ty[e];
-      const double cr = cross2(ex, capy - ty[e], ey, capx - tx[e]);
-      if (cr < mul(mul(-kCapMemberRel, href), el[e])) { inside = false; break; }
-    }
+    const double tol = mul(-kCapMemberRel, href);
+    // membership against the three edges, in order, stopping at the first miss
+    bool inside = cross2(T.x1 - T.x0, capy - T.y0, T.y1 - T.y0, capx - T.x0) >= mul(tol, el0);
+    if (inside) inside = cross2(T.x2 - T.x1, capy - T.y1, T.y2 - T.y1, capx - T.x1) >= mul(tol, el1);
+    if (inside) inside = cross2(T.x0 - T.x2, capy - T.y2, T.y0 - T.y2, capx - T.x2) >= mul(tol, el2);
     if (inside) { px[n] = capx; py[n] = capy; ++n; }
   }
   return n;
@@ -154,10 +162,11 @@ __device__ __noinline__ int insert_caps(const double* tx, const double* ty, cons
 
 // clip_square: Sutherland-Hodgman against the box of half width delta;
 // (bx, by) is scratch of kMaxPoly rows, the result lands in (px, py).
-__device__ __noinline__ int clip_square(const double* tx, const double* ty, double cx, double cy, double delta,
-                                        double* bx, double* by, double* px, double* py) {
+__device__ __noinline__ int clip_square(Tri T, double cx, double cy, double delta, double* bx, double* by,
+                                        double* px, double* py) {
   int n = 3;
-  for (int i = 0; i < 3; ++i) { bx[i] = tx[i]; by[i] = ty[i]; }
+  bx[0] = T.x0; bx[1] = T.x1; bx[2] = T.x2;
+  by[0] = T.y0; by[1] = T.y1; by[2] = T.y2;
 #pragma unroll 1
   for (int plane = 0; plane < 4; ++plane) {
     const bool axis1 = plane >= 2;
@@ -194,20 +203,22 @@ __device__ __noinline__ int clip_square(const double* tx, const double* ty, doub
   return nn < 3 ? 0 : nn;
 }
 
-// The truncated inner region of triangle (tx, ty) seen from outer point
-// (cx, cy), _engine._sweep :70-91 (ball 0 = nocaps, 1 = approxcaps, 2 = inf).
+// The truncated inner region of triangle T seen from outer point (cx, cy),
+// _engine._sweep :70-91 (ball 0 = nocaps, 1 = approxcaps, 2 = inf).
 // (sx, sy) is scratch of kMaxPoly rows; the polygon lands in (px, py).
+__device__ __forceinline__ int truncate_inner(Tri T, double cx, double cy, double delta, int ball, double* sx,
+                                              double* sy, double* px, double* py) {
+  if (ball == 2) return clip_square(T, cx, cy, delta, sx, sy, px, py);
+  unsigned f;
+  if (ball == 0) return clip_circle(T, cx, cy, delta, px, py, &f);
+  const int nb = clip_circle(T, cx, cy, delta, sx, sy, &f);
+  return insert_caps(T, sx, sy, f, nb, cx, cy, delta, px, py);
+}
+
 __device__ __forceinline__ int truncate_inner(const double* tx, const double* ty, double cx, double cy,
                                               double delta, int ball, double* sx, double* sy, double* px,
                                               double* py) {
-  if (ball == 2) return clip_square(tx, ty, cx, cy, delta, sx, sy, px, py);
-  if (ball == 0) {
-    unsigned f;
-    return clip_circle(tx, ty, cx, cy, delta, px, py, &f);
-  }
-  unsigned f;
-  const int nb = clip_circle(tx, ty, cx, cy, delta, sx, sy, &f);
-  return insert_caps(tx, ty, sx, sy, f, nb, cx, cy, delta, px, py);
+  return truncate_inner(make_tri(tx, ty), cx, cy, delta, ball, sx, sy, px, py);
 }
 
 // Small local polygon (for the thread-per-visit paths).
