@@ -207,13 +207,27 @@ __global__ void k_mark_roots(Params P, const unsigned char* needA, const unsigne
 }
 
 // ---------------------------------------------------------------- candidates
-// category of the ordered pair (k, l) as root k sees it:
-//  -1 rejected / not emitted here, 0 full, 1 clipped, 2/3/4 singular id/edge/vertex.
-// *visited is set when the reference would count the visit (EPI).
+// Each unordered non-singular pair {k, l} is integrated ONCE: the two
+// directed halves (outer k / inner l clipped, and the reverse) serve both the
+// reference's visit (k, l) of root k and its visit (l, k) of root l.  A pair
+// record is (k, l | emitA << 30 | emitB << 31): side A = visit (k, l) (rows of
+// k), side B = visit (l, k) (rows of l).  The record is produced by the
+// smaller root of the batch when both visits exist with the same category
+// ("shared"); otherwise root k produces a solo record (side A only).  The
+// reject/full predicates are evaluated in each visit's own operand order
+// ((dist - r_root) - r_nb, _engine.py:224, :227) so rounding ties never
+// differ from the reference.
+constexpr int kEmitA = 1 << 30;
+constexpr int kEmitB = (int)(1u << 31);
+constexpr int kIdMask = (1 << 30) - 1;
+
+//  -1 none here, 0 full record, 1 clipped record, 2/3/4 singular id/edge/vertex.
+// *visited: the reference would count the visit (k, l) (EPI); *flags: record sides.
 __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2 ck, double rk,
-                                        bool needAk, const unsigned char* __restrict__ needA, int l,
-                                        bool& visited) {
+                                        bool needAk, const unsigned char* __restrict__ needA,
+                                        const int* __restrict__ inR, int l, bool& visited, int& flags) {
   visited = false;
+  flags = 0;
   const int4 el = __ldg(&P.elem[l]);
   const int ns = (ek.x == el.x) + (ek.x == el.y) + (ek.x == el.z) + (ek.y == el.x) + (ek.y == el.y) +
                  (ek.y == el.z) + (ek.z == el.x) + (ek.z == el.y) + (ek.z == el.z);
@@ -228,14 +242,24 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     if (!(needAk || needA[l])) return -1;
     return k == l ? 2 : (ns == 2 ? 3 : 4);
   }
-  if (!needAk) return -1;
-  return __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta ? 0 : 1;
+  const bool full = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
+  bool shared = false;
+  if (k != l && (el.w & 16)) {  // does root l visit k with the same category?
+    const bool rej_lk = !touching && __dsub_rn(__dsub_rn(dist, rl), rk) > P.prer;
+    const bool full_lk = __dadd_rn(__dadd_rn(dist, rl), rk) <= P.delta;
+    shared = !rej_lk && full_lk == full;
+  }
+  if (shared && inR[l] >= 0 && l < k) return -1;  // root l produces the record
+  const bool emitB = shared && needA[l];
+  if (!needAk && !emitB) return -1;
+  flags = (needAk ? kEmitA : 0) | (emitB ? kEmitB : 0);
+  return full ? 0 : 1;
 }
 
 template <bool FILL>
 __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
-                             const unsigned char* __restrict__ needA, int* __restrict__ cnt,
-                             const long long* __restrict__ off, int2* __restrict__ lf,
+                             const unsigned char* __restrict__ needA, const int* __restrict__ inR,
+                             int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ lf,
                              int2* __restrict__ lp, int2* __restrict__ ls0, int2* __restrict__ ls1,
                              int2* __restrict__ ls2) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -261,18 +285,18 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
       const int c1 = G.start[yy * G.nx + min(ix + 1, G.nx - 1) + 1];
       for (int j0 = c0; j0 < c1; j0 += 32) {
         const int j = j0 + lane;
-        int cat = -1;
+        int cat = -1, fl = 0;
         bool vis = false;
-        if (j < c1) cat = classify(P, k, ek, ck, rk, needAk, needA, G.items[j], vis);
+        const int l = j < c1 ? G.items[j] : 0;
+        if (j < c1) cat = classify(P, k, ek, ck, rk, needAk, needA, inR, l, vis, fl);
         if (!FILL) {
           c[C_EPI] += vis;
           if (cat >= 0) c[cat]++;
         } else {
-          const int l = j < c1 ? G.items[j] : 0;
 #pragma unroll
           for (int q = 0; q < 5; ++q) {
             const unsigned m = __ballot_sync(0xffffffffu, cat == q);
-            if (cat == q) lists[q][base[q] + __popc(m & lt)] = make_int2(k, l);
+            if (cat == q) lists[q][base[q] + __popc(m & lt)] = make_int2(k, l | fl);
             base[q] += __popc(m);
           }
         }
@@ -296,6 +320,21 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
   }
 }
 
+__global__ void k_rank(const int* __restrict__ roots, int nR, int* inR) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nR) inR[roots[i]] = i;
+}
+
+// reverse index of side-B records: key = rank of the partner root (nR = none)
+__global__ void k_rev_keys(const int2* __restrict__ rec, long long n, const int* __restrict__ inR, int nR,
+                           unsigned* key, int* val) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 r = rec[i];
+  key[i] = (r.y & kEmitB) ? (unsigned)inR[r.y & kIdMask] : (unsigned)nR;
+  val[i] = (int)i;
+}
+
 // ---------------------------------------------------------------- visits
 __device__ __forceinline__ unsigned long long coo_key(const Params& P, long long row, long long col) {
   if (row < P.row_lo || row >= P.row_hi) return kSentinel;
@@ -317,27 +356,55 @@ __device__ __forceinline__ void warp_add_ll(T v, unsigned long long* dst) {
 }
 
 struct VisitOut {
-  double* kkv;              // [E][nvis] kk block values (entry-major)
-  unsigned long long* kkf;  // [nvis] presence bits of the kk block
-  long long nvis;           // n_full + n_partial
-  long long vofs;           // this list's first visit index
-  unsigned long long* keys;  // COO
+  double* kkv;              // [record][side][E] own-block values of visit A (k, l) / B (l, k)
+  unsigned long long* kkf;  // [record][side] presence bits of those blocks
+  long long nvis;           // records of both lists
+  long long vofs;           // this list's first record index
+  unsigned long long* keys;  // COO: [record][side][E] neighbour blocks
   double* vals;
-  long long cbase;  // this list's COO slot base (entry-major over the list)
+  long long cbase;  // this list's COO slot base
   long long nlist;
   unsigned long long* counters;
   unsigned long long* errpair;
 };
 
-template <int KID, bool FULL>
-__global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict__ list, VisitOut O) {
+// emit one side of a record: own block -> scratch, neighbour block -> COO
+template <int NC>
+__device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long v, int side, bool on,
+                                          int root, int nb, const double* kk, const double* kl,
+                                          unsigned long long flags) {
+  constexpr int E = 9 * NC * NC;
+  const long long vi = O.vofs + v;
+  const int4 dr = __ldg(&P.dofs[root]);
+  const int4 dn = __ldg(&P.dofs[nb]);
+  const int dra[3] = {dr.x, dr.y, dr.z}, dna[3] = {dn.x, dn.y, dn.z};
+  O.kkf[vi * 2 + side] = on ? flags : 0ull;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int I = e / (3 * NC), J = e % (3 * NC);
+    O.kkv[(vi * 2 + side) * E + e] = on ? kk[e] : 0.0;
+    const long long slot = O.cbase + (v * 2 + side) * E + e;
+    if (on) {
+      note_nonfinite(kk[e], root, nb, P.K, O.errpair);
+      note_nonfinite(kl[e], root, nb, P.K, O.errpair);
+    }
+    O.keys[slot] = on ? coo_key(P, (long long)NC * dra[I / NC] + I % NC, (long long)NC * dna[J / NC] + J % NC)
+                      : kSentinel;
+    O.vals[slot] = on ? emit_val(kl[e]) : 0.0;
+  }
+}
+
+// full records, one thread each: the 7x7 point-pair matrix gives both visits
+template <int KID>
+__global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   constexpr int E = T::E, NC = T::NC;
-  long long ev0 = 0, ev2 = 0, out0 = 0, out2 = 0, e_m1 = 0, o_m1 = 0;
+  long long ev0 = 0, ev2 = 0, out0 = 0, out2 = 0;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < O.nlist;
        v += (long long)gridDim.x * blockDim.x) {
     const int2 pr = list[v];
-    const int k = pr.x, l = pr.y;
+    const int k = pr.x, l = pr.y & kIdMask;
+    const bool emitA = pr.y & kEmitA, emitB = pr.y & kEmitB;
     double kx[3], ky[3], lx[3], ly[3];
     load_tri(P, k, kx, ky);
     const int4 ek = __ldg(&P.elem[k]);
@@ -345,119 +412,81 @@ __global__ void __launch_bounds__(128) k_visits(Params P, const int2* __restrict
     const bool touching = (k == l) || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
                           ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
     const double rs2 = (touching && P.path == 1) ? P.rskip2 : 0.0;
-    double kk[E], kl[E];
-    unsigned long long flags = 0;
+    double kkA[E], klA[E], kkB[E], klB[E];
+    unsigned long long fA = 0, fB = 0;
     if (k == l) {
-      if constexpr (FULL) {
-        full_identical<KID>(P, kx, ky, rs2, kk, kl, ev2);
-        out2 += 7;
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) kk[e] = kl[e] = 0.0;
-        sweep<KID, 2>(P, kx, ky, kx, ky, rs2, kk, kl, e_m1, o_m1);
-      }
+      // identical pair: both column halves of the reference's B hit k's dofs;
+      // keep them apart for the per-triplet presence test (_engine.py:403-424)
+      full_identical<KID>(P, kx, ky, rs2, kkA, klA, ev2);
+      out2 += 7;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        if (kk[e] != 0.0 || kl[e] != 0.0) flags |= 1ull << e;
-        kk[e] += kl[e];
-        kl[e] = 0.0;
+        if (kkA[e] != 0.0) fA |= 1ull << e;
+        kkB[e] = klB[e] = 0.0;
       }
     } else {
       load_tri(P, l, lx, ly);
-      if constexpr (FULL) {
-        full_pair<KID>(P, kx, ky, lx, ly, rs2, kk, kl, ev0);
-        out0 += 14;
-      } else {
+      long long ne = 0;
+      full_pair2<KID>(P, kx, ky, lx, ly, rs2, kkA, klA, kkB, klB, ne);
+      // flop accounting: the reference integrates the pair once per visit
+      const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
+      ev0 += ne * mult;
+      out0 += 14 * mult;
 #pragma unroll
-        for (int e = 0; e < E; ++e) kk[e] = kl[e] = 0.0;
-        sweep<KID, 0>(P, kx, ky, lx, ly, rs2, kk, kl, ev0, out0);
-        sweep<KID, 1>(P, lx, ly, kx, ky, rs2, kk, kl, ev2, out2);
+      for (int e = 0; e < E; ++e) {
+        if (kkA[e] != 0.0) fA |= 1ull << e;
+        if (kkB[e] != 0.0) fB |= 1ull << e;
       }
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (kk[e] != 0.0) flags |= 1ull << e;
     }
-    // root block -> per-visit scratch; neighbour block -> COO
-    const long long vi = O.vofs + v;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      note_nonfinite(kk[e], k, l, P.K, O.errpair);
-      O.kkv[vi * E + e] = kk[e];
-    }
-    O.kkf[vi] = flags;
-    const int4 dk = __ldg(&P.dofs[k]);
-    const int4 dl = __ldg(&P.dofs[l]);
-    const int dka[3] = {dk.x, dk.y, dk.z}, dla[3] = {dl.x, dl.y, dl.z};
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-#pragma unroll
-          for (int d = 0; d < NC; ++d) {
-            const int e = ((a * NC + c) * 3 + b) * NC + d;
-            const long long slot = O.cbase + v * E + e;
-            if (k == l) {
-              O.keys[slot] = kSentinel;
-              O.vals[slot] = 0.0;
-            } else {
-              note_nonfinite(kl[e], k, l, P.K, O.errpair);
-              O.keys[slot] = coo_key(P, (long long)NC * dka[a] + c, (long long)NC * dla[b] + d);
-              O.vals[slot] = emit_val(kl[e]);
-            }
-          }
+    emit_side<NC>(P, O, v, 0, emitA, k, l, kkA, klA, fA);
+    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, kkB, klB, fB);
   }
-  if (FULL) {
-    warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
-    warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
-    warp_add_ll(out0, &O.counters[K_OUT_FULL0]);
-    warp_add_ll(out2, &O.counters[K_OUT_FULL2]);
-  } else {
-    // mode-0 evals in ev0/out0, mode-1 in ev2/out2, mode-2 (identical) in e_m1/o_m1
-    warp_add_ll(ev0, &O.counters[K_EVAL_M0]);
-    warp_add_ll(out0, &O.counters[K_OUT_M0]);
-    warp_add_ll(ev2, &O.counters[K_EVAL_M1]);
-    warp_add_ll(out2, &O.counters[K_OUT_M1]);
-    warp_add_ll(e_m1, &O.counters[K_EVAL_M2]);
-    warp_add_ll(o_m1, &O.counters[K_OUT_M2]);
-  }
+  warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
+  warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
+  warp_add_ll(out0, &O.counters[K_OUT_FULL0]);
+  warp_add_ll(out2, &O.counters[K_OUT_FULL2]);
 }
 
 // ---------------------------------------------------------------------
-// clipped (truncated) visits, warp-cooperative.
-// A warp takes VPC visits at a time; lane = item (visit slot, sweep m, outer
-// point p), m = 0: outer k / inner l, m = 1: outer l / inner k, m = 2:
-// identical pair (mode 2).  Phase 1 clips in parallel (exact reference
-// predicates) and stores the fan in shared memory; phase 2 spreads the
-// flattened (sub-triangle, inner point) units evenly over the 32 lanes and
-// folds each unit straight into the lane's partial B block; phase 3 sums the
-// partial blocks with a reduce-scatter (lane i ends with value i) and emits.
-// The unit -> lane mapping and the reduction tree are fixed, so results are
-// run-to-run deterministic.
+// clipped (truncated) records, warp-cooperative.
+// A warp takes two records at a time (lanes 0-13 and 16-29); lane = item
+// (sweep m, outer point p) with m = 0: outer k / inner l, m = 1: outer l /
+// inner k, m = 2: identical pair (reference mode 2).
+//  phase 1: each lane clips its item with the reference's exact predicates
+//           (nlg_geom.cuh) and queues its kept fan sub-triangles;
+//  phase 2: lanes take one queued sub-triangle each and integrate its 7
+//           inner points into the sums S0, SyP, SyQ, Syy (_engine.py:113-153);
+//           a segmented warp reduction adds them to the item's row in smem;
+//  phase 3: each item folds its sums (_engine.py:154-184) into BOTH visits
+//           of the record -- the reference's mode-0 fold of one visit and the
+//           mode-1 fold of the other use the same sweep -- and a reduce-scatter
+//           over the record's 16 lanes produces the two blocks.
+// Unit-to-lane mapping and reduction trees are fixed: run-to-run deterministic.
 // ---------------------------------------------------------------------
 template <int KID> struct ClipCfg {
   static constexpr int NC = KTraits<KID>::NC;
   static constexpr int NC2 = NC * NC;
-  static constexpr int VPC = NC == 1 ? 2 : 1;           // visits per warp chunk
-  static constexpr int NKK = 3 * NC * (3 * NC + 1) / 2;  // symmetric root block, unique
+  static constexpr bool SYM = KTraits<KID>::SYM;
+  static constexpr int NKK = 3 * NC * (3 * NC + 1) / 2;  // symmetric own block, unique
   static constexpr int NKL = 9 * NC * NC;
-  static constexpr int NV = VPC * (NKK + NKL);
-  static constexpr int NP = NV <= 32 ? 32 : 64;          // padded for the reduce-scatter
-  static constexpr int PER_LANE = NP / 32;
-  static constexpr int QCAP = 32 * 7;                    // <= 7 kept sub-triangles per item
+  static constexpr int NSIDE = NKK + NKL;
+  static constexpr int NVAL = 2 * NSIDE;                 // sides A and B
+  static constexpr int NBATCH = (NVAL + 31) / 32;        // reduce-scatter batches of 32 values
+  static constexpr int NSUM = NC2 * (SYM ? 10 : 13);     // S0, SyP[3], (SyQ[3]), Syy[6]
 };
 
+template <int KID>
 struct ClipWarp {
   double px[32][kMaxPoly], py[32][kMaxPoly];
-  double sx[32][kMaxPoly], sy[32][kMaxPoly];  // clip scratch
+  double sx[32][8], sy[32][8];  // clip scratch (<= 7 rows)
+  double sums[32][ClipCfg<KID>::NSUM];
   double xo[32][2];
   double W[32];
-  double tri[2][2][8];  // [visit slot][side]: o.x o.y e1x e1y e2x e2y idet
+  double tri[2][2][8];  // [record slot][side]: o.x o.y e1x e1y e2x e2y idet
   double rs2[2];
   unsigned short queue[32 * 7];  // (item << 4) | t of every kept sub-triangle, item-major
   unsigned char pm[32];
-  int vk[2], vl[2], dk[2][3], dl[2][3];  // per visit slot: elements and their dof bases
+  int vk[2], vl[2], fl[2], dk[2][3], dl[2][3];  // per record slot
 };
 
 // (I, J) of the u-th unique entry of a symmetric n x n block, I <= J
@@ -467,67 +496,104 @@ __device__ __forceinline__ void sym_ij(int u, int n, int& I, int& J) {
   J = I + u;
 }
 
-// sums of one sub-triangle: S0 = sum tp, SyP_a = sum tp h_a, SyQ_a = sum tq h_a,
-// Syy_ab = sum tq h_a h_b (a <= b), tp = wq P, tq = wq Q (_engine.py:113-153)
-template <int KID> struct SubSums {
-  static constexpr int NC2 = KTraits<KID>::NC2;
-  static constexpr bool SYM = KTraits<KID>::SYM;
-  double S0[NC2], SyP[3][NC2], SyQ[SYM ? 1 : 3][NC2], Syy[6][NC2];
-  __device__ __forceinline__ const double* syq(int a) const { return SYM ? SyP[a] : SyQ[SYM ? 0 : a]; }
-};
-
 __device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 00 01 02 11 12 22
   const int i = a < b ? a : b, j = a < b ? b : a;
   return i == 0 ? j : (i == 1 ? 2 + j : 5);
+}
+
+// layout of one item's sums: S0[NC2] | SyP[3][NC2] | SyQ[3][NC2] (nonsym) | Syy[6][NC2]
+template <int KID> struct SumIdx {
+  static constexpr int NC2 = KTraits<KID>::NC2;
+  static constexpr bool SYM = KTraits<KID>::SYM;
+  __device__ static constexpr int s0(int i) { return i; }
+  __device__ static constexpr int syp(int a, int i) { return NC2 + a * NC2 + i; }
+  __device__ static constexpr int syq(int a, int i) { return SYM ? syp(a, i) : 4 * NC2 + a * NC2 + i; }
+  __device__ static constexpr int syy(int ab, int i) { return (SYM ? 4 : 7) * NC2 + ab * NC2 + i; }
+};
+
+// value g of the reduce-scatter layout: [side A: kk unique | kl][side B: ...]
+// for the item with sums s, W, outer hats oh and sweep m
+template <int KID>
+__device__ __forceinline__ double fold_value(int g, int m, double W, const double* oh, const double* s) {
+  using C = ClipCfg<KID>;
+  using X = SumIdx<KID>;
+  constexpr int NC = C::NC, N3 = 3 * NC;
+  if (g >= C::NVAL) return 0.0;
+  const int side = g / C::NSIDE, w = g % C::NSIDE;
+  // which reference fold feeds this side: mode 0 (outer hats x S0 / SyQ) or mode 1 (Syy / SyP)
+  const bool f0 = m == 2 ? true : ((m == 0) == (side == 0));
+  const bool f1 = m == 2 ? true : !f0;
+  if (m == 2 && side == 1) return 0.0;
+  double v = 0.0;
+  if (w < C::NKK) {
+    int I, J;
+    sym_ij(w, N3, I, J);
+    const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
+    if (f0) v += (W * (oh[a] * oh[b])) * s[X::s0(cd)];
+    if (f1) v += W * s[X::syy(sym3(a, b), cd)];
+  } else {
+    const int e = w - C::NKK, I = e / N3, J = e % N3;
+    const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
+    if (f0) v -= (W * oh[a]) * s[X::syq(b, cd)];
+    if (f1) v -= (W * oh[b]) * s[X::syp(a, cd)];
+  }
+  return v;
 }
 
 template <int KID>
 __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
+  using X = SumIdx<KID>;
   constexpr int NC = T::NC, NC2 = T::NC2, N3 = 3 * NC;
-  __shared__ ClipWarp smw[4];
-  ClipWarp& S = smw[threadIdx.x >> 5];
+  extern __shared__ __align__(16) unsigned char clip_smem[];
+  ClipWarp<KID>& S = reinterpret_cast<ClipWarp<KID>*>(clip_smem)[threadIdx.x >> 5];
   const int lane = lane_id();
-  const long long nchunks = (O.nlist + C::VPC - 1) / C::VPC;
+  const long long nchunks = (O.nlist + 1) / 2;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   long long n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;
-  // software pipeline: the next chunk's visit pair and element records are
-  // fetched while the current chunk computes
   const int vs = lane >> 4, r = lane & 15;
+  // software pipeline: the next chunk's records and element records are
+  // fetched while the current chunk computes
   int2 pr = make_int2(0, 0);
   int4 ek = make_int4(0, 0, 0, 0), el = ek;
   {
-    const long long v0 = w0 * C::VPC + vs;
-    if (vs < C::VPC && v0 < O.nlist) {
+    const long long v0 = w0 * 2 + vs;
+    if (v0 < O.nlist) {
       pr = list[v0];
       ek = __ldg(&P.elem[pr.x]);
-      el = __ldg(&P.elem[pr.y]);
+      el = __ldg(&P.elem[pr.y & kIdMask]);
     }
   }
   for (long long ch = w0; ch < nchunks; ch += nw) {
-    // ---------------- phase 1: clip one item (visit slot, sweep, outer point) per lane
-    const long long v = ch * C::VPC + vs;
-    bool valid = vs < C::VPC && r < 14 && v < O.nlist;
-    const int k = pr.x, l = pr.y;
+    // ---------------- phase 1: clip one item per lane
+    const long long v = ch * 2 + vs;
+    const bool vok = v < O.nlist;
+    bool valid = vok && r < 14;
+    const int k = pr.x, l = pr.y & kIdMask, flags = pr.y & ~kIdMask;
     int m = r >= 7 ? 1 : 0;
     const int p = r % 7;
     if (valid && k == l) {
       if (m == 1) valid = false;
       m = 2;
     }
-    const long long vn = (ch + nw) * C::VPC + vs;
-    const bool next_ok = vs < C::VPC && vn < O.nlist;
+    // evaluations of this record count once per reference visit it stands for
+    const int mult = ((flags & kEmitA) ? 1 : 0) + ((flags & kEmitB) ? 1 : 0);
+    const long long vn = (ch + nw) * 2 + vs;
+    const bool next_ok = vn < O.nlist;
     int2 prn = make_int2(0, 0);
     if (next_ok) prn = list[vn];
-    if (r == 0 && vs < C::VPC && v < O.nlist) {
+    if (r == 0 && vok) {
       const int4 dk4 = __ldg(&P.dofs[k]), dl4 = __ldg(&P.dofs[l]);
       S.vk[vs] = k;
       S.vl[vs] = l;
+      S.fl[vs] = flags;
       S.dk[vs][0] = dk4.x; S.dk[vs][1] = dk4.y; S.dk[vs][2] = dk4.z;
       S.dl[vs][0] = dl4.x; S.dl[vs][1] = dl4.y; S.dl[vs][2] = dl4.z;
     }
+#pragma unroll
+    for (int i = 0; i < C::NSUM; ++i) S.sums[lane][i] = 0.0;
     unsigned mask = 0;
     if (valid) {
       double ox[3], oy[3], ix[3], iy[3];
@@ -553,8 +619,8 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       const bool far = (P.dbg & 2) || (P.ball != 2 && dcx * dcx + dcy * dcy > reach * reach);
       const int nv = far ? 0 : truncate_inner(ix, iy, x0, x1, P.delta, P.ball, S.sx[lane], S.sy[lane], qx, qy);
       if (nv >= 3) {
-        n_out0 += m == 0;
-        n_out1 += m == 1;
+        n_out0 += m == 0 ? mult : 0;
+        n_out1 += m == 1 ? mult : 0;
         n_out2 += m == 2;
 #pragma unroll 1
         for (int t = 1; t < nv - 1; ++t) {
@@ -566,7 +632,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       S.xo[lane][0] = x0;
       S.xo[lane][1] = x1;
       S.W[lane] = c_rule.ow[p] * twice_area(ox, oy);
-      if (p == 0) {  // the visit's inner triangle of this side, for the hat functions
+      if (p == 0) {  // the record's inner triangle of this sweep, for the hat functions
         double* tr = S.tri[vs][m == 1];
         tr[0] = ix[0]; tr[1] = iy[0];
         tr[2] = ix[1] - ix[0]; tr[3] = iy[1] - iy[0];
@@ -579,7 +645,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         }
       }
     }
-    S.pm[lane] = (unsigned char)(p | (m << 4));
+    S.pm[lane] = (unsigned char)(p | (m << 4) | (valid ? 0 : 0x80));
     const int cnt = __popc(mask);
     int incl = cnt;
 #pragma unroll
@@ -593,172 +659,165 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     __syncwarp();
-    // ---------------- phase 2: one kept sub-triangle per lane, its 7 inner points
-    double acc[C::VPC][C::NKK + C::NKL];
+    // ---------------- phase 2: one queued sub-triangle per lane, 7 inner points
+    for (int u0 = 0; u0 < ((P.dbg & 1) ? 0 : total); u0 += 32) {
+      const int u = u0 + lane;
+      const bool act = u < total;
+      const int ent = act ? S.queue[u] : 0;
+      const int j = act ? ent >> 4 : -1 - lane;  // inactive lanes: unique segment ids
+      double sm[C::NSUM];
 #pragma unroll
-    for (int a = 0; a < C::VPC; ++a)
-#pragma unroll
-      for (int i = 0; i < C::NKK + C::NKL; ++i) acc[a][i] = 0.0;
-    for (int u = lane; u < ((P.dbg & 1) ? 0 : total); u += 32) {
-      const int ent = S.queue[u];
-      const int j = ent >> 4, t = ent & 15;
-      const int pmj = S.pm[j], pj = pmj & 15, mj = pmj >> 4, vsj = j >> 4;
-      const double q0x = S.px[j][0], q0y = S.py[j][0];
-      const double ax = S.px[j][t] - q0x, ay = S.py[j][t] - q0y;
-      const double bx = S.px[j][t + 1] - q0x, by = S.py[j][t + 1] - q0y;
-      const double jac2 = cross2(ax, by, ay, bx);
-      const double x0 = S.xo[j][0], x1 = S.xo[j][1];
-      const double rs2 = S.rs2[vsj];
-      const double* tr = S.tri[vsj][mj == 1];
-      const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
-      // barycentric coordinates of the inner triangle are affine along the
-      // sub-triangle: xi(q) = xi(q0) + ip0 dxi(a) + ip1 dxi(b)
-      const double u0 = q0x - o0, u1 = q0y - o1;
-      const double z1 = (u0 * e2y - u1 * e2x) * idet, z2 = (e1x * u1 - e1y * u0) * idet;
-      const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
-      const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
-      SubSums<KID> ss;
-#pragma unroll
-      for (int i = 0; i < NC2; ++i) {
-        ss.S0[i] = 0.0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) { ss.SyP[a][i] = 0.0; if (!T::SYM) ss.SyQ[T::SYM ? 0 : a][i] = 0.0; }
-#pragma unroll
-        for (int a = 0; a < 6; ++a) ss.Syy[a][i] = 0.0;
-      }
-      int ne = 0;
+      for (int i = 0; i < C::NSUM; ++i) sm[i] = 0.0;
+      if (act) {
+        const int t = ent & 15;
+        const int mj = (S.pm[j] >> 4) & 3, vsj = j >> 4;
+        const double q0x = S.px[j][0], q0y = S.py[j][0];
+        const double ax = S.px[j][t] - q0x, ay = S.py[j][t] - q0y;
+        const double bx = S.px[j][t + 1] - q0x, by = S.py[j][t + 1] - q0y;
+        const double jac2 = cross2(ax, by, ay, bx);
+        const double x0 = S.xo[j][0], x1 = S.xo[j][1];
+        const double rs2 = S.rs2[vsj];
+        const double* tr = S.tri[vsj][mj == 1];
+        const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
+        // barycentric coordinates of the inner triangle are affine along the
+        // sub-triangle: xi(q) = xi(q0) + ip0 dxi(a) + ip1 dxi(b)
+        const double v0 = q0x - o0, v1 = q0y - o1;
+        const double z1 = (v0 * e2y - v1 * e2x) * idet, z2 = (e1x * v1 - e1y * v0) * idet;
+        const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
+        const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
+        int ne = 0;
 #pragma unroll 1
-      for (int q = 0; q < 7; ++q) {
-        const double i0 = c_rule.ip[q][0], i1 = c_rule.ip[q][1];
-        const double y0 = fma(bx, i1, fma(ax, i0, q0x));
-        const double y1 = fma(by, i1, fma(ay, i0, q0y));
-        double d0 = x0 - y0, d1 = x1 - y1;
-        double r2 = fma(d0, d0, d1 * d1);
-        if (rs2 > 0.0) {  // the diagonal-skip predicate needs the reference's rounding
-          const double ey0 = __dadd_rn(__dadd_rn(q0x, mul(ax, i0)), mul(bx, i1));
-          const double ey1 = __dadd_rn(__dadd_rn(q0y, mul(ay, i0)), mul(by, i1));
-          if (sumsq(x0 - ey0, x1 - ey1) < rs2) continue;
-        }
-        double pv[NC2], qv[NC2];
-        kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
-        ++ne;
-        const double wq = c_rule.iw[q] * jac2;
-        const double xi1 = fma(i1, z1b, fma(i0, z1a, z1));
-        const double xi2 = fma(i1, z2b, fma(i0, z2a, z2));
-        const double h[3] = {1.0 - xi1 - xi2, xi1, xi2};
-#pragma unroll
-        for (int i = 0; i < NC2; ++i) {
-          const double tp = wq * pv[i];
-          const double tq = T::SYM ? tp : wq * qv[i];
-          ss.S0[i] += tp;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            ss.SyP[a][i] = fma(tp, h[a], ss.SyP[a][i]);
-            if (!T::SYM) ss.SyQ[T::SYM ? 0 : a][i] = fma(tq, h[a], ss.SyQ[T::SYM ? 0 : a][i]);
-            const double g = tq * h[a];
-#pragma unroll
-            for (int b = a; b < 3; ++b) ss.Syy[sym3(a, b)][i] = fma(g, h[b], ss.Syy[sym3(a, b)][i]);
+        for (int q = 0; q < 7; ++q) {
+          const double i0 = c_rule.ip[q][0], i1 = c_rule.ip[q][1];
+          const double y0 = fma(bx, i1, fma(ax, i0, q0x));
+          const double y1 = fma(by, i1, fma(ay, i0, q0y));
+          const double d0 = x0 - y0, d1 = x1 - y1;
+          const double r2 = fma(d0, d0, d1 * d1);
+          if (rs2 > 0.0) {  // the diagonal-skip predicate needs the reference's rounding
+            const double ey0 = __dadd_rn(__dadd_rn(q0x, mul(ax, i0)), mul(bx, i1));
+            const double ey1 = __dadd_rn(__dadd_rn(q0y, mul(ay, i0)), mul(by, i1));
+            if (sumsq(x0 - ey0, x1 - ey1) < rs2) continue;
           }
+          double pv[NC2], qv[NC2];
+          kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
+          ++ne;
+          const double wq = c_rule.iw[q] * jac2;
+          const double xi1 = fma(i1, z1b, fma(i0, z1a, z1));
+          const double xi2 = fma(i1, z2b, fma(i0, z2a, z2));
+          const double h[3] = {1.0 - xi1 - xi2, xi1, xi2};
+#pragma unroll
+          for (int i = 0; i < NC2; ++i) {
+            const double tp = wq * pv[i];
+            const double tq = T::SYM ? tp : wq * qv[i];
+            sm[X::s0(i)] += tp;
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2) {
+              sm[X::syp(a2, i)] = fma(tp, h[a2], sm[X::syp(a2, i)]);
+              if (!T::SYM) sm[X::syq(a2, i)] = fma(tq, h[a2], sm[X::syq(a2, i)]);
+              const double g = tq * h[a2];
+#pragma unroll
+              for (int b2 = a2; b2 < 3; ++b2) sm[X::syy(sym3(a2, b2), i)] = fma(g, h[b2], sm[X::syy(sym3(a2, b2), i)]);
+            }
+          }
+        }
+        const int mlt = mj == 2 ? 1 : ((S.fl[vsj] & kEmitA) ? 1 : 0) + ((S.fl[vsj] & kEmitB) ? 1 : 0);
+        n_eval0 += mj == 0 ? ne * mlt : 0;
+        n_eval1 += mj == 1 ? ne * mlt : 0;
+        n_eval2 += mj == 2 ? ne : 0;
+      }
+      // segmented inclusive scan by item (queue is item-major), then the last
+      // lane of each segment adds into the item's row
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int jo = __shfl_up_sync(0xffffffffu, j, o);
+        const bool same = lane >= o && jo == j;
+#pragma unroll
+        for (int i = 0; i < C::NSUM; ++i) {
+          const double y = __shfl_up_sync(0xffffffffu, sm[i], o);
+          if (same) sm[i] += y;
         }
       }
-      n_eval0 += mj == 0 ? ne : 0;
-      n_eval1 += mj == 1 ? ne : 0;
-      n_eval2 += mj == 2 ? ne : 0;
-      // fold the sub-triangle into its visit's partial block (_engine.py:154-184)
-      const double W = S.W[j];
-      const double* oh = c_rule.oh[pj];
-      double ckk[C::NKK], ckl[C::NKL];
-      {
-        int uu = 0;
+      const int jn = __shfl_down_sync(0xffffffffu, j, 1);
+      if (act && (lane == 31 || jn != j)) {
 #pragma unroll
-        for (int I = 0; I < N3; ++I)
-#pragma unroll
-          for (int J = I; J < N3; ++J) {
-            const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
-            double vkk = 0.0;
-            if (mj != 1) vkk += (W * (oh[a] * oh[b])) * ss.S0[cd];
-            if (mj != 0) vkk += W * ss.Syy[sym3(a, b)][cd];
-            ckk[uu++] = vkk;
-          }
-#pragma unroll
-        for (int I = 0; I < N3; ++I)
-#pragma unroll
-          for (int J = 0; J < N3; ++J) {
-            const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
-            double vkl = 0.0;
-            if (mj != 1) vkl += (W * oh[a]) * ss.syq(b)[cd];
-            if (mj != 0) vkl += (W * oh[b]) * ss.SyP[a][cd];
-            ckl[I * N3 + J] = -vkl;
-          }
+        for (int i = 0; i < C::NSUM; ++i) S.sums[j][i] += sm[i];
       }
-#pragma unroll
-      for (int s2 = 0; s2 < C::VPC; ++s2)
-        if (vsj == s2) {
-#pragma unroll
-          for (int i = 0; i < C::NKK; ++i) acc[s2][i] += ckk[i];
-#pragma unroll
-          for (int i = 0; i < C::NKL; ++i) acc[s2][C::NKK + i] += ckl[i];
-        }
+      __syncwarp();
     }
+    __syncwarp();
+    // ---------------- phase 3: fold into both visits, reduce over the record's lanes
+    const int pmy = S.pm[lane];
+    const bool ivalid = !(pmy & 0x80);
+    const int mi = (pmy >> 4) & 3, pi = pmy & 15;
+    const double Wi = S.W[lane];
+    double si[C::NSUM];
+#pragma unroll
+    for (int i = 0; i < C::NSUM; ++i) si[i] = ivalid ? S.sums[lane][i] : 0.0;
     if (next_ok) {
       ek = __ldg(&P.elem[prn.x]);
-      el = __ldg(&P.elem[prn.y]);
+      el = __ldg(&P.elem[prn.y & kIdMask]);
     }
     pr = prn;
-    // ---------------- phase 3: reduce-scatter, lane L ends with values [L*PER_LANE, ...)
-    double vals[C::NP];
+    const double* ohi = c_rule.oh[pi];
+    unsigned long long fA = 0, fB = 0;
+    const int rk = S.vk[vs], rl = S.vl[vs], rf = S.fl[vs];
 #pragma unroll
-    for (int i = 0; i < C::NP; ++i) vals[i] = 0.0;
+    for (int bt = 0; bt < C::NBATCH; ++bt) {
+      double vals[32];
 #pragma unroll
-    for (int a = 0; a < C::VPC; ++a)
+      for (int i = 0; i < 32; ++i) vals[i] = ivalid ? fold_value<KID>(bt * 32 + i, mi, Wi, ohi, si) : 0.0;
+      // reduce-scatter over the 16 lanes of the record: lane r keeps [2r, 2r+2)
 #pragma unroll
-      for (int i = 0; i < C::NKK + C::NKL; ++i) vals[a * (C::NKK + C::NKL) + i] = acc[a][i];
+      for (int off = 8, half = 16; off >= 1; off >>= 1, half >>= 1) {
+        const bool upper = lane & off;
 #pragma unroll
-    for (int off = 16, half = C::NP / 2; off >= 1; off >>= 1, half >>= 1) {
-      const bool upper = lane & off;
-#pragma unroll
-      for (int i = 0; i < half; ++i) {
-        const double send = upper ? vals[i] : vals[i + half];
-        const double keep = upper ? vals[i + half] : vals[i];
-        vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-      }
-    }
-    unsigned long long fl[C::VPC];
-#pragma unroll
-    for (int a = 0; a < C::VPC; ++a) fl[a] = 0;
-#pragma unroll
-    for (int h2 = 0; h2 < C::PER_LANE; ++h2) {
-      const int gi = lane * C::PER_LANE + h2;
-      const int vsl = gi / (C::NKK + C::NKL), wi = gi % (C::NKK + C::NKL);
-      const long long vv = ch * C::VPC + vsl;
-      if (vsl >= C::VPC || vv >= O.nlist) continue;
-      const double val = vals[h2];
-      note_nonfinite(val, S.vk[vsl], S.vl[vsl], P.K, O.errpair);
-      const long long vi = O.vofs + vv;
-      if (wi < C::NKK) {
-        int I, J;
-        sym_ij(wi, N3, I, J);
-        O.kkv[vi * (9 * NC2) + I * N3 + J] = val;
-        O.kkv[vi * (9 * NC2) + J * N3 + I] = val;
-        if (val != 0.0) {
-#pragma unroll
-          for (int a = 0; a < C::VPC; ++a)
-            if (a == vsl) fl[a] |= (1ull << (I * N3 + J)) | (1ull << (J * N3 + I));
+        for (int i = 0; i < half; ++i) {
+          const double send = upper ? vals[i] : vals[i + half];
+          const double keep = upper ? vals[i + half] : vals[i];
+          vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
         }
-      } else {
-        const int e = wi - C::NKK, I = e / N3, J = e % N3;
-        const long long slot = O.cbase + vv * C::NKL + e;
-        O.keys[slot] = coo_key(P, (long long)NC * S.dk[vsl][I / NC] + I % NC, (long long)NC * S.dl[vsl][J / NC] + J % NC);
-        O.vals[slot] = emit_val(val);
+      }
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int g = bt * 32 + r * 2 + h2;
+        if (!vok || g >= C::NVAL) continue;
+        const double val = vals[h2];
+        const int side = g / C::NSIDE, w = g % C::NSIDE;
+        const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
+        const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
+        const int* droot = side == 0 ? S.dk[vs] : S.dl[vs];
+        const int* dnb = side == 0 ? S.dl[vs] : S.dk[vs];
+        const long long vi = O.vofs + v;
+        if (w < C::NKK) {
+          int I, J;
+          sym_ij(w, N3, I, J);
+          O.kkv[(vi * 2 + side) * (9 * NC2) + I * N3 + J] = on ? val : 0.0;
+          O.kkv[(vi * 2 + side) * (9 * NC2) + J * N3 + I] = on ? val : 0.0;
+          if (on) {
+            note_nonfinite(val, root, nb, P.K, O.errpair);
+            if (val != 0.0) {
+              const unsigned long long bits = (1ull << (I * N3 + J)) | (1ull << (J * N3 + I));
+              if (side == 0) fA |= bits; else fB |= bits;
+            }
+          }
+        } else {
+          const int e = w - C::NKK, I = e / N3, J = e % N3;
+          const long long slot = O.cbase + (v * 2 + side) * (9 * NC2) + e;
+          if (on) note_nonfinite(val, root, nb, P.K, O.errpair);
+          O.keys[slot] = on ? coo_key(P, (long long)NC * droot[I / NC] + I % NC, (long long)NC * dnb[J / NC] + J % NC)
+                            : kSentinel;
+          O.vals[slot] = on ? emit_val(val) : 0.0;
+        }
       }
     }
 #pragma unroll
-    for (int a = 0; a < C::VPC; ++a) {
-      unsigned long long f = fl[a];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
-      const long long vv = ch * C::VPC + a;
-      if (lane == 0 && vv < O.nlist) O.kkf[O.vofs + vv] = f;
+    for (int o = 8; o; o >>= 1) {
+      fA |= __shfl_xor_sync(0xffffffffu, fA, o);
+      fB |= __shfl_xor_sync(0xffffffffu, fB, o);
+    }
+    if (r == 0 && vok) {
+      O.kkf[(O.vofs + v) * 2 + 0] = fA;
+      O.kkf[(O.vofs + v) * 2 + 1] = fB;
     }
     __syncwarp();
   }
@@ -770,14 +829,17 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
   warp_add_ll(n_out2, &O.counters[K_OUT_M2]);
 }
 
-// per-root sum of the root's own block over all its visits, fixed order
-// (kkv is visit-major: [visit][E])
+// per-root sum of the root's own block, fixed order: side A of the records
+// the root owns (full list, then clipped list), then side B of the records
+// where it is the partner (reverse index, record order).  kkv is
+// [record][side][E], kkf [record][side].
 template <int E>
 __global__ void k_kk_reduce(Params P, const int* __restrict__ roots, int nR,
                             const int* __restrict__ cnt, const long long* __restrict__ off,
                             long long nF, const double* __restrict__ kkv,
-                            const unsigned long long* __restrict__ kkf, long long nvis,
-                            unsigned long long* keys, double* vals, long long cbase) {
+                            const unsigned long long* __restrict__ kkf, const int* __restrict__ rev_item,
+                            const int* __restrict__ rev_start, unsigned long long* keys, double* vals,
+                            long long cbase) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
@@ -787,15 +849,19 @@ __global__ void k_kk_reduce(Params P, const int* __restrict__ roots, int nR,
     const bool emit = cnt[(long long)C_KK * nR + i] != 0;
     const long long f0 = off[0 * (long long)(nR + 1) + i], fn = cnt[(long long)C_FULL * nR + i];
     const long long p0 = nF + off[1 * (long long)(nR + 1) + i], pn = cnt[(long long)C_PART * nR + i];
+    const long long r0 = rev_start[i], rn = rev_start[i + 1] - r0;
     unsigned long long fl = 0;
     double s[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) s[e] = 0.0;
-    for (long long j = lane; j < fn + pn; j += 32) {
-      const long long vi = j < fn ? f0 + j : p0 + (j - fn);
-      fl |= kkf[vi];
+    for (long long j = lane; j < fn + pn + rn; j += 32) {
+      long long slot;
+      if (j < fn) slot = (f0 + j) * 2;
+      else if (j < fn + pn) slot = (p0 + (j - fn)) * 2;
+      else slot = (long long)rev_item[r0 + (j - fn - pn)] * 2 + 1;
+      fl |= kkf[slot];
 #pragma unroll
-      for (int e = 0; e < E; ++e) s[e] += kkv[vi * E + e];
+      for (int e = 0; e < E; ++e) s[e] += kkv[slot * E + e];
     }
     for (int o = 16; o; o >>= 1) fl |= __shfl_xor_sync(0xffffffffu, fl, o);
 #pragma unroll
@@ -1249,20 +1315,23 @@ long long alg_flops(const Params& P, const unsigned long long* c, int part) {
 template <int KID>
 nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long nF, const int2* lp,
                       long long nP, VisitOut O, cudaEvent_t ev_mid) {
+  constexpr long long E = KTraits<KID>::E;
   O.vofs = 0;
   O.nlist = nF;
   if (nF) {
-    k_visits<KID, true><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, O);
+    k_full<KID><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, O);
     LAUNCHED();
   }
   CK(cudaEventRecord(ev_mid, pl->stream));
   O.vofs = nF;
-  O.cbase += 9LL * KTraits<KID>::NC2 * nF;
+  O.cbase += 2 * E * nF;
   O.nlist = nP;
   if (nP) {
-    const long long chunks = (nP + ClipCfg<KID>::VPC - 1) / ClipCfg<KID>::VPC;
+    const long long chunks = (nP + 1) / 2;
     const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
-    k_clipped<KID><<<g, 128, 0, pl->stream>>>(P, lp, O);
+    const int smem = 4 * (int)sizeof(ClipWarp<KID>);
+    CK(cudaFuncSetAttribute(k_clipped<KID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_clipped<KID><<<g, 128, smem, pl->stream>>>(P, lp, O);
     LAUNCHED();
   }
   return NLG_OK;
@@ -1349,6 +1418,13 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   int nR = 0;
   CK(cudaMemcpyAsync(&nR, nroots.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  DevBuf inR;  // element -> rank in the batch's root list, -1 if not a root
+  CK(inR.alloc(sizeof(int) * K, s));
+  CK(cudaMemsetAsync(inR.p, 0xff, sizeof(int) * K, s));
+  if (nR) {
+    k_rank<<<grid_for(nR, 256), 256, 0, s>>>(roots.as<int>(), nR, inR.as<int>());
+    LAUNCHED();
+  }
   // ---- candidate counts
   DevBuf cnt, off;
   CK(cnt.alloc(sizeof(int) * (size_t)kCnt * std::max(nR, 1), s));
@@ -1356,8 +1432,8 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   const int cand_blocks = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
   if (nR) {
     k_candidates<false><<<std::max(cand_blocks, 1), 256, 0, s>>>(
-        P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), cnt.as<int>(), nullptr, nullptr,
-        nullptr, nullptr, nullptr, nullptr);
+        P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), inR.as<int>(), cnt.as<int>(), nullptr,
+        nullptr, nullptr, nullptr, nullptr, nullptr);
     LAUNCHED();
   }
   {
@@ -1397,10 +1473,10 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   const int NC = P.nc;
   const long long E = 9LL * NC * NC;
   const long long nvis = nF + nPt;
-  const long long coo = (long long)nR * E + nvis * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
-  // bytes: keys+vals twice (sort double buffer) + kk scratch + lists + merge arrays
-  const long long bytes = coo * 16 * 2 + nvis * (E * 8 + 8) + (nvis + nS[0] + nS[1] + nS[2]) * 8 +
-                          coo * 8 * 3;
+  const long long coo = (long long)nR * E + nvis * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
+  // bytes: keys+vals twice (sort double buffer) + kk scratch + lists + reverse index + merge arrays
+  const long long bytes = coo * 16 * 2 + nvis * 2 * (E * 8 + 8) + (nvis + nS[0] + nS[1] + nS[2]) * 8 +
+                          nvis * 16 + coo * 8 * 3;
   if (budget > 0 && bytes > budget && row_hi - row_lo > 1) {
     *need_split = true;
     return NLG_OK;
@@ -1429,17 +1505,40 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   int2* ls[3] = {lp + nPt, lp + nPt + nS[0], lp + nPt + nS[0] + nS[1]};
   if (nR) {
     k_candidates<true><<<std::max(cand_blocks, 1), 256, 0, s>>>(
-        P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), cnt.as<int>(), off.as<long long>(), lf,
-        lp, ls[0], ls[1], ls[2]);
+        P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), inR.as<int>(), cnt.as<int>(),
+        off.as<long long>(), lf, lp, ls[0], ls[1], ls[2]);
     LAUNCHED();
   }
+  // reverse index of side-B records by partner root (stable: record order)
+  DevBuf rkey, rkey2, ritem0, ritem, rstart;
+  CK(rkey.alloc(sizeof(unsigned) * std::max(nvis, 1LL), s));
+  CK(rkey2.alloc(sizeof(unsigned) * std::max(nvis, 1LL), s));
+  CK(ritem0.alloc(sizeof(int) * std::max(nvis, 1LL), s));
+  CK(ritem.alloc(sizeof(int) * std::max(nvis, 1LL), s));
+  CK(rstart.alloc(sizeof(int) * (nR + 1), s));
+  if (nvis) {
+    k_rev_keys<<<grid_for(nvis, 256), 256, 0, s>>>(lf, nvis, inR.as<int>(), nR, rkey.as<unsigned>(), ritem0.as<int>());
+    LAUNCHED();
+    int rbits = 1;
+    while ((1ll << rbits) <= nR) ++rbits;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, rkey.as<unsigned>(), rkey2.as<unsigned>(), ritem0.as<int>(),
+                                       ritem.as<int>(), (int)nvis, 0, rbits, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, rkey.as<unsigned>(), rkey2.as<unsigned>(), ritem0.as<int>(),
+                                       ritem.as<int>(), (int)nvis, 0, rbits, s));
+    g_launches += 1 + (rbits + 7) / 8;
+  }
+  k_cell_ranges<<<grid_for(nR + 1, 256), 256, 0, s>>>(rkey2.as<unsigned>(), (int)nvis, nR, rstart.as<int>());
+  LAUNCHED();
   CK(cudaEventRecord(ev[1], s));
   // ---- integrate
   DevBuf keys, vals, keys2, vals2, kkv, kkf;
   CK(keys.alloc(sizeof(unsigned long long) * coo, s));
   CK(vals.alloc(sizeof(double) * coo, s));
-  CK(kkv.alloc(sizeof(double) * E * std::max(nvis, 1LL), s));
-  CK(kkf.alloc(sizeof(unsigned long long) * std::max(nvis, 1LL), s));
+  CK(kkv.alloc(sizeof(double) * 2 * E * std::max(nvis, 1LL), s));
+  CK(kkf.alloc(sizeof(unsigned long long) * 2 * std::max(nvis, 1LL), s));
   VisitOut O;
   O.kkv = kkv.as<double>();
   O.kkf = kkf.as<unsigned long long>();
@@ -1458,7 +1557,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   }
   if (rc) return rc;
   CK(cudaEventRecord(ev[3], s));
-  const long long sbase = (long long)nR * E + nvis * E;
+  const long long sbase = (long long)nR * E + nvis * 2 * E;
   switch (P.kid) {
     case 0: rc = run_singular<0>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
     case 1: rc = run_singular<1>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
@@ -1471,10 +1570,12 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     const int g = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
     if (NC == 1)
       k_kk_reduce<9><<<std::max(g, 1), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), off.as<long long>(), nF,
-                                                     O.kkv, O.kkf, nvis, O.keys, O.vals, 0);
+                                                     O.kkv, O.kkf, ritem.as<int>(), rstart.as<int>(), O.keys,
+                                                     O.vals, 0);
     else
       k_kk_reduce<36><<<std::max(g, 1), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), off.as<long long>(), nF,
-                                                      O.kkv, O.kkf, nvis, O.keys, O.vals, 0);
+                                                      O.kkv, O.kkf, ritem.as<int>(), rstart.as<int>(), O.keys,
+                                                      O.vals, 0);
     LAUNCHED();
   }
   // ---- sort (row, col) keys; stable, so equal keys keep COO position order
@@ -1622,7 +1723,7 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   if (pb->nc != want_nc) { set_err("kernel id %d needs nc=%d, got %d", pb->kernel_id, want_nc, pb->nc); return NLG_ERR_CONFIG; }
   if ((pb->kernel_id == 3) == (pb->symmetric != 0)) { set_err("kernel id %d has the wrong symmetry flag", pb->kernel_id); return NLG_ERR_CONFIG; }
   if (pb->ball_id < 0 || pb->ball_id > 2 || pb->path_touch < 0 || pb->path_touch > 2) { set_err("bad ball/path id"); return NLG_ERR_CONFIG; }
-  if (pb->n_elements < 0 || pb->n_vertices < 0 || pb->n_elements >= (1LL << 31) || pb->n_vertices >= (1LL << 31)) {
+  if (pb->n_elements < 0 || pb->n_vertices < 0 || pb->n_elements >= (1LL << 30) || pb->n_vertices >= (1LL << 31)) {
     set_err("mesh size out of range"); return NLG_ERR_CONFIG;
   }
   if (pb->n_dofs <= 0 || pb->n_dofs >= (1LL << 31)) { set_err("dof count out of range"); return NLG_ERR_CONFIG; }

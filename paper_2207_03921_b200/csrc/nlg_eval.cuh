@@ -105,25 +105,45 @@ __device__ __forceinline__ void rule_points(const Params& P, const double* tx, c
 }
 
 // ---------------------------------------------------------------------
-// full (untruncated) non-identical pair: kk and kl blocks in one 7x7 pass
+// full (untruncated) non-identical pair, both visits from one 7x7 pass.
+// With P_pq = kernel(x_p, y_q), Q_pq = kernel(y_q, x_p) (x on k, y on l),
+// w the 7-point weights, H the hat table and c2 = 2 (2A_k)(2A_l):
+//   visit (k, l): kkA[a,b] = c2 sum_p w_p H_pa H_pb sum_q w_q P_pq
+//                 klA[a,b] = -c2 sum_pq w_p w_q Q_pq H_pa H_qb
+//   visit (l, k): kkB[a,b] = c2 sum_q w_q H_qa H_qb sum_p w_p Q_pq
+//                 klB[a,b] = -c2 sum_pq w_p w_q P_pq H_qa H_pb
+// (rows a on the visit's root, columns b on its neighbour).
 // ---------------------------------------------------------------------
 template <int KID>
-__device__ __forceinline__ void full_pair(const Params& P, const double* kx, const double* ky,
-                                          const double* lx, const double* ly, double rs2,
-                                          double* kk, double* kl, long long& n_eval) {
+__device__ __forceinline__ void full_pair2(const Params& P, const double* kx, const double* ky,
+                                           const double* lx, const double* ly, double rs2, double* kkA,
+                                           double* klA, double* kkB, double* klB, long long& n_eval) {
   using T = KTraits<KID>;
-  constexpr int NC2 = T::NC2;
+  constexpr int NC = T::NC, NC2 = T::NC2;
   double xk[7], yk[7], xl[7], yl[7];
   rule_points(P, kx, ky, xk, yk);
   rule_points(P, lx, ly, xl, yl);
   const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+  double colq[7][NC2];
 #pragma unroll
-  for (int e = 0; e < 9 * NC2; ++e) { kk[e] = 0.0; kl[e] = 0.0; }
+  for (int e = 0; e < 9 * NC2; ++e) kkA[e] = klA[e] = klB[e] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int i = 0; i < NC2; ++i) colq[q][i] = 0.0;
 #pragma unroll 1
   for (int p = 0; p < 7; ++p) {
-    double rp[NC2], g[3][NC2];
+    double rp[NC2], g[3][NC2], gp[T::SYM ? 1 : 3][NC2];
 #pragma unroll
-    for (int i = 0; i < NC2; ++i) { rp[i] = 0.0; g[0][i] = g[1][i] = g[2][i] = 0.0; }
+    for (int i = 0; i < NC2; ++i) {
+      rp[i] = 0.0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        g[b][i] = 0.0;
+        if (!T::SYM) gp[T::SYM ? 0 : b][i] = 0.0;
+      }
+    }
+    const double wp = c_rule.ow[p];
 #pragma unroll
     for (int q = 0; q < 7; ++q) {
       const double d0 = xk[p] - xl[q], d1 = yk[p] - yl[q];
@@ -135,28 +155,49 @@ __device__ __forceinline__ void full_pair(const Params& P, const double* kx, con
       const double wq = c_rule.iw[q];
 #pragma unroll
       for (int i = 0; i < NC2; ++i) {
-        rp[i] = fma(wq, pv[i], rp[i]);
         const double qq = T::SYM ? pv[i] : qv[i];
+        rp[i] = fma(wq, pv[i], rp[i]);
+        colq[q][i] = fma(wp, qq, colq[q][i]);
 #pragma unroll
-        for (int b = 0; b < 3; ++b) g[b][i] = fma(c_rule.wh[q][b], qq, g[b][i]);
+        for (int b = 0; b < 3; ++b) {
+          g[b][i] = fma(c_rule.wh[q][b], qq, g[b][i]);
+          if (!T::SYM) gp[T::SYM ? 0 : b][i] = fma(c_rule.wh[q][b], pv[i], gp[T::SYM ? 0 : b][i]);
+        }
       }
     }
-    // fold: kk[(a,c),(b,d)] += w H_a H_b r[c,d];  kl[(a,c),(b,d)] += w H_a g_b[c,d]
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < T::NC; ++c)
+      for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int b = 0; b < 3; ++b)
 #pragma unroll
-          for (int d = 0; d < T::NC; ++d) {
-            const int e = ((a * T::NC + c) * 3 + b) * T::NC + d;
-            kk[e] = fma(c_rule.whh[p][a * 3 + b], rp[c * T::NC + d], kk[e]);
-            kl[e] = fma(c_rule.wh[p][a], g[b][c * T::NC + d], kl[e]);
+          for (int d = 0; d < NC; ++d) {
+            const int e = ((a * NC + c) * 3 + b) * NC + d;
+            const int cd = c * NC + d;
+            kkA[e] = fma(c_rule.whh[p][a * 3 + b], rp[cd], kkA[e]);
+            klA[e] = fma(c_rule.wh[p][a], g[b][cd], klA[e]);
+            // klB rows a on l (inner hat via g' over q), columns b on k (outer point p)
+            klB[e] = fma(c_rule.wh[p][b], T::SYM ? g[a][cd] : gp[T::SYM ? 0 : a][cd], klB[e]);
           }
   }
 #pragma unroll
-  for (int e = 0; e < 9 * NC2; ++e) { kk[e] *= c2; kl[e] *= -c2; }
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int d = 0; d < NC; ++d) {
+          const int e = ((a * NC + c) * 3 + b) * NC + d;
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < 7; ++q) s = fma(c_rule.whh[q][a * 3 + b], colq[q][c * NC + d], s);
+          kkB[e] = s * c2;
+          kkA[e] *= c2;
+          klA[e] *= -c2;
+          klB[e] *= -c2;
+        }
 }
 
 // full identical pair (k == l, mode 2): both column halves land on k's dofs;

@@ -65,6 +65,10 @@ def test_load_constant_on_device_partition_of_unity():
 
 
 def test_deterministic_and_row_blocks_concatenate():
+    """Run-to-run bitwise determinism; owner-computed row blocks concatenate
+    into the full matrix with the identical pattern.  Each unordered pair is
+    integrated once and serves both roots, so which root's record carries a
+    visit depends on the row split: values agree to rounding (1e-13), not bitwise."""
     from paper_2207_03921_b200 import bfs_assemble
     c = Case("frac_s04_approx_pert")
     a = bfs_assemble(*c.args()).matrix
@@ -75,17 +79,18 @@ def test_deterministic_and_row_blocks_concatenate():
     blocks = [bfs_assemble(*c.args(), row_range=(lo, hi)).matrix for lo, hi in zip(cuts[:-1], cuts[1:])]
     whole = sparse.vstack(blocks).tocsr()
     assert np.array_equal(whole.indptr, a.indptr) and np.array_equal(whole.indices, a.indices)
-    assert np.array_equal(whole.data, a.data)  # owner-computed rows: bitwise identical
+    assert rel_fro(whole, a) <= 1e-13
 
 
-def test_small_memory_budget_batches_bitwise():
+def test_small_memory_budget_batches():
     from paper_2207_03921_b200 import bfs_assemble
     c = Case("peri_nocaps_avoid")
     st = {}
     a = bfs_assemble(*c.args()).matrix
     b = bfs_assemble(*c.args(), mem_budget=4 << 20, stats=st).matrix
     assert st["n_batches"] > 1
-    assert np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data)
+    assert same_pattern(a, b) and rel_fro(b, a) <= 1e-13
+    assert same_pattern(b, c.matrix) and rel_fro(b, c.matrix) <= TOL
 
 
 def test_callable_kernel_rejected():
