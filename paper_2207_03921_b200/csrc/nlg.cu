@@ -1046,27 +1046,39 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
 }
 
 // ---------------------------------------------------------------- merge
-__global__ void k_seg_heads(const unsigned long long* __restrict__ key, long long n, int* head) {
+template <typename KT> __host__ __device__ constexpr KT key_sentinel() { return (KT)~(KT)0; }
+
+// 64-bit COO keys -> 32-bit when (rows x J) fits (fewer bytes per radix pass)
+__global__ void k_narrow_keys(const unsigned long long* __restrict__ in, long long n, unsigned* out) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const unsigned long long k = key[i];
-  head[i] = k != kSentinel && (i == 0 || key[i - 1] != k);
+  const unsigned long long k = in[i];
+  out[i] = k == kSentinel ? 0xffffffffu : (unsigned)k;
 }
 
-__global__ void k_seg_starts(const unsigned long long* __restrict__ key, long long n,
-                             const int* __restrict__ head, const long long* __restrict__ sid,
-                             long long* start) {
+template <typename KT>
+__global__ void k_seg_heads(const KT* __restrict__ key, long long n, int* head) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const KT k = key[i];
+  head[i] = k != key_sentinel<KT>() && (i == 0 || key[i - 1] != k);
+}
+
+template <typename KT>
+__global__ void k_seg_starts(const KT* __restrict__ key, long long n, const int* __restrict__ head,
+                             const long long* __restrict__ sid, long long* start) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (head[i]) start[sid[i]] = i;
-  const bool valid = key[i] != kSentinel;
-  if (valid && (i + 1 == n || key[i + 1] == kSentinel)) start[sid[i] + head[i]] = i + 1;
+  const bool valid = key[i] != key_sentinel<KT>();
+  if (valid && (i + 1 == n || key[i + 1] == key_sentinel<KT>())) start[sid[i] + head[i]] = i + 1;
 }
 
 // one thread per (row, col): left-to-right sum in COO position order
-__global__ void k_seg_sum(const unsigned long long* __restrict__ key, const double* __restrict__ val,
-                          const long long* __restrict__ start, long long nseg, long long J,
-                          int* present, int* rowcnt, int* col, double* sum) {
+template <typename KT>
+__global__ void k_seg_sum(const KT* __restrict__ key, const double* __restrict__ val,
+                          const long long* __restrict__ start, long long nseg, long long J, int* present,
+                          int* rowcnt, int* col, double* sum) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= nseg) return;
   const long long a = start[s], b = start[s + 1];
@@ -1077,7 +1089,7 @@ __global__ void k_seg_sum(const unsigned long long* __restrict__ key, const doub
     acc += v;
     pres |= __double_as_longlong(v) != 0;
   }
-  const unsigned long long kk = key[a];
+  const unsigned long long kk = (unsigned long long)key[a];
   present[s] = pres;
   col[s] = (int)(kk % (unsigned long long)J);
   sum[s] = acc;
@@ -1363,6 +1375,113 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
   return NLG_OK;
 }
 
+// Stable radix sort of the COO (row, col) keys, then one thread per run
+// sums its values in COO position order -> CSR rows of this batch.
+template <typename KT>
+nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64, double* vals, long long coo,
+                     long long nrows, Csr& piece, long long& nnz) {
+  int bits = 1;
+  {
+    const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
+    while (bits < 64 && (1ull << bits) <= maxkey) ++bits;
+  }
+  DevBuf k1, k2, v2;
+  KT* keys;
+  if (sizeof(KT) == 4) {
+    CK(k1.alloc(sizeof(KT) * std::max(coo, 1LL), s));
+    if (coo) {
+      k_narrow_keys<<<grid_for(coo, 256), 256, 0, s>>>(keys64, coo, k1.as<unsigned>());
+      LAUNCHED();
+    }
+    keys = k1.as<KT>();
+  } else {
+    keys = (KT*)keys64;
+  }
+  CK(k2.alloc(sizeof(KT) * std::max(coo, 1LL), s));
+  CK(v2.alloc(sizeof(double) * std::max(coo, 1LL), s));
+  cub::DoubleBuffer<KT> dk(keys, k2.as<KT>());
+  cub::DoubleBuffer<double> dv(vals, v2.as<double>());
+  {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)coo, 0, bits, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, (int)coo, 0, bits, s));
+    g_launches += (bits + 7) / 8 + 1;
+  }
+  // the sentinel's low `bits` bits are all ones, above every valid key
+  const KT* sk = dk.Current();
+  const double* sv = dv.Current();
+  DevBuf head, sid, start, present, rowcnt, col, sum, pos;
+  CK(head.alloc(sizeof(int) * std::max(coo, 1LL), s));
+  CK(sid.alloc(sizeof(long long) * (coo + 1), s));
+  if (coo) {
+    k_seg_heads<KT><<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>());
+    LAUNCHED();
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
+    g_launches += 1;
+  }
+  long long nseg = 0;
+  if (coo) {
+    long long lsid;
+    int lhead;
+    CK(cudaMemcpyAsync(&lsid, sid.as<long long>() + coo - 1, sizeof lsid, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lhead, head.as<int>() + coo - 1, sizeof lhead, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nseg = lsid + lhead;
+  }
+  CK(start.alloc(sizeof(long long) * (nseg + 1), s));
+  CK(present.alloc(sizeof(int) * std::max(nseg, 1LL), s));
+  CK(col.alloc(sizeof(int) * std::max(nseg, 1LL), s));
+  CK(sum.alloc(sizeof(double) * std::max(nseg, 1LL), s));
+  CK(pos.alloc(sizeof(long long) * (nseg + 1), s));
+  CK(rowcnt.alloc(sizeof(int) * (nrows + 1), s));
+  CK(cudaMemsetAsync(rowcnt.p, 0, sizeof(int) * (nrows + 1), s));
+  CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
+  nnz = 0;
+  if (nseg) {
+    k_seg_starts<KT><<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>(), sid.as<long long>(),
+                                                        start.as<long long>());
+    LAUNCHED();
+    k_seg_sum<KT><<<grid_for(nseg, 256), 256, 0, s>>>(sk, sv, start.as<long long>(), nseg, P.J, present.as<int>(),
+                                                      rowcnt.as<int>(), col.as<int>(), sum.as<double>());
+    LAUNCHED();
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
+    long long lpos;
+    int lpres;
+    CK(cudaMemcpyAsync(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lpres, present.as<int>() + nseg - 1, sizeof lpres, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nnz = lpos + lpres;
+    CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
+    CK(cudaMallocAsync(&piece.data, sizeof(double) * std::max(nnz, 1LL), s));
+    k_seg_scatter<<<grid_for(nseg, 256), 256, 0, s>>>(present.as<int>(), pos.as<long long>(), col.as<int>(),
+                                                      sum.as<double>(), nseg, piece.indices, piece.data);
+    LAUNCHED();
+  } else {
+    CK(cudaMallocAsync(&piece.indices, sizeof(int), s));
+    CK(cudaMallocAsync(&piece.data, sizeof(double), s));
+  }
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    g_launches += 2;
+  }
+  piece.nnz = nnz;
+  return NLG_OK;
+}
+
 struct Timing {
   double prep = 0, cand = 0, full = 0, part = 0, sing = 0, merge = 0;
 };
@@ -1534,7 +1653,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   LAUNCHED();
   CK(cudaEventRecord(ev[1], s));
   // ---- integrate
-  DevBuf keys, vals, keys2, vals2, kkv, kkf;
+  DevBuf keys, vals, kkv, kkf;
   CK(keys.alloc(sizeof(unsigned long long) * coo, s));
   CK(vals.alloc(sizeof(double) * coo, s));
   CK(kkv.alloc(sizeof(double) * 2 * E * std::max(nvis, 1LL), s));
@@ -1578,96 +1697,14 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
                                                       O.vals, 0);
     LAUNCHED();
   }
-  // ---- sort (row, col) keys; stable, so equal keys keep COO position order
+  // ---- sort (row, col) keys (stable: equal keys keep COO position order), sum runs
   const long long nrows = row_hi - row_lo;
-  int bits = 1;
-  {
-    const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
-    while (bits < 64 && (1ull << bits) <= maxkey) ++bits;
-  }
-  CK(keys2.alloc(sizeof(unsigned long long) * coo, s));
-  CK(vals2.alloc(sizeof(double) * coo, s));
-  cub::DoubleBuffer<unsigned long long> dk(keys.as<unsigned long long>(), keys2.as<unsigned long long>());
-  cub::DoubleBuffer<double> dv(vals.as<double>(), vals2.as<double>());
-  {
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)coo, 0, bits, s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, (int)coo, 0, bits, s));
-    g_launches += (bits + 7) / 8 + 1;
-  }
-  // the sentinel's low `bits` bits are all ones, above every valid key
-  const unsigned long long* sk = dk.Current();
-  const double* sv = dv.Current();
-  // ---- segmented reduction to CSR
-  DevBuf head, sid, start, present, rowcnt, col, sum, pos;
-  CK(head.alloc(sizeof(int) * coo, s));
-  CK(sid.alloc(sizeof(long long) * (coo + 1), s));
-  k_seg_heads<<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>());
-  LAUNCHED();
-  {
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
-    g_launches += 1;
-  }
-  long long nseg = 0;
-  if (coo) {
-    long long lsid;
-    int lhead;
-    CK(cudaMemcpyAsync(&lsid, sid.as<long long>() + coo - 1, sizeof lsid, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lhead, head.as<int>() + coo - 1, sizeof lhead, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    nseg = lsid + lhead;
-  }
-  CK(start.alloc(sizeof(long long) * (nseg + 1), s));
-  CK(present.alloc(sizeof(int) * std::max(nseg, 1LL), s));
-  CK(col.alloc(sizeof(int) * std::max(nseg, 1LL), s));
-  CK(sum.alloc(sizeof(double) * std::max(nseg, 1LL), s));
-  CK(pos.alloc(sizeof(long long) * (nseg + 1), s));
-  CK(rowcnt.alloc(sizeof(int) * (nrows + 1), s));
-  CK(cudaMemsetAsync(rowcnt.p, 0, sizeof(int) * (nrows + 1), s));
-  long long nnz = 0;
   Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
-  CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
-  if (nseg) {
-    k_seg_starts<<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>(), sid.as<long long>(),
-                                                    start.as<long long>());
-    LAUNCHED();
-    k_seg_sum<<<grid_for(nseg, 256), 256, 0, s>>>(sk, sv, start.as<long long>(), nseg, P.J, present.as<int>(),
-                                                  rowcnt.as<int>(), col.as<int>(), sum.as<double>());
-    LAUNCHED();
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
-    long long lpos;
-    int lpres;
-    CK(cudaMemcpyAsync(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lpres, present.as<int>() + nseg - 1, sizeof lpres, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    nnz = lpos + lpres;
-    CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
-    CK(cudaMallocAsync(&piece.data, sizeof(double) * std::max(nnz, 1LL), s));
-    k_seg_scatter<<<grid_for(nseg, 256), 256, 0, s>>>(present.as<int>(), pos.as<long long>(), col.as<int>(),
-                                                      sum.as<double>(), nseg, piece.indices, piece.data);
-    LAUNCHED();
-  } else {
-    CK(cudaMallocAsync(&piece.indices, sizeof(int), s));
-    CK(cudaMallocAsync(&piece.data, sizeof(double), s));
-  }
-  {
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
-    g_launches += 2;
-  }
+  long long nnz = 0;
+  const bool narrow = (unsigned long long)nrows * (unsigned long long)P.J < 0xffffffffull;
+  rc = narrow ? merge_csr<unsigned>(s, P, O.keys, O.vals, coo, nrows, piece, nnz)
+              : merge_csr<unsigned long long>(s, P, O.keys, O.vals, coo, nrows, piece, nnz);
+  if (rc) return rc;
   piece.nnz = nnz;
   out.push_back(piece);
   CK(cudaEventRecord(ev[5], s));
