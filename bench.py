@@ -98,19 +98,6 @@ def dist_env():
     return ws, rank, local
 
 
-def row_split(J, nc, ws, rank, epi_weights=None):
-    """Contiguous dof-row ranges (vertex-aligned), balanced by weight when given."""
-    nb = J // nc
-    if epi_weights is None:
-        cuts = [nc * (nb * r // ws) for r in range(ws + 1)]
-    else:
-        c = np.concatenate([[0], np.cumsum(epi_weights)])
-        targets = c[-1] * np.arange(ws + 1) / ws
-        cuts = [nc * int(np.searchsorted(c, t)) for t in targets]
-        cuts[0], cuts[-1] = 0, J
-    return cuts[rank], cuts[rank + 1]
-
-
 def cpu_reference(cfg, budget_s, threads):
     """The reference algorithm (oracle port, bit-identical) on a bounded band
     of outer elements: returns EPI/s, the sample description and seconds."""
@@ -193,7 +180,8 @@ def main():
 
     inp = marshal(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
     J = inp.n_dofs
-    lo, hi = row_split(J, inp.nc, ws, rank)
+    from paper_2207_03921_b200 import shard
+    lo, hi = shard.my_rows(J, inp.nc, rank, ws, shard.vertex_work(cfg.mesh, cfg.ansatz))
     plan = DevicePlan(inp, device=local, on_device=True)  # mesh arrays resident in HBM
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")  # > 126 MB L2
 

@@ -71,3 +71,38 @@ def same_pattern(a, b):
     a.sort_indices()
     b.sort_indices()
     return np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+
+
+def sample_vertices(mesh, n=40, seed=0, extra=()):
+    """Deterministic vertex sample: corners of the bounding box plus n random."""
+    rng = np.random.default_rng(seed)
+    V = mesh.vertices
+    picks = set(int(i) for i in extra)
+    for fx in (np.argmin, np.argmax):
+        picks.add(int(fx(V[:, 0] + V[:, 1])))
+        picks.add(int(fx(V[:, 0] - V[:, 1])))
+    picks.update(int(i) for i in rng.choice(mesh.n_vertices, size=min(n, mesh.n_vertices), replace=False))
+    return np.array(sorted(picks), dtype=np.int64)
+
+
+def oracle_rows(inp, adjacency, mesh, verts, nthreads=0):
+    """CPU-oracle CSR rows of the given vertices (all components).
+
+    Runs the reference restatement only on the outer elements that reach
+    those rows: elements containing a vertex, plus (touching-pair owner rule
+    on the regularizing path) every element touching one of them.
+    """
+    from oracle import oracle
+    E = mesh.elements
+    inc = np.isin(E, verts).any(axis=1)
+    roots = set(np.flatnonzero(inc).tolist())
+    if inp.path_touch == 2:
+        vs = np.unique(E[inc])
+        roots |= set(np.flatnonzero(np.isin(E, vs).any(axis=1)).tolist())
+    roots = np.array(sorted(roots), dtype=np.int64)
+    op = oracle.OracleProblem(inp, adjacency)
+    r = op.run(starts=roots, ends=roots + 1, nthreads=nthreads)
+    J = inp.n_dofs
+    full = sparse.csr_matrix((r["data"], r["indices"], r["indptr"]), shape=(J, J))
+    rows = (inp.nc * verts[:, None] + np.arange(inp.nc)[None, :]).ravel()
+    return rows, full[rows]

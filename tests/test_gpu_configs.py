@@ -1,0 +1,101 @@
+"""BASELINE configs 3-5 (and 2's properties) on the GPU: sampled complete
+rows against the CPU oracle (same seeded meshes), plus the structural
+properties the SPEC guarantees at full size."""
+
+import numpy as np
+import pytest
+from scipy import sparse
+
+from golden_io import oracle_rows, rel_fro, same_pattern, sample_vertices
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _cfg(n, **kw):
+    from paper_2207_03921_b200 import configs
+    return configs.build(n, **kw)
+
+
+def _check_rows(cfg, A_rows_fn, nverts=40, seed=0):
+    from paper_2207_03921_b200.problem import marshal
+    inp = marshal(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
+    verts = sample_vertices(cfg.mesh, nverts, seed)
+    rows, R = oracle_rows(inp, cfg.adjacency, cfg.mesh, verts)
+    G = A_rows_fn(rows)
+    assert same_pattern(G, R), "sampled rows: pattern differs"
+    err = rel_fro(G, R)
+    assert err <= TOL, f"sampled rows: rel Frobenius {err:.3e}"
+    return rows
+
+
+@pytest.mark.parametrize("transform", [False, True])
+def test_cfg3_peridynamic_nc2(transform):
+    from paper_2207_03921_b200 import bfs_assemble
+    cfg = _cfg(3, transform=transform)
+    st = {}
+    A = bfs_assemble(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad, stats=st).matrix
+    _check_rows(cfg, lambda rows: A[rows])
+    assert abs(A - A.T).max() <= 1e-12 * abs(A).max()
+
+
+def test_cfg4_row_strip():
+    """N=2048 (8.4M triangles): an owner-computed strip of rows around sampled vertices."""
+    from paper_2207_03921_b200 import bfs_assemble
+    cfg = _cfg(4)
+    verts = sample_vertices(cfg.mesh, 6, seed=4)
+    from paper_2207_03921_b200.problem import marshal
+    inp = marshal(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
+    rows, R = oracle_rows(inp, cfg.adjacency, cfg.mesh, verts)
+    from paper_2207_03921_b200.assembly import DevicePlan, csr_from_parts
+    plan = DevicePlan(inp)
+    J = cfg.ansatz.dof_count
+    try:
+        for i, r in enumerate(rows):
+            indptr, indices, data, st = plan.assemble(int(r), int(r) + 1)
+            G = csr_from_parts(indptr, indices, data, 1, J)
+            assert same_pattern(G, R[i])
+            assert rel_fro(G, R[i]) <= TOL
+    finally:
+        plan.close()
+
+
+def test_cfg5_lshape_nonsymmetric_full_and_reduced():
+    from paper_2207_03921_b200 import bfs_assemble
+    # reduced size: the whole matrix against the oracle
+    small = _cfg(5, grid_n=48)
+    from oracle import oracle
+    ref, _ = oracle.assemble(small.mesh, small.adjacency, small.kernel, small.ansatz, small.quad)
+    G = bfs_assemble(small.mesh, small.adjacency, small.kernel, small.ansatz, small.quad).matrix
+    assert same_pattern(G, ref) and rel_fro(G, ref) <= TOL
+    # full size: sampled rows; pure Neumann -> column sums vanish
+    cfg = _cfg(5)
+    A = bfs_assemble(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad).matrix
+    _check_rows(cfg, lambda rows: A[rows], nverts=24)
+    colsum = np.abs(np.ones(A.shape[0]) @ A).max()
+    assert colsum <= 1e-12 * abs(A).max() * A.shape[0]
+
+
+def test_cfg5_bfs_equals_brute_on_reduced_lshape():
+    """Assumption 4 on the jittered L: the reference's BFS reaches every
+    interacting pair, so the device's exhaustive search equals BFS."""
+    from oracle import oracle
+    small = _cfg(5, grid_n=32)
+    a, _ = oracle.assemble(small.mesh, small.adjacency, small.kernel, small.ansatz, small.quad, traversal="bfs")
+    b, _ = oracle.assemble(small.mesh, small.adjacency, small.kernel, small.ansatz, small.quad, traversal="brute")
+    assert np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data)
+
+
+def test_cfg2_symmetry_and_nocaps():
+    from paper_2207_03921_b200 import bfs_assemble
+    cfg = _cfg(2, ball="nocaps")
+    A = bfs_assemble(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz).matrix
+    assert abs(A - A.T).max() <= 1e-12 * abs(A).max()
+    _check_rows(cfg, lambda rows: A[rows], nverts=30, seed=2)
