@@ -511,33 +511,34 @@ template <int KID> struct SumIdx {
   __device__ static constexpr int syy(int ab, int i) { return (SYM ? 4 : 7) * NC2 + ab * NC2 + i; }
 };
 
-// value g of the reduce-scatter layout: [side A: kk unique | kl][side B: ...]
-// for the item with sums s, W, outer hats oh and sweep m
+// The two reference folds of one item's sums (_engine.py:154-184), as one
+// block each in the layout [kk unique (I <= J) | kl]:
+//   F0 (outer-test terms): kk += W oh_a oh_b S0,  kl -= W oh_a SyQ_b
+//   F1 (inner-test terms): kk += W Syy_ab,        kl -= W oh_b SyP_a
 template <int KID>
-__device__ __forceinline__ double fold_value(int g, int m, double W, const double* oh, const double* s) {
+__device__ __forceinline__ void item_folds(double W, const double* oh, const double* s, double* F0, double* F1) {
   using C = ClipCfg<KID>;
   using X = SumIdx<KID>;
   constexpr int NC = C::NC, N3 = 3 * NC;
-  if (g >= C::NVAL) return 0.0;
-  const int side = g / C::NSIDE, w = g % C::NSIDE;
-  // which reference fold feeds this side: mode 0 (outer hats x S0 / SyQ) or mode 1 (Syy / SyP)
-  const bool f0 = m == 2 ? true : ((m == 0) == (side == 0));
-  const bool f1 = m == 2 ? true : !f0;
-  if (m == 2 && side == 1) return 0.0;
-  double v = 0.0;
-  if (w < C::NKK) {
-    int I, J;
-    sym_ij(w, N3, I, J);
-    const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
-    if (f0) v += (W * (oh[a] * oh[b])) * s[X::s0(cd)];
-    if (f1) v += W * s[X::syy(sym3(a, b), cd)];
-  } else {
-    const int e = w - C::NKK, I = e / N3, J = e % N3;
-    const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
-    if (f0) v -= (W * oh[a]) * s[X::syq(b, cd)];
-    if (f1) v -= (W * oh[b]) * s[X::syp(a, cd)];
-  }
-  return v;
+  const double Woh[3] = {W * oh[0], W * oh[1], W * oh[2]};
+  int u = 0;
+#pragma unroll
+  for (int I = 0; I < N3; ++I)
+#pragma unroll
+    for (int J = I; J < N3; ++J) {
+      const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
+      F0[u] = (Woh[a] * oh[b]) * s[X::s0(cd)];
+      F1[u] = W * s[X::syy(sym3(a, b), cd)];
+      ++u;
+    }
+#pragma unroll
+  for (int I = 0; I < N3; ++I)
+#pragma unroll
+    for (int J = 0; J < N3; ++J) {
+      const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
+      F0[C::NKK + I * N3 + J] = -Woh[a] * s[X::syq(b, cd)];
+      F1[C::NKK + I * N3 + J] = -Woh[b] * s[X::syp(a, cd)];
+    }
 }
 
 template <int KID>
@@ -749,7 +750,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     const int pmy = S.pm[lane];
     const bool ivalid = !(pmy & 0x80);
     const int mi = (pmy >> 4) & 3, pi = pmy & 15;
-    const double Wi = S.W[lane];
+    const double Wi = ivalid ? S.W[lane] : 0.0;
     double si[C::NSUM];
 #pragma unroll
     for (int i = 0; i < C::NSUM; ++i) si[i] = ivalid ? S.sums[lane][i] : 0.0;
@@ -761,11 +762,29 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     const double* ohi = c_rule.oh[pi];
     unsigned long long fA = 0, fB = 0;
     const int rk = S.vk[vs], rl = S.vl[vs], rf = S.fl[vs];
+    // side A (visit (k, l)) gets the fold of the sweep it calls mode 0 / 1,
+    // side B (visit (l, k)) the other one; an identical pair (m = 2) gets both on A
+    double FA[C::NSIDE], FB[C::NSIDE];
+    {
+      double F0[C::NSIDE], F1[C::NSIDE];
+      item_folds<KID>(Wi, ohi, si, F0, F1);
+      const bool m1 = mi == 1, m2 = ivalid && mi == 2;
+#pragma unroll
+      for (int i = 0; i < C::NSIDE; ++i) {
+        const double a0 = ivalid ? (m1 ? F1[i] : F0[i]) : 0.0;
+        const double b0 = ivalid && !m2 ? (m1 ? F0[i] : F1[i]) : 0.0;
+        FA[i] = m2 ? a0 + F1[i] : a0;
+        FB[i] = b0;
+      }
+    }
 #pragma unroll
     for (int bt = 0; bt < C::NBATCH; ++bt) {
       double vals[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) vals[i] = ivalid ? fold_value<KID>(bt * 32 + i, mi, Wi, ohi, si) : 0.0;
+      for (int i = 0; i < 32; ++i) {
+        const int g = bt * 32 + i;
+        vals[i] = g < C::NSIDE ? FA[g] : (g < C::NVAL ? FB[g - C::NSIDE] : 0.0);
+      }
       // reduce-scatter over the 16 lanes of the record: lane r keeps [2r, 2r+2)
 #pragma unroll
       for (int off = 8, half = 16; off >= 1; off >>= 1, half >>= 1) {
