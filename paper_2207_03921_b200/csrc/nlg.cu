@@ -1394,15 +1394,165 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
   return NLG_OK;
 }
 
+// Window pre-reduction: one warp takes kWin consecutive COO slots (records of
+// mostly one root: they share the root's rows and their neighbours share
+// vertices) and reduces equal keys through a shared-memory hash table.  Each
+// 32-slot round sums equal keys in lane order (broadcast loop) and one lane
+// per key adds the round's sum to the table, rounds in slot order, so every
+// key's sum is formed in COO slot order: deterministic.  Absent keys (all
+// contributions +0.0) are dropped; a present sum of 0 is kept as -0.0.
+constexpr int kWin = 512;               // slots per warp window
+constexpr int kWinTab = 1024;           // hash slots (>= 2 kWin: never full)
+constexpr int kWinWarps = 4;
+struct WinTable {
+  unsigned long long key[kWinTab];
+  double val[kWinTab];
+  unsigned char pres[kWinTab];
+};
+
+__global__ void __launch_bounds__(32 * kWinWarps) k_window_reduce(const unsigned long long* __restrict__ keys,
+                                                                  const double* __restrict__ vals, long long n,
+                                                                  unsigned long long* okeys, double* ovals,
+                                                                  int* counts) {
+  extern __shared__ __align__(16) unsigned char win_smem[];
+  WinTable& T = reinterpret_cast<WinTable*>(win_smem)[threadIdx.x >> 5];
+  const int lane = lane_id();
+  const long long w = (long long)blockIdx.x * kWinWarps + (threadIdx.x >> 5);
+  const long long base = w * kWin;
+  if (base >= n) return;
+  constexpr int R = kWin / 32;
+  unsigned long long kr[R];
+  double vr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {  // all loads in flight at once
+    const long long g = base + r * 32 + lane;
+    kr[r] = g < n ? __ldcs(&keys[g]) : kSentinel;
+    vr[r] = g < n ? __ldcs(&vals[g]) : 0.0;
+  }
+  for (int i = lane; i < kWinTab; i += 32) T.key[i] = kSentinel;
+  __syncwarp();
+#pragma unroll 1
+  for (int r = 0; r < R; ++r) {
+    unsigned long long k = kr[0];
+    double v = vr[0];
+#pragma unroll
+    for (int q = 1; q < R; ++q)
+      if (q == r) { k = kr[q]; v = vr[q]; }
+    const bool p = __double_as_longlong(v) != 0;
+    // group the lanes holding the same key (32-bit match on a folded key,
+    // verified; an exact broadcast loop covers the rare collision)
+    unsigned gm = __match_any_sync(0xffffffffu, (unsigned)(k ^ (k >> 32)));
+    const unsigned long long kl = __shfl_sync(0xffffffffu, k, __ffs(gm) - 1);
+    if (__any_sync(0xffffffffu, kl != k)) {
+      gm = 0;
+      for (int src = 0; src < 32; ++src)
+        if (__shfl_sync(0xffffffffu, k, src) == k) gm |= 1u << src;
+    }
+    const int gsize = __popc(gm);
+    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)gsize);
+    const bool lead = (__ffs(gm) - 1) == lane;
+    double acc = 0.0;
+    bool pres = false;
+    unsigned rem = gm;
+    for (int t = 0; t < maxg; ++t) {  // lane-ordered sum over the group
+      const int src = rem ? __ffs(rem) - 1 : lane;
+      rem &= rem - 1;
+      const double vs = __shfl_sync(0xffffffffu, v, src);
+      const int ps = __shfl_sync(0xffffffffu, (int)p, src);
+      if (t < gsize) {
+        acc += vs;
+        pres |= ps != 0;
+      }
+    }
+    if (lead && k != kSentinel) {
+      unsigned h = (unsigned)((k * 0x9E3779B97F4A7C15ull) >> 54) & (kWinTab - 1);
+      while (true) {
+        const unsigned long long prev = atomicCAS(&T.key[h], kSentinel, k);
+        if (prev == kSentinel) {
+          T.val[h] = acc;
+          T.pres[h] = pres;
+          break;
+        }
+        if (prev == k) {
+          T.val[h] += acc;
+          T.pres[h] |= pres;
+          break;
+        }
+        h = (h + 1) & (kWinTab - 1);
+      }
+    }
+    __syncwarp();
+  }
+  // emit the present keys of the table (slot order) into the window's region
+  int cnt = 0;
+  for (int i0 = 0; i0 < kWinTab; i0 += 32) {
+    const int i = i0 + lane;
+    const bool keep = T.key[i] != kSentinel && T.pres[i];
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+      const double sv = T.val[i];
+      okeys[base + pos] = T.key[i];
+      ovals[base + pos] = sv != 0.0 ? sv : -0.0;
+    }
+    cnt += __popc(m);
+  }
+  if (lane == 0) counts[w] = cnt;
+}
+
+__global__ void k_window_compact(const unsigned long long* __restrict__ keys, const double* __restrict__ vals,
+                                 const int* __restrict__ counts, const long long* __restrict__ offs,
+                                 unsigned long long* okeys, double* ovals) {
+  const long long w = blockIdx.x;
+  const int c = counts[w];
+  const long long src = w * kWin, dst = offs[w];
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    okeys[dst + i] = keys[src + i];
+    ovals[dst + i] = vals[src + i];
+  }
+}
+
 // Stable radix sort of the COO (row, col) keys, then one thread per run
 // sums its values in COO position order -> CSR rows of this batch.
 template <typename KT>
 nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64, double* vals, long long coo,
-                     long long nrows, Csr& piece, long long& nnz) {
+                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept) {
   int bits = 1;
   {
     const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
     while (bits < 64 && (1ull << bits) <= maxkey) ++bits;
+  }
+  // ---- window pre-reduction + compaction (deterministic)
+  DevBuf wk, wv, wc, wo;
+  if (coo > kWin) {
+    const long long nwin = (coo + kWin - 1) / kWin;
+    CK(wk.alloc(sizeof(unsigned long long) * nwin * kWin, s));
+    CK(wv.alloc(sizeof(double) * nwin * kWin, s));
+    CK(wc.alloc(sizeof(int) * nwin, s));
+    CK(wo.alloc(sizeof(long long) * (nwin + 1), s));
+    {
+      const int smem = kWinWarps * (int)sizeof(WinTable);
+      CK(cudaFuncSetAttribute(k_window_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_window_reduce<<<(unsigned)((nwin + kWinWarps - 1) / kWinWarps), 32 * kWinWarps, smem, s>>>(
+          keys64, vals, coo, wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>());
+      LAUNCHED();
+    }
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, wc.as<int>(), wo.as<long long>(), (int)nwin, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, wc.as<int>(), wo.as<long long>(), (int)nwin, s));
+    long long lo;
+    int lc;
+    CK(cudaMemcpyAsync(&lo, wo.as<long long>() + nwin - 1, sizeof lo, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lc, wc.as<int>() + nwin - 1, sizeof lc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const long long kept = lo + lc;
+    k_window_compact<<<(unsigned)nwin, 256, 0, s>>>(wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>(),
+                                                    wo.as<long long>(), keys64, vals);
+    LAUNCHED();
+    g_launches += 1;
+    coo = kept;
   }
   DevBuf k1, k2, v2;
   KT* keys;
@@ -1428,6 +1578,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, (int)coo, 0, bits, s));
     g_launches += (bits + 7) / 8 + 1;
   }
+  if (coo_kept) *coo_kept = coo;
   // the sentinel's low `bits` bits are all ones, above every valid key
   const KT* sk = dk.Current();
   const double* sv = dv.Current();
@@ -1721,8 +1872,10 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
   long long nnz = 0;
   const bool narrow = (unsigned long long)nrows * (unsigned long long)P.J < 0xffffffffull;
-  rc = narrow ? merge_csr<unsigned>(s, P, O.keys, O.vals, coo, nrows, piece, nnz)
-              : merge_csr<unsigned long long>(s, P, O.keys, O.vals, coo, nrows, piece, nnz);
+  long long kept = 0;
+  rc = narrow ? merge_csr<unsigned>(s, P, O.keys, O.vals, coo, nrows, piece, nnz, &kept)
+              : merge_csr<unsigned long long>(s, P, O.keys, O.vals, coo, nrows, piece, nnz, &kept);
+  st->coo_reduced += kept;
   if (rc) return rc;
   piece.nnz = nnz;
   out.push_back(piece);
