@@ -1404,49 +1404,54 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
 constexpr int kWin = 512;               // slots per warp window
 constexpr int kWinTab = 1024;           // hash slots (>= 2 kWin: never full)
 constexpr int kWinWarps = 4;
+template <typename KT>
 struct WinTable {
-  unsigned long long key[kWinTab];
+  KT key[kWinTab];
   double val[kWinTab];
   unsigned char pres[kWinTab];
 };
 
+// KT = u32 when every non-sentinel key of the batch fits in 32 bits
+template <typename KT>
 __global__ void __launch_bounds__(32 * kWinWarps) k_window_reduce(const unsigned long long* __restrict__ keys,
                                                                   const double* __restrict__ vals, long long n,
                                                                   unsigned long long* okeys, double* ovals,
                                                                   int* counts) {
   extern __shared__ __align__(16) unsigned char win_smem[];
-  WinTable& T = reinterpret_cast<WinTable*>(win_smem)[threadIdx.x >> 5];
+  WinTable<KT>& T = reinterpret_cast<WinTable<KT>*>(win_smem)[threadIdx.x >> 5];
+  const KT SENT = (KT)~(KT)0;
   const int lane = lane_id();
   const long long w = (long long)blockIdx.x * kWinWarps + (threadIdx.x >> 5);
   const long long base = w * kWin;
   if (base >= n) return;
-  constexpr int R = kWin / 32;
-  unsigned long long kr[R];
-  double vr[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {  // all loads in flight at once
+  for (int i = lane; i < kWinTab; i += 32) T.key[i] = SENT;
+  auto load = [&](int r, KT& k, double& v) {
     const long long g = base + r * 32 + lane;
-    kr[r] = g < n ? __ldcs(&keys[g]) : kSentinel;
-    vr[r] = g < n ? __ldcs(&vals[g]) : 0.0;
-  }
-  for (int i = lane; i < kWinTab; i += 32) T.key[i] = kSentinel;
+    const unsigned long long k64 = g < n ? __ldcs(&keys[g]) : kSentinel;
+    k = k64 == kSentinel ? SENT : (KT)k64;
+    v = g < n ? __ldcs(&vals[g]) : 0.0;
+  };
+  KT kn;
+  double vn;
+  load(0, kn, vn);
   __syncwarp();
 #pragma unroll 1
-  for (int r = 0; r < R; ++r) {
-    unsigned long long k = kr[0];
-    double v = vr[0];
-#pragma unroll
-    for (int q = 1; q < R; ++q)
-      if (q == r) { k = kr[q]; v = vr[q]; }
+  for (int r = 0; r < kWin / 32; ++r) {
+    const KT k = kn;
+    const double v = vn;
+    if (r + 1 < kWin / 32) load(r + 1, kn, vn);  // prefetch the next round
     const bool p = __double_as_longlong(v) != 0;
-    // group the lanes holding the same key (32-bit match on a folded key,
+    // group the lanes holding the same key (32-bit match on the folded key,
     // verified; an exact broadcast loop covers the rare collision)
-    unsigned gm = __match_any_sync(0xffffffffu, (unsigned)(k ^ (k >> 32)));
-    const unsigned long long kl = __shfl_sync(0xffffffffu, k, __ffs(gm) - 1);
-    if (__any_sync(0xffffffffu, kl != k)) {
-      gm = 0;
-      for (int src = 0; src < 32; ++src)
-        if (__shfl_sync(0xffffffffu, k, src) == k) gm |= 1u << src;
+    const unsigned fold = sizeof(KT) == 4 ? (unsigned)k : (unsigned)((unsigned long long)k ^ ((unsigned long long)k >> 32));
+    unsigned gm = __match_any_sync(0xffffffffu, fold);
+    if (sizeof(KT) > 4) {
+      const KT kl = __shfl_sync(0xffffffffu, k, __ffs(gm) - 1);
+      if (__any_sync(0xffffffffu, kl != k)) {
+        gm = 0;
+        for (int src = 0; src < 32; ++src)
+          if (__shfl_sync(0xffffffffu, k, src) == k) gm |= 1u << src;
+      }
     }
     const int gsize = __popc(gm);
     const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)gsize);
@@ -1464,11 +1469,11 @@ __global__ void __launch_bounds__(32 * kWinWarps) k_window_reduce(const unsigned
         pres |= ps != 0;
       }
     }
-    if (lead && k != kSentinel) {
-      unsigned h = (unsigned)((k * 0x9E3779B97F4A7C15ull) >> 54) & (kWinTab - 1);
+    if (lead && k != SENT) {
+      unsigned h = (unsigned)(((unsigned long long)k * 0x9E3779B97F4A7C15ull) >> 54) & (kWinTab - 1);
       while (true) {
-        const unsigned long long prev = atomicCAS(&T.key[h], kSentinel, k);
-        if (prev == kSentinel) {
+        const KT prev = atomicCAS(&T.key[h], SENT, k);
+        if (prev == SENT) {
           T.val[h] = acc;
           T.pres[h] = pres;
           break;
@@ -1487,12 +1492,12 @@ __global__ void __launch_bounds__(32 * kWinWarps) k_window_reduce(const unsigned
   int cnt = 0;
   for (int i0 = 0; i0 < kWinTab; i0 += 32) {
     const int i = i0 + lane;
-    const bool keep = T.key[i] != kSentinel && T.pres[i];
+    const bool keep = T.key[i] != SENT && T.pres[i];
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (keep) {
       const int pos = cnt + __popc(m & ((1u << lane) - 1u));
       const double sv = T.val[i];
-      okeys[base + pos] = T.key[i];
+      okeys[base + pos] = (unsigned long long)T.key[i];
       ovals[base + pos] = sv != 0.0 ? sv : -0.0;
     }
     cnt += __popc(m);
@@ -1531,10 +1536,18 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(wc.alloc(sizeof(int) * nwin, s));
     CK(wo.alloc(sizeof(long long) * (nwin + 1), s));
     {
-      const int smem = kWinWarps * (int)sizeof(WinTable);
-      CK(cudaFuncSetAttribute(k_window_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_window_reduce<<<(unsigned)((nwin + kWinWarps - 1) / kWinWarps), 32 * kWinWarps, smem, s>>>(
-          keys64, vals, coo, wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>());
+      const unsigned g = (unsigned)((nwin + kWinWarps - 1) / kWinWarps);
+      if (bits <= 32) {
+        const int smem = kWinWarps * (int)sizeof(WinTable<unsigned>);
+        CK(cudaFuncSetAttribute(k_window_reduce<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_window_reduce<unsigned><<<g, 32 * kWinWarps, smem, s>>>(keys64, vals, coo, wk.as<unsigned long long>(),
+                                                                 wv.as<double>(), wc.as<int>());
+      } else {
+        const int smem = kWinWarps * (int)sizeof(WinTable<unsigned long long>);
+        CK(cudaFuncSetAttribute(k_window_reduce<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_window_reduce<unsigned long long><<<g, 32 * kWinWarps, smem, s>>>(
+            keys64, vals, coo, wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>());
+      }
       LAUNCHED();
     }
     size_t tb = 0;
