@@ -567,7 +567,11 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       el = __ldg(&P.elem[pr.y & kIdMask]);
     }
   }
-  for (long long ch = w0; ch < nchunks; ch += nw) {
+  // block-uniform trip count: the block's warps run the phases in step (the
+  // __syncthreads below keep their instruction footprint to one phase)
+  const long long wib = threadIdx.x >> 5;
+  for (long long cb = w0 - wib; cb < nchunks; cb += nw) {
+    const long long ch = cb + wib;
     // ---------------- phase 1: clip one item per lane
     const long long v = ch * 2 + vs;
     const bool vok = v < O.nlist;
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       for (unsigned mm = mask; mm; mm &= mm - 1) S.queue[pos++] = (unsigned short)((lane << 4) | (__ffs(mm) - 1));
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    __syncwarp();
+    __syncthreads();
     // ---------------- phase 2: one queued sub-triangle per lane, 7 inner points
     for (int u0 = 0; u0 < ((P.dbg & 1) ? 0 : total); u0 += 32) {
       const int u = u0 + lane;
@@ -745,7 +749,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       }
       __syncwarp();
     }
-    __syncwarp();
+    __syncthreads();
     // ---------------- phase 3: fold into both visits, reduce over the record's lanes
     const int pmy = S.pm[lane];
     const bool ivalid = !(pmy & 0x80);
