@@ -221,9 +221,52 @@ constexpr int kEmitA = 1 << 30;
 constexpr int kEmitB = (int)(1u << 31);
 constexpr int kIdMask = (1 << 30) - 1;
 
+// Per-item truncation class of a clipped pair, with the reference's exact
+// predicates: every inner vertex inside the widened ball of every outer
+// point (the clip returns the triangle itself, _geom_scalar.py:53-66) or the
+// inner element's bounding disk beyond the ball by a margin no rounding can
+// bridge (the clip is empty).  Returns 2 if all 14 items are "inside", 1 if
+// all are empty, 0 otherwise.
+__device__ __forceinline__ int pair_trunc_class(const Params& P, const double* kx, const double* ky,
+                                                const double* xk, const double* yk, double2 ck, double rk,
+                                                const double* lx, const double* ly, double2 cl, double rl) {
+  const double rad = mul(P.delta, 1.0 + kBallTieRel);
+  const double r2 = mul(rad, rad);
+  const double far2k = (P.delta * (1.0 + 1e-6) + rk) * (P.delta * (1.0 + 1e-6) + rk);
+  const double far2l = (P.delta * (1.0 + 1e-6) + rl) * (P.delta * (1.0 + 1e-6) + rl);
+  double xl[7], yl[7];
+  {
+    const double e1x = lx[1] - lx[0], e2x = lx[2] - lx[0], e1y = ly[1] - ly[0], e2y = ly[2] - ly[0];
+#pragma unroll
+    for (int p = 0; p < 7; ++p) {
+      xl[p] = __dadd_rn(__dadd_rn(lx[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+      yl[p] = __dadd_rn(__dadd_rn(ly[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+    }
+  }
+  bool all_in = true, all_far = true;
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    // outer point on k, inner l / outer point on l, inner k
+    const double dkx = cl.x - xk[p], dky = cl.y - yk[p];
+    const double dlx = ck.x - xl[p], dly = ck.y - yl[p];
+    all_far = all_far && dkx * dkx + dky * dky > far2l && dlx * dlx + dly * dly > far2k;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      all_in = all_in && __dsub_rn(sumsq(lx[i] - xk[p], ly[i] - yk[p]), r2) <= 0.0 &&
+               __dsub_rn(sumsq(kx[i] - xl[p], ky[i] - yl[p]), r2) <= 0.0;
+    }
+  }
+  return P.ball == 2 ? 0 : (all_in ? 2 : (all_far ? 1 : 0));
+}
+
 //  -1 none here, 0 full record, 1 clipped record, 2/3/4 singular id/edge/vertex.
 // *visited: the reference would count the visit (k, l) (EPI); *flags: record sides.
+// Clipped pairs whose every sweep item is untruncated take the full path (same
+// arithmetic: the fan of the untruncated triangle is the triangle); pairs
+// whose every item is empty contribute nothing and produce no record.
+template <bool LIGHT>
 __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2 ck, double rk,
+                                        const double* kx, const double* ky, const double* xk, const double* yk,
                                         bool needAk, const unsigned char* __restrict__ needA,
                                         const int* __restrict__ inR, int l, bool& visited, int& flags) {
   visited = false;
@@ -242,26 +285,46 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     if (!(needAk || needA[l])) return -1;
     return k == l ? 2 : (ns == 2 ? 3 : 4);
   }
+  if (LIGHT) return (needAk || ((el.w & 16) && needA[l])) ? 0 : -1;  // upper bound for the count pass
   const bool full = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
+  bool full_lk = full, rej_lk = false;
+  if (k != l && (el.w & 16)) {  // root l's view of the same pair
+    rej_lk = !touching && __dsub_rn(__dsub_rn(dist, rl), rk) > P.prer;
+    full_lk = __dadd_rn(__dadd_rn(dist, rl), rk) <= P.delta;
+  }
+  // exact truncation class of the pair (symmetric in k, l)
+  int tcls = 0;
+  if (k != l && (!full || !full_lk)) {
+    double lx[3], ly[3];
+    const double2 a = __ldg(&P.vtx[el.x]), b = __ldg(&P.vtx[el.y]), c = __ldg(&P.vtx[el.z]);
+    lx[0] = a.x; ly[0] = a.y; lx[1] = b.x; ly[1] = b.y; lx[2] = c.x; ly[2] = c.y;
+    tcls = pair_trunc_class(P, kx, ky, xk, yk, ck, rk, lx, ly, cl, rl);
+  }
+  const int cat_kl = full || tcls == 2 ? 0 : 1;
+  if (tcls == 1) return -1;  // every item empty in both visits: nothing to emit
   bool shared = false;
-  if (k != l && (el.w & 16)) {  // does root l visit k with the same category?
-    const bool rej_lk = !touching && __dsub_rn(__dsub_rn(dist, rl), rk) > P.prer;
-    const bool full_lk = __dadd_rn(__dadd_rn(dist, rl), rk) <= P.delta;
-    shared = !rej_lk && full_lk == full;
+  if (k != l && (el.w & 16)) {
+    const int cat_lk = full_lk || tcls == 2 ? 0 : 1;
+    shared = !rej_lk && cat_lk == cat_kl;
   }
   if (shared && inR[l] >= 0 && l < k) return -1;  // root l produces the record
   const bool emitB = shared && needA[l];
   if (!needAk && !emitB) return -1;
   flags = (needAk ? kEmitA : 0) | (emitB ? kEmitB : 0);
-  return full ? 0 : 1;
+  return cat_kl;
 }
+
+// count pass (FILL = false): exact singular counts, an upper bound of the
+// non-singular records per root (column C_FULL) and the EPI; fill pass:
+// records into the root's upper-bound range of `comb` (k | clipped << 30),
+// singular pairs into their lists, and the actual full / clipped counts.
+constexpr int kCatClip = 1 << 30;
 
 template <bool FILL>
 __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
                              const unsigned char* __restrict__ needA, const int* __restrict__ inR,
-                             int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ lf,
-                             int2* __restrict__ lp, int2* __restrict__ ls0, int2* __restrict__ ls1,
-                             int2* __restrict__ ls2) {
+                             int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ comb,
+                             int2* __restrict__ ls0, int2* __restrict__ ls1, int2* __restrict__ ls2) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
@@ -272,14 +335,22 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
     const double2 ck = P.ctr[k];
     const double rk = P.rad[k];
     const bool needAk = needA[k];
+    double kx[3], ky[3], xk[7], yk[7];
+    if (FILL) {
+      load_tri(P, k, kx, ky);
+      rule_points(P, kx, ky, xk, yk);
+    }
     int ix = (int)floor((ck.x - G.ox) / G.cs), iy = (int)floor((ck.y - G.oy) / G.cs);
     ix = min(max(ix, 0), G.nx - 1);
     iy = min(max(iy, 0), G.ny - 1);
     int c[7] = {0, 0, 0, 0, 0, 0, 0};
-    long long base[5];
-    int2* lists[5] = {lf, lp, ls0, ls1, ls2};
-    if (FILL)
-      for (int j = 0; j < 5; ++j) base[j] = off[(long long)j * (nR + 1) + i];
+    long long base[4];
+    int2* lists[4] = {comb, ls0, ls1, ls2};
+    if (FILL) {
+      base[0] = off[(long long)C_FULL * (nR + 1) + i];
+      for (int j = 1; j < 4; ++j) base[j] = off[(long long)(C_SID + j - 1) * (nR + 1) + i];
+    }
+    int nfull = 0, nclip = 0;
     for (int yy = max(iy - 1, 0); yy <= min(iy + 1, G.ny - 1); ++yy) {
       const int c0 = G.start[yy * G.nx + max(ix - 1, 0)];
       const int c1 = G.start[yy * G.nx + min(ix + 1, G.nx - 1) + 1];
@@ -288,15 +359,20 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
         int cat = -1, fl = 0;
         bool vis = false;
         const int l = j < c1 ? G.items[j] : 0;
-        if (j < c1) cat = classify(P, k, ek, ck, rk, needAk, needA, inR, l, vis, fl);
         if (!FILL) {
+          if (j < c1) cat = classify<true>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, vis, fl);
           c[C_EPI] += vis;
-          if (cat >= 0) c[cat]++;
+          if (cat >= 0) c[cat == 0 ? C_FULL : cat]++;
         } else {
+          if (j < c1) cat = classify<false>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, vis, fl);
+          nfull += cat == 0;
+          nclip += cat == 1;
+          // lists: 0 = combined (full or clipped), 1..3 = singular families
+          const int q0 = cat < 0 ? -1 : (cat <= 1 ? 0 : cat - 1);
 #pragma unroll
-          for (int q = 0; q < 5; ++q) {
-            const unsigned m = __ballot_sync(0xffffffffu, cat == q);
-            if (cat == q) lists[q][base[q] + __popc(m & lt)] = make_int2(k, l | fl);
+          for (int q = 0; q < 4; ++q) {
+            const unsigned m = __ballot_sync(0xffffffffu, q0 == q);
+            if (q0 == q) lists[q][base[q] + __popc(m & lt)] = make_int2(k | (cat == 1 ? kCatClip : 0), l | fl);
             base[q] += __popc(m);
           }
         }
@@ -316,9 +392,25 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
         const long long rmin = (long long)P.nc * min(d.x, min(d.y, d.z));
         cnt[(long long)C_KK * nR + i] = needAk ? ((rmin >= P.row_lo && rmin < P.row_hi) ? 2 : 1) : 0;
       }
+    } else {
+      for (int o = 16; o; o >>= 1) {
+        nfull += __shfl_xor_sync(0xffffffffu, nfull, o);
+        nclip += __shfl_xor_sync(0xffffffffu, nclip, o);
+      }
+      if (lane == 0) {
+        cnt[(long long)C_FULL * nR + i] = nfull;
+        cnt[(long long)C_PART * nR + i] = nclip;
+      }
     }
   }
 }
+
+struct IsRecord {
+  int want;  // 0 full, 1 clipped
+  __host__ __device__ bool operator()(const int2& r) const {
+    return r.x != -1 && ((r.x & kCatClip) ? 1 : 0) == want;
+  }
+};
 
 __global__ void k_rank(const int* __restrict__ roots, int nR, int* inR) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -563,6 +655,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     const long long v0 = w0 * 2 + vs;
     if (v0 < O.nlist) {
       pr = list[v0];
+      pr.x &= kIdMask;
       ek = __ldg(&P.elem[pr.x]);
       el = __ldg(&P.elem[pr.y & kIdMask]);
     }
@@ -588,7 +681,10 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     const long long vn = (ch + nw) * 2 + vs;
     const bool next_ok = vn < O.nlist;
     int2 prn = make_int2(0, 0);
-    if (next_ok) prn = list[vn];
+    if (next_ok) {
+      prn = list[vn];
+      prn.x &= kIdMask;
+    }
     if (r == 0 && vok) {
       const int4 dk4 = __ldg(&P.dofs[k]), dl4 = __ldg(&P.dofs[l]);
       S.vk[vs] = k;
@@ -1239,25 +1335,53 @@ struct nlg_plan {
   int* act = nullptr;
   int nact = -1;
   int nbase = 0;
+  // scratch arena: one allocation reused by every assembly (grown to the
+  // observed peak), so steady-state calls never go to the allocator
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0, arena_peak = 0;
 };
 
 namespace {
 
-struct DevBuf {  // stream-ordered scratch
+thread_local nlg_plan* g_arena_plan = nullptr;  // plan whose arena backs DevBuf
+
+struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-ordered
   void* p = nullptr;
   cudaStream_t s = nullptr;
+  bool arena = false;
   cudaError_t alloc(size_t n, cudaStream_t st) {
     s = st;
-    return cudaMallocAsync(&p, std::max<size_t>(n, 16), st);
+    n = (std::max<size_t>(n, 16) + 255) & ~(size_t)255;
+    if (nlg_plan* pl = g_arena_plan) {
+      pl->arena_peak = std::max(pl->arena_peak, pl->arena_used + n);
+      if (pl->arena && pl->arena_used + n <= pl->arena_cap) {
+        p = pl->arena + pl->arena_used;
+        pl->arena_used += n;
+        arena = true;
+        return cudaSuccess;
+      }
+    }
+    return cudaMallocAsync(&p, n, st);
   }
   ~DevBuf() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !arena) cudaFreeAsync(p, s);
   }
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
+// arena allocations made inside a scope are released when it ends (LIFO)
+struct ArenaScope {
+  nlg_plan* pl;
+  size_t mark;
+  explicit ArenaScope(nlg_plan* p) : pl(p), mark(p ? p->arena_used : 0) {}
+  ~ArenaScope() {
+    if (pl) pl->arena_used = mark;
+  }
+};
+
 nlg_status prep(nlg_plan* pl) {
   if (pl->prepped) return NLG_OK;
+  ArenaScope arena_scope(g_arena_plan);
   Params& P = pl->P;
   cudaStream_t st = pl->stream;
   const int K = P.K;
@@ -1678,6 +1802,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
                      std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
                      unsigned long long* d_counters, unsigned long long* d_err, bool* need_split) {
   *need_split = false;
+  ArenaScope arena_scope(pl);
   Params P = pl->P;
   P.row_lo = row_lo;
   P.row_hi = row_hi;
@@ -1739,7 +1864,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   if (nR) {
     k_candidates<false><<<std::max(cand_blocks, 1), 256, 0, s>>>(
         P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), inR.as<int>(), cnt.as<int>(), nullptr,
-        nullptr, nullptr, nullptr, nullptr, nullptr);
+        nullptr, nullptr, nullptr, nullptr);
     LAUNCHED();
   }
   {
@@ -1774,23 +1899,23 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
                          cudaMemcpyHostToDevice, s));
     }
   }
-  const long long nF = tot[C_FULL], nPt = tot[C_PART];
+  const long long nUB = tot[C_FULL];  // upper bound of full + clipped records
   const long long nS[3] = {tot[C_SID], tot[C_SED], tot[C_SVX]};
   const int NC = P.nc;
   const long long E = 9LL * NC * NC;
-  const long long nvis = nF + nPt;
-  const long long coo = (long long)nR * E + nvis * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
-  // bytes: keys+vals twice (sort double buffer) + kk scratch + lists + reverse index + merge arrays
-  const long long bytes = coo * 16 * 2 + nvis * 2 * (E * 8 + 8) + (nvis + nS[0] + nS[1] + nS[2]) * 8 +
-                          nvis * 16 + coo * 8 * 3;
-  if (budget > 0 && bytes > budget && row_hi - row_lo > 1) {
-    *need_split = true;
-    return NLG_OK;
-  }
-  if (coo >= (1LL << 31)) {
-    if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
-    set_err("a single row needs %lld COO slots", coo);
-    return NLG_ERR_CUDA;
+  {
+    const long long coo_ub = (long long)nR * E + nUB * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
+    const long long bytes = coo_ub * 16 * 2 + nUB * 2 * (E * 8 + 8) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
+                            nUB * 16 + coo_ub * 8 * 3;
+    if (budget > 0 && bytes > budget && row_hi - row_lo > 1) {
+      *need_split = true;
+      return NLG_OK;
+    }
+    if (coo_ub >= (1LL << 31)) {
+      if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
+      set_err("a single row needs %lld COO slots", coo_ub);
+      return NLG_ERR_CUDA;
+    }
   }
   // EPI of the roots whose home is this batch: sum cnt[EPI] where cnt[KK] == 2
   {
@@ -1803,18 +1928,52 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     for (int i = 0; i < nR; ++i)
       if (hc[nR + i] == 2) { st->epi += hc[i]; st->n_roots += 1; }
   }
-  // ---- candidate lists
-  DevBuf lists;
-  CK(lists.alloc(sizeof(int2) * (size_t)std::max(1LL, nvis + nS[0] + nS[1] + nS[2]), s));
-  int2* lf = lists.as<int2>();
-  int2* lp = lf + nF;
-  int2* ls[3] = {lp + nPt, lp + nPt + nS[0], lp + nPt + nS[0] + nS[1]};
+  // ---- fill: records into per-root upper-bound ranges, then stable compaction
+  DevBuf comb, lists, nsel;
+  CK(comb.alloc(sizeof(int2) * (size_t)std::max(1LL, nUB), s));
+  CK(cudaMemsetAsync(comb.p, 0xff, sizeof(int2) * (size_t)std::max(1LL, nUB), s));
+  CK(lists.alloc(sizeof(int2) * (size_t)std::max(1LL, nUB + nS[0] + nS[1] + nS[2]), s));
+  CK(nsel.alloc(sizeof(long long) * 2, s));
+  int2* lsing = lists.as<int2>() + nUB;
+  int2* ls[3] = {lsing, lsing + nS[0], lsing + nS[0] + nS[1]};
   if (nR) {
     k_candidates<true><<<std::max(cand_blocks, 1), 256, 0, s>>>(
         P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), inR.as<int>(), cnt.as<int>(),
-        off.as<long long>(), lf, lp, ls[0], ls[1], ls[2]);
+        off.as<long long>(), comb.as<int2>(), ls[0], ls[1], ls[2]);
     LAUNCHED();
   }
+  long long nsel_h[2] = {0, 0};
+  if (nUB) {
+    size_t tb = 0, tb2 = 0;
+    CK(cub::DeviceSelect::If(nullptr, tb, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>(), nUB, IsRecord{0}, s));
+    CK(cub::DeviceSelect::If(nullptr, tb2, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>() + 1, nUB, IsRecord{1}, s));
+    DevBuf tmp;
+    CK(tmp.alloc(std::max(tb, tb2), s));
+    CK(cub::DeviceSelect::If(tmp.p, tb, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>(), nUB, IsRecord{0}, s));
+    CK(cudaMemcpyAsync(nsel_h, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cub::DeviceSelect::If(tmp.p, tb2, comb.as<int2>(), lists.as<int2>() + nsel_h[0], nsel.as<long long>() + 1, nUB,
+                             IsRecord{1}, s));
+    CK(cudaMemcpyAsync(nsel_h + 1, nsel.as<long long>() + 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    g_launches += 4;
+  }
+  const long long nF = nsel_h[0], nPt = nsel_h[1];
+  int2* lf = lists.as<int2>();
+  int2* lp = lf + nF;
+  // actual per-root full / clipped counts -> offsets for the own-block reduction
+  if (nR) {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int>(), off.as<long long>(), nR, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    for (int q : {C_FULL, C_PART})
+      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
+                                       off.as<long long>() + (size_t)q * (nR + 1), nR, s));
+    g_launches += 2;
+  }
+  const long long nvis = nF + nPt;
+  const long long coo = (long long)nR * E + nvis * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
   // reverse index of side-B records by partner root (stable: record order)
   DevBuf rkey, rkey2, ritem0, ritem, rstart;
   CK(rkey.alloc(sizeof(unsigned) * std::max(nvis, 1LL), s));
@@ -2089,6 +2248,7 @@ void nlg_plan_destroy(nlg_plan* pl) {
     for (double* p : f)
       if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
+  if (pl->arena) cudaFree(pl->arena);
   delete pl;
 }
 
@@ -2098,6 +2258,20 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   if (row_lo < 0 || row_hi > pl->P.J || row_lo > row_hi) { set_err("row range out of bounds"); return NLG_ERR_CONFIG; }
   CK(cudaSetDevice(pl->device));
   cudaStream_t s = pl->stream;
+  // grow the scratch arena to the peak the previous call needed
+  if (pl->arena_peak > pl->arena_cap) {
+    if (pl->arena) cudaFree(pl->arena);
+    pl->arena = nullptr;
+    pl->arena_cap = 0;
+    size_t cap = pl->arena_peak + pl->arena_peak / 8;
+    if (cudaMalloc((void**)&pl->arena, cap) == cudaSuccess) pl->arena_cap = cap;
+    else cudaGetLastError();
+  }
+  pl->arena_used = 0;
+  struct ArenaActivate {
+    ArenaActivate(nlg_plan* p) { g_arena_plan = p; }
+    ~ArenaActivate() { g_arena_plan = nullptr; }
+  } arena_on(pl);
   nlg_stats st;
   memset(&st, 0, sizeof st);
   st.err_k = st.err_l = -1;
