@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -47,48 +46,56 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled (in-process NVML) during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    HW, HW_THERM, SW_THERM, SW_POWER = 0x8, 0x40, 0x20, 0x4  # nvmlClocksEventReason* bits
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period=float(os.environ.get("NLG_CLOCK_PERIOD", "0.25"))):
         self.index = index
+        self.period = period
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self._h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+            self.max_mhz = None
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                sm = self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+                rs = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((sm, rs))
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].strip() == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        names = {self.HW: "hw_slowdown", self.HW_THERM: "hw_thermal_slowdown",
+                 self.SW_THERM: "sw_thermal_slowdown", self.SW_POWER: "sw_power_cap"}
+        reasons = sorted({n for _, rs in self.rows for bit, n in names.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, in-process"}
 
 
 def dist_env():
@@ -151,7 +158,7 @@ def run_reference(args, cfg, ws, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -191,7 +198,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        plan.assemble(lo, hi, out_on_host=False)
+        plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
     barrier()
     launches0 = _native.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -201,7 +208,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))  # evict L2 between steps (outside the timed pair)
             ev[i][0].record()
-            _, _, _, st = plan.assemble(lo, hi, out_on_host=False)
+            _, _, _, st = plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
             ev[i][1].record()
             stats.append(st)
         barrier()
@@ -284,6 +291,7 @@ def main():
                        "l2": "flushed between steps (512 MB write)", "inputs": "mesh arrays resident in HBM",
                        "output": "CSR resident in HBM"},
             "assembly_ms": ms_per_step,
+            "step_ms": [round(x, 3) for x in ms_steps],
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -128,23 +128,34 @@ def fp64_peak_tflops(device=0):
 
 
 class OutputSink:
-    """Allocation callback target: numpy buffers (host) or torch tensors (device)."""
+    """Allocation callback target: numpy buffers (host) or torch tensors (device).
 
-    def __init__(self, on_host, device=0):
+    ``reuse`` keeps the buffers of earlier calls and hands them out again when
+    they are large enough (device outputs of repeated assemblies).
+    """
+
+    def __init__(self, on_host, device=0, reuse=None):
         self.on_host = on_host
         self.device = device
         self.bufs = {}
+        self._pool = reuse if reuse is not None else {}
         self._cb = ALLOC_FN(self._alloc)
 
     def _alloc(self, user, nbytes, which):
         try:
+            n = max(int(nbytes), 8)
+            old = self._pool.get(which)
+            if old is not None and old.numel() >= n and not self.on_host:
+                self.bufs[which] = old
+                return old.data_ptr()
             if self.on_host:
-                buf = np.empty(max(int(nbytes), 8), dtype=np.uint8)
+                buf = np.empty(n, dtype=np.uint8)
                 self.bufs[which] = buf
                 return buf.ctypes.data
             import torch
-            buf = torch.empty(max(int(nbytes), 8), dtype=torch.uint8, device=f"cuda:{self.device}")
+            buf = torch.empty((n + n // 8 + 15) // 16 * 16, dtype=torch.uint8, device=f"cuda:{self.device}")
             self.bufs[which] = buf
+            self._pool[which] = buf
             return buf.data_ptr()
         except Exception:  # noqa: BLE001 -- returning NULL makes the library fail cleanly
             return None

@@ -144,6 +144,7 @@ class DevicePlan:
         _native.check(self.lib.nlg_plan_create(device, ctypes.byref(pb), s, ctypes.byref(handle)),
                       "nlg_plan_create")
         self.handle = handle
+        self._out_pool = {}  # device output buffers reused across assemble() calls
 
     def close(self):
         if getattr(self, "handle", None):
@@ -153,11 +154,16 @@ class DevicePlan:
     def __del__(self):
         self.close()
 
-    def assemble(self, row_lo=0, row_hi=None, out_on_host=True, mem_budget=0):
-        """CSR rows [row_lo, row_hi): (indptr int64, indices int32, data f64, stats dict)."""
+    def assemble(self, row_lo=0, row_hi=None, out_on_host=True, mem_budget=0, reuse_output=False):
+        """CSR rows [row_lo, row_hi): (indptr int64, indices int32, data f64, stats dict).
+
+        ``reuse_output`` (device outputs only) recycles the previous call's
+        buffers: the returned tensors are then overwritten by the next call.
+        """
         J = self.inp.n_dofs
         row_hi = J if row_hi is None else row_hi
-        sink = _native.OutputSink(out_on_host, self.device)
+        sink = _native.OutputSink(out_on_host, self.device,
+                                  reuse=self._out_pool if reuse_output and not out_on_host else None)
         st = _native.Stats()
         rc = self.lib.nlg_assemble(self.handle, int(row_lo), int(row_hi), 1 if out_on_host else 0,
                                    sink.callback, None, int(mem_budget), ctypes.byref(st))

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -37,6 +38,14 @@ using namespace nlg;
 namespace {
 
 thread_local std::string g_err;
+const bool g_trace = getenv("NLG_TRACE") != nullptr;
+double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#define TRACE(tag)                                                                  \
+  do {                                                                              \
+    if (g_trace) fprintf(stderr, "[nlg %10.3f] %s\n", host_ms(), tag);             \
+  } while (0)
 std::atomic<long long> g_launches{0};
 
 void set_err(const char* fmt, ...) {
@@ -1096,7 +1105,14 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
     int mk[U], ml[U];
 #pragma unroll
     for (int m = 0; m < U; ++m) { mk[m] = sMk[m]; ml[m] = sMl[m]; }
-    for (int i = threadIdx.x; i < R.n; i += blockDim.x) {
+    // identical pair, symmetric kernel: each sub-rule's mirrored half (x <-> y,
+    // quadrature.py:197-207) repeats its first half exactly (d -> -d, tm -> -tm),
+    // so only the first halves are evaluated and the weights doubled
+    constexpr bool HALF = FAM == 0 && T::SYM;
+    const int m4 = R.n / 6;  // points per half sector (identical family: 6 blocks)
+    const int npts_eval = HALF ? R.n / 2 : R.n;
+    for (int ii0 = threadIdx.x; ii0 < npts_eval; ii0 += blockDim.x) {
+      const int i = HALF ? (ii0 / m4) * 2 * m4 + (ii0 % m4) : ii0;
       const double xs0 = __ldg(&R.xs[2 * i]), xs1 = __ldg(&R.xs[2 * i + 1]);
       const double ys0 = __ldg(&R.ys[2 * i]), ys1 = __ldg(&R.ys[2 * i + 1]);
       const double x0 = __dadd_rn(__dadd_rn(t0x, mul(e1kx, xs0)), mul(e2kx, xs1));
@@ -1108,7 +1124,7 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
       if (r2 <= 0.0) continue;
       double pv[NC * NC], qv[NC * NC];
       kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
-      ++npts;
+      npts += HALF ? 2 : 1;
       double phx[U], phy[U], tm[U];
 #pragma unroll
       for (int m = 0; m < U; ++m) {
@@ -1116,25 +1132,39 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
         phy[m] = ml[m] >= 0 ? __ldg(&R.hy[3 * i + ml[m]]) : 0.0;
         tm[m] = phx[m] - phy[m];
       }
-      const double wi = __ldg(&R.w[i]);
+      const double wi = HALF ? 2.0 * __ldg(&R.w[i]) : __ldg(&R.w[i]);
+      if (T::SYM) {
+        // Bu[(m,c),(m',d)] += w tm_m tm_m' P_cd  as  g[m][cd] = w P_cd tm_m, then g tm_m'
+        double g[U][NC * NC];
 #pragma unroll
-      for (int m = 0; m < U; ++m)
+        for (int m = 0; m < U; ++m)
 #pragma unroll
-        for (int mp = 0; mp < U; ++mp) {
-          if (T::SYM && mp < m) continue;
-          const double cf = wi * (tm[m] * tm[mp]);
+          for (int cd = 0; cd < NC * NC; ++cd) g[m][cd] = (wi * pv[cd]) * tm[m];
 #pragma unroll
-          for (int c = 0; c < NC; ++c)
+        for (int m = 0; m < U; ++m)
 #pragma unroll
-            for (int d = 0; d < NC; ++d) {
-              const int ii = m * NC + c, jj = mp * NC + d;
-              if (T::SYM && m == mp && jj < ii) continue;
-              if (T::SYM)
-                acc[A::idx(ii, jj)] = fma(cf, pv[c * NC + d], acc[A::idx(ii, jj)]);
-              else
+          for (int mp = m; mp < U; ++mp)
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+              for (int d = 0; d < NC; ++d) {
+                const int ii = m * NC + c, jj = mp * NC + d;
+                if (m == mp && jj < ii) continue;
+                acc[A::idx(ii, jj)] = fma(g[m][c * NC + d], tm[mp], acc[A::idx(ii, jj)]);
+              }
+      } else {
+#pragma unroll
+        for (int m = 0; m < U; ++m)
+#pragma unroll
+          for (int mp = 0; mp < U; ++mp)
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+              for (int d = 0; d < NC; ++d) {
+                const int ii = m * NC + c, jj = mp * NC + d;
                 acc[A::idx(ii, jj)] += (wi * tm[m]) * (pv[c * NC + d] * phx[mp] - qv[c * NC + d] * phy[mp]);
-            }
-        }
+              }
+      }
     }
     // deterministic block reduction
 #pragma unroll
@@ -1688,6 +1718,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(cudaMemcpyAsync(&lo, wo.as<long long>() + nwin - 1, sizeof lo, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&lc, wc.as<int>() + nwin - 1, sizeof lc, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    TRACE("sync 1720");
     const long long kept = lo + lc;
     k_window_compact<<<(unsigned)nwin, 256, 0, s>>>(wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>(),
                                                     wo.as<long long>(), keys64, vals);
@@ -1743,6 +1774,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(cudaMemcpyAsync(&lsid, sid.as<long long>() + coo - 1, sizeof lsid, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&lhead, head.as<int>() + coo - 1, sizeof lhead, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    TRACE("sync 1775");
     nseg = lsid + lhead;
   }
   CK(start.alloc(sizeof(long long) * (nseg + 1), s));
@@ -1771,6 +1803,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(cudaMemcpyAsync(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&lpres, present.as<int>() + nseg - 1, sizeof lpres, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    TRACE("sync 1803");
     nnz = lpos + lpres;
     CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
     CK(cudaMallocAsync(&piece.data, sizeof(double) * std::max(nnz, 1LL), s));
@@ -1849,6 +1882,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   int nR = 0;
   CK(cudaMemcpyAsync(&nR, nroots.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  TRACE("sync 1881");
   DevBuf inR;  // element -> rank in the batch's root list, -1 if not a root
   CK(inR.alloc(sizeof(int) * K, s));
   CK(cudaMemsetAsync(inR.p, 0xff, sizeof(int) * K, s));
@@ -1893,6 +1927,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
                          cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s));
+    TRACE("sync 1925");
     for (int q = 0; q < 6; ++q) {
       tot[q] = lastoff[q] + lastcnt[q];
       CK(cudaMemcpyAsync(off.as<long long>() + (size_t)q * (nR + 1) + nR, &tot[q], sizeof(long long),
@@ -1924,6 +1959,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       CK(cudaMemcpyAsync(hc.data(), cnt.as<int>() + (size_t)C_EPI * nR, sizeof(int) * nR, cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(hc.data() + nR, cnt.as<int>() + (size_t)C_KK * nR, sizeof(int) * nR, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      TRACE("sync 1956");
     }
     for (int i = 0; i < nR; ++i)
       if (hc[nR + i] == 2) { st->epi += hc[i]; st->n_roots += 1; }
@@ -1952,10 +1988,12 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     CK(cub::DeviceSelect::If(tmp.p, tb, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>(), nUB, IsRecord{0}, s));
     CK(cudaMemcpyAsync(nsel_h, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    TRACE("sync 1984");
     CK(cub::DeviceSelect::If(tmp.p, tb2, comb.as<int2>(), lists.as<int2>() + nsel_h[0], nsel.as<long long>() + 1, nUB,
                              IsRecord{1}, s));
     CK(cudaMemcpyAsync(nsel_h + 1, nsel.as<long long>() + 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    TRACE("sync 1988");
     g_launches += 4;
   }
   const long long nF = nsel_h[0], nPt = nsel_h[1];
@@ -2057,6 +2095,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   out.push_back(piece);
   CK(cudaEventRecord(ev[5], s));
   CK(cudaStreamSynchronize(s));
+  TRACE("sync 2089");
   float ms;
   CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); tm.cand += ms;
   CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); tm.full += ms;
@@ -2275,9 +2314,13 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   nlg_stats st;
   memset(&st, 0, sizeof st);
   st.err_k = st.err_l = -1;
+  TRACE("assemble begin");
   if (budget <= 0) {
-    size_t fr = 0, totm = 0;
-    CK(cudaMemGetInfo(&fr, &totm));
+    static thread_local size_t totm = 0;
+    if (!totm) {
+      size_t fr = 0;
+      CK(cudaMemGetInfo(&fr, &totm));
+    }
     budget = (long long)(0.6 * (double)totm);
   }
   cudaEvent_t e0, e1, e2;
@@ -2286,7 +2329,9 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   CK(cudaEventCreate(&e2));
   CK(cudaEventRecord(e0, s));
   pl->prepped = false;  // bounds and grid are part of every assembly
+  TRACE("prep");
   nlg_status rc = prep(pl);
+  TRACE("prep done");
   if (rc) return rc;
   CK(cudaEventRecord(e1, s));
   DevBuf dctr, derr;
@@ -2317,6 +2362,7 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
     return rc;
   }
+  TRACE("batches done");
   // pieces are produced in ascending row order (ranges are popped low-first)
   long long nnz = 0;
   for (auto& p : pieces) nnz += p.nnz;
@@ -2345,10 +2391,12 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   if (nrows == 0) CK(cudaMemsetAsync(ptrbuf.p, 0, sizeof(long long), s));
   CK(cudaMemcpyAsync(o_ptr, ptrbuf.p, sizeof(long long) * (nrows + 1), cudaMemcpyDefault, s));
   CK(cudaEventRecord(e2, s));
+  TRACE("outputs queued");
   unsigned long long hc[K_NCOUNTERS], herr;
   CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&herr, derr.p, sizeof herr, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  TRACE("sync 2389");
   for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -2405,6 +2453,7 @@ static nlg_status ensure_active(nlg_plan* pl) {
   int h = 0;
   CK(cudaMemcpyAsync(&h, n.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  TRACE("sync 2445");
   pl->nact = h;
   pl->nbase = (int)(pl->P.J / pl->P.nc);
   return NLG_OK;
@@ -2432,6 +2481,7 @@ nlg_status nlg_load_points(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc
   }
   if (out_on_host && np) CK(cudaMemcpyAsync(out, dst, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  TRACE("sync 2472");
   (void)out_on_host;
   return NLG_OK;
 }
@@ -2493,6 +2543,7 @@ static nlg_status load_impl(nlg_plan* pl, const double* fx, int fx_on_device, in
   LAUNCHED();
   if (out_on_host) CK(cudaMemcpyAsync(out, dst, sizeof(double) * J, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  TRACE("sync 2533");
   return NLG_OK;
 }
 
