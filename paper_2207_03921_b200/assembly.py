@@ -162,8 +162,14 @@ class DevicePlan:
         """
         J = self.inp.n_dofs
         row_hi = J if row_hi is None else row_hi
-        sink = _native.OutputSink(out_on_host, self.device,
-                                  reuse=self._out_pool if reuse_output and not out_on_host else None)
+        if reuse_output and not out_on_host:
+            # one persistent sink (and ctypes callback) recycling its device buffers
+            if getattr(self, "_sink", None) is None:
+                self._sink = _native.OutputSink(False, self.device, reuse=self._out_pool)
+            sink = self._sink
+            sink.bufs = {}
+        else:
+            sink = _native.OutputSink(out_on_host, self.device)
         st = _native.Stats()
         rc = self.lib.nlg_assemble(self.handle, int(row_lo), int(row_hi), 1 if out_on_host else 0,
                                    sink.callback, None, int(mem_budget), ctypes.byref(st))

@@ -89,6 +89,7 @@ enum {
   K_EVAL_M0, K_EVAL_M1, K_EVAL_M2,
   K_OUT_M0, K_OUT_M1, K_OUT_M2,
   K_SPTS3, K_SPTS4, K_SPTS5, K_SPTS6,
+  K_DBG_SUBTRI, K_DBG_ROUNDS, K_DBG_CHUNKS,
   K_NCOUNTERS
 };
 
@@ -104,6 +105,7 @@ __host__ __device__ inline double ord2d(unsigned long long o) {
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__constant__ int g_trace_dev;  // NLG_TRACE: device-side debug counters
 
 // ---------------------------------------------------------------- prep
 __global__ void k_convert(const double* __restrict__ vin, const long long* __restrict__ ein,
@@ -445,6 +447,14 @@ __device__ __forceinline__ unsigned long long coo_key(const Params& P, long long
 // entry is stored as +0.0, a present one that is exactly zero as -0.0
 __device__ __forceinline__ double emit_val(double v) { return v != 0.0 ? v : 0.0; }
 
+// inf/nan <=> all exponent bits set; checked with integer ops, reported once
+__device__ __forceinline__ bool nonfinite(double v) {
+  return ((unsigned long long)__double_as_longlong(v) & 0x7ff0000000000000ull) == 0x7ff0000000000000ull;
+}
+__device__ __forceinline__ void report_nonfinite(bool bad, int k, int l, int K, unsigned long long* errpair) {
+  if (bad) atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
+}
+
 __device__ __forceinline__ void note_nonfinite(double v, int k, int l, int K,
                                                unsigned long long* errpair) {
   if (!isfinite(v)) atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
@@ -472,27 +482,24 @@ struct VisitOut {
 // emit one side of a record: own block -> scratch, neighbour block -> COO
 template <int NC>
 __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long v, int side, bool on,
-                                          int root, int nb, const double* kk, const double* kl,
+                                          int root, int nb, int4 dr, int4 dn, const double* kk, const double* kl,
                                           unsigned long long flags) {
   constexpr int E = 9 * NC * NC;
   const long long vi = O.vofs + v;
-  const int4 dr = __ldg(&P.dofs[root]);
-  const int4 dn = __ldg(&P.dofs[nb]);
   const int dra[3] = {dr.x, dr.y, dr.z}, dna[3] = {dn.x, dn.y, dn.z};
   O.kkf[vi * 2 + side] = on ? flags : 0ull;
+  bool bad = false;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int I = e / (3 * NC), J = e % (3 * NC);
     O.kkv[(vi * 2 + side) * E + e] = on ? kk[e] : 0.0;
     const long long slot = O.cbase + (v * 2 + side) * E + e;
-    if (on) {
-      note_nonfinite(kk[e], root, nb, P.K, O.errpair);
-      note_nonfinite(kl[e], root, nb, P.K, O.errpair);
-    }
+    bad |= nonfinite(kk[e]) | nonfinite(kl[e]);
     O.keys[slot] = on ? coo_key(P, (long long)NC * dra[I / NC] + I % NC, (long long)NC * dna[J / NC] + J % NC)
                       : kSentinel;
     O.vals[slot] = on ? emit_val(kl[e]) : 0.0;
   }
+  report_nonfinite(on && bad, root, nb, P.K, O.errpair);
 }
 
 // full records, one thread each: the 7x7 point-pair matrix gives both visits
@@ -506,6 +513,7 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     const int2 pr = list[v];
     const int k = pr.x, l = pr.y & kIdMask;
     const bool emitA = pr.y & kEmitA, emitB = pr.y & kEmitB;
+    const int4 dk = __ldg(&P.dofs[k]), dl = __ldg(&P.dofs[l]);  // issued early, used at emission
     double kx[3], ky[3], lx[3], ly[3];
     load_tri(P, k, kx, ky);
     const int4 ek = __ldg(&P.elem[k]);
@@ -539,8 +547,8 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
         if (kkB[e] != 0.0) fB |= 1ull << e;
       }
     }
-    emit_side<NC>(P, O, v, 0, emitA, k, l, kkA, klA, fA);
-    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, kkB, klB, fB);
+    emit_side<NC>(P, O, v, 0, emitA, k, l, dk, dl, kkA, klA, fA);
+    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, dl, dk, kkB, klB, fB);
   }
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
   warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
@@ -768,6 +776,11 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       for (unsigned mm = mask; mm; mm &= mm - 1) S.queue[pos++] = (unsigned short)((lane << 4) | (__ffs(mm) - 1));
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (g_trace_dev && lane == 0) {
+      atomicAdd(&O.counters[K_DBG_SUBTRI], (unsigned long long)total);
+      atomicAdd(&O.counters[K_DBG_ROUNDS], (unsigned long long)((total + 31) / 32));
+      atomicAdd(&O.counters[K_DBG_CHUNKS], 1ull);
+    }
     __syncthreads();
     // ---------------- phase 2: one queued sub-triangle per lane, 7 inner points
     for (int u0 = 0; u0 < ((P.dbg & 1) ? 0 : total); u0 += 32) {
@@ -922,7 +935,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
           O.kkv[(vi * 2 + side) * (9 * NC2) + I * N3 + J] = on ? val : 0.0;
           O.kkv[(vi * 2 + side) * (9 * NC2) + J * N3 + I] = on ? val : 0.0;
           if (on) {
-            note_nonfinite(val, root, nb, P.K, O.errpair);
+            report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
             if (val != 0.0) {
               const unsigned long long bits = (1ull << (I * N3 + J)) | (1ull << (J * N3 + I));
               if (side == 0) fA |= bits; else fB |= bits;
@@ -931,7 +944,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         } else {
           const int e = w - C::NKK, I = e / N3, J = e % N3;
           const long long slot = O.cbase + (v * 2 + side) * (9 * NC2) + e;
-          if (on) note_nonfinite(val, root, nb, P.K, O.errpair);
+          if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
           O.keys[slot] = on ? coo_key(P, (long long)NC * droot[I / NC] + I % NC, (long long)NC * dnb[J / NC] + J % NC)
                             : kSentinel;
           O.vals[slot] = on ? emit_val(val) : 0.0;
@@ -1184,7 +1197,7 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
       }
       const int ai = A::idx(ii, jj);
       const double v = (((red[0][ai] + red[1][ai]) + red[2][ai]) + red[3][ai]) * sScale;
-      note_nonfinite(v, k, l, P.K, errpair);
+      report_nonfinite(nonfinite(v), k, l, P.K, errpair);
       const int m = ii / NC, c = ii % NC, mp = jj / NC, d = jj % NC;
       keys[slot] = coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d);
       vals[slot] = emit_val(v);
@@ -1383,10 +1396,14 @@ struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-o
     s = st;
     n = (std::max<size_t>(n, 16) + 255) & ~(size_t)255;
     if (nlg_plan* pl = g_arena_plan) {
-      pl->arena_peak = std::max(pl->arena_peak, pl->arena_used + n);
-      if (pl->arena && pl->arena_used + n <= pl->arena_cap) {
-        p = pl->arena + pl->arena_used;
-        pl->arena_used += n;
+      // arena_used is a virtual bump offset advanced for every scratch
+      // allocation, so arena_peak is the true cumulative peak even when the
+      // arena is absent or too small (the next call grows it once)
+      const size_t off = pl->arena_used;
+      pl->arena_used += n;
+      pl->arena_peak = std::max(pl->arena_peak, pl->arena_used);
+      if (pl->arena && off + n <= pl->arena_cap) {
+        p = pl->arena + off;
         arena = true;
         return cudaSuccess;
       }
@@ -2202,6 +2219,10 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
       hr.wh[p][a] = hr.ow[p] * hr.oh[p][a];
       for (int b = 0; b < 3; ++b) hr.whh[p][a * 3 + b] = hr.ow[p] * hr.oh[p][a] * hr.oh[p][b];
     }
+  {
+    const int tr = g_trace ? 1 : 0;
+    cudaMemcpyToSymbolAsync(g_trace_dev, &tr, sizeof tr, 0, cudaMemcpyHostToDevice, s);
+  }
   if (cudaMemcpyToSymbolAsync(c_rule, &hr, sizeof hr, 0, cudaMemcpyHostToDevice, s) != cudaSuccess) {
     set_err("rule upload failed");
     delete pl;
@@ -2416,6 +2437,11 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   st.inner_evals = (long long)(hc[K_EVAL_M0] + hc[K_EVAL_M1] + hc[K_EVAL_M2]);
   st.outer_nonempty = (long long)(hc[K_OUT_M0] + hc[K_OUT_M1] + hc[K_OUT_M2]);
   st.sing_points = (long long)(hc[K_SPTS3] + hc[K_SPTS4] + hc[K_SPTS5] + hc[K_SPTS6]);
+  TRACE("assemble end");
+  if (g_trace)
+    fprintf(stderr, "[nlg] clipped: %llu sub-triangles, %llu rounds, %llu chunks -> lane use %.3f\n",
+            hc[K_DBG_SUBTRI], hc[K_DBG_ROUNDS], hc[K_DBG_CHUNKS],
+            hc[K_DBG_ROUNDS] ? (double)hc[K_DBG_SUBTRI] / (32.0 * hc[K_DBG_ROUNDS]) : 0.0);
   st.alg_flops_full = alg_flops(pl->P, hc, 0);
   st.alg_flops_partial = alg_flops(pl->P, hc, 1);
   st.alg_flops_singular = alg_flops(pl->P, hc, 2);

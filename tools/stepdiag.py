@@ -9,13 +9,17 @@ cfg = configs.build(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 inp = marshal(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
 plan = DevicePlan(inp, on_device=True)
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-for i in range(12):
+import gc
+gc.disable()
+for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 12):
     flush.fill_(float(i))
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    print(f'[py  {time.monotonic()*1e3:10.3f}] call', file=sys.stderr, flush=True)
     a.record()
-    _, _, _, st = plan.assemble(out_on_host=False)
+    _, _, _, st = plan.assemble(out_on_host=False, reuse_output=True)
+    print(f'[py  {time.monotonic()*1e3:10.3f}] returned', file=sys.stderr, flush=True)
     b.record()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
