@@ -200,9 +200,24 @@ class DevicePlan:
         return sink.array(3, np.float64, self.inp.n_dofs)
 
 
-def csr_from_parts(indptr, indices, data, n_rows, n_cols):
-    return sparse.csr_matrix((np.asarray(data), np.asarray(indices), np.asarray(indptr)),
-                             shape=(n_rows, n_cols))
+def csr_from_parts(indptr, indices, data, n_rows, n_cols, canonical=False):
+    """scipy CSR from the library's arrays.  ``canonical=True`` (library
+    output: sorted, duplicate-free rows, int32 columns) attaches the arrays
+    without scipy's O(nnz) format re-scan."""
+    indptr, indices, data = np.asarray(indptr), np.asarray(indices), np.asarray(data)
+    if not canonical:
+        return sparse.csr_matrix((data, indices, indptr), shape=(n_rows, n_cols))
+    m = sparse.csr_matrix((n_rows, n_cols), dtype=np.float64)
+    if indices.dtype == np.int32 and (indptr.size == 0 or indptr[-1] < 2**31):
+        indptr = indptr.astype(np.int32)
+    else:
+        indices = indices.astype(np.int64)
+    if indptr.shape != (n_rows + 1,) or indices.shape != data.shape:
+        raise ValueError("inconsistent CSR parts")
+    m.indptr, m.indices, m.data = indptr, indices, data
+    m.has_sorted_indices = True
+    m.has_canonical_format = True
+    return m
 
 
 def bfs_assemble(mesh, adjacency, kernel, ansatz, quad=None, n_threads=1, rows="all",
@@ -223,7 +238,7 @@ def bfs_assemble(mesh, adjacency, kernel, ansatz, quad=None, n_threads=1, rows="
         plan.close()
     if stats is not None:
         stats.update(st)
-    matrix = csr_from_parts(indptr, indices, data, hi - lo, J)
+    matrix = csr_from_parts(indptr, indices, data, hi - lo, J, canonical=True)
     return SparseSystem(matrix=matrix, free_mask=ansatz.free_mask.copy())
 
 

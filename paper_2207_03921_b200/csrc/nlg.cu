@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
+#include <thread>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -1378,15 +1380,25 @@ struct nlg_plan {
   int* act = nullptr;
   int nact = -1;
   int nbase = 0;
-  // scratch arena: one allocation reused by every assembly (grown to the
-  // observed peak), so steady-state calls never go to the allocator
-  char* arena = nullptr;
-  size_t arena_cap = 0, arena_used = 0, arena_peak = 0;
+  size_t arena_used = 0;  // virtual bump offset into the device arena during a call
 };
 
 namespace {
 
-thread_local nlg_plan* g_arena_plan = nullptr;  // plan whose arena backs DevBuf
+// Process-wide per-device scratch arena, reused by every plan and call on the
+// device (grown once to the cumulative peak a call needed), so steady-state
+// assemblies never reach the allocator; plus a pinned host staging buffer for
+// host-resident outputs.  A per-device mutex serialises calls that share them.
+struct DeviceScratch {
+  std::mutex mu;
+  char* arena = nullptr;
+  size_t cap = 0, peak = 0;
+  char* pinned = nullptr;
+  size_t pinned_cap = 0;
+};
+DeviceScratch g_scratch[64];
+
+thread_local nlg_plan* g_arena_plan = nullptr;  // plan whose device arena backs DevBuf
 
 struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-ordered
   void* p = nullptr;
@@ -1399,11 +1411,12 @@ struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-o
       // arena_used is a virtual bump offset advanced for every scratch
       // allocation, so arena_peak is the true cumulative peak even when the
       // arena is absent or too small (the next call grows it once)
+      DeviceScratch& ds = g_scratch[pl->device];
       const size_t off = pl->arena_used;
       pl->arena_used += n;
-      pl->arena_peak = std::max(pl->arena_peak, pl->arena_used);
-      if (pl->arena && off + n <= pl->arena_cap) {
-        p = pl->arena + off;
+      ds.peak = std::max(ds.peak, pl->arena_used);
+      if (ds.arena && off + n <= ds.cap) {
+        p = ds.arena + off;
         arena = true;
         return cudaSuccess;
       }
@@ -2308,7 +2321,6 @@ void nlg_plan_destroy(nlg_plan* pl) {
     for (double* p : f)
       if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
-  if (pl->arena) cudaFree(pl->arena);
   delete pl;
 }
 
@@ -2318,13 +2330,17 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   if (row_lo < 0 || row_hi > pl->P.J || row_lo > row_hi) { set_err("row range out of bounds"); return NLG_ERR_CONFIG; }
   CK(cudaSetDevice(pl->device));
   cudaStream_t s = pl->stream;
-  // grow the scratch arena to the peak the previous call needed
-  if (pl->arena_peak > pl->arena_cap) {
-    if (pl->arena) cudaFree(pl->arena);
-    pl->arena = nullptr;
-    pl->arena_cap = 0;
-    size_t cap = pl->arena_peak + pl->arena_peak / 8;
-    if (cudaMalloc((void**)&pl->arena, cap) == cudaSuccess) pl->arena_cap = cap;
+  if (pl->device < 0 || pl->device >= 64) { set_err("device index out of range"); return NLG_ERR_CONFIG; }
+  DeviceScratch& ds = g_scratch[pl->device];
+  std::lock_guard<std::mutex> scratch_lock(ds.mu);
+  // grow the device arena to the peak an earlier call needed
+  if (ds.peak > ds.cap) {
+    CK(cudaStreamSynchronize(s));
+    if (ds.arena) cudaFree(ds.arena);
+    ds.arena = nullptr;
+    ds.cap = 0;
+    const size_t cap = ds.peak + ds.peak / 8;
+    if (cudaMalloc((void**)&ds.arena, cap) == cudaSuccess) ds.cap = cap;
     else cudaGetLastError();
   }
   pl->arena_used = 0;
@@ -2388,10 +2404,34 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   long long nnz = 0;
   for (auto& p : pieces) nnz += p.nnz;
   const long long nrows = row_hi - row_lo;
-  long long* o_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
-  int* o_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
-  double* o_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
-  if (!o_ptr || !o_idx || !o_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  long long* u_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
+  int* u_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
+  double* u_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
+  if (!u_ptr || !u_idx || !u_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  // host outputs: D2H into pinned staging (full PCIe/C2C speed), then a
+  // threaded copy into the caller's pageable buffers
+  long long* o_ptr = u_ptr;
+  int* o_idx = u_idx;
+  double* o_dat = u_dat;
+  const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
+               b_ptr = sizeof(long long) * (nrows + 1);
+  const size_t b_all = b_dat + ((b_idx + 15) & ~(size_t)15) + b_ptr;
+  if (out_on_host) {
+    if (ds.pinned_cap < b_all) {
+      if (ds.pinned) cudaFreeHost(ds.pinned);
+      ds.pinned = nullptr;
+      ds.pinned_cap = 0;
+      if (cudaHostAlloc((void**)&ds.pinned, b_all + b_all / 8, cudaHostAllocPortable) == cudaSuccess)
+        ds.pinned_cap = b_all + b_all / 8;
+      else
+        cudaGetLastError();
+    }
+    if (ds.pinned) {
+      o_dat = (double*)ds.pinned;
+      o_idx = (int*)(ds.pinned + b_dat);
+      o_ptr = (long long*)(ds.pinned + b_dat + ((b_idx + 15) & ~(size_t)15));
+    }
+  }
   DevBuf ptrbuf;
   CK(ptrbuf.alloc(sizeof(long long) * (nrows + 1), s));
   long long run = 0;
@@ -2417,7 +2457,23 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&herr, derr.p, sizeof herr, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  TRACE("sync 2389");
+  TRACE("outputs synced");
+  if (out_on_host && o_dat != u_dat) {  // pinned staging -> caller buffers
+    struct Part { void* dst; const void* src; size_t n; };
+    const Part parts[3] = {{u_dat, o_dat, b_dat}, {u_idx, o_idx, b_idx}, {u_ptr, o_ptr, b_ptr}};
+    const int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t]() {
+        for (const Part& q : parts) {
+          const size_t chunk = (q.n + nt - 1) / nt, a = std::min(q.n, chunk * t), b = std::min(q.n, a + chunk);
+          if (b > a) memcpy((char*)q.dst + a, (const char*)q.src + a, b - a);
+        }
+      });
+    for (auto& x : th) x.join();
+    TRACE("host copy done");
+  }
+
   for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
