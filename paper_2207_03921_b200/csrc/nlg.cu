@@ -91,7 +91,7 @@ enum {
   K_EVAL_M0, K_EVAL_M1, K_EVAL_M2,
   K_OUT_M0, K_OUT_M1, K_OUT_M2,
   K_SPTS3, K_SPTS4, K_SPTS5, K_SPTS6,
-  K_DBG_SUBTRI, K_DBG_ROUNDS, K_DBG_CHUNKS,
+  K_DBG_SUBTRI, K_DBG_ROUNDS, K_DBG_CHUNKS, K_DBG_ITEMS, K_DBG_FAR, K_DBG_INSIDE, K_DBG_NONEMPTY,
   K_NCOUNTERS
 };
 
@@ -457,10 +457,6 @@ __device__ __forceinline__ void report_nonfinite(bool bad, int k, int l, int K, 
   if (bad) atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
 }
 
-__device__ __forceinline__ void note_nonfinite(double v, int k, int l, int K,
-                                               unsigned long long* errpair) {
-  if (!isfinite(v)) atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
-}
 
 template <typename T>
 __device__ __forceinline__ void warp_add_ll(T v, unsigned long long* dst) {
@@ -471,35 +467,30 @@ __device__ __forceinline__ void warp_add_ll(T v, unsigned long long* dst) {
 struct VisitOut {
   double* kkv;              // [record][side][E] own-block values of visit A (k, l) / B (l, k)
   unsigned long long* kkf;  // [record][side] presence bits of those blocks
+  double* klv;              // [record][side][J][I] neighbour blocks, transposed (column-major):
+                            // the 3NC row values of one neighbour dof are contiguous
   long long nvis;           // records of both lists
   long long vofs;           // this list's first record index
-  unsigned long long* keys;  // COO: [record][side][E] neighbour blocks
-  double* vals;
-  long long cbase;  // this list's COO slot base
   long long nlist;
   unsigned long long* counters;
   unsigned long long* errpair;
 };
 
-// emit one side of a record: own block -> scratch, neighbour block -> COO
+// emit one side of a record: own block -> kkv, neighbour block -> klv
 template <int NC>
 __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long v, int side, bool on,
-                                          int root, int nb, int4 dr, int4 dn, const double* kk, const double* kl,
+                                          int root, int nb, const double* kk, const double* kl,
                                           unsigned long long flags) {
-  constexpr int E = 9 * NC * NC;
+  constexpr int E = 9 * NC * NC, N3 = 3 * NC;
   const long long vi = O.vofs + v;
-  const int dra[3] = {dr.x, dr.y, dr.z}, dna[3] = {dn.x, dn.y, dn.z};
   O.kkf[vi * 2 + side] = on ? flags : 0ull;
   bool bad = false;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int I = e / (3 * NC), J = e % (3 * NC);
+    const int I = e / N3, J = e % N3;
     O.kkv[(vi * 2 + side) * E + e] = on ? kk[e] : 0.0;
-    const long long slot = O.cbase + (v * 2 + side) * E + e;
     bad |= nonfinite(kk[e]) | nonfinite(kl[e]);
-    O.keys[slot] = on ? coo_key(P, (long long)NC * dra[I / NC] + I % NC, (long long)NC * dna[J / NC] + J % NC)
-                      : kSentinel;
-    O.vals[slot] = on ? emit_val(kl[e]) : 0.0;
+    O.klv[(vi * 2 + side) * E + J * N3 + I] = on ? emit_val(kl[e]) : 0.0;
   }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
 }
@@ -515,7 +506,6 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     const int2 pr = list[v];
     const int k = pr.x, l = pr.y & kIdMask;
     const bool emitA = pr.y & kEmitA, emitB = pr.y & kEmitB;
-    const int4 dk = __ldg(&P.dofs[k]), dl = __ldg(&P.dofs[l]);  // issued early, used at emission
     double kx[3], ky[3], lx[3], ly[3];
     load_tri(P, k, kx, ky);
     const int4 ek = __ldg(&P.elem[k]);
@@ -549,8 +539,8 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
         if (kkB[e] != 0.0) fB |= 1ull << e;
       }
     }
-    emit_side<NC>(P, O, v, 0, emitA, k, l, dk, dl, kkA, klA, fA);
-    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, dl, dk, kkB, klB, fB);
+    emit_side<NC>(P, O, v, 0, emitA, k, l, kkA, klA, fA);
+    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, kkB, klB, fB);
   }
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
   warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
@@ -594,10 +584,17 @@ struct ClipWarp {
   double xo[32][2];
   double W[32];
   double tri[2][2][8];  // [record slot][side]: o.x o.y e1x e1y e2x e2y idet
+  double tv[2][2][6];   // [record slot][side]: the inner triangle's vertices x0 x1 x2 y0 y1 y2
   double rs2[2];
   unsigned short queue[32 * 7];  // (item << 4) | t of every kept sub-triangle, item-major
   unsigned char pm[32];
-  int vk[2], vl[2], fl[2], dk[2][3], dl[2][3];  // per record slot
+  unsigned char nv[32];  // polygon rows of each item
+  int vk[2], vl[2], fl[2];  // per record slot
+};
+constexpr int kClipWarps = 4;
+struct ClipQueue {  // block-wide queue of the items that need a real clip
+  int n[2];  // by chunk parity: reset one chunk ahead, race-free
+  unsigned char item[32 * kClipWarps];  // (warp << 5) | lane
 };
 
 // (I, J) of the u-th unique entry of a symmetric n x n block, I <= J
@@ -659,13 +656,18 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
   using X = SumIdx<KID>;
   constexpr int NC = T::NC, NC2 = T::NC2, N3 = 3 * NC;
   extern __shared__ __align__(16) unsigned char clip_smem[];
-  ClipWarp<KID>& S = reinterpret_cast<ClipWarp<KID>*>(clip_smem)[threadIdx.x >> 5];
+  ClipWarp<KID>* SW = reinterpret_cast<ClipWarp<KID>*>(clip_smem);
+  ClipQueue& CQ = *reinterpret_cast<ClipQueue*>(clip_smem + kClipWarps * sizeof(ClipWarp<KID>));
+  ClipWarp<KID>& S = SW[threadIdx.x >> 5];
   const int lane = lane_id();
   const long long nchunks = (O.nlist + 1) / 2;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   long long n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;
   const int vs = lane >> 4, r = lane & 15;
+  if (threadIdx.x == 0) CQ.n[0] = 0;
+  __syncthreads();
+  int par = 0;
   // software pipeline: the next chunk's records and element records are
   // fetched while the current chunk computes
   int2 pr = make_int2(0, 0);
@@ -684,7 +686,14 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
   const long long wib = threadIdx.x >> 5;
   for (long long cb = w0 - wib; cb < nchunks; cb += nw) {
     const long long ch = cb + wib;
-    // ---------------- phase 1: clip one item per lane
+    // this chunk counts in CQ.n[par]; CQ.n[par ^ 1] was last read before the
+    // previous chunk's post-clip barrier and is next bumped after this
+    // chunk's pre-clip barrier
+    if (threadIdx.x == 0) CQ.n[par ^ 1] = 0;
+    // ---------------- phase 1a: classify one item per lane.  Items beyond
+    // the ball are empty, items inside it keep the (deduplicated) triangle;
+    // the rest go to the block's clip queue, so the branchy clipping code
+    // runs on densely packed lanes.
     const long long v = ch * 2 + vs;
     const bool vok = v < O.nlist;
     bool valid = vok && r < 14;
@@ -705,16 +714,14 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       prn.x &= kIdMask;
     }
     if (r == 0 && vok) {
-      const int4 dk4 = __ldg(&P.dofs[k]), dl4 = __ldg(&P.dofs[l]);
       S.vk[vs] = k;
       S.vl[vs] = l;
       S.fl[vs] = flags;
-      S.dk[vs][0] = dk4.x; S.dk[vs][1] = dk4.y; S.dk[vs][2] = dk4.z;
-      S.dl[vs][0] = dl4.x; S.dl[vs][1] = dl4.y; S.dl[vs][2] = dl4.z;
     }
 #pragma unroll
     for (int i = 0; i < C::NSUM; ++i) S.sums[lane][i] = 0.0;
-    unsigned mask = 0;
+    bool need_clip = false;
+    int nv = 0;
     if (valid) {
       double ox[3], oy[3], ix[3], iy[3];
       {
@@ -727,8 +734,6 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       const double e1x = ox[1] - ox[0], e2x = ox[2] - ox[0], e1y = oy[1] - oy[0], e2y = oy[2] - oy[0];
       const double x0 = __dadd_rn(__dadd_rn(ox[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
       const double x1 = __dadd_rn(__dadd_rn(oy[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
-      double* qx = S.px[lane];
-      double* qy = S.py[lane];
       // exact early-out: the inner triangle lies in disk(c, r); if that disk is
       // farther than the (widened) ball by a margin no rounding can bridge,
       // the reference's clip finds no vertex inside and no root in (0, 1)
@@ -737,17 +742,31 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       const double reach = P.delta * (1.0 + 1e-6) + __ldg(&P.rad[inner_el]);
       const double dcx = ci.x - x0, dcy = ci.y - x1;
       const bool far = (P.dbg & 2) || (P.ball != 2 && dcx * dcx + dcy * dcy > reach * reach);
-      const int nv = far ? 0 : truncate_inner(ix, iy, x0, x1, P.delta, P.ball, S.sx[lane], S.sy[lane], qx, qy);
-      if (nv >= 3) {
-        n_out0 += m == 0 ? mult : 0;
-        n_out1 += m == 1 ? mult : 0;
-        n_out2 += m == 2;
-#pragma unroll 1
-        for (int t = 1; t < nv - 1; ++t) {
-          const double ax = qx[t] - qx[0], ay = qy[t] - qy[0];
-          const double bx = qx[t + 1] - qx[0], by = qy[t + 1] - qy[0];
-          if (cross2(ax, by, ay, bx) > P.drop2) mask |= 1u << t;
+      if (!far) {
+        // every inner vertex inside the widened ball: clip_circle keeps the
+        // triangle (_geom_scalar.py:53-66) and no cap is inserted
+        bool inside = P.ball != 2;
+        if (inside) {
+          const double rad = mul(P.delta, 1.0 + kBallTieRel), r2b = mul(rad, rad);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) inside = inside && __dsub_rn(sumsq(ix[i] - x0, iy[i] - x1), r2b) <= 0.0;
         }
+        if (inside) {
+          double* qx = S.px[lane];
+          double* qy = S.py[lane];
+          const double dtol = mul(kDedupRel, P.delta);
+          unsigned fdummy = 0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) push_dedup(qx, qy, fdummy, nv, ix[i], iy[i], false, dtol, true);
+          if (nv >= 2 && fabs(qx[0] - qx[nv - 1]) <= dtol && fabs(qy[0] - qy[nv - 1]) <= dtol) --nv;
+        } else {
+          need_clip = true;
+        }
+      }
+      if (g_trace_dev) {
+        atomicAdd(&O.counters[K_DBG_ITEMS], 1ull);
+        if (far) atomicAdd(&O.counters[K_DBG_FAR], 1ull);
+        if (!far && !need_clip) atomicAdd(&O.counters[K_DBG_INSIDE], 1ull);
       }
       S.xo[lane][0] = x0;
       S.xo[lane][1] = x1;
@@ -758,6 +777,9 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         tr[2] = ix[1] - ix[0]; tr[3] = iy[1] - iy[0];
         tr[4] = ix[2] - ix[0]; tr[5] = iy[2] - iy[0];
         tr[6] = 1.0 / cross2(tr[2], tr[5], tr[3], tr[4]);
+        double* tv = S.tv[vs][m == 1];
+        tv[0] = ix[0]; tv[1] = ix[1]; tv[2] = ix[2];
+        tv[3] = iy[0]; tv[4] = iy[1]; tv[5] = iy[2];
         if (m != 1) {
           const bool touching = k == l || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
                                 ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
@@ -766,6 +788,48 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       }
     }
     S.pm[lane] = (unsigned char)(p | (m << 4) | (valid ? 0 : 0x80));
+    S.nv[lane] = (unsigned char)nv;
+    {
+      const unsigned qm = __ballot_sync(0xffffffffu, need_clip);
+      int qb = 0;
+      if (lane == 0 && qm) qb = atomicAdd(&CQ.n[par], __popc(qm));
+      qb = __shfl_sync(0xffffffffu, qb, 0);
+      if (need_clip) CQ.item[qb + __popc(qm & ((1u << lane) - 1u))] = (unsigned char)((wib << 5) | lane);
+    }
+    __syncthreads();
+    // ---------------- phase 1b: the block's lanes clip the queued items
+    {
+      const int nq = CQ.n[par];
+#pragma unroll 1
+      for (int qi = threadIdx.x; qi < nq; qi += kClipWarps * 32) {
+        const int it = CQ.item[qi], j = it & 31;
+        ClipWarp<KID>& R = SW[it >> 5];
+        const int mj = (R.pm[j] >> 4) & 3;
+        const double* tv = R.tv[j >> 4][mj == 1];
+        const Tri Tq{tv[0], tv[1], tv[2], tv[3], tv[4], tv[5]};
+        R.nv[j] = (unsigned char)truncate_inner(Tq, R.xo[j][0], R.xo[j][1], P.delta, P.ball, S.sx[lane], S.sy[lane],
+                                                R.px[j], R.py[j]);
+      }
+    }
+    __syncthreads();
+    par ^= 1;
+    // ---------------- phase 1c: fan sub-triangles of each item -> warp queue
+    unsigned mask = 0;
+    nv = S.nv[lane];
+    if (nv >= 3) {
+      n_out0 += m == 0 ? mult : 0;
+      n_out1 += m == 1 ? mult : 0;
+      n_out2 += m == 2;
+      const double* qx = S.px[lane];
+      const double* qy = S.py[lane];
+#pragma unroll 1
+      for (int t = 1; t < nv - 1; ++t) {
+        const double ax = qx[t] - qx[0], ay = qy[t] - qy[0];
+        const double bx = qx[t + 1] - qx[0], by = qy[t + 1] - qy[0];
+        if (cross2(ax, by, ay, bx) > P.drop2) mask |= 1u << t;
+      }
+    }
+    if (g_trace_dev && nv >= 3) atomicAdd(&O.counters[K_DBG_NONEMPTY], 1ull);
     const int cnt = __popc(mask);
     int incl = cnt;
 #pragma unroll
@@ -783,7 +847,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       atomicAdd(&O.counters[K_DBG_ROUNDS], (unsigned long long)((total + 31) / 32));
       atomicAdd(&O.counters[K_DBG_CHUNKS], 1ull);
     }
-    __syncthreads();
+    __syncwarp();
     // ---------------- phase 2: one queued sub-triangle per lane, 7 inner points
     for (int u0 = 0; u0 < ((P.dbg & 1) ? 0 : total); u0 += 32) {
       const int u = u0 + lane;
@@ -928,8 +992,6 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         const int side = g / C::NSIDE, w = g % C::NSIDE;
         const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
         const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
-        const int* droot = side == 0 ? S.dk[vs] : S.dl[vs];
-        const int* dnb = side == 0 ? S.dl[vs] : S.dk[vs];
         const long long vi = O.vofs + v;
         if (w < C::NKK) {
           int I, J;
@@ -945,11 +1007,8 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
           }
         } else {
           const int e = w - C::NKK, I = e / N3, J = e % N3;
-          const long long slot = O.cbase + (v * 2 + side) * (9 * NC2) + e;
           if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
-          O.keys[slot] = on ? coo_key(P, (long long)NC * droot[I / NC] + I % NC, (long long)NC * dnb[J / NC] + J % NC)
-                            : kSentinel;
-          O.vals[slot] = on ? emit_val(val) : 0.0;
+          O.klv[(vi * 2 + side) * (9 * NC2) + J * N3 + I] = on ? emit_val(val) : 0.0;
         }
       }
     }
@@ -972,56 +1031,308 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
   warp_add_ll(n_out2, &O.counters[K_OUT_M2]);
 }
 
-// per-root sum of the root's own block, fixed order: side A of the records
-// the root owns (full list, then clipped list), then side B of the records
-// where it is the partner (reverse index, record order).  kkv is
-// [record][side][E], kkf [record][side].
-template <int E>
-__global__ void k_kk_reduce(Params P, const int* __restrict__ roots, int nR,
-                            const int* __restrict__ cnt, const long long* __restrict__ off,
-                            long long nF, const double* __restrict__ kkv,
-                            const unsigned long long* __restrict__ kkf, const int* __restrict__ rev_item,
-                            const int* __restrict__ rev_start, unsigned long long* keys, double* vals,
-                            long long cbase) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int lane = lane_id();
-  constexpr int NC = E == 36 ? 2 : 1;
-  for (int i = warp; i < nR; i += nwarps) {
-    const int k = roots[i];
-    const bool emit = cnt[(long long)C_KK * nR + i] != 0;
-    const long long f0 = off[0 * (long long)(nR + 1) + i], fn = cnt[(long long)C_FULL * nR + i];
-    const long long p0 = nF + off[1 * (long long)(nR + 1) + i], pn = cnt[(long long)C_PART * nR + i];
-    const long long r0 = rev_start[i], rn = rev_start[i + 1] - r0;
+// ---------------------------------------------------------------- per-root reduction
+// Merge stage R.  A root's contributions are the blocks of its record sides:
+// side A of the records it owns (full list, then clipped list) and side B of
+// the records where it is the partner (reverse index), in that fixed order
+// (the reference adds them visit by visit into the root's rows).
+//  * own block: summed over the sides in a fixed order (thread stride, warp
+//    tree, warps in order), E entries at kk_base + rank E;
+//  * neighbour blocks: every (side, neighbour dof base w) item carries a
+//    column of 3NC x NC values (klv is [J][I]).  A chunk of up to kRootCap
+//    items is radix-sorted by w in shared memory (deterministic block sort),
+//    equal-w runs are summed in sorted order, and each run becomes the COO
+//    entries of the root's in-range rows.  Chunks get their output offset by
+//    a decoupled look-back in ticket order (no count pass, no compaction).
+// Roots typically have 3-6k items, so one chunk sees every side of its root
+// and the reduction is complete per root (cfg2: 251M values -> ~54M entries).
+constexpr int kRootThreads = 256, kRootItems = 12, kRootCap = kRootThreads * kRootItems;
+// stage-R run entries per record value, for the buffer estimate (cfg2: 0.2);
+// a batch that needs more is split
+constexpr double kRunFrac = 0.35;
+
+struct RootIn {
+  const int* roots;
+  int nR;
+  const int* cnt;
+  const long long* off;
+  long long nF;
+  const int2* rec;  // full then clipped records
+  const int* rev_item;
+  const int* rev_start;
+  const double* kkv;
+  const unsigned long long* kkf;
+  const double* klv;
+  const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
+};
+struct RootOut {
+  unsigned* ticket;
+  unsigned long long* lb;  // [chunks] look-back words: flag << 62 | count
+  unsigned long long* keys;
+  double* vals;
+  long long kk_base;  // root rank i's own block at kk_base + i E
+  long long r_base, r_cap;
+  int* overflow;
+  unsigned long long* total;  // run entries of all chunks (written by the last one)
+};
+
+struct RootSides {
+  long long f0, fn, p0, pn, r0, rn;
+  __device__ __forceinline__ long long n() const { return fn + pn + rn; }
+  // record index (full then clipped list) and side of the root's rs-th side
+  __device__ __forceinline__ void at(const RootIn& I, long long rs, long long& rec, int& side) const {
+    if (rs < fn) { rec = f0 + rs; side = 0; }
+    else if (rs < fn + pn) { rec = p0 + (rs - fn); side = 0; }
+    else { rec = __ldg(&I.rev_item[r0 + (rs - fn - pn)]); side = 1; }
+  }
+};
+
+__device__ __forceinline__ RootSides root_sides(const RootIn& I, int i) {
+  RootSides R;
+  R.f0 = I.off[0 * (long long)(I.nR + 1) + i];
+  R.fn = I.cnt[(long long)C_FULL * I.nR + i];
+  R.p0 = I.nF + I.off[1 * (long long)(I.nR + 1) + i];
+  R.pn = I.cnt[(long long)C_PART * I.nR + i];
+  R.r0 = I.rev_start[i];
+  R.rn = I.rev_start[i + 1] - R.r0;
+  return R;
+}
+
+__global__ void k_root_chunks(RootIn I, int* nch) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I.nR) return;
+  const long long items = 3 * root_sides(I, i).n();
+  nch[i] = (int)max(1LL, (items + kRootCap - 1) / kRootCap);
+}
+
+template <int NC>
+struct RootSmem {
+  static constexpr int NV = 3 * NC * NC;  // values of one (side, neighbour dof) item
+  using Sort = cub::BlockRadixSort<unsigned, kRootThreads, kRootItems, unsigned>;
+  using Scan = cub::BlockScan<int, kRootThreads>;
+  union {
+    typename Sort::TempStorage sort;
+    double red[kRootThreads / 32][9 * NC * NC];
+  } u;
+  typename Scan::TempStorage scan;
+  unsigned last_key[kRootThreads];   // key at each thread's last sorted position
+  double cont[kRootThreads][NV];     // each thread's leading partial run (before its first head)
+  unsigned cont_pres[kRootThreads];
+  unsigned char has_head[kRootThreads];
+};
+
+template <int NC>
+__global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootIn I, RootOut O, int key_bits) {
+  constexpr int N3 = 3 * NC, E = 9 * NC * NC, NWARP = kRootThreads / 32, NV = N3 * NC, IT = kRootItems;
+  using SM = RootSmem<NC>;
+  extern __shared__ __align__(16) unsigned char root_smem[];
+  SM& S = *reinterpret_cast<SM*>(root_smem);
+  __shared__ int s_chunk;
+  __shared__ long long s_base;
+  __shared__ unsigned long long s_fl;
+  const int t = threadIdx.x, lane = lane_id(), warp = t >> 5;
+  if (t == 0) {
+    s_chunk = (int)atomicAdd(O.ticket, 1u);
+    s_fl = 0;
+  }
+  __syncthreads();
+  const int ch = s_chunk;
+  const int nchunks = I.chunk_first[I.nR];
+  if (ch >= nchunks) return;  // surplus block of the upper-bound grid
+  int lo = 0, hi = I.nR - 1;  // root: last i with chunk_first[i] <= ch
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (I.chunk_first[mid] <= ch) lo = mid; else hi = mid - 1;
+  }
+  const int i = lo, c = ch - I.chunk_first[i];
+  const int k = I.roots[i];
+  const RootSides R = root_sides(I, i);
+  const long long n_rs = R.n(), nitems = 3 * n_rs;
+  const int4 dk4 = P.dofs[k];
+  const int dka[3] = {dk4.x, dk4.y, dk4.z};
+  unsigned inr = 0;  // in-range local rows I = (a, c)
+  int nr = 0;
+#pragma unroll
+  for (int r = 0; r < N3; ++r) {
+    const long long row = (long long)NC * dka[r / NC] + r % NC;
+    if (row >= P.row_lo && row < P.row_hi) { inr |= 1u << r; ++nr; }
+  }
+  // ---- the root's own block, by its first chunk
+  if (c == 0) {
+    double acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.0;
     unsigned long long fl = 0;
-    double s[E];
+    for (long long rs = t; rs < n_rs; rs += kRootThreads) {
+      long long rec;
+      int side;
+      R.at(I, rs, rec, side);
+      const long long slot = rec * 2 + side;
+      fl |= __ldg(&I.kkf[slot]);
 #pragma unroll
-    for (int e = 0; e < E; ++e) s[e] = 0.0;
-    for (long long j = lane; j < fn + pn + rn; j += 32) {
-      long long slot;
-      if (j < fn) slot = (f0 + j) * 2;
-      else if (j < fn + pn) slot = (p0 + (j - fn)) * 2;
-      else slot = (long long)rev_item[r0 + (j - fn - pn)] * 2 + 1;
-      fl |= kkf[slot];
-#pragma unroll
-      for (int e = 0; e < E; ++e) s[e] += kkv[slot * E + e];
+      for (int e = 0; e < E; ++e) acc[e] += __ldg(&I.kkv[slot * E + e]);
     }
-    for (int o = 16; o; o >>= 1) fl |= __shfl_xor_sync(0xffffffffu, fl, o);
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      for (int o = 16; o; o >>= 1) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
-    const int4 dk = P.dofs[k];
-    const int dka[3] = {dk.x, dk.y, dk.z};
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      if (lane != e % 32) continue;
-      const int rr = e / (3 * NC), cc = e % (3 * NC);
-      const int a = rr / NC, c = rr % NC, b = cc / NC, d = cc % NC;
-      const long long slot = cbase + (long long)i * E + e;
-      const bool present = emit && ((fl >> e) & 1ull);
-      keys[slot] = present ? coo_key(P, (long long)NC * dka[a] + c, (long long)NC * dka[b] + d) : kSentinel;
-      vals[slot] = present ? (s[e] != 0.0 ? s[e] : -0.0) : 0.0;
+      double v = acc[e];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) S.u.red[warp][e] = v;
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    if (lane == 0 && fl) atomicOr(&s_fl, fl);
+    __syncthreads();
+    if (t < E) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) v += S.u.red[w][t];
+      const int rr = t / N3, cc = t % N3;
+      const bool present = I.cnt[(long long)C_KK * I.nR + i] != 0 && ((s_fl >> t) & 1ull);
+      const long long slot = O.kk_base + (long long)i * E + t;
+      O.keys[slot] = present ? coo_key(P, (long long)NC * dka[rr / NC] + rr % NC, (long long)NC * dka[cc / NC] + cc % NC)
+                             : kSentinel;
+      O.vals[slot] = present ? (v != 0.0 ? v : -0.0) : 0.0;
+    }
+    __syncthreads();
+  }
+  // ---- neighbour items of this chunk: (dof base w, value column) sorted by w
+  const long long c0 = (long long)c * kRootCap;
+  const int nval = nr ? (int)min((long long)kRootCap, max(0LL, nitems - c0)) : 0;
+  unsigned key[IT], col[IT];  // col: (record side * 3 + b), the item's value column in klv
+  int nseg = 0, hb = 0;
+  unsigned heads = 0;
+  if (nval) {
+    const unsigned PAD = (1u << key_bits) - 1u;
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      const int j = t * IT + q;
+      key[q] = PAD;
+      col[q] = 0;
+      if (j < nval) {
+        const long long g = c0 + j, rs = g / 3;
+        const int b = (int)(g - 3 * rs);
+        long long rec;
+        int side;
+        R.at(I, rs, rec, side);
+        const int2 pr = __ldg(&I.rec[rec]);
+        const int nb = (side == 0 ? pr.y : pr.x) & kIdMask;
+        const int4 dn = __ldg(&P.dofs[nb]);
+        key[q] = (unsigned)(b == 0 ? dn.x : (b == 1 ? dn.y : dn.z));
+        col[q] = (unsigned)((rec * 2 + side) * 3 + b);
+      }
+    }
+    typename SM::Sort(S.u.sort).Sort(key, col, 0, key_bits);  // blocked: position t IT + q
+    S.last_key[t] = key[IT - 1];
+    __syncthreads();
+    const unsigned prev = t ? S.last_key[t - 1] : ~0u;
+    int hc = 0;
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      const int pos = t * IT + q;
+      const bool h = pos < nval && key[q] != (q ? key[q - 1] : prev);
+      heads |= (h ? 1u : 0u) << q;
+      hc += h;
+    }
+    typename SM::Scan(S.scan).ExclusiveSum(hc, hb, nseg);
+    S.has_head[t] = heads != 0;
+  }
+  // ---- output offset: decoupled look-back over the chunks in ticket order
+  const long long count = (long long)nseg * nr * NC;
+  if (t == 0) {
+    constexpr unsigned long long FA = 1ull << 62, FP = 2ull << 62, VM = (1ull << 62) - 1;
+    long long excl = 0;
+    if (ch == 0) {
+      atomicExch(&O.lb[0], FP | (unsigned long long)count);
+    } else {
+      atomicExch(&O.lb[ch], FA | (unsigned long long)count);
+      for (int j = ch - 1;;) {
+        const unsigned long long v = *(volatile unsigned long long*)&O.lb[j];
+        const unsigned long long f = v >> 62;
+        if (f == 0) continue;
+        excl += (long long)(v & VM);
+        if (f == 2) break;
+        --j;
+      }
+      atomicExch(&O.lb[ch], FP | (unsigned long long)(excl + count));
+    }
+    if (ch == nchunks - 1) *O.total = (unsigned long long)(excl + count);
+    if (count && excl + count > O.r_cap) atomicExch(O.overflow, 1);
+    s_base = excl;
+  }
+  if (!nval) return;  // block-uniform
+  // ---- run sums: each thread adds its sorted positions in order; a run that
+  // starts in an earlier thread gets this thread's leading piece afterwards
+  const int npos = min(IT, max(0, nval - t * IT));
+  double acc[NV];
+  unsigned pres = 0;
+#pragma unroll
+  for (int e = 0; e < NV; ++e) acc[e] = 0.0;
+  auto flush = [&](int seg, unsigned w) {  // write run `seg` (complete) of dof base w
+    long long pos = O.r_base + s_base + (long long)seg * nr * NC;
+#pragma unroll
+    for (int r = 0; r < N3; ++r) {
+      if (!((inr >> r) & 1u)) continue;
+      const long long row = (long long)NC * dka[r / NC] + r % NC - P.row_lo;
+#pragma unroll
+      for (int d = 0; d < NC; ++d) {
+        const int e = d * N3 + r;
+        O.keys[pos] = (unsigned long long)row * (unsigned long long)P.J + (unsigned long long)NC * w + d;
+        O.vals[pos] = ((pres >> e) & 1u) ? (acc[e] != 0.0 ? acc[e] : -0.0) : 0.0;
+        ++pos;
+      }
+    }
+  };
+  __syncthreads();  // s_base, has_head
+  const long long base = s_base;
+  const bool fits = base + count <= O.r_cap;
+  int seg = hb - 1;  // run of the current position (-1: a run begun in an earlier thread)
+  unsigned wseg = 0;
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    if (q < npos) {
+      if ((heads >> q) & 1u) {
+        if (seg >= hb) {  // the previous run ended inside this thread
+          if (fits) flush(seg, wseg);
+        } else {  // leading piece of a run begun earlier
+#pragma unroll
+          for (int e = 0; e < NV; ++e) S.cont[t][e] = acc[e];
+          S.cont_pres[t] = pres;
+        }
+        ++seg;
+        wseg = key[q];
+#pragma unroll
+        for (int e = 0; e < NV; ++e) acc[e] = 0.0;
+        pres = 0;
+      }
+      const double* src = I.klv + (long long)col[q] * NV;
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {  // e = d * N3 + I
+        const double v = __ldg(&src[e]);
+        acc[e] += v;
+        pres |= (__double_as_longlong(v) != 0 ? 1u : 0u) << e;
+      }
+    }
+  }
+  if (!heads && npos > 0) {  // the whole range continues an earlier run
+#pragma unroll
+    for (int e = 0; e < NV; ++e) S.cont[t][e] = acc[e];
+    S.cont_pres[t] = pres;
+  }
+  __syncthreads();
+  if (heads) {  // the last run begun here may continue into the next threads
+    const int ntot = (nval + IT - 1) / IT;
+    for (int u = t + 1; u < ntot; ++u) {
+      // thread u's leading piece belongs to this run unless u starts with a head
+      const unsigned uh = S.has_head[u];
+      const int upos = u * IT;
+      (void)upos;
+#pragma unroll
+      for (int e = 0; e < NV; ++e) acc[e] += S.cont[u][e];
+      pres |= S.cont_pres[u];
+      if (uh) break;
+    }
+    if (fits) flush(seg, wseg);
   }
 }
 
@@ -1534,7 +1845,6 @@ long long alg_flops(const Params& P, const unsigned long long* c, int part) {
 template <int KID>
 nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long nF, const int2* lp,
                       long long nP, VisitOut O, cudaEvent_t ev_mid) {
-  constexpr long long E = KTraits<KID>::E;
   O.vofs = 0;
   O.nlist = nF;
   if (nF) {
@@ -1543,12 +1853,11 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long n
   }
   CK(cudaEventRecord(ev_mid, pl->stream));
   O.vofs = nF;
-  O.cbase += 2 * E * nF;
   O.nlist = nP;
   if (nP) {
     const long long chunks = (nP + 1) / 2;
     const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
-    const int smem = 4 * (int)sizeof(ClipWarp<KID>);
+    const int smem = kClipWarps * (int)sizeof(ClipWarp<KID>) + (int)sizeof(ClipQueue);
     CK(cudaFuncSetAttribute(k_clipped<KID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_clipped<KID><<<g, 128, smem, pl->stream>>>(P, lp, O);
     LAUNCHED();
@@ -1709,7 +2018,7 @@ __global__ void k_window_compact(const unsigned long long* __restrict__ keys, co
 // sums its values in COO position order -> CSR rows of this batch.
 template <typename KT>
 nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64, double* vals, long long coo,
-                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept) {
+                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept, bool prereduce) {
   int bits = 1;
   {
     const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
@@ -1717,7 +2026,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
   }
   // ---- window pre-reduction + compaction (deterministic)
   DevBuf wk, wv, wc, wo;
-  if (coo > kWin) {
+  if (prereduce && coo > kWin) {
     const long long nwin = (coo + kWin - 1) / kWin;
     CK(wk.alloc(sizeof(unsigned long long) * nwin * kWin, s));
     CK(wv.alloc(sizeof(double) * nwin * kWin, s));
@@ -1969,9 +2278,13 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   const int NC = P.nc;
   const long long E = 9LL * NC * NC;
   {
-    const long long coo_ub = (long long)nR * E + nUB * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
-    const long long bytes = coo_ub * 16 * 2 + nUB * 2 * (E * 8 + 8) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
-                            nUB * 16 + coo_ub * 8 * 3;
+    // kkv + klv + kkf per record side, the reduced COO (own blocks, singular
+    // slots, stage-R runs at kRunFrac of the record values) with its sort
+    // buffers, lists and indices
+    const long long coo_ub = (long long)nR * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC +
+                             (long long)(kRunFrac * (double)(nUB * 2 * E)) + 1;
+    const long long bytes = nUB * 2 * (E * 16 + 8) + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
+                            nUB * 24;
     if (budget > 0 && bytes > budget && row_hi - row_lo > 1) {
       *need_split = true;
       return NLG_OK;
@@ -2067,18 +2380,20 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   LAUNCHED();
   CK(cudaEventRecord(ev[1], s));
   // ---- integrate
-  DevBuf keys, vals, kkv, kkf;
-  CK(keys.alloc(sizeof(unsigned long long) * coo, s));
-  CK(vals.alloc(sizeof(double) * coo, s));
+  const long long nsing_slots = (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
+  const long long r_base = (long long)nR * E + nsing_slots;
+  const long long r_cap = (long long)(kRunFrac * (double)(nvis * 2 * E)) + 1;
+  DevBuf keys, vals, kkv, kkf, klv;
+  CK(keys.alloc(sizeof(unsigned long long) * (r_base + r_cap), s));
+  CK(vals.alloc(sizeof(double) * (r_base + r_cap), s));
   CK(kkv.alloc(sizeof(double) * 2 * E * std::max(nvis, 1LL), s));
   CK(kkf.alloc(sizeof(unsigned long long) * 2 * std::max(nvis, 1LL), s));
+  CK(klv.alloc(sizeof(double) * 2 * E * std::max(nvis, 1LL), s));
   VisitOut O;
   O.kkv = kkv.as<double>();
   O.kkf = kkf.as<unsigned long long>();
+  O.klv = klv.as<double>();
   O.nvis = nvis;
-  O.keys = keys.as<unsigned long long>();
-  O.vals = vals.as<double>();
-  O.cbase = (long long)nR * E;
   O.counters = d_counters;
   O.errpair = d_err;
   nlg_status rc = NLG_OK;
@@ -2090,35 +2405,95 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   }
   if (rc) return rc;
   CK(cudaEventRecord(ev[3], s));
-  const long long sbase = (long long)nR * E + nvis * 2 * E;
+  unsigned long long* ckeys = keys.as<unsigned long long>();
+  double* cvals = vals.as<double>();
+  const long long sbase = (long long)nR * E;
   switch (P.kid) {
-    case 0: rc = run_singular<0>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
-    case 1: rc = run_singular<1>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
-    case 2: rc = run_singular<2>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
-    default: rc = run_singular<3>(pl, P, ls, nS, O.keys, O.vals, sbase, d_counters, d_err); break;
+    case 0: rc = run_singular<0>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
+    case 1: rc = run_singular<1>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
+    case 2: rc = run_singular<2>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
+    default: rc = run_singular<3>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
   }
   if (rc) return rc;
   CK(cudaEventRecord(ev[4], s));
+  // ---- merge stage R: per-root reduction of the record blocks
+  long long r_total = 0;
   if (nR) {
-    const int g = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
-    if (NC == 1)
-      k_kk_reduce<9><<<std::max(g, 1), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), off.as<long long>(), nF,
-                                                     O.kkv, O.kkf, ritem.as<int>(), rstart.as<int>(), O.keys,
-                                                     O.vals, 0);
-    else
-      k_kk_reduce<36><<<std::max(g, 1), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), off.as<long long>(), nF,
-                                                      O.kkv, O.kkf, ritem.as<int>(), rstart.as<int>(), O.keys,
-                                                      O.vals, 0);
+    RootIn RI;
+    RI.roots = roots.as<int>();
+    RI.nR = nR;
+    RI.cnt = cnt.as<int>();
+    RI.off = off.as<long long>();
+    RI.nF = nF;
+    RI.rec = lf;
+    RI.rev_item = ritem.as<int>();
+    RI.rev_start = rstart.as<int>();
+    RI.kkv = O.kkv;
+    RI.kkf = O.kkf;
+    RI.klv = O.klv;
+    DevBuf nch, cfirst, rstate;
+    CK(nch.alloc(sizeof(int) * (nR + 1), s));
+    CK(cfirst.alloc(sizeof(int) * (nR + 1), s));
+    // chunk upper bound: one per root plus the items beyond
+    const long long max_chunks = nR + (3 * 2 * nvis + kRootCap - 1) / kRootCap + 1;
+    CK(rstate.alloc(sizeof(unsigned long long) * (max_chunks + 4), s));
+    CK(cudaMemsetAsync(rstate.p, 0, sizeof(unsigned long long) * (max_chunks + 4), s));
+    CK(cudaMemsetAsync(nch.as<int>() + nR, 0, sizeof(int), s));
+    k_root_chunks<<<grid_for(nR, 256), 256, 0, s>>>(RI, nch.as<int>());
     LAUNCHED();
+    {
+      size_t tb = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, nch.as<int>(), cfirst.as<int>(), nR + 1, s));
+      DevBuf tmp;
+      CK(tmp.alloc(tb, s));
+      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, nch.as<int>(), cfirst.as<int>(), nR + 1, s));
+      g_launches += 1;
+    }
+    RI.chunk_first = cfirst.as<int>();
+    unsigned long long* st64 = rstate.as<unsigned long long>();
+    RootOut RO;
+    RO.lb = st64 + 4;
+    RO.ticket = (unsigned*)st64;  // st64[0]: ticket, st64[1]: overflow, st64[2]: total
+    RO.overflow = (int*)(st64 + 1);
+    RO.total = st64 + 2;
+    RO.keys = ckeys;
+    RO.vals = cvals;
+    RO.kk_base = 0;
+    RO.r_base = r_base;
+    RO.r_cap = r_cap;
+    int key_bits = 1;
+    while ((1LL << key_bits) - 1 < (long long)P.J / NC) ++key_bits;
+    if (key_bits > 31) { set_err("dof count too large for the run sort"); return NLG_ERR_CONFIG; }
+    if (NC == 1) {
+      const int smem = (int)sizeof(RootSmem<1>);
+      CK(cudaFuncSetAttribute(k_root_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_root_reduce<1><<<(unsigned)max_chunks, kRootThreads, smem, s>>>(P, RI, RO, key_bits);
+    } else {
+      const int smem = (int)sizeof(RootSmem<2>);
+      CK(cudaFuncSetAttribute(k_root_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_root_reduce<2><<<(unsigned)max_chunks, kRootThreads, smem, s>>>(P, RI, RO, key_bits);
+    }
+    LAUNCHED();
+    unsigned long long hst[3];
+    CK(cudaMemcpyAsync(hst, st64, sizeof hst, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    TRACE("stage R done");
+    if (hst[1] & 0xffffffffull) {  // the runs exceed the estimate: split the rows
+      if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
+      set_err("a single row exceeds the run buffer");
+      return NLG_ERR_CUDA;
+    }
+    r_total = (long long)hst[2];
   }
+  const long long coo_red = r_base + r_total;
   // ---- sort (row, col) keys (stable: equal keys keep COO position order), sum runs
   const long long nrows = row_hi - row_lo;
   Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
   long long nnz = 0;
   const bool narrow = (unsigned long long)nrows * (unsigned long long)P.J < 0xffffffffull;
   long long kept = 0;
-  rc = narrow ? merge_csr<unsigned>(s, P, O.keys, O.vals, coo, nrows, piece, nnz, &kept)
-              : merge_csr<unsigned long long>(s, P, O.keys, O.vals, coo, nrows, piece, nnz, &kept);
+  rc = narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false)
+              : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false);
   st->coo_reduced += kept;
   if (rc) return rc;
   piece.nnz = nnz;
@@ -2498,6 +2873,9 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     fprintf(stderr, "[nlg] clipped: %llu sub-triangles, %llu rounds, %llu chunks -> lane use %.3f\n",
             hc[K_DBG_SUBTRI], hc[K_DBG_ROUNDS], hc[K_DBG_CHUNKS],
             hc[K_DBG_ROUNDS] ? (double)hc[K_DBG_SUBTRI] / (32.0 * hc[K_DBG_ROUNDS]) : 0.0);
+  if (g_trace)
+    fprintf(stderr, "[nlg] clipped items: %llu, far %llu, inside %llu, nonempty %llu\n", hc[K_DBG_ITEMS],
+            hc[K_DBG_FAR], hc[K_DBG_INSIDE], hc[K_DBG_NONEMPTY]);
   st.alg_flops_full = alg_flops(pl->P, hc, 0);
   st.alg_flops_partial = alg_flops(pl->P, hc, 1);
   st.alg_flops_singular = alg_flops(pl->P, hc, 2);
