@@ -580,7 +580,7 @@ template <int KID>
 struct ClipWarp {
   double px[32][kMaxPoly], py[32][kMaxPoly];
   double sx[32][8], sy[32][8];  // clip scratch (<= 7 rows)
-  double sums[32][ClipCfg<KID>::NSUM];
+  double tile[32][ClipCfg<KID>::NSUM + 1];  // phase 2: one round's sub-triangle sums (padded rows)
   double xo[32][2];
   double W[32];
   double tri[2][2][8];  // [record slot][side]: o.x o.y e1x e1y e2x e2y idet
@@ -718,8 +718,6 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       S.vl[vs] = l;
       S.fl[vs] = flags;
     }
-#pragma unroll
-    for (int i = 0; i < C::NSUM; ++i) S.sums[lane][i] = 0.0;
     bool need_clip = false;
     int nv = 0;
     if (valid) {
@@ -842,6 +840,10 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       for (unsigned mm = mask; mm; mm &= mm - 1) S.queue[pos++] = (unsigned short)((lane << 4) | (__ffs(mm) - 1));
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int qs = incl - cnt, qe = incl;  // this item's sub-triangles in the queue
+    double si[C::NSUM];                    // and their sums
+#pragma unroll
+    for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
     if (g_trace_dev && lane == 0) {
       atomicAdd(&O.counters[K_DBG_SUBTRI], (unsigned long long)total);
       atomicAdd(&O.counters[K_DBG_ROUNDS], (unsigned long long)((total + 31) / 32));
@@ -914,22 +916,15 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         n_eval1 += mj == 1 ? ne * mlt : 0;
         n_eval2 += mj == 2 ? ne : 0;
       }
-      // segmented inclusive scan by item (queue is item-major), then the last
-      // lane of each segment adds into the item's row
+      // the round's sums go through shared memory; each item's lane adds the
+      // rows of its sub-triangles (the queue is item-major) in queue order
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int jo = __shfl_up_sync(0xffffffffu, j, o);
-        const bool same = lane >= o && jo == j;
+      for (int i = 0; i < C::NSUM; ++i) S.tile[lane][i] = sm[i];
+      __syncwarp();
+      const int p0 = max(qs, u0), p1 = min(qe, u0 + 32);
+      for (int pp = p0; pp < p1; ++pp) {
 #pragma unroll
-        for (int i = 0; i < C::NSUM; ++i) {
-          const double y = __shfl_up_sync(0xffffffffu, sm[i], o);
-          if (same) sm[i] += y;
-        }
-      }
-      const int jn = __shfl_down_sync(0xffffffffu, j, 1);
-      if (act && (lane == 31 || jn != j)) {
-#pragma unroll
-        for (int i = 0; i < C::NSUM; ++i) S.sums[j][i] += sm[i];
+        for (int i = 0; i < C::NSUM; ++i) si[i] += S.tile[pp - u0][i];
       }
       __syncwarp();
     }
@@ -939,9 +934,6 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     const bool ivalid = !(pmy & 0x80);
     const int mi = (pmy >> 4) & 3, pi = pmy & 15;
     const double Wi = ivalid ? S.W[lane] : 0.0;
-    double si[C::NSUM];
-#pragma unroll
-    for (int i = 0; i < C::NSUM; ++i) si[i] = ivalid ? S.sums[lane][i] : 0.0;
     if (next_ok) {
       ek = __ldg(&P.elem[prn.x]);
       el = __ldg(&P.elem[prn.y & kIdMask]);
@@ -1064,6 +1056,7 @@ struct RootIn {
   const unsigned long long* kkf;
   const double* klv;
   const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
+  const int* chunk_root;   // [chunks] root rank of each chunk
 };
 struct RootOut {
   unsigned* ticket;
@@ -1096,6 +1089,12 @@ __device__ __forceinline__ RootSides root_sides(const RootIn& I, int i) {
   R.r0 = I.rev_start[i];
   R.rn = I.rev_start[i + 1] - R.r0;
   return R;
+}
+
+__global__ void k_root_chunk_map(RootIn I, int* chunk_root) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I.nR) return;
+  for (int c = I.chunk_first[i]; c < I.chunk_first[i + 1]; ++c) chunk_root[c] = i;
 }
 
 __global__ void k_root_chunks(RootIn I, int* nch) {
@@ -1139,12 +1138,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
   const int ch = s_chunk;
   const int nchunks = I.chunk_first[I.nR];
   if (ch >= nchunks) return;  // surplus block of the upper-bound grid
-  int lo = 0, hi = I.nR - 1;  // root: last i with chunk_first[i] <= ch
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (I.chunk_first[mid] <= ch) lo = mid; else hi = mid - 1;
-  }
-  const int i = lo, c = ch - I.chunk_first[i];
+  const int i = I.chunk_root[ch], c = ch - I.chunk_first[i];
   const int k = I.roots[i];
   const RootSides R = root_sides(I, i);
   const long long n_rs = R.n(), nitems = 3 * n_rs;
@@ -1163,6 +1157,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = 0.0;
     unsigned long long fl = 0;
+#pragma unroll 2
     for (long long rs = t; rs < n_rs; rs += kRootThreads) {
       long long rec;
       int side;
@@ -1283,6 +1278,11 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
       }
     }
   };
+  // the value columns of this thread's positions, fetched while the block
+  // waits for its output offset
+#pragma unroll
+  for (int q = 0; q < IT; ++q)
+    if (q < npos) asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + (long long)col[q] * NV));
   __syncthreads();  // s_base, has_head
   const long long base = s_base;
   const bool fits = base + count <= O.r_cap;
@@ -2450,6 +2450,11 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       g_launches += 1;
     }
     RI.chunk_first = cfirst.as<int>();
+    DevBuf croot;
+    CK(croot.alloc(sizeof(int) * max_chunks, s));
+    k_root_chunk_map<<<grid_for(nR, 256), 256, 0, s>>>(RI, croot.as<int>());
+    LAUNCHED();
+    RI.chunk_root = croot.as<int>();
     unsigned long long* st64 = rstate.as<unsigned long long>();
     RootOut RO;
     RO.lb = st64 + 4;

@@ -58,11 +58,11 @@ template <int KID> struct KTraits {
 
 // kernel matrix at offset d = x - y (r2 = |d|^2): _engine._kernel_mat :30-43;
 // id 3 returns P = value(x, y) and Q = value(y, x) (_pyengine._pq :38-45).
-template <int KID>
+template <int KID, bool CBANK = true>
 __device__ __forceinline__ void kval(const Params& P, double x0, double y0, double d0, double d1,
                                      double r2, double* p, double* q) {
   if constexpr (KID == 0) {
-    p[0] = P.cst * fast_pow_pos(r2, P.kexp);
+    p[0] = P.cst * fast_pow_pos<CBANK>(r2, P.kexp);
   } else if constexpr (KID == 1) {
     const double f = P.cst / (r2 * sqrt(r2));
     const double v01 = f * d0 * d1;
@@ -150,7 +150,7 @@ __device__ __forceinline__ void full_pair2(const Params& P, const double* kx, co
       const double r2 = sumsq(d0, d1);
       if (rs2 > 0.0 && r2 < rs2) continue;
       double pv[NC2], qv[NC2];
-      kval<KID>(P, xk[p], xl[q], d0, d1, r2, pv, qv);
+      kval<KID, false>(P, xk[p], xl[q], d0, d1, r2, pv, qv);
       ++n_eval;
       const double wq = c_rule.iw[q];
 #pragma unroll

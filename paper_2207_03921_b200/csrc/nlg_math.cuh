@@ -48,7 +48,39 @@ __host__ __device__ __forceinline__ double fast_rcp(double d) {
 #endif
 }
 
+// series coefficients: atanh (1/21 ... 1/3), exp (1/12! ... 1/2), ln2 hi/lo, 1/ln2.
+// On the device they live in constant memory so every FMA takes its
+// coefficient as a constant-bank operand (a 64-bit immediate would cost two
+// register moves per FMA).
+#define NLG_POW_COEFFS                                                                                           \
+  {1.0 / 21.0, 1.0 / 19.0, 1.0 / 17.0, 1.0 / 15.0, 1.0 / 13.0, 1.0 / 11.0, 1.0 / 9.0, 1.0 / 7.0, 1.0 / 5.0,       \
+   1.0 / 3.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0, 1.0 / 5040.0, \
+   1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 6.93147180369123816490e-01, 1.90821492927058770002e-10,  \
+   1.44269504088896338700e+00}
+#ifdef __CUDACC__
+__constant__ double c_powk[24] = NLG_POW_COEFFS;
+#endif
+
+// coefficient i as a literal (folds to an immediate when i is a constant)
+__host__ __device__ constexpr double powk_lit(int i) {
+  constexpr double t[24] = NLG_POW_COEFFS;
+  return t[i];
+}
+
+// CBANK: coefficients from constant memory (loops that are not unrolled, where
+// 64-bit immediates are re-materialised per use) or as literals (fully
+// unrolled loops, where the compiler keeps them in registers).
+template <bool CBANK>
+__host__ __device__ __forceinline__ double powk(int i) {
+#ifdef __CUDA_ARCH__
+  if (CBANK) return c_powk[i];
+#endif
+  return powk_lit(i);
+}
+
+template <bool CBANK = true>
 __host__ __device__ __forceinline__ double fast_pow_pos(double x, double e) {
+#define K(i) powk<CBANK>(i)
   const uint64_t b = d2bits(x);
   int k = (int)((b >> 52) & 0x7ff) - 1023;
   uint64_t mb = (b & 0x000fffffffffffffull) | 0x3ff0000000000000ull;  // m in [1, 2)
@@ -60,39 +92,23 @@ __host__ __device__ __forceinline__ double fast_pow_pos(double x, double e) {
   const double z = (m - 1.0) * fast_rcp(m + 1.0);
   const double z2 = z * z;
   // atanh series: 2z (1 + z2/3 + z2^2/5 + ... + z2^10/21)
-  double s = 1.0 / 21.0;
-  s = fma(s, z2, 1.0 / 19.0);
-  s = fma(s, z2, 1.0 / 17.0);
-  s = fma(s, z2, 1.0 / 15.0);
-  s = fma(s, z2, 1.0 / 13.0);
-  s = fma(s, z2, 1.0 / 11.0);
-  s = fma(s, z2, 1.0 / 9.0);
-  s = fma(s, z2, 1.0 / 7.0);
-  s = fma(s, z2, 1.0 / 5.0);
-  s = fma(s, z2, 1.0 / 3.0);
+  double s = K(0);
+#pragma unroll
+  for (int i = 1; i < 10; ++i) s = fma(s, z2, K(i));
   const double lnm = fma(2.0 * z, s * z2, 2.0 * z);
-  const double ln2_hi = 6.93147180369123816490e-01;  // 0x3fe62e42fee00000
-  const double ln2_lo = 1.90821492927058770002e-10;
   const double kd = (double)k;
   // t = e * ln x; k*ln2_hi is exact for |k| < 2^11
-  const double t = e * (fma(kd, ln2_hi, fma(kd, ln2_lo, lnm)));
+  const double t = e * (fma(kd, K(21), fma(kd, K(22), lnm)));
   // exp(t) = 2^n exp(r), r = t - n ln2
-  const double n = rint(t * 1.44269504088896338700e+00);
-  const double r = fma(-n, ln2_lo, fma(-n, ln2_hi, t));
-  double p = 1.0 / 479001600.0;  // 1/12!
-  p = fma(p, r, 1.0 / 39916800.0);
-  p = fma(p, r, 1.0 / 3628800.0);
-  p = fma(p, r, 1.0 / 362880.0);
-  p = fma(p, r, 1.0 / 40320.0);
-  p = fma(p, r, 1.0 / 5040.0);
-  p = fma(p, r, 1.0 / 720.0);
-  p = fma(p, r, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
+  const double n = rint(t * K(23));
+  const double r = fma(-n, K(22), fma(-n, K(21), t));
+  double p = K(10);
+#pragma unroll
+  for (int i = 11; i < 21; ++i) p = fma(p, r, K(i));
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   return bits2d(d2bits(p) + ((uint64_t)(int64_t)n << 52));
+#undef K
 }
 
 }  // namespace nlg
