@@ -14,7 +14,7 @@ import numpy as np
 from .errors import ConfigurationError, DeviceError, NumericalError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnlg.so")
+LIB_PATH = os.environ.get("NLG_LIBRARY") or os.path.join(_HERE, "libnlg.so")
 
 NLG_OK, NLG_ERR_CONFIG, NLG_ERR_NUMERICAL, NLG_ERR_CUDA = 0, 1, 2, 3
 

@@ -580,21 +580,23 @@ template <int KID>
 struct ClipWarp {
   double px[32][kMaxPoly], py[32][kMaxPoly];
   double sx[32][8], sy[32][8];  // clip scratch (<= 7 rows)
-  double tile[32][ClipCfg<KID>::NSUM + 1];  // phase 2: one round's sub-triangle sums (padded rows)
   double xo[32][2];
   double W[32];
   double tri[2][2][8];  // [record slot][side]: o.x o.y e1x e1y e2x e2y idet
   double tv[2][2][6];   // [record slot][side]: the inner triangle's vertices x0 x1 x2 y0 y1 y2
   double rs2[2];
-  unsigned short queue[32 * 7];  // (item << 4) | t of every kept sub-triangle, item-major
   unsigned char pm[32];
   unsigned char nv[32];  // polygon rows of each item
   int vk[2], vl[2], fl[2];  // per record slot
 };
 constexpr int kClipWarps = 4;
-struct ClipQueue {  // block-wide queue of the items that need a real clip
-  int n[2];  // by chunk parity: reset one chunk ahead, race-free
-  unsigned char item[32 * kClipWarps];  // (warp << 5) | lane
+template <int KID>
+struct ClipBlock {  // block-wide work queues
+  int n[2];                                 // clip queue length, by chunk parity (reset one chunk ahead)
+  int wtot[kClipWarps];                     // sub-triangles per warp
+  unsigned char item[32 * kClipWarps];      // clip queue: (warp << 5) | lane
+  unsigned short sub[32 * kClipWarps * 7];  // sub-triangle queue: (item << 4) | t, item-major
+  double tile[32 * kClipWarps][ClipCfg<KID>::NSUM + 1];  // one round's sub-triangle sums (padded rows)
 };
 
 // (I, J) of the u-th unique entry of a symmetric n x n block, I <= J
@@ -657,7 +659,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
   constexpr int NC = T::NC, NC2 = T::NC2, N3 = 3 * NC;
   extern __shared__ __align__(16) unsigned char clip_smem[];
   ClipWarp<KID>* SW = reinterpret_cast<ClipWarp<KID>*>(clip_smem);
-  ClipQueue& CQ = *reinterpret_cast<ClipQueue*>(clip_smem + kClipWarps * sizeof(ClipWarp<KID>));
+  ClipBlock<KID>& CQ = *reinterpret_cast<ClipBlock<KID>*>(clip_smem + kClipWarps * sizeof(ClipWarp<KID>));
   ClipWarp<KID>& S = SW[threadIdx.x >> 5];
   const int lane = lane_id();
   const long long nchunks = (O.nlist + 1) / 2;
@@ -811,7 +813,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
     }
     __syncthreads();
     par ^= 1;
-    // ---------------- phase 1c: fan sub-triangles of each item -> warp queue
+    // ---------------- phase 1c: fan sub-triangles of each item -> block queue
     unsigned mask = 0;
     nv = S.nv[lane];
     if (nv >= 3) {
@@ -835,40 +837,50 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    {
-      int pos = incl - cnt;
-      for (unsigned mm = mask; mm; mm &= mm - 1) S.queue[pos++] = (unsigned short)((lane << 4) | (__ffs(mm) - 1));
+    if (lane == 31) CQ.wtot[wib] = incl;
+    __syncthreads();
+    int total = 0, wofs = 0;
+#pragma unroll
+    for (int w = 0; w < kClipWarps; ++w) {
+      const int c = CQ.wtot[w];
+      wofs += w < wib ? c : 0;
+      total += c;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const int qs = incl - cnt, qe = incl;  // this item's sub-triangles in the queue
-    double si[C::NSUM];                    // and their sums
+    const int qs = wofs + incl - cnt, qe = wofs + incl;  // this item's sub-triangles in the queue
+    {
+      int pos = qs;
+      const int it = ((int)wib << 5) | lane;
+      for (unsigned mm = mask; mm; mm &= mm - 1) CQ.sub[pos++] = (unsigned short)((it << 4) | (__ffs(mm) - 1));
+    }
+    double si[C::NSUM];  // and their sums
 #pragma unroll
     for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
-    if (g_trace_dev && lane == 0) {
+    if (g_trace_dev && threadIdx.x == 0) {
       atomicAdd(&O.counters[K_DBG_SUBTRI], (unsigned long long)total);
-      atomicAdd(&O.counters[K_DBG_ROUNDS], (unsigned long long)((total + 31) / 32));
+      atomicAdd(&O.counters[K_DBG_ROUNDS], (unsigned long long)((total + 127) / 128));
       atomicAdd(&O.counters[K_DBG_CHUNKS], 1ull);
     }
-    __syncwarp();
-    // ---------------- phase 2: one queued sub-triangle per lane, 7 inner points
-    for (int u0 = 0; u0 < ((P.dbg & 1) ? 0 : total); u0 += 32) {
-      const int u = u0 + lane;
-      const bool act = u < total;
-      const int ent = act ? S.queue[u] : 0;
-      const int j = act ? ent >> 4 : -1 - lane;  // inactive lanes: unique segment ids
+    __syncthreads();
+    // ---------------- phase 2: the block's lanes take one queued sub-triangle
+    // each and integrate its 7 inner points
+    constexpr int BT = kClipWarps * 32;
+    for (int u0 = 0; u0 < ((P.dbg & 1) ? 0 : total); u0 += BT) {
+      const int u = u0 + (int)threadIdx.x;
       double sm[C::NSUM];
 #pragma unroll
       for (int i = 0; i < C::NSUM; ++i) sm[i] = 0.0;
-      if (act) {
-        const int t = ent & 15;
-        const int mj = (S.pm[j] >> 4) & 3, vsj = j >> 4;
-        const double q0x = S.px[j][0], q0y = S.py[j][0];
-        const double ax = S.px[j][t] - q0x, ay = S.py[j][t] - q0y;
-        const double bx = S.px[j][t + 1] - q0x, by = S.py[j][t + 1] - q0y;
+      if (u < total) {
+        const int ent = CQ.sub[u];
+        const int t = ent & 15, it = ent >> 4, j = it & 31;
+        const ClipWarp<KID>& R = SW[it >> 5];
+        const int mj = (R.pm[j] >> 4) & 3, vsj = j >> 4;
+        const double q0x = R.px[j][0], q0y = R.py[j][0];
+        const double ax = R.px[j][t] - q0x, ay = R.py[j][t] - q0y;
+        const double bx = R.px[j][t + 1] - q0x, by = R.py[j][t + 1] - q0y;
         const double jac2 = cross2(ax, by, ay, bx);
-        const double x0 = S.xo[j][0], x1 = S.xo[j][1];
-        const double rs2 = S.rs2[vsj];
-        const double* tr = S.tri[vsj][mj == 1];
+        const double x0 = R.xo[j][0], x1 = R.xo[j][1];
+        const double rs2 = R.rs2[vsj];
+        const double* tr = R.tri[vsj][mj == 1];
         const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
         // barycentric coordinates of the inner triangle are affine along the
         // sub-triangle: xi(q) = xi(q0) + ip0 dxi(a) + ip1 dxi(b)
@@ -911,7 +923,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
             }
           }
         }
-        const int mlt = mj == 2 ? 1 : ((S.fl[vsj] & kEmitA) ? 1 : 0) + ((S.fl[vsj] & kEmitB) ? 1 : 0);
+        const int mlt = mj == 2 ? 1 : ((R.fl[vsj] & kEmitA) ? 1 : 0) + ((R.fl[vsj] & kEmitB) ? 1 : 0);
         n_eval0 += mj == 0 ? ne * mlt : 0;
         n_eval1 += mj == 1 ? ne * mlt : 0;
         n_eval2 += mj == 2 ? ne : 0;
@@ -919,14 +931,14 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       // the round's sums go through shared memory; each item's lane adds the
       // rows of its sub-triangles (the queue is item-major) in queue order
 #pragma unroll
-      for (int i = 0; i < C::NSUM; ++i) S.tile[lane][i] = sm[i];
-      __syncwarp();
-      const int p0 = max(qs, u0), p1 = min(qe, u0 + 32);
+      for (int i = 0; i < C::NSUM; ++i) CQ.tile[threadIdx.x][i] = sm[i];
+      __syncthreads();
+      const int p0 = max(qs, u0), p1 = min(qe, u0 + BT);
       for (int pp = p0; pp < p1; ++pp) {
 #pragma unroll
-        for (int i = 0; i < C::NSUM; ++i) si[i] += S.tile[pp - u0][i];
+        for (int i = 0; i < C::NSUM; ++i) si[i] += CQ.tile[pp - u0][i];
       }
-      __syncwarp();
+      __syncthreads();
     }
     __syncthreads();
     // ---------------- phase 3: fold into both visits, reduce over the record's lanes
@@ -1857,7 +1869,7 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long n
   if (nP) {
     const long long chunks = (nP + 1) / 2;
     const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
-    const int smem = kClipWarps * (int)sizeof(ClipWarp<KID>) + (int)sizeof(ClipQueue);
+    const int smem = kClipWarps * (int)sizeof(ClipWarp<KID>) + (int)sizeof(ClipBlock<KID>);
     CK(cudaFuncSetAttribute(k_clipped<KID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_clipped<KID><<<g, 128, smem, pl->stream>>>(P, lp, O);
     LAUNCHED();
@@ -2242,15 +2254,15 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   }
   {
     size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int>(), off.as<long long>(), nR + 1, s));
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, tb, cnt.as<int>(), off.as<long long>(), cub::Sum(), 0LL, nR + 1, s));
     DevBuf tmp;
     CK(tmp.alloc(tb, s));
     for (int q = 0; q < 6; ++q) {
       // off[q] = exclusive scan of cnt[q] over nR+1 entries (last = total);
       // the (nR+1)-th input reads the next column's first entry, so scan nR
       // entries and write the total separately
-      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
-                                       off.as<long long>() + (size_t)q * (nR + 1), nR, s));
+      CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
+                                        off.as<long long>() + (size_t)q * (nR + 1), cub::Sum(), 0LL, nR, s));
       g_launches += 1;
     }
   }
@@ -2289,7 +2301,8 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       *need_split = true;
       return NLG_OK;
     }
-    if (coo_ub >= (1LL << 31)) {
+    // 32-bit sort payloads: record sides x 3 (stage R) and COO entries must fit
+    if (coo_ub >= (1LL << 31) || nUB * 6 >= (1LL << 32)) {
       if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
       set_err("a single row needs %lld COO slots", coo_ub);
       return NLG_ERR_CUDA;
@@ -2345,12 +2358,12 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   // actual per-root full / clipped counts -> offsets for the own-block reduction
   if (nR) {
     size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int>(), off.as<long long>(), nR, s));
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, tb, cnt.as<int>(), off.as<long long>(), cub::Sum(), 0LL, nR, s));
     DevBuf tmp;
     CK(tmp.alloc(tb, s));
     for (int q : {C_FULL, C_PART})
-      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
-                                       off.as<long long>() + (size_t)q * (nR + 1), nR, s));
+      CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
+                                        off.as<long long>() + (size_t)q * (nR + 1), cub::Sum(), 0LL, nR, s));
     g_launches += 2;
   }
   const long long nvis = nF + nPt;
@@ -2877,7 +2890,7 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   if (g_trace)
     fprintf(stderr, "[nlg] clipped: %llu sub-triangles, %llu rounds, %llu chunks -> lane use %.3f\n",
             hc[K_DBG_SUBTRI], hc[K_DBG_ROUNDS], hc[K_DBG_CHUNKS],
-            hc[K_DBG_ROUNDS] ? (double)hc[K_DBG_SUBTRI] / (32.0 * hc[K_DBG_ROUNDS]) : 0.0);
+            hc[K_DBG_ROUNDS] ? (double)hc[K_DBG_SUBTRI] / (32.0 * kClipWarps * hc[K_DBG_ROUNDS]) : 0.0);
   if (g_trace)
     fprintf(stderr, "[nlg] clipped items: %llu, far %llu, inside %llu, nonempty %llu\n", hc[K_DBG_ITEMS],
             hc[K_DBG_FAR], hc[K_DBG_INSIDE], hc[K_DBG_NONEMPTY]);
