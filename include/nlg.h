@@ -91,9 +91,10 @@ typedef struct nlg_stats {
   int64_t alg_flops;    /* reference-algorithmic FP64 flops, all phases */
   int64_t alg_flops_full, alg_flops_partial, alg_flops_singular; /* per integration kernel */
   int64_t coo_entries;  /* COO slots emitted by the integration kernels */
-  int64_t coo_reduced;  /* entries left after the window pre-reduction (globally sorted) */
+  int64_t coo_reduced;  /* entries left after the per-root reduction (globally sorted) */
   int64_t nnz;
   int64_t n_batches;
+  int64_t n_replans;    /* batch attempts that did not fit and were re-cut */
   int64_t err_k, err_l; /* first nonfinite pair (lexicographic min), or -1 */
   double ms_prep, ms_candidates, ms_full, ms_partial, ms_singular, ms_merge, ms_total;
   double ms_integrate_kernels; /* full + partial + singular kernel time */

@@ -46,7 +46,7 @@ class Problem(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "n_roots", "epi", "n_full", "n_partial", "n_singular", "inner_evals", "outer_nonempty",
-        "sing_points", "alg_flops", "alg_flops_full", "alg_flops_partial", "alg_flops_singular", "coo_entries", "coo_reduced", "nnz", "n_batches", "err_k", "err_l")] + [
+        "sing_points", "alg_flops", "alg_flops_full", "alg_flops_partial", "alg_flops_singular", "coo_entries", "coo_reduced", "nnz", "n_batches", "n_replans", "err_k", "err_l")] + [
         (n, ctypes.c_double) for n in (
             "ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge",
             "ms_total", "ms_integrate_kernels")]

@@ -149,7 +149,8 @@ __global__ void k_bounds(Params P, double2* ctr, double* rad, unsigned long long
 
 struct Grid {
   double ox, oy, cs;
-  int nx, ny;
+  double reach;  // candidate radius around a barycentre: prer + 2 r_max (widened)
+  int nx, ny, span;
   const int* __restrict__ start;  // [ncell + 1]
   const int* __restrict__ items;  // active element ids sorted by cell
 };
@@ -334,7 +335,7 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
 constexpr int kCatClip = 1 << 30;
 
 template <bool FILL>
-__global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
+__global__ void __launch_bounds__(256, 2) k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
                              const unsigned char* __restrict__ needA, const int* __restrict__ inR,
                              int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ comb,
                              int2* __restrict__ ls0, int2* __restrict__ ls1, int2* __restrict__ ls2) {
@@ -353,8 +354,10 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
       load_tri(P, k, kx, ky);
       rule_points(P, kx, ky, xk, yk);
     }
-    int ix = (int)floor((ck.x - G.ox) / G.cs), iy = (int)floor((ck.y - G.oy) / G.cs);
-    ix = min(max(ix, 0), G.nx - 1);
+    // candidate cells: those within G.reach of the root's barycentre (the
+    // grid pitch is half the reach: ~half the candidates of a 3x3 block of
+    // reach-sized cells)
+    int iy = (int)floor((ck.y - G.oy) / G.cs);
     iy = min(max(iy, 0), G.ny - 1);
     int c[7] = {0, 0, 0, 0, 0, 0, 0};
     long long base[4];
@@ -364,9 +367,16 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
       for (int j = 1; j < 4; ++j) base[j] = off[(long long)(C_SID + j - 1) * (nR + 1) + i];
     }
     int nfull = 0, nclip = 0;
-    for (int yy = max(iy - 1, 0); yy <= min(iy + 1, G.ny - 1); ++yy) {
-      const int c0 = G.start[yy * G.nx + max(ix - 1, 0)];
-      const int c1 = G.start[yy * G.nx + min(ix + 1, G.nx - 1) + 1];
+    for (int yy = max(iy - G.span, 0); yy <= min(iy + G.span, G.ny - 1); ++yy) {
+      const double ylo = G.oy + yy * G.cs, yhi = ylo + G.cs;
+      const double dy = ck.y < ylo ? ylo - ck.y : (ck.y > yhi ? ck.y - yhi : 0.0);
+      if (dy > G.reach) continue;
+      const double hw = sqrt(G.reach * G.reach - dy * dy);
+      const int x0 = max((int)floor((ck.x - hw - G.ox) / G.cs), 0);
+      const int x1 = min((int)floor((ck.x + hw - G.ox) / G.cs), G.nx - 1);
+      if (x0 > x1) continue;
+      const int c0 = G.start[yy * G.nx + x0];
+      const int c1 = G.start[yy * G.nx + x1 + 1];
       for (int j0 = c0; j0 < c1; j0 += 32) {
         const int j = j0 + lane;
         int cat = -1, fl = 0;
@@ -416,6 +426,31 @@ __global__ void k_candidates(Params P, Grid G, const int* __restrict__ roots, in
       }
     }
   }
+}
+
+// per-row cost of a batch attempt that does not fit (batch planning): each
+// root's memory (bytes), record and COO-slot counts go to its first in-range row
+__global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, const int* __restrict__ cnt,
+                            double rec_bytes, double sing_bytes, double root_bytes, double rec_slots,
+                            double sing_slots, unsigned long long* row_cost) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nR) return;
+  const int4 d = P.dofs[roots[i]];
+  const int da[3] = {d.x, d.y, d.z};
+  long long home = -1;
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < P.nc; ++c) {
+      const long long r = (long long)P.nc * da[a] + c;
+      if (r >= P.row_lo && r < P.row_hi && (home < 0 || r < home)) home = r;
+    }
+  if (home < 0) home = P.row_lo;
+  const long long rec = cnt[(long long)C_FULL * nR + i];
+  const long long sing = (long long)cnt[(long long)C_SID * nR + i] + cnt[(long long)C_SED * nR + i] +
+                         cnt[(long long)C_SVX * nR + i];
+  unsigned long long* rc = row_cost + 3 * (home - P.row_lo);
+  atomicAdd(&rc[0], (unsigned long long)(rec * rec_bytes + sing * sing_bytes + root_bytes));
+  atomicAdd(&rc[1], (unsigned long long)rec);
+  atomicAdd(&rc[2], (unsigned long long)(rec * rec_slots + sing * sing_slots + 9 * P.nc * P.nc));
 }
 
 struct IsRecord {
@@ -1779,12 +1814,15 @@ nlg_status prep(nlg_plan* pl) {
   CK(cudaStreamSynchronize(st));
   double ox = ord2d(h[0]), oy = ord2d(h[1]), mx = ord2d(h[2]), my = ord2d(h[3]), rmax = ord2d(h[4]);
   if (h[2] == 0ull) { ox = oy = mx = my = 0.0; rmax = 0.0; }  // no active element
-  double cs = (P.prer + 2.0 * rmax) * (1.0 + 1e-9) + 1e-300;
+  const double reach = (P.prer + 2.0 * rmax) * (1.0 + 1e-9) + 1e-300;
+  double cs = 0.5 * reach;
   // keep the cell count bounded (tiny horizons on huge meshes)
   const double ext_x = mx - ox, ext_y = my - oy;
   while ((ext_x / cs + 1.0) * (ext_y / cs + 1.0) > 6.0e7) cs *= 2.0;
   Grid G;
   G.ox = ox; G.oy = oy; G.cs = cs;
+  G.reach = reach;
+  G.span = (int)ceil(reach / cs);
   G.nx = (int)floor(ext_x / cs) + 1;
   G.ny = (int)floor(ext_y / cs) + 1;
   const int ncell = G.nx * G.ny;
@@ -2184,8 +2222,10 @@ struct Timing {
 // one row batch: returns NLG_OK and appends to `out`, or asks for a split
 nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget,
                      std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
-                     unsigned long long* d_counters, unsigned long long* d_err, bool* need_split) {
+                     unsigned long long* d_counters, unsigned long long* d_err, bool* need_split,
+                     std::vector<long long>* cuts) {
   *need_split = false;
+  cuts->clear();
   ArenaScope arena_scope(pl);
   Params P = pl->P;
   P.row_lo = row_lo;
@@ -2297,17 +2337,48 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
                              (long long)(kRunFrac * (double)(nUB * 2 * E)) + 1;
     const long long bytes = nUB * 2 * (E * 16 + 8) + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
                             nUB * 24;
-    if (budget > 0 && bytes > budget && row_hi - row_lo > 1) {
-      *need_split = true;
-      return NLG_OK;
-    }
     // 32-bit sort payloads: record sides x 3 (stage R) and COO entries must fit
-    if (coo_ub >= (1LL << 31) || nUB * 6 >= (1LL << 32)) {
-      if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
+    const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB * 6 >= (1LL << 32);
+    if (too_big && row_hi - row_lo <= P.nc) {
+      if (coo_ub < (1LL << 31) && nUB * 6 < (1LL << 32)) goto fits;  // one vertex's rows: try anyway
       set_err("a single row needs %lld COO slots", coo_ub);
       return NLG_ERR_CUDA;
     }
+    if (too_big) {
+      // plan the row cuts from this attempt's counts: per-row cost of the
+      // roots (at their first in-range row), greedy cuts at 70% of each limit
+      *need_split = true;
+      const long long nrows = row_hi - row_lo;
+      DevBuf rcost;
+      CK(rcost.alloc(sizeof(unsigned long long) * 3 * nrows, s));
+      CK(cudaMemsetAsync(rcost.p, 0, sizeof(unsigned long long) * 3 * nrows, s));
+      const double rec_bytes = 2.0 * (E * 16 + 8) + kRunFrac * 2 * E * 32 + 40;
+      const double sing_bytes = 36.0 * NC * NC * 32 + 8, root_bytes = E * 32.0 + 64;
+      if (nR)
+        k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, sing_bytes,
+                                                      root_bytes, kRunFrac * 2 * E, 36.0 * NC * NC,
+                                                      rcost.as<unsigned long long>());
+      LAUNCHED();
+      std::vector<unsigned long long> hcost((size_t)3 * nrows);
+      CK(cudaMemcpyAsync(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const double lim[3] = {budget > 0 ? 0.7 * (double)budget : 1e300, 0.7 * (double)(1LL << 32) / 6.0,
+                             0.7 * (double)(1LL << 31)};
+      double acc[3] = {0, 0, 0};
+      for (long long r = 0; r < nrows; ++r) {
+        const long long row = row_lo + r;
+        bool over = false;
+        for (int q = 0; q < 3; ++q) over |= acc[q] + (double)hcost[3 * r + q] > lim[q];
+        if (over && row % P.nc == 0 && row > row_lo && (cuts->empty() || cuts->back() < row)) {
+          cuts->push_back(row);
+          acc[0] = acc[1] = acc[2] = 0;
+        }
+        for (int q = 0; q < 3; ++q) acc[q] += (double)hcost[3 * r + q];
+      }
+      return NLG_OK;
+    }
   }
+fits:
   // EPI of the roots whose home is this batch: sum cnt[EPI] where cnt[KK] == 2
   {
     std::vector<int> hc((size_t)2 * nR);
@@ -2779,13 +2850,23 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     auto rg = todo.back();
     todo.pop_back();
     bool split = false;
+    std::vector<long long> cuts;
     rc = run_batch(pl, rg.first, rg.second, budget, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
-                   derr.as<unsigned long long>(), &split);
+                   derr.as<unsigned long long>(), &split, &cuts);
     if (rc) break;
     if (split) {
-      const long long mid = rg.first + (rg.second - rg.first) / 2;
-      todo.push_back({mid, rg.second});
-      todo.push_back({rg.first, mid});
+      if (cuts.empty()) cuts.push_back(rg.first + (rg.second - rg.first) / (2 * pl->P.nc) * pl->P.nc);
+      if (cuts.front() <= rg.first) cuts.front() = rg.first + pl->P.nc;
+      // ranges pushed in reverse so they run in row order
+      long long hi = rg.second;
+      for (size_t c = cuts.size(); c-- > 0;) {
+        if (cuts[c] > rg.first && cuts[c] < hi) {
+          todo.push_back({cuts[c], hi});
+          hi = cuts[c];
+        }
+      }
+      todo.push_back({rg.first, hi});
+      st.n_replans += 1;
     }
   }
   if (rc) {

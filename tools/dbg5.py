@@ -8,4 +8,4 @@ budget = int(float(sys.argv[2])) if len(sys.argv) > 2 else 0
 cfg = configs.build(5, grid_n=n)
 st = {}
 A = bfs_assemble(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad, mem_budget=budget, stats=st).matrix
-print("nnz", A.nnz, "batches", st["n_batches"], "coo", st["coo_entries"], st["coo_reduced"])
+print("nnz", A.nnz, "batches", st["n_batches"], "replans", st["n_replans"], "coo", st["coo_entries"], st["coo_reduced"])
