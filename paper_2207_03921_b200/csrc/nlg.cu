@@ -607,14 +607,14 @@ template <int KID> struct ClipCfg {
   static constexpr int NKL = 9 * NC * NC;
   static constexpr int NSIDE = NKK + NKL;
   static constexpr int NVAL = 2 * NSIDE;                 // sides A and B
-  static constexpr int NBATCH = (NVAL + 31) / 32;        // reduce-scatter batches of 32 values
   static constexpr int NSUM = NC2 * (SYM ? 10 : 13);     // S0, SyP[3], (SyQ[3]), Syy[6]
 };
 
-template <int KID>
+// SQ: the square ball needs clip scratch rows; the circle balls clip in place
+template <int KID, bool SQ>
 struct ClipWarp {
   double px[32][kMaxPoly], py[32][kMaxPoly];
-  double sx[32][8], sy[32][8];  // clip scratch (<= 7 rows)
+  double sx[SQ ? 32 : 1][kMaxPoly], sy[SQ ? 32 : 1][kMaxPoly];  // clip scratch (square ball)
   double xo[32][2];
   double W[32];
   double tri[2][2][8];  // [record slot][side]: o.x o.y e1x e1y e2x e2y idet
@@ -686,16 +686,17 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
     }
 }
 
-template <int KID>
-__global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
+template <int KID, bool SQ>
+__global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
   using X = SumIdx<KID>;
   constexpr int NC = T::NC, NC2 = T::NC2, N3 = 3 * NC;
   extern __shared__ __align__(16) unsigned char clip_smem[];
-  ClipWarp<KID>* SW = reinterpret_cast<ClipWarp<KID>*>(clip_smem);
-  ClipBlock<KID>& CQ = *reinterpret_cast<ClipBlock<KID>*>(clip_smem + kClipWarps * sizeof(ClipWarp<KID>));
-  ClipWarp<KID>& S = SW[threadIdx.x >> 5];
+  using CW = ClipWarp<KID, SQ>;
+  CW* SW = reinterpret_cast<CW*>(clip_smem);
+  ClipBlock<KID>& CQ = *reinterpret_cast<ClipBlock<KID>*>(clip_smem + kClipWarps * sizeof(CW));
+  CW& S = SW[threadIdx.x >> 5];
   const int lane = lane_id();
   const long long nchunks = (O.nlist + 1) / 2;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -838,12 +839,16 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
 #pragma unroll 1
       for (int qi = threadIdx.x; qi < nq; qi += kClipWarps * 32) {
         const int it = CQ.item[qi], j = it & 31;
-        ClipWarp<KID>& R = SW[it >> 5];
+        CW& R = SW[it >> 5];
         const int mj = (R.pm[j] >> 4) & 3;
         const double* tv = R.tv[j >> 4][mj == 1];
         const Tri Tq{tv[0], tv[1], tv[2], tv[3], tv[4], tv[5]};
-        R.nv[j] = (unsigned char)truncate_inner(Tq, R.xo[j][0], R.xo[j][1], P.delta, P.ball, S.sx[lane], S.sy[lane],
-                                                R.px[j], R.py[j]);
+        int nvq;
+        if constexpr (SQ)
+          nvq = truncate_inner(Tq, R.xo[j][0], R.xo[j][1], P.delta, P.ball, S.sx[lane], S.sy[lane], R.px[j], R.py[j]);
+        else
+          nvq = truncate_inner_inplace(Tq, R.xo[j][0], R.xo[j][1], P.delta, P.ball, R.px[j], R.py[j]);
+        R.nv[j] = (unsigned char)nvq;
       }
     }
     __syncthreads();
@@ -907,7 +912,7 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
       if (u < total) {
         const int ent = CQ.sub[u];
         const int t = ent & 15, it = ent >> 4, j = it & 31;
-        const ClipWarp<KID>& R = SW[it >> 5];
+        const CW& R = SW[it >> 5];
         const int mj = (R.pm[j] >> 4) & 3, vsj = j >> 4;
         const double q0x = R.px[j][0], q0y = R.py[j][0];
         const double ax = R.px[j][t] - q0x, ay = R.py[j][t] - q0y;
@@ -1004,8 +1009,9 @@ __global__ void __launch_bounds__(128, 4) k_clipped(Params P, const int2* __rest
         FB[i] = b0;
       }
     }
+    constexpr int NBATCH = (C::NVAL + 31) / 32;  // reduce-scatter batches of 32 values
 #pragma unroll
-    for (int bt = 0; bt < C::NBATCH; ++bt) {
+    for (int bt = 0; bt < NBATCH; ++bt) {
       double vals[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -1907,9 +1913,15 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long n
   if (nP) {
     const long long chunks = (nP + 1) / 2;
     const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
-    const int smem = kClipWarps * (int)sizeof(ClipWarp<KID>) + (int)sizeof(ClipBlock<KID>);
-    CK(cudaFuncSetAttribute(k_clipped<KID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_clipped<KID><<<g, 128, smem, pl->stream>>>(P, lp, O);
+    if (P.ball == 2) {
+      const int smem = kClipWarps * (int)sizeof(ClipWarp<KID, true>) + (int)sizeof(ClipBlock<KID>);
+      CK(cudaFuncSetAttribute(k_clipped<KID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_clipped<KID, true><<<g, 128, smem, pl->stream>>>(P, lp, O);
+    } else {
+      const int smem = kClipWarps * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
+      CK(cudaFuncSetAttribute(k_clipped<KID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_clipped<KID, false><<<g, 128, smem, pl->stream>>>(P, lp, O);
+    }
     LAUNCHED();
   }
   return NLG_OK;

@@ -122,6 +122,7 @@ __device__ __noinline__ int insert_caps(Tri T, const double* bx, const double* b
     return nb;
   }
   const double rad = mul(delta, 1.0 + kBallTieRel);
+  const double b0x = bx[0], b0y = by[0];  // (px, py) may overwrite it (in-place use below)
   // a cap needs a crossing followed (cyclically) by a crossing
   const unsigned next = (bflag >> 1) | ((bflag & 1u) << (nb - 1));
   double el0 = 0.0, el1 = 0.0, el2 = 0.0, href = 0.0;
@@ -141,11 +142,12 @@ __device__ __noinline__ int insert_caps(Tri T, const double* bx, const double* b
     py[n] = by[i];
     ++n;
     if (!((bflag >> i) & 1u) || !((bflag >> j) & 1u)) continue;
-    const double chx = bx[j] - bx[i], chy = by[j] - by[i];
+    const double bjx = j ? bx[j] : b0x, bjy = j ? by[j] : b0y;
+    const double chx = bjx - bx[i], chy = bjy - by[i];
     const double chord = sqrt(sumsq(chx, chy));
     if (chord < mul(kChordSkipRel, delta)) continue;
-    const double mx = __dsub_rn(mul(0.5, __dadd_rn(bx[i], bx[j])), cx);
-    const double my = __dsub_rn(mul(0.5, __dadd_rn(by[i], by[j])), cy);
+    const double mx = __dsub_rn(mul(0.5, __dadd_rn(bx[i], bjx)), cx);
+    const double my = __dsub_rn(mul(0.5, __dadd_rn(by[i], bjy)), cy);
     const double nd = sqrt(sumsq(mx, my));
     if (nd < mul(1e-14, delta)) continue;
     const double capx = __dadd_rn(cx, mul(rad, mx) / nd);
@@ -201,6 +203,17 @@ __device__ __noinline__ int clip_square(Tri T, double cx, double cy, double delt
   }
   if (nn >= 2 && fabs(px[0] - px[nn - 1]) <= dtol && fabs(py[0] - py[nn - 1]) <= dtol) --nn;
   return nn < 3 ? 0 : nn;
+}
+
+// Balls 0 / 1 without scratch rows: clip_circle writes its (<= 6) rows at
+// offset 4 of (px, py) and insert_caps compacts them to the front, adding
+// (<= 3) caps; output row n never passes input row 4 + i before reading it.
+__device__ __forceinline__ int truncate_inner_inplace(Tri T, double cx, double cy, double delta, int ball,
+                                                      double* px, double* py) {
+  unsigned f;
+  if (ball == 0) return clip_circle(T, cx, cy, delta, px, py, &f);
+  const int nb = clip_circle(T, cx, cy, delta, px + 4, py + 4, &f);
+  return insert_caps(T, px + 4, py + 4, f, nb, cx, cy, delta, px, py);
 }
 
 // The truncated inner region of triangle T seen from outer point (cx, cy),
