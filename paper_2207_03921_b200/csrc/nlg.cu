@@ -623,6 +623,7 @@ struct ClipWarp {
   unsigned char pm[32];
   unsigned char nv[32];  // polygon rows of each item
   int vk[2], vl[2], fl[2];  // per record slot
+  int4 ek[2], el[2];        // element records (vertices, label) of the slot's record
 };
 constexpr int kClipWarps = 4;
 template <int KID>
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
   const long long nchunks = (O.nlist + 1) / 2;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  long long n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;
+  unsigned n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;  // per thread: < 2^32
   const int vs = lane >> 4, r = lane & 15;
   if (threadIdx.x == 0) CQ.n[0] = 0;
   __syncthreads();
@@ -709,16 +710,18 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
   // software pipeline: the next chunk's records and element records are
   // fetched while the current chunk computes
   int2 pr = make_int2(0, 0);
-  int4 ek = make_int4(0, 0, 0, 0), el = ek;
   {
     const long long v0 = w0 * 2 + vs;
     if (v0 < O.nlist) {
       pr = list[v0];
       pr.x &= kIdMask;
-      ek = __ldg(&P.elem[pr.x]);
-      el = __ldg(&P.elem[pr.y & kIdMask]);
+      if (r == 0) {  // element records of the chunk's records, via shared memory
+        S.ek[vs] = __ldg(&P.elem[pr.x]);
+        S.el[vs] = __ldg(&P.elem[pr.y & kIdMask]);
+      }
     }
   }
+  __syncwarp();
   // block-uniform trip count: the block's warps run the phases in step (the
   // __syncthreads below keep their instruction footprint to one phase)
   const long long wib = threadIdx.x >> 5;
@@ -736,6 +739,7 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
     const bool vok = v < O.nlist;
     bool valid = vok && r < 14;
     const int k = pr.x, l = pr.y & kIdMask, flags = pr.y & ~kIdMask;
+    const int4 ek = S.ek[vs], el = S.el[vs];
     int m = r >= 7 ? 1 : 0;
     const int p = r % 7;
     if (valid && k == l) {
@@ -986,9 +990,9 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
     const bool ivalid = !(pmy & 0x80);
     const int mi = (pmy >> 4) & 3, pi = pmy & 15;
     const double Wi = ivalid ? S.W[lane] : 0.0;
-    if (next_ok) {
-      ek = __ldg(&P.elem[prn.x]);
-      el = __ldg(&P.elem[prn.y & kIdMask]);
+    if (next_ok && r == 0) {
+      S.ek[vs] = __ldg(&P.elem[prn.x]);
+      S.el[vs] = __ldg(&P.elem[prn.y & kIdMask]);
     }
     pr = prn;
     const double* ohi = c_rule.oh[pi];
@@ -1068,12 +1072,12 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
     }
     __syncwarp();
   }
-  warp_add_ll(n_eval0, &O.counters[K_EVAL_M0]);
-  warp_add_ll(n_out0, &O.counters[K_OUT_M0]);
-  warp_add_ll(n_eval1, &O.counters[K_EVAL_M1]);
-  warp_add_ll(n_out1, &O.counters[K_OUT_M1]);
-  warp_add_ll(n_eval2, &O.counters[K_EVAL_M2]);
-  warp_add_ll(n_out2, &O.counters[K_OUT_M2]);
+  warp_add_ll((unsigned long long)n_eval0, &O.counters[K_EVAL_M0]);
+  warp_add_ll((unsigned long long)n_out0, &O.counters[K_OUT_M0]);
+  warp_add_ll((unsigned long long)n_eval1, &O.counters[K_EVAL_M1]);
+  warp_add_ll((unsigned long long)n_out1, &O.counters[K_OUT_M1]);
+  warp_add_ll((unsigned long long)n_eval2, &O.counters[K_EVAL_M2]);
+  warp_add_ll((unsigned long long)n_out2, &O.counters[K_OUT_M2]);
 }
 
 // ---------------------------------------------------------------- per-root reduction

@@ -57,7 +57,7 @@ __device__ __forceinline__ void push_dedup(double* ox, double* oy, unsigned& fla
 // clip_circle: vertices of the convex CCW triangle T inside the closed disk
 // around (cx, cy) plus edge/circle crossings; bit i of *flags_out marks row i
 // as a crossing.  Returns the row count (< 3: empty/degenerate).
-__device__ __noinline__ int clip_circle(Tri T, double cx, double cy, double delta, double* ox, double* oy,
+__device__ __forceinline__ int clip_circle(Tri T, double cx, double cy, double delta, double* ox, double* oy,
                                         unsigned* flags_out) {
   const double rad = mul(delta, 1.0 + kBallTieRel);
   const double r2 = mul(rad, rad);
@@ -115,7 +115,7 @@ __device__ __noinline__ int clip_circle(Tri T, double cx, double cy, double delt
 
 // insert_caps: copy the clip rows to (px, py), adding the arc midpoint behind
 // every chord between consecutive crossings when it lies inside the triangle.
-__device__ __noinline__ int insert_caps(Tri T, const double* bx, const double* by, unsigned bflag, int nb,
+__device__ __forceinline__ int insert_caps(Tri T, const double* bx, const double* by, unsigned bflag, int nb,
                                         double cx, double cy, double delta, double* px, double* py) {
   if (nb < 2) {
     for (int i = 0; i < nb; ++i) { px[i] = bx[i]; py[i] = by[i]; }
