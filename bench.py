@@ -155,6 +155,32 @@ def run_reference(args, cfg, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+
+_KERNEL_OF_PHASE = {"pair_full": "k_full", "pair_clipped": "k_clipped", "touching_singular": "k_singular"}
+
+
+def _ncu_traffic(phase, config):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the
+    newest committed `ncu --set full` summary of config 2 (profiles/); None
+    for other configs or when no summary exists."""
+    import glob
+    import re
+    if config != 2:
+        return None, None
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                          f"r*_{_KERNEL_OF_PHASE[phase]}_ncu_summary.txt")))
+    if not files:
+        return None, None
+    txt = open(files[-1]).read()
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    total = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        m = re.search(rf"^{re.escape(key)}\s+([0-9.]+) (\w+)", txt, re.M)
+        if not m:
+            return None, None
+        total += float(m.group(1)) * scale.get(m.group(2), 1)
+    return total, os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -239,9 +265,10 @@ def main():
     dom_flops = st0[phases[dom][1]]
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
     integ_ms = float(np.mean([s["ms_integrate_kernels"] for s in stats]))
+    traffic, traffic_src = _ncu_traffic(dom, args.config)
     roofline = {
         "bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
-        "frac": achieved / peak_fp64 if peak_fp64 else None, "traffic": None,
+        "frac": achieved / peak_fp64 if peak_fp64 else None, "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": "measured DFMA microbenchmark (nlg_fp64_peak) on this GPU, this run",
         "alg_flops_per_launch": dom_flops, "kernel_ms": dom_ms,
         "all_integration": {"alg_flops": st0["alg_flops"], "ms": integ_ms,
