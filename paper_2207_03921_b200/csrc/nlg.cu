@@ -2,20 +2,24 @@
 // per-batch pipeline and the C ABI declared in include/nlg.h.
 //
 // Pipeline of one nlg_assemble call (rows [row_lo, row_hi)):
-//   prep      k_bounds (barycentre/radius, assembly.py:130-134), k_bbox,
+//   prep      k_bounds (barycentre/radius, assembly.py:130-134),
 //             k_cell + radix sort + k_cell_ranges: uniform grid of
-//             barycentres with cell >= prer + 2 r_max (replaces the BFS of
+//             barycentres, pitch (prer + 2 r_max)/2 (replaces the BFS of
 //             _engine.py:530-599 with the exhaustive "brute" semantics,
 //             _engine.py:486-529, which the reference equals bitwise under
 //             its Assumption 4)
 //   batch     k_mark_*: owner-computes root selection for the row range
-//             k_count / k_fill: candidate pairs per root, split into full,
-//             clipped and singular (identical / edge / vertex) lists
-//             k_full, k_partial: one thread per visit (nlg_eval.cuh)
+//             k_candidates<count / fill>: pair records per root (each
+//             unordered pair once, serving both visits), split into full and
+//             clipped lists, plus singular (identical / edge / vertex) lists
+//             k_full: one thread per full record (7x7 point matrix)
+//             k_clipped: block-cooperative clipped records (clip queue,
+//             sub-triangle queue, fold)
 //             k_singular<U>: one CTA per touching pair, tensor rules
-//             k_kk_reduce: per-root, fixed-order sum of the root's own block
-//             radix sort of (row, col) keys + k_seg_* : deterministic
-//             segmented sum -> CSR (replaces _merge_triplets)
+//   merge     k_root_reduce (stage R): per-root block sort-reduce of the
+//             record blocks -> COO runs; radix sort of the (row, col) keys
+//             + k_seg_*: deterministic segmented sums -> CSR (replaces
+//             _merge_triplets, assembly.py:137-173)
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
