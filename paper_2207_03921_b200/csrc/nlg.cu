@@ -504,9 +504,8 @@ __device__ __forceinline__ void warp_add_ll(T v, unsigned long long* dst) {
 }
 
 struct VisitOut {
-  double* kkv;              // [record][side][E] own-block values of visit A (k, l) / B (l, k)
-  unsigned long long* kkf;  // [record][side] presence bits of those blocks
-  double* klv;              // [record][side][J][I] neighbour blocks, transposed (column-major):
+  double* kkv;              // [record][side][NKK] own blocks of visit A (k, l) / B (l, k), symmetric: I <= J
+  double* klv;              // [record][side][b][NVP] neighbour blocks, column-major and padded:
                             // the 3NC row values of one neighbour dof are contiguous
   long long nvis;           // records of both lists
   long long vofs;           // this list's first record index
@@ -515,21 +514,29 @@ struct VisitOut {
   unsigned long long* errpair;
 };
 
+// per-record-side block layouts: the own block is symmetric (I <= J, packed
+// in (I <= J) row-major order, presence = value != 0); the neighbour block is stored by
+// neighbour dof b as a 3nc x nc column (d * 3nc + I), padded to 32 B for nc = 1
+template <int NC> struct Blk {
+  static constexpr int N3 = 3 * NC, E = 9 * NC * NC, NKK = N3 * (N3 + 1) / 2;
+  static constexpr int NV = N3 * NC, NVP = NC == 1 ? 4 : NV, KLS = 3 * NVP;
+  __host__ __device__ static constexpr int sym(int I, int J) { return I * N3 - I * (I - 1) / 2 + (J - I); }
+  __host__ __device__ static constexpr int kl(int I, int J) { return (J / NC) * NVP + (J % NC) * N3 + I; }
+};
+
 // emit one side of a record: own block -> kkv, neighbour block -> klv
 template <int NC>
 __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long v, int side, bool on,
-                                          int root, int nb, const double* kk, const double* kl,
-                                          unsigned long long flags) {
-  constexpr int E = 9 * NC * NC, N3 = 3 * NC;
+                                          int root, int nb, const double* kk, const double* kl) {
+  using B = Blk<NC>;
   const long long vi = O.vofs + v;
-  O.kkf[vi * 2 + side] = on ? flags : 0ull;
   bool bad = false;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int I = e / N3, J = e % N3;
-    O.kkv[(vi * 2 + side) * E + e] = on ? kk[e] : 0.0;
+  for (int e = 0; e < B::E; ++e) {
+    const int I = e / B::N3, J = e % B::N3;
+    if (I <= J) O.kkv[(vi * 2 + side) * B::NKK + B::sym(I, J)] = on ? kk[e] : 0.0;
     bad |= nonfinite(kk[e]) | nonfinite(kl[e]);
-    O.klv[(vi * 2 + side) * E + J * N3 + I] = on ? emit_val(kl[e]) : 0.0;
+    O.klv[(vi * 2 + side) * B::KLS + B::kl(I, J)] = on ? emit_val(kl[e]) : 0.0;
   }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
 }
@@ -553,17 +560,13 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
                           ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
     const double rs2 = (touching && P.path == 1) ? P.rskip2 : 0.0;
     double kkA[E], klA[E], kkB[E], klB[E];
-    unsigned long long fA = 0, fB = 0;
     if (k == l) {
       // identical pair: both column halves of the reference's B hit k's dofs;
       // keep them apart for the per-triplet presence test (_engine.py:403-424)
       full_identical<KID>(P, kx, ky, rs2, kkA, klA, ev2);
       out2 += 7;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (kkA[e] != 0.0) fA |= 1ull << e;
-        kkB[e] = klB[e] = 0.0;
-      }
+      for (int e = 0; e < E; ++e) kkB[e] = klB[e] = 0.0;
     } else {
       load_tri(P, l, lx, ly);
       long long ne = 0;
@@ -572,14 +575,9 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
       const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
       ev0 += ne * mult;
       out0 += 14 * mult;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (kkA[e] != 0.0) fA |= 1ull << e;
-        if (kkB[e] != 0.0) fB |= 1ull << e;
-      }
     }
-    emit_side<NC>(P, O, v, 0, emitA, k, l, kkA, klA, fA);
-    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, kkB, klB, fB);
+    emit_side<NC>(P, O, v, 0, emitA, k, l, kkA, klA);
+    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, kkB, klB);
   }
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
   warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
@@ -638,13 +636,6 @@ struct ClipBlock {  // block-wide work queues
   unsigned short sub[32 * kClipWarps * 7];  // sub-triangle queue: (item << 4) | t, item-major
   double tile[32 * kClipWarps][ClipCfg<KID>::NSUM + 1];  // one round's sub-triangle sums (padded rows)
 };
-
-// (I, J) of the u-th unique entry of a symmetric n x n block, I <= J
-__device__ __forceinline__ void sym_ij(int u, int n, int& I, int& J) {
-  I = 0;
-  while (u >= n - I) { u -= n - I; ++I; }
-  J = I + u;
-}
 
 __device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 00 01 02 11 12 22
   const int i = a < b ? a : b, j = a < b ? b : a;
@@ -1000,7 +991,6 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
     }
     pr = prn;
     const double* ohi = c_rule.oh[pi];
-    unsigned long long fA = 0, fB = 0;
     const int rk = S.vk[vs], rl = S.vl[vs], rf = S.fl[vs];
     // side A (visit (k, l)) gets the fold of the sweep it calls mode 0 / 1,
     // side B (visit (l, k)) the other one; an identical pair (m = 2) gets both on A
@@ -1046,33 +1036,14 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
         const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
         const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
         const long long vi = O.vofs + v;
+        if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
         if (w < C::NKK) {
-          int I, J;
-          sym_ij(w, N3, I, J);
-          O.kkv[(vi * 2 + side) * (9 * NC2) + I * N3 + J] = on ? val : 0.0;
-          O.kkv[(vi * 2 + side) * (9 * NC2) + J * N3 + I] = on ? val : 0.0;
-          if (on) {
-            report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
-            if (val != 0.0) {
-              const unsigned long long bits = (1ull << (I * N3 + J)) | (1ull << (J * N3 + I));
-              if (side == 0) fA |= bits; else fB |= bits;
-            }
-          }
+          O.kkv[(vi * 2 + side) * Blk<NC>::NKK + w] = on ? val : 0.0;  // unique (I <= J) order
         } else {
           const int e = w - C::NKK, I = e / N3, J = e % N3;
-          if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
-          O.klv[(vi * 2 + side) * (9 * NC2) + J * N3 + I] = on ? emit_val(val) : 0.0;
+          O.klv[(vi * 2 + side) * Blk<NC>::KLS + Blk<NC>::kl(I, J)] = on ? emit_val(val) : 0.0;
         }
       }
-    }
-#pragma unroll
-    for (int o = 8; o; o >>= 1) {
-      fA |= __shfl_xor_sync(0xffffffffu, fA, o);
-      fB |= __shfl_xor_sync(0xffffffffu, fB, o);
-    }
-    if (r == 0 && vok) {
-      O.kkf[(O.vofs + v) * 2 + 0] = fA;
-      O.kkf[(O.vofs + v) * 2 + 1] = fB;
     }
     __syncwarp();
   }
@@ -1113,9 +1084,8 @@ struct RootIn {
   const int2* rec;  // full then clipped records
   const int* rev_item;
   const int* rev_start;
-  const double* kkv;
-  const unsigned long long* kkf;
-  const double* klv;
+  const double* kkv;  // [side][NKK]
+  const double* klv;  // [side][3][NVP]
   const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
   const int* chunk_root;   // [chunks] root rank of each chunk
 };
@@ -1212,24 +1182,28 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     const long long row = (long long)NC * dka[r / NC] + r % NC;
     if (row >= P.row_lo && row < P.row_hi) { inr |= 1u << r; ++nr; }
   }
-  // ---- the root's own block, by its first chunk
+  // ---- the root's own block (symmetric, packed), by its first chunk
   if (c == 0) {
-    double acc[E];
+    constexpr int NKK = Blk<NC>::NKK;
+    double acc[NKK];
 #pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = 0.0;
-    unsigned long long fl = 0;
+    for (int e = 0; e < NKK; ++e) acc[e] = 0.0;
+    unsigned fl = 0;  // presence: some side's value is nonzero
 #pragma unroll 2
     for (long long rs = t; rs < n_rs; rs += kRootThreads) {
       long long rec;
       int side;
       R.at(I, rs, rec, side);
-      const long long slot = rec * 2 + side;
-      fl |= __ldg(&I.kkf[slot]);
+      const double* src = I.kkv + (rec * 2 + side) * NKK;
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] += __ldg(&I.kkv[slot * E + e]);
+      for (int e = 0; e < NKK; ++e) {
+        const double v = __ldg(&src[e]);
+        acc[e] += v;
+        fl |= (v != 0.0 ? 1u : 0u) << e;
+      }
     }
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < NKK; ++e) {
       double v = acc[e];
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1237,14 +1211,15 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) fl |= __shfl_xor_sync(0xffffffffu, fl, o);
-    if (lane == 0 && fl) atomicOr(&s_fl, fl);
+    if (lane == 0 && fl) atomicOr(&s_fl, (unsigned long long)fl);
     __syncthreads();
     if (t < E) {
+      const int rr = t / N3, cc = t % N3;
+      const int u = Blk<NC>::sym(min(rr, cc), max(rr, cc));
       double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < NWARP; ++w) v += S.u.red[w][t];
-      const int rr = t / N3, cc = t % N3;
-      const bool present = I.cnt[(long long)C_KK * I.nR + i] != 0 && ((s_fl >> t) & 1ull);
+      for (int w = 0; w < NWARP; ++w) v += S.u.red[w][u];
+      const bool present = I.cnt[(long long)C_KK * I.nR + i] != 0 && ((s_fl >> u) & 1ull);
       const long long slot = O.kk_base + (long long)i * E + t;
       O.keys[slot] = present ? coo_key(P, (long long)NC * dka[rr / NC] + rr % NC, (long long)NC * dka[cc / NC] + cc % NC)
                              : kSentinel;
@@ -1343,7 +1318,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
   // waits for its output offset
 #pragma unroll
   for (int q = 0; q < IT; ++q)
-    if (q < npos) asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + (long long)col[q] * NV));
+    if (q < npos) asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + (long long)col[q] * Blk<NC>::NVP));
   __syncthreads();  // s_base, has_head
   const long long base = s_base;
   const bool fits = base + count <= O.r_cap;
@@ -1366,7 +1341,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
         for (int e = 0; e < NV; ++e) acc[e] = 0.0;
         pres = 0;
       }
-      const double* src = I.klv + (long long)col[q] * NV;
+      const double* src = I.klv + (long long)col[q] * Blk<NC>::NVP;
 #pragma unroll
       for (int e = 0; e < NV; ++e) {  // e = d * N3 + I
         const double v = __ldg(&src[e]);
@@ -2350,12 +2325,13 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   const int NC = P.nc;
   const long long E = 9LL * NC * NC;
   {
-    // kkv + klv + kkf per record side, the reduced COO (own blocks, singular
-    // slots, stage-R runs at kRunFrac of the record values) with its sort
-    // buffers, lists and indices
+    // kkv + klv per record side, the reduced COO (own blocks, singular slots,
+    // stage-R runs at kRunFrac of the record values) with its sort buffers,
+    // lists and indices
     const long long coo_ub = (long long)nR * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC +
                              (long long)(kRunFrac * (double)(nUB * 2 * E)) + 1;
-    const long long bytes = nUB * 2 * (E * 16 + 8) + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
+    const long long side_bytes = 8LL * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));  // kkv + klv
+    const long long bytes = nUB * 2 * side_bytes + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
                             nUB * 24;
     // 32-bit sort payloads: record sides x 3 (stage R) and COO entries must fit
     const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB * 6 >= (1LL << 32);
@@ -2372,7 +2348,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       DevBuf rcost;
       CK(rcost.alloc(sizeof(unsigned long long) * 3 * nrows, s));
       CK(cudaMemsetAsync(rcost.p, 0, sizeof(unsigned long long) * 3 * nrows, s));
-      const double rec_bytes = 2.0 * (E * 16 + 8) + kRunFrac * 2 * E * 32 + 40;
+      const double rec_bytes = 16.0 * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36)) + kRunFrac * 2 * E * 32 + 40;
       const double sing_bytes = 36.0 * NC * NC * 32 + 8, root_bytes = E * 32.0 + 64;
       if (nR)
         k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, sing_bytes,
@@ -2487,15 +2463,14 @@ fits:
   const long long nsing_slots = (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
   const long long r_base = (long long)nR * E + nsing_slots;
   const long long r_cap = (long long)(kRunFrac * (double)(nvis * 2 * E)) + 1;
-  DevBuf keys, vals, kkv, kkf, klv;
+  DevBuf keys, vals, kkv, klv;
   CK(keys.alloc(sizeof(unsigned long long) * (r_base + r_cap), s));
   CK(vals.alloc(sizeof(double) * (r_base + r_cap), s));
-  CK(kkv.alloc(sizeof(double) * 2 * E * std::max(nvis, 1LL), s));
-  CK(kkf.alloc(sizeof(unsigned long long) * 2 * std::max(nvis, 1LL), s));
-  CK(klv.alloc(sizeof(double) * 2 * E * std::max(nvis, 1LL), s));
+  const long long nkk = 3LL * NC * (3 * NC + 1) / 2, kls = NC == 1 ? 12 : 36;  // Blk<NC>::NKK, KLS
+  CK(kkv.alloc(sizeof(double) * 2 * nkk * std::max(nvis, 1LL), s));
+  CK(klv.alloc(sizeof(double) * 2 * kls * std::max(nvis, 1LL), s));
   VisitOut O;
   O.kkv = kkv.as<double>();
-  O.kkf = kkf.as<unsigned long long>();
   O.klv = klv.as<double>();
   O.nvis = nvis;
   O.counters = d_counters;
@@ -2533,7 +2508,6 @@ fits:
     RI.rev_item = ritem.as<int>();
     RI.rev_start = rstart.as<int>();
     RI.kkv = O.kkv;
-    RI.kkf = O.kkf;
     RI.klv = O.klv;
     DevBuf nch, cfirst, rstate;
     CK(nch.alloc(sizeof(int) * (nR + 1), s));
