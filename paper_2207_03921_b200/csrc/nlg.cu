@@ -609,7 +609,7 @@ template <int KID> struct ClipCfg {
   static constexpr int NKL = 9 * NC * NC;
   static constexpr int NSIDE = NKK + NKL;
   static constexpr int NVAL = 2 * NSIDE;                 // sides A and B
-  static constexpr int NSUM = NC2 * (SYM ? 10 : 13);     // S0, SyP[3], (SyQ[3]), Syy[6]
+  static constexpr int NSUM = NC2 * (SYM ? 7 : 10);      // S0, SyP[3], (SyQ[3]), Syy00 Syy01 Syy11
 };
 
 // SQ: the square ball needs clip scratch rows; the circle balls clip in place
@@ -642,14 +642,16 @@ __device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 0
   return i == 0 ? j : (i == 1 ? 2 + j : 5);
 }
 
-// layout of one item's sums: S0[NC2] | SyP[3][NC2] | SyQ[3][NC2] (nonsym) | Syy[6][NC2]
+// layout of one item's sums: S0[NC2] | SyP[3][NC2] | SyQ[3][NC2] (nonsym) | Syy3[3][NC2]
+// Only Syy_00, Syy_01, Syy_11 are accumulated: the hats sum to one, so
+// sum_b Syy_ab = SyQ_a and the other three follow (item_folds).
 template <int KID> struct SumIdx {
   static constexpr int NC2 = KTraits<KID>::NC2;
   static constexpr bool SYM = KTraits<KID>::SYM;
   __device__ static constexpr int s0(int i) { return i; }
   __device__ static constexpr int syp(int a, int i) { return NC2 + a * NC2 + i; }
   __device__ static constexpr int syq(int a, int i) { return SYM ? syp(a, i) : 4 * NC2 + a * NC2 + i; }
-  __device__ static constexpr int syy(int ab, int i) { return (SYM ? 4 : 7) * NC2 + ab * NC2 + i; }
+  __device__ static constexpr int syy3(int k, int i) { return (SYM ? 4 : 7) * NC2 + k * NC2 + i; }  // 00 01 11
 };
 
 // The two reference folds of one item's sums (_engine.py:154-184), as one
@@ -662,6 +664,14 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
   using X = SumIdx<KID>;
   constexpr int NC = C::NC, N3 = 3 * NC;
   const double Woh[3] = {W * oh[0], W * oh[1], W * oh[2]};
+  double syy[6][C::NC2];  // 00 01 02 11 12 22
+#pragma unroll
+  for (int cd = 0; cd < C::NC2; ++cd) {
+    const double s00 = s[X::syy3(0, cd)], s01 = s[X::syy3(1, cd)], s11 = s[X::syy3(2, cd)];
+    const double s02 = (s[X::syq(0, cd)] - s00) - s01, s12 = (s[X::syq(1, cd)] - s01) - s11;
+    syy[0][cd] = s00; syy[1][cd] = s01; syy[2][cd] = s02;
+    syy[3][cd] = s11; syy[4][cd] = s12; syy[5][cd] = (s[X::syq(2, cd)] - s02) - s12;
+  }
   int u = 0;
 #pragma unroll
   for (int I = 0; I < N3; ++I)
@@ -669,7 +679,7 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
     for (int J = I; J < N3; ++J) {
       const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
       F0[u] = (Woh[a] * oh[b]) * s[X::s0(cd)];
-      F1[u] = W * s[X::syy(sym3(a, b), cd)];
+      F1[u] = W * syy[sym3(a, b)][cd];
       ++u;
     }
 #pragma unroll
@@ -956,9 +966,14 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
             for (int a2 = 0; a2 < 3; ++a2) {
               sm[X::syp(a2, i)] = fma(tp, h[a2], sm[X::syp(a2, i)]);
               if (!T::SYM) sm[X::syq(a2, i)] = fma(tq, h[a2], sm[X::syq(a2, i)]);
-              const double g = tq * h[a2];
+              if (a2 < 2) {  // Syy_00, Syy_01, Syy_11 (the rest follow from sum_b h_b = 1)
+                const double g = tq * h[a2];
 #pragma unroll
-              for (int b2 = a2; b2 < 3; ++b2) sm[X::syy(sym3(a2, b2), i)] = fma(g, h[b2], sm[X::syy(sym3(a2, b2), i)]);
+                for (int b2 = a2; b2 < 2; ++b2) {
+                  const int k3 = a2 + b2;  // 00 -> 0, 01 -> 1, 11 -> 2
+                  sm[X::syy3(k3, i)] = fma(g, h[b2], sm[X::syy3(k3, i)]);
+                }
+              }
             }
           }
         }
