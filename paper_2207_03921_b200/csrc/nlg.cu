@@ -609,7 +609,7 @@ template <int KID> struct ClipCfg {
   static constexpr int NKL = 9 * NC * NC;
   static constexpr int NSIDE = NKK + NKL;
   static constexpr int NVAL = 2 * NSIDE;                 // sides A and B
-  static constexpr int NSUM = NC2 * (SYM ? 7 : 10);      // S0, SyP[3], (SyQ[3]), Syy00 Syy01 Syy11
+  static constexpr int NSUM = NC2 * (SYM ? 6 : 9);       // barycentric moments (SumIdx)
 };
 
 // SQ: the square ball needs clip scratch rows; the circle balls clip in place
@@ -642,16 +642,21 @@ __device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 0
   return i == 0 ? j : (i == 1 ? 2 + j : 5);
 }
 
-// layout of one item's sums: S0[NC2] | SyP[3][NC2] | SyQ[3][NC2] (nonsym) | Syy3[3][NC2]
-// Only Syy_00, Syy_01, Syy_11 are accumulated: the hats sum to one, so
-// sum_b Syy_ab = SyQ_a and the other three follow (item_folds).
+// An item's sums are barycentric moments of the weighted kernel values over
+// its sub-triangles' inner points, in the inner triangle's coordinates
+// (xi1, xi2) (hats h = (1 - xi1 - xi2, xi1, xi2)):
+//   P moments: M0 = sum tp, M1 = sum tp xi1, M2 = sum tp xi2
+//   Q moments: the same of tq, plus M11, M12, M22 = sum tq xi_a xi_b
+// (tq = tp for symmetric kernels, which share the first three).  The
+// reference's S0, Sy = sum t h_a and Syy = sum tq h_a h_b are linear in
+// these (item_folds); 8 FP64 ops per point instead of 13.
 template <int KID> struct SumIdx {
   static constexpr int NC2 = KTraits<KID>::NC2;
   static constexpr bool SYM = KTraits<KID>::SYM;
-  __device__ static constexpr int s0(int i) { return i; }
-  __device__ static constexpr int syp(int a, int i) { return NC2 + a * NC2 + i; }
-  __device__ static constexpr int syq(int a, int i) { return SYM ? syp(a, i) : 4 * NC2 + a * NC2 + i; }
-  __device__ static constexpr int syy3(int k, int i) { return (SYM ? 4 : 7) * NC2 + k * NC2 + i; }  // 00 01 11
+  __device__ static constexpr int mp(int k, int i) { return k * NC2 + i; }  // k: 0 -> M0, 1 -> M1, 2 -> M2
+  __device__ static constexpr int mq(int k, int i) {                        // k: 0..2 as mp, 3 M11, 4 M12, 5 M22
+    return SYM ? k * NC2 + i : (k < 3 ? (3 + k) * NC2 + i : (3 + k) * NC2 + i);
+  }
 };
 
 // The two reference folds of one item's sums (_engine.py:154-184), as one
@@ -664,13 +669,19 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
   using X = SumIdx<KID>;
   constexpr int NC = C::NC, N3 = 3 * NC;
   const double Woh[3] = {W * oh[0], W * oh[1], W * oh[2]};
-  double syy[6][C::NC2];  // 00 01 02 11 12 22
+  // moments -> S0, SyP_a, SyQ_a, Syy_ab (00 01 02 11 12 22)
+  double s0[C::NC2], syp[3][C::NC2], syq[3][C::NC2], syy[6][C::NC2];
 #pragma unroll
   for (int cd = 0; cd < C::NC2; ++cd) {
-    const double s00 = s[X::syy3(0, cd)], s01 = s[X::syy3(1, cd)], s11 = s[X::syy3(2, cd)];
-    const double s02 = (s[X::syq(0, cd)] - s00) - s01, s12 = (s[X::syq(1, cd)] - s01) - s11;
-    syy[0][cd] = s00; syy[1][cd] = s01; syy[2][cd] = s02;
-    syy[3][cd] = s11; syy[4][cd] = s12; syy[5][cd] = (s[X::syq(2, cd)] - s02) - s12;
+    const double p0 = s[X::mp(0, cd)], p1 = s[X::mp(1, cd)], p2 = s[X::mp(2, cd)];
+    const double q0 = s[X::mq(0, cd)], q1 = s[X::mq(1, cd)], q2 = s[X::mq(2, cd)];
+    s0[cd] = p0;
+    syp[0][cd] = (p0 - p1) - p2; syp[1][cd] = p1; syp[2][cd] = p2;
+    syq[0][cd] = (q0 - q1) - q2; syq[1][cd] = q1; syq[2][cd] = q2;
+    const double m11 = s[X::mq(3, cd)], m12 = s[X::mq(4, cd)], m22 = s[X::mq(5, cd)];
+    const double s01 = (q1 - m11) - m12, s02 = (q2 - m12) - m22;
+    syy[0][cd] = (syq[0][cd] - s01) - s02; syy[1][cd] = s01; syy[2][cd] = s02;
+    syy[3][cd] = m11; syy[4][cd] = m12; syy[5][cd] = m22;
   }
   int u = 0;
 #pragma unroll
@@ -678,7 +689,7 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
 #pragma unroll
     for (int J = I; J < N3; ++J) {
       const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
-      F0[u] = (Woh[a] * oh[b]) * s[X::s0(cd)];
+      F0[u] = (Woh[a] * oh[b]) * s0[cd];
       F1[u] = W * syy[sym3(a, b)][cd];
       ++u;
     }
@@ -687,8 +698,8 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
 #pragma unroll
     for (int J = 0; J < N3; ++J) {
       const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, cd = c * NC + d;
-      F0[C::NKK + I * N3 + J] = -Woh[a] * s[X::syq(b, cd)];
-      F1[C::NKK + I * N3 + J] = -Woh[b] * s[X::syp(a, cd)];
+      F0[C::NKK + I * N3 + J] = -Woh[a] * syq[b][cd];
+      F1[C::NKK + I * N3 + J] = -Woh[b] * syp[a][cd];
     }
 }
 
@@ -956,25 +967,26 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
           const double wq = c_rule.iw[q] * jac2;
           const double xi1 = fma(i1, z1b, fma(i0, z1a, z1));
           const double xi2 = fma(i1, z2b, fma(i0, z2a, z2));
-          const double h[3] = {1.0 - xi1 - xi2, xi1, xi2};
 #pragma unroll
           for (int i = 0; i < NC2; ++i) {
             const double tp = wq * pv[i];
             const double tq = T::SYM ? tp : wq * qv[i];
-            sm[X::s0(i)] += tp;
-#pragma unroll
-            for (int a2 = 0; a2 < 3; ++a2) {
-              sm[X::syp(a2, i)] = fma(tp, h[a2], sm[X::syp(a2, i)]);
-              if (!T::SYM) sm[X::syq(a2, i)] = fma(tq, h[a2], sm[X::syq(a2, i)]);
-              if (a2 < 2) {  // Syy_00, Syy_01, Syy_11 (the rest follow from sum_b h_b = 1)
-                const double g = tq * h[a2];
-#pragma unroll
-                for (int b2 = a2; b2 < 2; ++b2) {
-                  const int k3 = a2 + b2;  // 00 -> 0, 01 -> 1, 11 -> 2
-                  sm[X::syy3(k3, i)] = fma(g, h[b2], sm[X::syy3(k3, i)]);
-                }
-              }
+            const double g1 = tq * xi1, g2 = tq * xi2;
+            if (T::SYM) {
+              sm[X::mp(0, i)] += tp;
+              sm[X::mp(1, i)] += g1;
+              sm[X::mp(2, i)] += g2;
+            } else {
+              sm[X::mp(0, i)] += tp;
+              sm[X::mp(1, i)] = fma(tp, xi1, sm[X::mp(1, i)]);
+              sm[X::mp(2, i)] = fma(tp, xi2, sm[X::mp(2, i)]);
+              sm[X::mq(0, i)] += tq;
+              sm[X::mq(1, i)] += g1;
+              sm[X::mq(2, i)] += g2;
             }
+            sm[X::mq(3, i)] = fma(g1, xi1, sm[X::mq(3, i)]);
+            sm[X::mq(4, i)] = fma(g1, xi2, sm[X::mq(4, i)]);
+            sm[X::mq(5, i)] = fma(g2, xi2, sm[X::mq(5, i)]);
           }
         }
         const int mlt = mj == 2 ? 1 : ((R.fl[vsj] & kEmitA) ? 1 : 0) + ((R.fl[vsj] & kEmitB) ? 1 : 0);
