@@ -138,6 +138,11 @@ nlg_status nlg_load(nlg_plan *plan, const double *fx, int32_t fx_on_device, int3
 nlg_status nlg_load_const(nlg_plan *plan, const double *fconst, int32_t out_on_host,
                           nlg_alloc_fn alloc, void *user);
 
+/* Mass matrix over all dofs, J x J CSR (assembly.py:484-506: the exact P1
+ * element mass area * (1 + delta_ab) / 12 on every component of the active
+ * elements), written through alloc like nlg_assemble (which = 0, 1, 2). */
+nlg_status nlg_mass(nlg_plan *plan, int32_t out_on_host, nlg_alloc_fn alloc, void *alloc_user);
+
 /* DFMA throughput microbenchmark on `device` (the FP64 roofline denominator). */
 nlg_status nlg_fp64_peak(int32_t device, double *tflops);
 

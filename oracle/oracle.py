@@ -245,3 +245,25 @@ def assemble_load(mesh, ansatz, f, quad=None):
     lib().orc_assemble_load(E.shape[0], _p(V), _p(E), _p(Lb), _p(D), nc, op.shape[0],
                             _p(opc), _p(owc), _p(ohc), _p(fx), _p(b))
     return b
+
+
+def assemble_mass(mesh, ansatz):
+    """assembly.assemble_mass (:484-506) restated: per active element the
+    exact P1 mass block area * (1 + delta_ab) / 12 on each component, summed
+    into a J x J CSR.  Areas follow mesh.signed_areas (mesh.py:36-42)."""
+    nc = ansatz.n
+    active = np.flatnonzero(mesh.labels != 0)
+    E = mesh.elements[active]
+    p = [mesh.vertices[E[:, i]] for i in range(3)]
+    area = 0.5 * ((p[1][:, 0] - p[0][:, 0]) * (p[2][:, 1] - p[0][:, 1])
+                  - (p[1][:, 1] - p[0][:, 1]) * (p[2][:, 0] - p[0][:, 0]))
+    loc = np.array([[2.0, 1.0, 1.0], [1.0, 2.0, 1.0], [1.0, 1.0, 2.0]]) / 12.0
+    dk = ansatz.dof_map[active]
+    J = ansatz.dof_count
+    rows = np.concatenate([(nc * dk[:, a] + c) for c in range(nc) for a in range(3) for b in range(3)])
+    cols = np.concatenate([(nc * dk[:, b] + c) for c in range(nc) for a in range(3) for b in range(3)])
+    vals = np.concatenate([area * loc[a, b] for c in range(nc) for a in range(3) for b in range(3)])
+    m = sparse.coo_matrix((vals, (rows, cols)), shape=(J, J)).tocsr()
+    m.sum_duplicates()
+    m.sort_indices()
+    return m

@@ -1,7 +1,7 @@
 """B200-native nonlocal FE stiffness assembly (drop-in for nlfem's
 bfs_assemble / assemble_load hot path, arXiv 2207.03921)."""
 
-from .assembly import (AnsatzSpace, DevicePlan, SparseSystem, assemble_load, bfs_assemble,
+from .assembly import (AnsatzSpace, DevicePlan, SparseSystem, assemble_load, assemble_mass, bfs_assemble,
                        build_ansatz)
 from .errors import ConfigurationError, DeviceError, MeshFormatError, NumericalError
 from .geometry import BALL_IDS, BALL_KINDS, PairClass, classify_pair
@@ -12,7 +12,7 @@ from .mesh import (AdjacencyGraph, Label, Mesh, build_adjacency_graph, generate_
 from .quadrature import Path, QuadratureConfig, dispatch, gauss_legendre, rule_7point, singular_rule
 
 __all__ = [
-    "AnsatzSpace", "DevicePlan", "SparseSystem", "assemble_load", "bfs_assemble", "build_ansatz",
+    "AnsatzSpace", "DevicePlan", "SparseSystem", "assemble_load", "assemble_mass", "bfs_assemble", "build_ansatz",
     "ConfigurationError", "DeviceError", "MeshFormatError", "NumericalError",
     "BALL_IDS", "BALL_KINDS", "PairClass", "classify_pair",
     "KernelSpec", "affine_kernel", "constant_kernel", "constant_kernel_infinity",

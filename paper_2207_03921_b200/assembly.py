@@ -192,6 +192,14 @@ class DevicePlan:
                                         sink.callback, None), "nlg_load")
         return sink.array(3, np.float64, self.inp.n_dofs)
 
+    def mass(self, out_on_host=True):
+        sink = _native.OutputSink(out_on_host, self.device)
+        _native.check(self.lib.nlg_mass(self.handle, 1 if out_on_host else 0, sink.callback, None), "nlg_mass")
+        J = self.inp.n_dofs
+        indptr = sink.array(0, np.int64, J + 1)
+        nnz = int(indptr[-1]) if out_on_host else int(indptr[-1].item())
+        return indptr, sink.array(1, np.int32, nnz), sink.array(2, np.float64, nnz)
+
     def load_const(self, fvals, out_on_host=True):
         fv = np.ascontiguousarray(np.broadcast_to(np.asarray(fvals, dtype=np.float64), (self.inp.nc,)))
         sink = _native.OutputSink(out_on_host, self.device)
@@ -275,5 +283,17 @@ def assemble_load(mesh, ansatz, f, quad=None, *, device=0):
         plan.close()
 
 
-__all__ = ["AnsatzSpace", "build_ansatz", "SparseSystem", "bfs_assemble", "assemble_load",
+def assemble_mass(mesh, ansatz, *, device=0):
+    """Mass matrix over all dofs (scipy CSR, J x J) from the exact linear-element
+    formula, assembled on the GPU (assembly.py:484-506)."""
+    J = ansatz.dof_count
+    plan = DevicePlan(_dummy_inputs(mesh, ansatz, QuadratureConfig()), device=device)
+    try:
+        indptr, indices, data = plan.mass()
+    finally:
+        plan.close()
+    return csr_from_parts(indptr, indices, data, J, J, canonical=True)
+
+
+__all__ = ["AnsatzSpace", "build_ansatz", "SparseSystem", "bfs_assemble", "assemble_load", "assemble_mass",
            "DevicePlan", "csr_from_parts", "quad_arrays"]

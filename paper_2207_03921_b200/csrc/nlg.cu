@@ -1702,6 +1702,31 @@ __global__ void k_load_inc(Params P, const int* __restrict__ act, int nact, unsi
   item[t] = (int)t;  // m * 3 + a, element-major
 }
 
+// ---------------------------------------------------------------- mass matrix
+// assemble_mass (assembly.py:484-506): per active element the exact P1
+// block area * (1 + delta_ab) / 12 on every component, as COO for merge_csr.
+// area = signed_areas (mesh.py:36-42) in the reference's operation order.
+__global__ void k_mass(Params P, const int* __restrict__ act, int nact, unsigned long long* keys, double* vals) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nact) return;
+  const int k = act[t];
+  const int4 e = P.elem[k], d = P.dofs[k];
+  const double2 p0 = P.vtx[e.x], p1 = P.vtx[e.y], p2 = P.vtx[e.z];
+  const double area =
+      mul(0.5, __dsub_rn(mul(p1.x - p0.x, p2.y - p0.y), mul(p1.y - p0.y, p2.x - p0.x)));
+  const int da[3] = {d.x, d.y, d.z};
+  const int NC = P.nc;
+  const long long base = (long long)t * 9 * NC;
+  for (int c = 0; c < NC; ++c)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        const long long row = (long long)NC * da[a] + c, col = (long long)NC * da[b] + c;
+        const long long slot = base + c * 9 + a * 3 + b;
+        keys[slot] = (unsigned long long)row * (unsigned long long)P.J + (unsigned long long)col;
+        vals[slot] = mul(area, (a == b ? 2.0 : 1.0) / 12.0);
+      }
+}
+
 __global__ void k_active(Params P, int* flag) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < P.K) flag[k] = (P.elem[k].w & 15) != 0;
@@ -2626,6 +2651,88 @@ fits:
   return NLG_OK;
 }
 
+// Concatenate row-ordered CSR pieces into the caller's buffers (alloc which
+// = 0 indptr, 1 indices, 2 data), on the host through pinned staging and a
+// threaded copy when out_on_host; frees the pieces.
+nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces, long long row_lo, long long row_hi,
+                       int out_on_host, nlg_alloc_fn alloc, void* user, cudaEvent_t e_done, long long* nnz_out) {
+  cudaStream_t s = pl->stream;
+  long long nnz = 0;
+  for (auto& p : pieces) nnz += p.nnz;
+  const long long nrows = row_hi - row_lo;
+  long long* u_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
+  int* u_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
+  double* u_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
+  if (!u_ptr || !u_idx || !u_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  // host outputs: D2H into pinned staging (full PCIe/C2C speed), then a
+  // threaded copy into the caller's pageable buffers
+  long long* o_ptr = u_ptr;
+  int* o_idx = u_idx;
+  double* o_dat = u_dat;
+  const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
+               b_ptr = sizeof(long long) * (nrows + 1);
+  const size_t b_all = b_dat + ((b_idx + 15) & ~(size_t)15) + b_ptr;
+  if (out_on_host) {
+    if (ds.pinned_cap < b_all) {
+      if (ds.pinned) cudaFreeHost(ds.pinned);
+      ds.pinned = nullptr;
+      ds.pinned_cap = 0;
+      if (cudaHostAlloc((void**)&ds.pinned, b_all + b_all / 8, cudaHostAllocPortable) == cudaSuccess)
+        ds.pinned_cap = b_all + b_all / 8;
+      else
+        cudaGetLastError();
+    }
+    if (ds.pinned) {
+      o_dat = (double*)ds.pinned;
+      o_idx = (int*)(ds.pinned + b_dat);
+      o_ptr = (long long*)(ds.pinned + b_dat + ((b_idx + 15) & ~(size_t)15));
+    }
+  }
+  DevBuf ptrbuf;
+  CK(ptrbuf.alloc(sizeof(long long) * (nrows + 1), s));
+  long long run = 0;
+  for (auto& p : pieces) {
+    const long long nr = p.row_hi - p.row_lo;
+    if (run) {
+      k_add_offset<<<grid_for(nr + 1, 256), 256, 0, s>>>(p.indptr, nr + 1, run);
+      LAUNCHED();
+    }
+    CK(cudaMemcpyAsync(ptrbuf.as<long long>() + (p.row_lo - row_lo), p.indptr, sizeof(long long) * (nr + 1),
+                       cudaMemcpyDeviceToDevice, s));
+    if (p.nnz) {
+      CK(cudaMemcpyAsync(o_idx + run, p.indices, sizeof(int) * p.nnz, cudaMemcpyDefault, s));
+      CK(cudaMemcpyAsync(o_dat + run, p.data, sizeof(double) * p.nnz, cudaMemcpyDefault, s));
+    }
+    run += p.nnz;
+  }
+  if (nrows == 0) CK(cudaMemsetAsync(ptrbuf.p, 0, sizeof(long long), s));
+  CK(cudaMemcpyAsync(o_ptr, ptrbuf.p, sizeof(long long) * (nrows + 1), cudaMemcpyDefault, s));
+  if (e_done) CK(cudaEventRecord(e_done, s));
+  TRACE("outputs queued");
+  CK(cudaStreamSynchronize(s));
+  TRACE("outputs synced");
+  if (out_on_host && o_dat != u_dat) {  // pinned staging -> caller buffers
+    struct Part { void* dst; const void* src; size_t n; };
+    const Part parts[3] = {{u_dat, o_dat, b_dat}, {u_idx, o_idx, b_idx}, {u_ptr, o_ptr, b_ptr}};
+    const int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t]() {
+        for (const Part& q : parts) {
+          const size_t chunk = (q.n + nt - 1) / nt, a = std::min(q.n, chunk * t), b = std::min(q.n, a + chunk);
+          if (b > a) memcpy((char*)q.dst + a, (const char*)q.src + a, b - a);
+        }
+      });
+    for (auto& x : th) x.join();
+    TRACE("host copy done");
+  }
+
+  for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
+  pieces.clear();
+  *nnz_out = nnz;
+  return NLG_OK;
+}
+
 nlg_status upload_table(const double* h, size_t n, double** d, cudaStream_t s) {
   CK(cudaMallocAsync(d, sizeof(double) * std::max<size_t>(n, 1), s));
   if (n) CK(cudaMemcpyAsync(*d, h, sizeof(double) * n, cudaMemcpyHostToDevice, s));
@@ -2897,79 +3004,12 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   TRACE("batches done");
   // pieces are produced in ascending row order (ranges are popped low-first)
   long long nnz = 0;
-  for (auto& p : pieces) nnz += p.nnz;
-  const long long nrows = row_hi - row_lo;
-  long long* u_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
-  int* u_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
-  double* u_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
-  if (!u_ptr || !u_idx || !u_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
-  // host outputs: D2H into pinned staging (full PCIe/C2C speed), then a
-  // threaded copy into the caller's pageable buffers
-  long long* o_ptr = u_ptr;
-  int* o_idx = u_idx;
-  double* o_dat = u_dat;
-  const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
-               b_ptr = sizeof(long long) * (nrows + 1);
-  const size_t b_all = b_dat + ((b_idx + 15) & ~(size_t)15) + b_ptr;
-  if (out_on_host) {
-    if (ds.pinned_cap < b_all) {
-      if (ds.pinned) cudaFreeHost(ds.pinned);
-      ds.pinned = nullptr;
-      ds.pinned_cap = 0;
-      if (cudaHostAlloc((void**)&ds.pinned, b_all + b_all / 8, cudaHostAllocPortable) == cudaSuccess)
-        ds.pinned_cap = b_all + b_all / 8;
-      else
-        cudaGetLastError();
-    }
-    if (ds.pinned) {
-      o_dat = (double*)ds.pinned;
-      o_idx = (int*)(ds.pinned + b_dat);
-      o_ptr = (long long*)(ds.pinned + b_dat + ((b_idx + 15) & ~(size_t)15));
-    }
-  }
-  DevBuf ptrbuf;
-  CK(ptrbuf.alloc(sizeof(long long) * (nrows + 1), s));
-  long long run = 0;
-  for (auto& p : pieces) {
-    const long long nr = p.row_hi - p.row_lo;
-    if (run) {
-      k_add_offset<<<grid_for(nr + 1, 256), 256, 0, s>>>(p.indptr, nr + 1, run);
-      LAUNCHED();
-    }
-    CK(cudaMemcpyAsync(ptrbuf.as<long long>() + (p.row_lo - row_lo), p.indptr, sizeof(long long) * (nr + 1),
-                       cudaMemcpyDeviceToDevice, s));
-    if (p.nnz) {
-      CK(cudaMemcpyAsync(o_idx + run, p.indices, sizeof(int) * p.nnz, cudaMemcpyDefault, s));
-      CK(cudaMemcpyAsync(o_dat + run, p.data, sizeof(double) * p.nnz, cudaMemcpyDefault, s));
-    }
-    run += p.nnz;
-  }
-  if (nrows == 0) CK(cudaMemsetAsync(ptrbuf.p, 0, sizeof(long long), s));
-  CK(cudaMemcpyAsync(o_ptr, ptrbuf.p, sizeof(long long) * (nrows + 1), cudaMemcpyDefault, s));
-  CK(cudaEventRecord(e2, s));
-  TRACE("outputs queued");
+  rc = emit_pieces(pl, ds, pieces, row_lo, row_hi, out_on_host, alloc, user, e2, &nnz);
+  if (rc) return rc;
   unsigned long long hc[K_NCOUNTERS], herr;
   CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&herr, derr.p, sizeof herr, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  TRACE("outputs synced");
-  if (out_on_host && o_dat != u_dat) {  // pinned staging -> caller buffers
-    struct Part { void* dst; const void* src; size_t n; };
-    const Part parts[3] = {{u_dat, o_dat, b_dat}, {u_idx, o_idx, b_idx}, {u_ptr, o_ptr, b_ptr}};
-    const int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t)
-      th.emplace_back([&, t]() {
-        for (const Part& q : parts) {
-          const size_t chunk = (q.n + nt - 1) / nt, a = std::min(q.n, chunk * t), b = std::min(q.n, a + chunk);
-          if (b > a) memcpy((char*)q.dst + a, (const char*)q.src + a, b - a);
-        }
-      });
-    for (auto& x : th) x.join();
-    TRACE("host copy done");
-  }
-
-  for (auto& p : pieces) { cudaFreeAsync(p.indptr, s); cudaFreeAsync(p.indices, s); cudaFreeAsync(p.data, s); }
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   st.ms_prep = ms;
@@ -3134,6 +3174,45 @@ nlg_status nlg_load(nlg_plan* pl, const double* fx, int32_t fx_on_device, int32_
 
 nlg_status nlg_load_const(nlg_plan* pl, const double* fconst, int32_t out_on_host, nlg_alloc_fn alloc, void* user) {
   return load_impl(pl, fconst, 0, 1, out_on_host, alloc, user);
+}
+
+nlg_status nlg_mass(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc, void* user) {
+  if (!pl || !alloc) { set_err("null plan or allocator"); return NLG_ERR_CONFIG; }
+  CK(cudaSetDevice(pl->device));
+  if (pl->device < 0 || pl->device >= 64) { set_err("device index out of range"); return NLG_ERR_CONFIG; }
+  DeviceScratch& ds = g_scratch[pl->device];
+  std::lock_guard<std::mutex> scratch_lock(ds.mu);
+  nlg_status rc = ensure_active(pl);
+  if (rc) return rc;
+  cudaStream_t s = pl->stream;
+  Params P = pl->P;
+  P.row_lo = 0;
+  P.row_hi = P.J;
+  const long long coo = (long long)pl->nact * 9 * P.nc;
+  if (coo >= (1LL << 31)) { set_err("mesh too large for one mass-matrix batch"); return NLG_ERR_CONFIG; }
+  std::vector<Csr> pieces;
+  {
+    DevBuf keys, vals;
+    CK(keys.alloc(sizeof(unsigned long long) * std::max(coo, 1LL), s));
+    CK(vals.alloc(sizeof(double) * std::max(coo, 1LL), s));
+    if (pl->nact) {
+      k_mass<<<grid_for(pl->nact, 256), 256, 0, s>>>(P, pl->act, pl->nact, keys.as<unsigned long long>(),
+                                                     vals.as<double>());
+      LAUNCHED();
+    }
+    Csr piece{0, P.J, 0, nullptr, nullptr, nullptr};
+    long long nnz = 0, kept = 0;
+    const bool narrow = (unsigned long long)P.J * (unsigned long long)P.J < 0xffffffffull;
+    rc = narrow ? merge_csr<unsigned>(s, P, keys.as<unsigned long long>(), vals.as<double>(), coo, P.J, piece, nnz,
+                                      &kept, false)
+                : merge_csr<unsigned long long>(s, P, keys.as<unsigned long long>(), vals.as<double>(), coo, P.J,
+                                                piece, nnz, &kept, false);
+    if (rc) return rc;
+    piece.nnz = nnz;
+    pieces.push_back(piece);
+  }
+  long long nnz = 0;
+  return emit_pieces(pl, ds, pieces, 0, P.J, out_on_host, alloc, user, nullptr, &nnz);
 }
 
 nlg_status nlg_fp64_peak(int32_t device, double* tflops) {
