@@ -143,6 +143,15 @@ nlg_status nlg_load_const(nlg_plan *plan, const double *fconst, int32_t out_on_h
  * elements), written through alloc like nlg_assemble (which = 0, 1, 2). */
 nlg_status nlg_mass(nlg_plan *plan, int32_t out_on_host, nlg_alloc_fn alloc, void *alloc_user);
 
+/* Conjugate gradients for A x = b on `device` (all pointers are device
+ * memory): A is an n x n CSR (int64 indptr, int32 indices, f64 data), x holds
+ * the initial guess and receives the solution.  Stops when
+ * ||b - A x|| <= rtol ||b|| or after maxit iterations.  Deterministic
+ * (fixed reduction trees).  Used on the free block of a Dirichlet split
+ * (SparseSystem.split, assembly.py:102-107). */
+nlg_status nlg_cg(int32_t device, int64_t n, const int64_t *indptr, const int32_t *indices, const double *data,
+                  const double *b, double *x, double rtol, int32_t maxit, int32_t *iters, double *relres);
+
 /* DFMA throughput microbenchmark on `device` (the FP64 roofline denominator). */
 nlg_status nlg_fp64_peak(int32_t device, double *tflops);
 

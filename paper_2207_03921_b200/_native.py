@@ -74,6 +74,9 @@ SIGNATURES = {
     "nlg_load_const": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ALLOC_FN,
                                         ctypes.c_void_p]),
     "nlg_mass": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ALLOC_FN, ctypes.c_void_p]),
+    "nlg_cg": (ctypes.c_int32, [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
+                                ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]),
     "nlg_fp64_peak": (ctypes.c_int32, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "nlg_launch_count": (ctypes.c_int64, []),
 }

@@ -3246,3 +3246,149 @@ nlg_status nlg_fp64_peak(int32_t device, double* tflops) {
 }
 
 }  // extern "C"
+
+// ===================================================================== CG solve
+// Conjugate gradients on a device CSR (the free block of a Dirichlet split,
+// SURVEY.md 8f): warp-per-row SpMV and two-stage dot products with fixed
+// reduction trees, so the iteration is run-to-run deterministic.  Scalars
+// stay on the device; the host reads the residual every few iterations.
+namespace {
+
+constexpr int kCgThreads = 256, kCgBlocks = 592;  // 4 blocks per SM
+
+__global__ void k_cg_spmv(long long n, const long long* __restrict__ ptr, const int* __restrict__ idx,
+                          const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double acc = 0.0;
+  for (long long j = ptr[row] + lane; j < ptr[row + 1]; j += 32) acc = fma(__ldg(&val[j]), __ldg(&x[idx[j]]), acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[row] = acc;
+}
+
+// per-block partial of dot(a, b) (fixed striding and tree)
+__global__ void k_cg_dot_part(long long n, const double* __restrict__ a, const double* __restrict__ b, double* part) {
+  __shared__ double red[kCgThreads / 32];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc = fma(a[i], b[i], acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kCgThreads / 32; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// sum of the partials in block order -> *out (one warp)
+__global__ void k_cg_dot_fin(const double* __restrict__ part, int np, double* out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += 32) acc += part[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+// s[0] = rr, s[1] = pAp, s[2] = rr_new
+__global__ void k_cg_update_xr(long long n, const double* __restrict__ s, const double* __restrict__ p,
+                               const double* __restrict__ ap, double* x, double* r) {
+  const double alpha = s[1] != 0.0 ? s[0] / s[1] : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    r[i] = fma(-alpha, ap[i], r[i]);
+  }
+}
+
+__global__ void k_cg_update_p(long long n, double* s, const double* __restrict__ r, double* p) {
+  const double beta = s[0] != 0.0 ? s[2] / s[0] : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], r[i]);
+}
+
+__global__ void k_cg_shift(double* s) { s[0] = s[2]; }
+
+__global__ void k_cg_residual(long long n, const double* __restrict__ b, const double* __restrict__ ax, double* r,
+                              double* p) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = b[i] - ax[i];
+    r[i] = v;
+    p[i] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" nlg_status nlg_cg(int32_t device, int64_t n, const int64_t* indptr, const int32_t* indices,
+                             const double* data, const double* b, double* x, double rtol, int32_t maxit,
+                             int32_t* iters, double* relres) {
+  if (n < 0 || !indptr || !indices || !data || !b || !x || !iters || !relres) {
+    set_err("nlg_cg: bad arguments");
+    return NLG_ERR_CONFIG;
+  }
+  CK(cudaSetDevice(device));
+  *iters = 0;
+  *relres = 0.0;
+  if (n == 0) return NLG_OK;
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+  } sg{st};
+  const long long* ptr = (const long long*)indptr;
+  double *r, *p, *ap, *part, *sc;
+  CK(cudaMallocAsync(&r, sizeof(double) * n, st));
+  CK(cudaMallocAsync(&p, sizeof(double) * n, st));
+  CK(cudaMallocAsync(&ap, sizeof(double) * n, st));
+  CK(cudaMallocAsync(&part, sizeof(double) * kCgBlocks, st));
+  CK(cudaMallocAsync(&sc, sizeof(double) * 4, st));
+  struct FreeGuard {
+    cudaStream_t s;
+    void* q[5];
+    ~FreeGuard() { for (void* v : q) cudaFreeAsync(v, s); }
+  } fg{st, {r, p, ap, part, sc}};
+  const unsigned gs = (unsigned)std::min<long long>((n * 32 + 255) / 256, 1LL << 30);
+  auto dot = [&](const double* a, const double* c, double* out) {
+    k_cg_dot_part<<<kCgBlocks, kCgThreads, 0, st>>>(n, a, c, part);
+    k_cg_dot_fin<<<1, 32, 0, st>>>(part, kCgBlocks, out);
+    g_launches += 2;
+  };
+  // r = b - A x, p = r
+  k_cg_spmv<<<gs, 256, 0, st>>>(n, ptr, indices, data, x, ap);
+  LAUNCHED();
+  k_cg_residual<<<kCgBlocks, kCgThreads, 0, st>>>(n, b, ap, r, p);
+  LAUNCHED();
+  dot(b, b, sc + 3);
+  dot(r, r, sc + 0);
+  double h[4];
+  CK(cudaMemcpyAsync(h, sc, sizeof h, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double bn = sqrt(h[3]) > 0.0 ? sqrt(h[3]) : 1.0;
+  double rr = h[0];
+  int it = 0;
+  const int check = 8;
+  while (it < maxit && sqrt(rr) > rtol * bn) {
+    for (int k = 0; k < check && it < maxit; ++k, ++it) {
+      k_cg_spmv<<<gs, 256, 0, st>>>(n, ptr, indices, data, p, ap);
+      dot(p, ap, sc + 1);
+      k_cg_update_xr<<<kCgBlocks, kCgThreads, 0, st>>>(n, sc, p, ap, x, r);
+      dot(r, r, sc + 2);
+      k_cg_update_p<<<kCgBlocks, kCgThreads, 0, st>>>(n, sc, r, p);
+      k_cg_shift<<<1, 1, 0, st>>>(sc);
+      g_launches += 4;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    rr = h[0];
+    if (!std::isfinite(rr)) { set_err("nlg_cg: residual is not finite"); return NLG_ERR_NUMERICAL; }
+  }
+  *iters = it;
+  *relres = sqrt(rr) / bn;
+  return NLG_OK;
+}
