@@ -546,6 +546,12 @@ template <int KID>
 __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   constexpr int E = T::E, NC = T::NC;
+  __shared__ PowTab s_tab;
+  if (KID == 0) {
+    for (int i = threadIdx.x; i < (int)(sizeof(PowTab) / sizeof(double)); i += blockDim.x)
+      reinterpret_cast<double*>(&s_tab)[i] = reinterpret_cast<const double*>(&c_powtab)[i];
+    __syncthreads();
+  }
   long long ev0 = 0, ev2 = 0, out0 = 0, out2 = 0;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < O.nlist;
        v += (long long)gridDim.x * blockDim.x) {
@@ -563,14 +569,14 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     if (k == l) {
       // identical pair: both column halves of the reference's B hit k's dofs;
       // keep them apart for the per-triplet presence test (_engine.py:403-424)
-      full_identical<KID>(P, kx, ky, rs2, kkA, klA, ev2);
+      full_identical<KID>(P, kx, ky, rs2, kkA, klA, ev2, &s_tab);
       out2 += 7;
 #pragma unroll
       for (int e = 0; e < E; ++e) kkB[e] = klB[e] = 0.0;
     } else {
       load_tri(P, l, lx, ly);
       long long ne = 0;
-      full_pair2<KID>(P, kx, ky, lx, ly, rs2, kkA, klA, kkB, klB, ne);
+      full_pair2<KID>(P, kx, ky, lx, ly, rs2, kkA, klA, kkB, klB, ne, &s_tab);
       // flop accounting: the reference integrates the pair once per visit
       const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
       ev0 += ne * mult;
@@ -635,6 +641,7 @@ struct ClipBlock {  // block-wide work queues
   unsigned char item[32 * kClipWarps];      // clip queue: (warp << 5) | lane
   unsigned short sub[32 * kClipWarps * 7];  // sub-triangle queue: (item << 4) | t, item-major
   double tile[32 * kClipWarps][ClipCfg<KID>::NSUM + 1];  // one round's sub-triangle sums (padded rows)
+  PowTab tab;                                            // pow_tab tables (fractional kernel)
 };
 
 __device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 00 01 02 11 12 22
@@ -721,6 +728,9 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
   unsigned n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;  // per thread: < 2^32
   const int vs = lane >> 4, r = lane & 15;
   if (threadIdx.x == 0) CQ.n[0] = 0;
+  if (KID == 0)
+    for (int i = threadIdx.x; i < (int)(sizeof(PowTab) / sizeof(double)); i += blockDim.x)
+      reinterpret_cast<double*>(&CQ.tab)[i] = reinterpret_cast<const double*>(&c_powtab)[i];
   __syncthreads();
   int par = 0;
   // software pipeline: the next chunk's records and element records are
@@ -962,7 +972,7 @@ __global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __rest
             if (sumsq(x0 - ey0, x1 - ey1) < rs2) continue;
           }
           double pv[NC2], qv[NC2];
-          kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
+          kval<KID, true, true>(P, x0, y0, d0, d1, r2, pv, qv, &CQ.tab);
           ++ne;
           const double wq = c_rule.iw[q] * jac2;
           const double xi1 = fma(i1, z1b, fma(i0, z1a, z1));
@@ -2827,6 +2837,12 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   {
     const int tr = g_trace ? 1 : 0;
     cudaMemcpyToSymbolAsync(g_trace_dev, &tr, sizeof tr, 0, cudaMemcpyHostToDevice, s);
+  }
+  {
+    static PowTab ptab;
+    static std::once_flag ptab_once;
+    std::call_once(ptab_once, [] { pow_tab_fill(&ptab); });
+    cudaMemcpyToSymbolAsync(c_powtab, &ptab, sizeof ptab, 0, cudaMemcpyHostToDevice, s);
   }
   if (cudaMemcpyToSymbolAsync(c_rule, &hr, sizeof hr, 0, cudaMemcpyHostToDevice, s) != cudaSuccess) {
     set_err("rule upload failed");

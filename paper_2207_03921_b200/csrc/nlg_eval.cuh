@@ -48,6 +48,7 @@ struct Params {
 // the 7-point rule and its weighted hat products (identical for every plan:
 // QuadratureConfig only accepts "7point", quadrature.py:20)
 __constant__ Rule7 c_rule;
+__constant__ PowTab c_powtab;  // pow_tab tables (nlg_math.cuh)
 
 template <int KID> struct KTraits {
   static constexpr int NC = KID == 1 ? 2 : 1;
@@ -58,11 +59,16 @@ template <int KID> struct KTraits {
 
 // kernel matrix at offset d = x - y (r2 = |d|^2): _engine._kernel_mat :30-43;
 // id 3 returns P = value(x, y) and Q = value(y, x) (_pyengine._pq :38-45).
-template <int KID, bool CBANK = true>
+// tab: pow tables in shared memory (pow_tab) for the fractional kernel, or
+// nullptr for the polynomial fast_pow_pos
+template <int KID, bool CBANK = true, bool TAB = false>
 __device__ __forceinline__ void kval(const Params& P, double x0, double y0, double d0, double d1,
-                                     double r2, double* p, double* q) {
+                                     double r2, double* p, double* q, const PowTab* tab = nullptr) {
   if constexpr (KID == 0) {
-    p[0] = P.cst * fast_pow_pos<CBANK>(r2, P.kexp);
+    if constexpr (TAB)
+      p[0] = P.cst * pow_tab(r2, P.kexp, tab->rc, tab->lc, tab->e2);
+    else
+      p[0] = P.cst * fast_pow_pos<CBANK>(r2, P.kexp);
   } else if constexpr (KID == 1) {
     const double f = P.cst / (r2 * sqrt(r2));
     const double v01 = f * d0 * d1;
@@ -117,7 +123,8 @@ __device__ __forceinline__ void rule_points(const Params& P, const double* tx, c
 template <int KID>
 __device__ __forceinline__ void full_pair2(const Params& P, const double* kx, const double* ky,
                                            const double* lx, const double* ly, double rs2, double* kkA,
-                                           double* klA, double* kkB, double* klB, long long& n_eval) {
+                                           double* klA, double* kkB, double* klB, long long& n_eval,
+                                           const PowTab* tab) {
   using T = KTraits<KID>;
   constexpr int NC = T::NC, NC2 = T::NC2;
   double xk[7], yk[7], xl[7], yl[7];
@@ -150,7 +157,7 @@ __device__ __forceinline__ void full_pair2(const Params& P, const double* kx, co
       const double r2 = sumsq(d0, d1);
       if (rs2 > 0.0 && r2 < rs2) continue;
       double pv[NC2], qv[NC2];
-      kval<KID, false>(P, xk[p], xl[q], d0, d1, r2, pv, qv);
+      kval<KID, false, true>(P, xk[p], xl[q], d0, d1, r2, pv, qv, tab);
       ++n_eval;
       const double wq = c_rule.iw[q];
 #pragma unroll
@@ -205,7 +212,8 @@ __device__ __forceinline__ void full_pair2(const Params& P, const double* kx, co
 // per-triplet `v != 0` (_engine.py:403-424).
 template <int KID>
 __device__ __forceinline__ void full_identical(const Params& P, const double* kx, const double* ky,
-                                               double rs2, double* h0, double* h1, long long& n_eval) {
+                                               double rs2, double* h0, double* h1, long long& n_eval,
+                                               const PowTab* tab) {
   using T = KTraits<KID>;
   constexpr int NC = T::NC, NC2 = T::NC2;
   double xk[7], yk[7];
@@ -225,7 +233,7 @@ __device__ __forceinline__ void full_identical(const Params& P, const double* kx
       const double r2 = sumsq(d0, d1);
       if (rs2 > 0.0 && r2 < rs2) continue;
       double pv[NC2], qv[NC2];
-      kval<KID>(P, xk[p], xk[q], d0, d1, r2, pv, qv);
+      kval<KID, true, true>(P, xk[p], xk[q], d0, d1, r2, pv, qv, tab);
       ++n_eval;
       for (int i = 0; i < NC2; ++i) {
         const double qq = T::SYM ? pv[i] : qv[i];

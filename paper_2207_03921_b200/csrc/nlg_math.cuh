@@ -10,6 +10,7 @@
 // libm pow over the whole r2 range the meshes produce), far inside the
 // 1e-10 parity bar.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 
@@ -109,6 +110,63 @@ __host__ __device__ __forceinline__ double fast_pow_pos(double x, double e) {
   p = fma(p, r, 1.0);
   return bits2d(d2bits(p) + ((uint64_t)(int64_t)n << 52));
 #undef K
+}
+
+// Table-driven x^e (x > 0, finite, normal) for the clipped-pair inner loop:
+// fewer FP64 ops than fast_pow_pos (about 24 against 40), same accuracy class.
+//   ln x = k ln2 + ln c_j + ln(1 + u),  m = x / 2^k in [1, 2),
+//          c_j = 1 + (j + 1/2)/128 (j = top 7 mantissa bits), u = (m - c_j)/c_j,
+//          |u| < 2^-8, ln(1+u) to u^7
+//   exp t = 2^(n >> 6) 2^((n & 63)/64) exp(r),  n = rint(64 t / ln 2),
+//          |r| <= ln2/128, exp(r) - 1 to r^6
+// Tables (PowTab): 1/c_j and ln c_j for 128 j, 2^(i/64) for 64 i, built by
+// pow_tab_fill; the clipped kernel keeps them in shared memory.
+struct PowTab {
+  double rc[128], lc[128], e2[64];
+};
+
+inline void pow_tab_fill(PowTab* t) {
+  for (int j = 0; j < 128; ++j) {
+    const double c = 1.0 + (j + 0.5) / 128.0;  // exact
+    t->rc[j] = 1.0 / c;
+    t->lc[j] = std::log(c);
+  }
+  for (int i = 0; i < 64; ++i) t->e2[i] = std::exp2(i / 64.0);
+}
+
+__host__ __device__ __forceinline__ double pow_tab(double x, double e, const double* __restrict__ rc,
+                                                   const double* __restrict__ lc, const double* __restrict__ e2) {
+  const uint64_t b = d2bits(x);
+  const int k = (int)((b >> 52) & 0x7ff) - 1023;
+  const int j = (int)((b >> 45) & 127);
+  const double m = bits2d((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
+  const double c = 1.0 + (j + 0.5) * (1.0 / 128.0);
+  const double u = (m - c) * rc[j];
+  // ln(1+u) = u (1 - u/2 + u^2/3 - ... - u^6/7... ) : P(u) of degree 6
+  double s = 1.0 / 7.0;
+  s = fma(s, u, -1.0 / 6.0);
+  s = fma(s, u, 1.0 / 5.0);
+  s = fma(s, u, -1.0 / 4.0);
+  s = fma(s, u, 1.0 / 3.0);
+  s = fma(s, u, -0.5);
+  s = fma(s, u, 1.0);
+  const double l1 = u * s;
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double kd = (double)k;
+  const double t = e * fma(kd, ln2_hi, lc[j] + fma(kd, ln2_lo, l1));
+  const double n = rint(t * (64.0 / 6.93147180559945309417e-01));
+  const double r = fma(-n, ln2_lo / 64.0, fma(-n, ln2_hi / 64.0, t));
+  double p = 1.0 / 720.0;
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = p * r;  // exp(r) - 1
+  const long long ni = (long long)n;
+  const double tj = e2[ni & 63];
+  const double v = fma(tj, p, tj);
+  return bits2d(d2bits(v) + ((uint64_t)(ni >> 6) << 52));
 }
 
 }  // namespace nlg
