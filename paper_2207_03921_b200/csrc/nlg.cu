@@ -1524,11 +1524,15 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
       double pv[NC * NC], qv[NC * NC];
       kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
       npts += HALF ? 2 : 1;
+      // hat values at the rule points, (1 - p0) - p1, p0, p1 as quadrature._hats
+      // (quadrature.py:129-135) computes them: no table reads
+      const double hxa[3] = {__dsub_rn(__dsub_rn(1.0, xs0), xs1), xs0, xs1};
+      const double hya[3] = {__dsub_rn(__dsub_rn(1.0, ys0), ys1), ys0, ys1};
       double phx[U], phy[U], tm[U];
 #pragma unroll
       for (int m = 0; m < U; ++m) {
-        phx[m] = mk[m] >= 0 ? __ldg(&R.hx[3 * i + mk[m]]) : 0.0;
-        phy[m] = ml[m] >= 0 ? __ldg(&R.hy[3 * i + ml[m]]) : 0.0;
+        phx[m] = mk[m] >= 0 ? (mk[m] == 0 ? hxa[0] : (mk[m] == 1 ? hxa[1] : hxa[2])) : 0.0;
+        phy[m] = ml[m] >= 0 ? (ml[m] == 0 ? hya[0] : (ml[m] == 1 ? hya[1] : hya[2])) : 0.0;
         tm[m] = phx[m] - phy[m];
       }
       const double wi = HALF ? 2.0 * __ldg(&R.w[i]) : __ldg(&R.w[i]);
