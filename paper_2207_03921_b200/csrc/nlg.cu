@@ -711,7 +711,7 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
 }
 
 template <int KID, bool SQ>
-__global__ void __launch_bounds__(128, 5) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
+__global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
   using X = SumIdx<KID>;

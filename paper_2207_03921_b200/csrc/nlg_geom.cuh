@@ -20,7 +20,7 @@ constexpr double kBallTieRel = 1e-12;    // _geom_scalar.py:15
 constexpr double kDedupRel = 1e-13;      // _geom_scalar.py:18
 constexpr double kChordSkipRel = 1e-10;  // _geom_scalar.py:21
 constexpr double kCapMemberRel = 1e-12;  // _geom_scalar.py:24
-constexpr int kMaxPoly = 10;             // triangle -> <= 6 clip rows, <= 9 with caps
+constexpr int kMaxPoly = 9;              // triangle -> <= 6 clip rows, <= 9 with (<= 3) caps
 constexpr int kMaxBase = 7;
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -206,14 +206,16 @@ __device__ __noinline__ int clip_square(Tri T, double cx, double cy, double delt
 }
 
 // Balls 0 / 1 without scratch rows: clip_circle writes its (<= 6) rows at
-// offset 4 of (px, py) and insert_caps compacts them to the front, adding
-// (<= 3) caps; output row n never passes input row 4 + i before reading it.
+// offset 3 of (px, py) and insert_caps compacts them to the front, adding
+// (<= 3) caps.  Row i's output lands at i + (caps so far) <= 3 + i, and a cap
+// after it needs caps so far <= 2, so no input row is overwritten before it
+// is read (row 0 is kept in registers).
 __device__ __forceinline__ int truncate_inner_inplace(Tri T, double cx, double cy, double delta, int ball,
                                                       double* px, double* py) {
   unsigned f;
   if (ball == 0) return clip_circle(T, cx, cy, delta, px, py, &f);
-  const int nb = clip_circle(T, cx, cy, delta, px + 4, py + 4, &f);
-  return insert_caps(T, px + 4, py + 4, f, nb, cx, cy, delta, px, py);
+  const int nb = clip_circle(T, cx, cy, delta, px + 3, py + 3, &f);
+  return insert_caps(T, px + 3, py + 3, f, nb, cx, cy, delta, px, py);
 }
 
 // The truncated inner region of triangle T seen from outer point (cx, cy),
