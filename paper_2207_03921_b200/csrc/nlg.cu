@@ -615,7 +615,9 @@ template <int KID> struct ClipCfg {
   static constexpr int NKL = 9 * NC * NC;
   static constexpr int NSIDE = NKK + NKL;
   static constexpr int NVAL = 2 * NSIDE;                 // sides A and B
-  static constexpr int NSUM = NC2 * (SYM ? 6 : 9);       // barycentric moments (SumIdx)
+  // kernel-matrix components carried: the peridynamic matrix is symmetric (P_01 = P_10)
+  static constexpr int NCU = KID == 1 ? 3 : NC2;
+  static constexpr int NSUM = NCU * (SYM ? 6 : 9);       // barycentric moments (SumIdx)
 };
 
 // SQ: the square ball needs clip scratch rows; the circle balls clip in place
@@ -658,11 +660,15 @@ __device__ __forceinline__ int sym3(int a, int b) {  // index of (min, max) in 0
 // reference's S0, Sy = sum t h_a and Syy = sum tq h_a h_b are linear in
 // these (item_folds); 8 FP64 ops per point instead of 13.
 template <int KID> struct SumIdx {
-  static constexpr int NC2 = KTraits<KID>::NC2;
+  static constexpr int NCU = ClipCfg<KID>::NCU;  // stored components
   static constexpr bool SYM = KTraits<KID>::SYM;
-  __device__ static constexpr int mp(int k, int i) { return k * NC2 + i; }  // k: 0 -> M0, 1 -> M1, 2 -> M2
+  // stored component of kernel-matrix entry cd (nc = 2 symmetric: 00 01 11)
+  __device__ static constexpr int uc(int cd) { return NCU == 3 ? (cd == 3 ? 2 : (cd == 2 ? 1 : cd)) : cd; }
+  // matrix entry of stored component i
+  __device__ static constexpr int ucd(int i) { return NCU == 3 ? (i == 2 ? 3 : i) : i; }
+  __device__ static constexpr int mp(int k, int i) { return k * NCU + i; }  // k: 0 -> M0, 1 -> M1, 2 -> M2
   __device__ static constexpr int mq(int k, int i) {                        // k: 0..2 as mp, 3 M11, 4 M12, 5 M22
-    return SYM ? k * NC2 + i : (k < 3 ? (3 + k) * NC2 + i : (3 + k) * NC2 + i);
+    return SYM ? k * NCU + i : (3 + k) * NCU + i;
   }
 };
 
@@ -680,12 +686,13 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
   double s0[C::NC2], syp[3][C::NC2], syq[3][C::NC2], syy[6][C::NC2];
 #pragma unroll
   for (int cd = 0; cd < C::NC2; ++cd) {
-    const double p0 = s[X::mp(0, cd)], p1 = s[X::mp(1, cd)], p2 = s[X::mp(2, cd)];
-    const double q0 = s[X::mq(0, cd)], q1 = s[X::mq(1, cd)], q2 = s[X::mq(2, cd)];
+    const int u = X::uc(cd);
+    const double p0 = s[X::mp(0, u)], p1 = s[X::mp(1, u)], p2 = s[X::mp(2, u)];
+    const double q0 = s[X::mq(0, u)], q1 = s[X::mq(1, u)], q2 = s[X::mq(2, u)];
     s0[cd] = p0;
     syp[0][cd] = (p0 - p1) - p2; syp[1][cd] = p1; syp[2][cd] = p2;
     syq[0][cd] = (q0 - q1) - q2; syq[1][cd] = q1; syq[2][cd] = q2;
-    const double m11 = s[X::mq(3, cd)], m12 = s[X::mq(4, cd)], m22 = s[X::mq(5, cd)];
+    const double m11 = s[X::mq(3, u)], m12 = s[X::mq(4, u)], m22 = s[X::mq(5, u)];
     const double s01 = (q1 - m11) - m12, s02 = (q2 - m12) - m22;
     syy[0][cd] = (syq[0][cd] - s01) - s02; syy[1][cd] = s01; syy[2][cd] = s02;
     syy[3][cd] = m11; syy[4][cd] = m12; syy[5][cd] = m22;
@@ -978,9 +985,9 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
           const double xi1 = fma(i1, z1b, fma(i0, z1a, z1));
           const double xi2 = fma(i1, z2b, fma(i0, z2a, z2));
 #pragma unroll
-          for (int i = 0; i < NC2; ++i) {
-            const double tp = wq * pv[i];
-            const double tq = T::SYM ? tp : wq * qv[i];
+          for (int i = 0; i < C::NCU; ++i) {
+            const double tp = wq * pv[X::ucd(i)];
+            const double tq = T::SYM ? tp : wq * qv[X::ucd(i)];
             const double g1 = tq * xi1, g2 = tq * xi2;
             if (T::SYM) {
               sm[X::mp(0, i)] += tp;
