@@ -484,6 +484,13 @@ __device__ __forceinline__ unsigned long long coo_key(const Params& P, long long
   if (row < P.row_lo || row >= P.row_hi) return kSentinel;
   return (unsigned long long)(row - P.row_lo) * (unsigned long long)P.J + (unsigned long long)col;
 }
+// COO key store: 32-bit when the batch's keys fit (the radix sort then reads
+// half the key bytes), the sentinel truncating to the 32-bit sentinel
+__device__ __forceinline__ void put_key(const Params& P, unsigned long long* keys, long long slot,
+                                        unsigned long long k) {
+  if (P.narrow) reinterpret_cast<unsigned*>(keys)[slot] = (unsigned)k;
+  else keys[slot] = k;
+}
 // reference emits a triplet iff v != 0 (_engine.py:410-424); an absent
 // entry is stored as +0.0, a present one that is exactly zero as -0.0
 __device__ __forceinline__ double emit_val(double v) { return v != 0.0 ? v : 0.0; }
@@ -1265,8 +1272,9 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
       for (int w = 0; w < NWARP; ++w) v += S.u.red[w][u];
       const bool present = I.cnt[(long long)C_KK * I.nR + i] != 0 && ((s_fl >> u) & 1ull);
       const long long slot = O.kk_base + (long long)i * E + t;
-      O.keys[slot] = present ? coo_key(P, (long long)NC * dka[rr / NC] + rr % NC, (long long)NC * dka[cc / NC] + cc % NC)
-                             : kSentinel;
+      put_key(P, O.keys, slot,
+              present ? coo_key(P, (long long)NC * dka[rr / NC] + rr % NC, (long long)NC * dka[cc / NC] + cc % NC)
+                      : kSentinel);
       O.vals[slot] = present ? (v != 0.0 ? v : -0.0) : 0.0;
     }
     __syncthreads();
@@ -1352,7 +1360,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
 #pragma unroll
       for (int d = 0; d < NC; ++d) {
         const int e = d * N3 + r;
-        O.keys[pos] = (unsigned long long)row * (unsigned long long)P.J + (unsigned long long)NC * w + d;
+        put_key(P, O.keys, pos, (unsigned long long)row * (unsigned long long)P.J + (unsigned long long)NC * w + d);
         O.vals[pos] = ((pres >> e) & 1u) ? (acc[e] != 0.0 ? acc[e] : -0.0) : 0.0;
         ++pos;
       }
@@ -1588,7 +1596,7 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
       const long long slot = cbase + pi * SLOTS + s;
       const int ii = s / (6 * NC), jj = s % (6 * NC);
       if (ii >= UN || jj >= UN) {
-        keys[slot] = kSentinel;
+        put_key(P, keys, slot, kSentinel);
         vals[slot] = 0.0;
         continue;
       }
@@ -1596,7 +1604,7 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
       const double v = (((red[0][ai] + red[1][ai]) + red[2][ai]) + red[3][ai]) * sScale;
       report_nonfinite(nonfinite(v), k, l, P.K, errpair);
       const int m = ii / NC, c = ii % NC, mp = jj / NC, d = jj % NC;
-      keys[slot] = coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d);
+      put_key(P, keys, slot, coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d));
       vals[slot] = emit_val(v);
     }
     __syncthreads();
@@ -2136,7 +2144,8 @@ __global__ void k_window_compact(const unsigned long long* __restrict__ keys, co
 // sums its values in COO position order -> CSR rows of this batch.
 template <typename KT>
 nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64, double* vals, long long coo,
-                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept, bool prereduce) {
+                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept, bool prereduce,
+                     bool keys_narrow = false) {
   int bits = 1;
   {
     const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
@@ -2185,7 +2194,9 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
   }
   DevBuf k1, k2, v2;
   KT* keys;
-  if (sizeof(KT) == 4) {
+  if (sizeof(KT) == 4 && keys_narrow) {
+    keys = reinterpret_cast<KT*>(keys64);  // written as 32-bit keys (put_key)
+  } else if (sizeof(KT) == 4) {
     CK(k1.alloc(sizeof(KT) * std::max(coo, 1LL), s));
     if (coo) {
       k_narrow_keys<<<grid_for(coo, 256), 256, 0, s>>>(keys64, coo, k1.as<unsigned>());
@@ -2298,6 +2309,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   Params P = pl->P;
   P.row_lo = row_lo;
   P.row_hi = row_hi;
+  P.narrow = (unsigned long long)(row_hi - row_lo) * (unsigned long long)P.J < 0xffffffffull;
   cudaStream_t s = pl->stream;
   const int K = P.K;
   cudaEvent_t ev[8];
@@ -2646,10 +2658,9 @@ fits:
   const long long nrows = row_hi - row_lo;
   Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
   long long nnz = 0;
-  const bool narrow = (unsigned long long)nrows * (unsigned long long)P.J < 0xffffffffull;
   long long kept = 0;
-  rc = narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false)
-              : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false);
+  rc = P.narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false, true)
+                : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false);
   st->coo_reduced += kept;
   if (rc) return rc;
   piece.nnz = nnz;

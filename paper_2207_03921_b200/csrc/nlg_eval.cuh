@@ -42,6 +42,7 @@ struct Params {
   int nc, kid, ball, path, sym, is_dg;
   double s, kexp, cst, delta, prer, rskip2, drop2, kp0, kp1;
   long long J, row_lo, row_hi;
+  int narrow;  // COO keys of this batch are written as 32-bit (rows x J < 2^32)
   int dbg;  // NLG_DEBUG bit mask (experiments only; 0 in production)
 };
 
