@@ -479,6 +479,17 @@ __global__ void k_rev_keys(const int2* __restrict__ rec, long long n, const int*
   val[i] = (int)i;
 }
 
+// position of each record in the reverse order (its side B block goes there)
+// and, for the emitted ones, the record's root (the partner of side B)
+__global__ void k_rev_pos(const int* __restrict__ rev_item, long long n, const int2* __restrict__ rec, int* revpos,
+                          int* partB) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = rev_item[i];
+  revpos[r] = (int)i;
+  partB[i] = rec[r].x & kIdMask;
+}
+
 // ---------------------------------------------------------------- visits
 __device__ __forceinline__ unsigned long long coo_key(const Params& P, long long row, long long col) {
   if (row < P.row_lo || row >= P.row_hi) return kSentinel;
@@ -515,6 +526,7 @@ struct VisitOut {
   double* klv;              // [record][side][b][NVP] neighbour blocks, column-major and padded:
                             // the 3NC row values of one neighbour dof are contiguous
   long long nvis;           // records of both lists
+  const int* revpos;        // record -> its side B's block: nvis + revpos[record] (reverse-index order)
   long long vofs;           // this list's first record index
   long long nlist;
   unsigned long long* counters;
@@ -533,17 +545,16 @@ template <int NC> struct Blk {
 
 // emit one side of a record: own block -> kkv, neighbour block -> klv
 template <int NC>
-__device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long v, int side, bool on,
+__device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long slot, bool on,
                                           int root, int nb, const double* kk, const double* kl) {
   using B = Blk<NC>;
-  const long long vi = O.vofs + v;
   bool bad = false;
 #pragma unroll
   for (int e = 0; e < B::E; ++e) {
     const int I = e / B::N3, J = e % B::N3;
-    if (I <= J) O.kkv[(vi * 2 + side) * B::NKK + B::sym(I, J)] = on ? kk[e] : 0.0;
+    if (I <= J) O.kkv[slot * B::NKK + B::sym(I, J)] = on ? kk[e] : 0.0;
     bad |= nonfinite(kk[e]) | nonfinite(kl[e]);
-    O.klv[(vi * 2 + side) * B::KLS + B::kl(I, J)] = on ? emit_val(kl[e]) : 0.0;
+    O.klv[slot * B::KLS + B::kl(I, J)] = on ? emit_val(kl[e]) : 0.0;
   }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
 }
@@ -589,8 +600,9 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
       ev0 += ne * mult;
       out0 += 14 * mult;
     }
-    emit_side<NC>(P, O, v, 0, emitA, k, l, kkA, klA);
-    emit_side<NC>(P, O, v, 1, emitB && k != l, l, k, kkB, klB);
+    const long long vi = O.vofs + v;
+    emit_side<NC>(P, O, vi, emitA, k, l, kkA, klA);
+    emit_side<NC>(P, O, O.nvis + __ldg(&O.revpos[vi]), emitB && k != l, l, k, kkB, klB);
   }
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
   warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
@@ -1087,12 +1099,13 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
         const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
         const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
         const long long vi = O.vofs + v;
+        const long long slot = side ? O.nvis + __ldg(&O.revpos[vi]) : vi;
         if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
         if (w < C::NKK) {
-          O.kkv[(vi * 2 + side) * Blk<NC>::NKK + w] = on ? val : 0.0;  // unique (I <= J) order
+          O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;  // unique (I <= J) order
         } else {
           const int e = w - C::NKK, I = e / N3, J = e % N3;
-          O.klv[(vi * 2 + side) * Blk<NC>::KLS + Blk<NC>::kl(I, J)] = on ? emit_val(val) : 0.0;
+          O.klv[slot * Blk<NC>::KLS + Blk<NC>::kl(I, J)] = on ? emit_val(val) : 0.0;
         }
       }
     }
@@ -1133,8 +1146,9 @@ struct RootIn {
   const long long* off;
   long long nF;
   const int2* rec;  // full then clipped records
-  const int* rev_item;
   const int* rev_start;
+  const int* partB;  // [reverse position] the record's root (side B's partner)
+  long long nvis;
   const double* kkv;  // [side][NKK]
   const double* klv;  // [side][3][NVP]
   const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
@@ -1154,11 +1168,18 @@ struct RootOut {
 struct RootSides {
   long long f0, fn, p0, pn, r0, rn;
   __device__ __forceinline__ long long n() const { return fn + pn + rn; }
-  // record index (full then clipped list) and side of the root's rs-th side
-  __device__ __forceinline__ void at(const RootIn& I, long long rs, long long& rec, int& side) const {
-    if (rs < fn) { rec = f0 + rs; side = 0; }
-    else if (rs < fn + pn) { rec = p0 + (rs - fn); side = 0; }
-    else { rec = __ldg(&I.rev_item[r0 + (rs - fn - pn)]); side = 1; }
+  // block slot of the root's rs-th side: side A of its own records (full
+  // then clipped list), then side B of the records where it is the partner,
+  // stored contiguously in reverse-index order
+  __device__ __forceinline__ long long slot(const RootIn& I, long long rs) const {
+    if (rs < fn) return f0 + rs;
+    if (rs < fn + pn) return p0 + (rs - fn);
+    return I.nvis + r0 + (rs - fn - pn);
+  }
+  // the other element of that side's pair
+  __device__ __forceinline__ int partner(const RootIn& I, long long rs) const {
+    if (rs < fn + pn) return __ldg(&I.rec[slot(I, rs)].y) & kIdMask;
+    return __ldg(&I.partB[r0 + (rs - fn - pn)]);
   }
 };
 
@@ -1242,10 +1263,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     unsigned fl = 0;  // presence: some side's value is nonzero
 #pragma unroll 2
     for (long long rs = t; rs < n_rs; rs += kRootThreads) {
-      long long rec;
-      int side;
-      R.at(I, rs, rec, side);
-      const double* src = I.kkv + (rec * 2 + side) * NKK;
+      const double* src = I.kkv + R.slot(I, rs) * NKK;
 #pragma unroll
       for (int e = 0; e < NKK; ++e) {
         const double v = __ldg(&src[e]);
@@ -1295,14 +1313,9 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
       if (j < nval) {
         const long long g = c0 + j, rs = g / 3;
         const int b = (int)(g - 3 * rs);
-        long long rec;
-        int side;
-        R.at(I, rs, rec, side);
-        const int2 pr = __ldg(&I.rec[rec]);
-        const int nb = (side == 0 ? pr.y : pr.x) & kIdMask;
-        const int4 dn = __ldg(&P.dofs[nb]);
+        const int4 dn = __ldg(&P.dofs[R.partner(I, rs)]);
         key[q] = (unsigned)(b == 0 ? dn.x : (b == 1 ? dn.y : dn.z));
-        col[q] = (unsigned)((rec * 2 + side) * 3 + b);
+        col[q] = (unsigned)(R.slot(I, rs) * 3 + b);
       }
     }
     typename SM::Sort(S.u.sort).Sort(key, col, 0, key_bits);  // blocked: position t IT + q
@@ -2543,6 +2556,13 @@ fits:
   }
   k_cell_ranges<<<grid_for(nR + 1, 256), 256, 0, s>>>(rkey2.as<unsigned>(), (int)nvis, nR, rstart.as<int>());
   LAUNCHED();
+  DevBuf revpos, partB;  // side-B blocks are stored in reverse-index order (contiguous per root)
+  CK(revpos.alloc(sizeof(int) * std::max(nvis, 1LL), s));
+  CK(partB.alloc(sizeof(int) * std::max(nvis, 1LL), s));
+  if (nvis) {
+    k_rev_pos<<<grid_for(nvis, 256), 256, 0, s>>>(ritem.as<int>(), nvis, lf, revpos.as<int>(), partB.as<int>());
+    LAUNCHED();
+  }
   CK(cudaEventRecord(ev[1], s));
   // ---- integrate
   const long long nsing_slots = (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
@@ -2558,6 +2578,7 @@ fits:
   O.kkv = kkv.as<double>();
   O.klv = klv.as<double>();
   O.nvis = nvis;
+  O.revpos = revpos.as<int>();
   O.counters = d_counters;
   O.errpair = d_err;
   nlg_status rc = NLG_OK;
@@ -2590,7 +2611,8 @@ fits:
     RI.off = off.as<long long>();
     RI.nF = nF;
     RI.rec = lf;
-    RI.rev_item = ritem.as<int>();
+    RI.partB = partB.as<int>();
+    RI.nvis = nvis;
     RI.rev_start = rstart.as<int>();
     RI.kkv = O.kkv;
     RI.klv = O.klv;
