@@ -132,6 +132,47 @@ __device__ __forceinline__ void full_pair2(const Params& P, const double* kx, co
   rule_points(P, kx, ky, xk, yk);
   rule_points(P, lx, ly, xl, yl);
   const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+  if constexpr (KID == 2 || KID == 3) {
+    if (!(rs2 > 0.0)) {
+      // P_pq = P(x_p) and Q_pq = Q(y_q) (constant kernel: both constant): the
+      // 7 x 7 sums factor into 7-term sums (same quantities, other rounding)
+      //   kkA = c2 (sum_q w_q) sum_p w_p H_pa H_pb P_p    klA = -c2 (sum_p w_p H_pa)(sum_q w_q H_qb Q_q)
+      //   kkB = c2 (sum_p w_p) sum_q w_q H_qa H_qb Q_q    klB = -c2 (sum_q w_q H_qa)(sum_p w_p H_pb P_p)
+      double sw = 0.0, whs[3] = {0.0, 0.0, 0.0}, ph[3] = {0.0, 0.0, 0.0}, qh[3] = {0.0, 0.0, 0.0};
+      double php[9], qhq[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) php[e] = qhq[e] = 0.0;
+#pragma unroll
+      for (int p = 0; p < 7; ++p) {
+        const double Pp = KID == 2 ? P.cst : (1.0 + P.kp0 * xk[p]) * P.kp1;
+        const double Qq = KID == 2 ? P.cst : (1.0 + P.kp0 * xl[p]) * P.kp1;
+        sw += c_rule.ow[p];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          whs[a] += c_rule.wh[p][a];
+          ph[a] = fma(c_rule.wh[p][a], Pp, ph[a]);
+          qh[a] = fma(c_rule.wh[p][a], Qq, qh[a]);
+        }
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          php[e] = fma(c_rule.whh[p][e], Pp, php[e]);
+          qhq[e] = fma(c_rule.whh[p][e], Qq, qhq[e]);
+        }
+      }
+      n_eval += 49;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int e = a * 3 + b;
+          kkA[e] = (c2 * sw) * php[e];
+          kkB[e] = (c2 * sw) * qhq[e];
+          klA[e] = -c2 * whs[a] * qh[b];
+          klB[e] = -c2 * whs[a] * ph[b];
+        }
+      return;
+    }
+  }
   double colq[7][NC2];
 #pragma unroll
   for (int e = 0; e < 9 * NC2; ++e) kkA[e] = klA[e] = klB[e] = 0.0;
