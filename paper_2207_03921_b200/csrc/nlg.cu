@@ -1438,6 +1438,8 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
 }
 
 // ---------------------------------------------------------------- singular pairs
+constexpr int kSingThreads = 32;  // threads per touching pair (points strided over them)
+
 struct SingRule {
   const double* __restrict__ xs;
   const double* __restrict__ ys;
@@ -1460,7 +1462,7 @@ struct SingAcc {
 // FAM 0 identical (U = 3), 1 edge (U = 4, DG 6), 2 vertex (U = 5, DG 6);
 // frames and union tables follow _engine._visit_pair :230-308.
 template <int KID, int FAM, int U>
-__global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restrict__ list,
+__global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2* __restrict__ list,
                                                   long long n, SingRule R,
                                                   unsigned long long* keys, double* vals,
                                                   long long cbase, unsigned long long* counters,
@@ -1471,7 +1473,7 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
   constexpr int SLOTS = 36 * NC * NC;
   __shared__ double sTA[3][2], sTB[3][2], sScale;
   __shared__ int sMk[6], sMl[6], sUb[6];
-  __shared__ double red[4][A::N];
+  __shared__ double red[kSingThreads / 32][A::N];
   long long npts = 0;
   for (long long pi = blockIdx.x; pi < n; pi += gridDim.x) {
     const int k = list[pi].x, l = list[pi].y;
@@ -1614,7 +1616,10 @@ __global__ void __launch_bounds__(128) k_singular(Params P, const int2* __restri
         continue;
       }
       const int ai = A::idx(ii, jj);
-      const double v = (((red[0][ai] + red[1][ai]) + red[2][ai]) + red[3][ai]) * sScale;
+      double v = red[0][ai];
+#pragma unroll
+      for (int w = 1; w < kSingThreads / 32; ++w) v += red[w][ai];
+      v *= sScale;
       report_nonfinite(nonfinite(v), k, l, P.K, errpair);
       const int m = ii / NC, c = ii % NC, mp = jj / NC, d = jj % NC;
       put_key(P, keys, slot, coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d));
@@ -2016,14 +2021,14 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
                pl->sing_tab[f][4], pl->sing_n[f]};
     const unsigned g = (unsigned)std::min<long long>(nS[f], 1 << 20);
     if (f == 0)
-      k_singular<KID, 0, 3><<<g, 128, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair);
+      k_singular<KID, 0, 3><<<g, kSingThreads, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair);
     else if (P.is_dg)
-      (f == 1 ? k_singular<KID, 1, 6> : k_singular<KID, 2, 6>)<<<g, 128, 0, pl->stream>>>(
+      (f == 1 ? k_singular<KID, 1, 6> : k_singular<KID, 2, 6>)<<<g, kSingThreads, 0, pl->stream>>>(
           P, ls[f], nS[f], R, keys, vals, cbase, counters, errpair);
     else if (f == 1)
-      k_singular<KID, 1, 4><<<g, 128, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair);
+      k_singular<KID, 1, 4><<<g, kSingThreads, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair);
     else
-      k_singular<KID, 2, 5><<<g, 128, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair);
+      k_singular<KID, 2, 5><<<g, kSingThreads, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair);
     LAUNCHED();
     cbase += nS[f] * slots;
   }
