@@ -2035,180 +2035,15 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
   return NLG_OK;
 }
 
-// Window pre-reduction: one warp takes kWin consecutive COO slots (records of
-// mostly one root: they share the root's rows and their neighbours share
-// vertices) and reduces equal keys through a shared-memory hash table.  Each
-// 32-slot round sums equal keys in lane order (broadcast loop) and one lane
-// per key adds the round's sum to the table, rounds in slot order, so every
-// key's sum is formed in COO slot order: deterministic.  Absent keys (all
-// contributions +0.0) are dropped; a present sum of 0 is kept as -0.0.
-constexpr int kWin = 512;               // slots per warp window
-constexpr int kWinTab = 1024;           // hash slots (>= 2 kWin: never full)
-constexpr int kWinWarps = 4;
-template <typename KT>
-struct WinTable {
-  KT key[kWinTab];
-  double val[kWinTab];
-  unsigned char pres[kWinTab];
-};
-
-// KT = u32 when every non-sentinel key of the batch fits in 32 bits
-template <typename KT>
-__global__ void __launch_bounds__(32 * kWinWarps) k_window_reduce(const unsigned long long* __restrict__ keys,
-                                                                  const double* __restrict__ vals, long long n,
-                                                                  unsigned long long* okeys, double* ovals,
-                                                                  int* counts) {
-  extern __shared__ __align__(16) unsigned char win_smem[];
-  WinTable<KT>& T = reinterpret_cast<WinTable<KT>*>(win_smem)[threadIdx.x >> 5];
-  const KT SENT = (KT)~(KT)0;
-  const int lane = lane_id();
-  const long long w = (long long)blockIdx.x * kWinWarps + (threadIdx.x >> 5);
-  const long long base = w * kWin;
-  if (base >= n) return;
-  for (int i = lane; i < kWinTab; i += 32) T.key[i] = SENT;
-  auto load = [&](int r, KT& k, double& v) {
-    const long long g = base + r * 32 + lane;
-    const unsigned long long k64 = g < n ? __ldcs(&keys[g]) : kSentinel;
-    k = k64 == kSentinel ? SENT : (KT)k64;
-    v = g < n ? __ldcs(&vals[g]) : 0.0;
-  };
-  KT kn;
-  double vn;
-  load(0, kn, vn);
-  __syncwarp();
-#pragma unroll 1
-  for (int r = 0; r < kWin / 32; ++r) {
-    const KT k = kn;
-    const double v = vn;
-    if (r + 1 < kWin / 32) load(r + 1, kn, vn);  // prefetch the next round
-    const bool p = __double_as_longlong(v) != 0;
-    // group the lanes holding the same key (32-bit match on the folded key,
-    // verified; an exact broadcast loop covers the rare collision)
-    const unsigned fold = sizeof(KT) == 4 ? (unsigned)k : (unsigned)((unsigned long long)k ^ ((unsigned long long)k >> 32));
-    unsigned gm = __match_any_sync(0xffffffffu, fold);
-    if (sizeof(KT) > 4) {
-      const KT kl = __shfl_sync(0xffffffffu, k, __ffs(gm) - 1);
-      if (__any_sync(0xffffffffu, kl != k)) {
-        gm = 0;
-        for (int src = 0; src < 32; ++src)
-          if (__shfl_sync(0xffffffffu, k, src) == k) gm |= 1u << src;
-      }
-    }
-    const int gsize = __popc(gm);
-    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)gsize);
-    const bool lead = (__ffs(gm) - 1) == lane;
-    double acc = 0.0;
-    bool pres = false;
-    unsigned rem = gm;
-    for (int t = 0; t < maxg; ++t) {  // lane-ordered sum over the group
-      const int src = rem ? __ffs(rem) - 1 : lane;
-      rem &= rem - 1;
-      const double vs = __shfl_sync(0xffffffffu, v, src);
-      const int ps = __shfl_sync(0xffffffffu, (int)p, src);
-      if (t < gsize) {
-        acc += vs;
-        pres |= ps != 0;
-      }
-    }
-    if (lead && k != SENT) {
-      unsigned h = (unsigned)(((unsigned long long)k * 0x9E3779B97F4A7C15ull) >> 54) & (kWinTab - 1);
-      while (true) {
-        const KT prev = atomicCAS(&T.key[h], SENT, k);
-        if (prev == SENT) {
-          T.val[h] = acc;
-          T.pres[h] = pres;
-          break;
-        }
-        if (prev == k) {
-          T.val[h] += acc;
-          T.pres[h] |= pres;
-          break;
-        }
-        h = (h + 1) & (kWinTab - 1);
-      }
-    }
-    __syncwarp();
-  }
-  // emit the present keys of the table (slot order) into the window's region
-  int cnt = 0;
-  for (int i0 = 0; i0 < kWinTab; i0 += 32) {
-    const int i = i0 + lane;
-    const bool keep = T.key[i] != SENT && T.pres[i];
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int pos = cnt + __popc(m & ((1u << lane) - 1u));
-      const double sv = T.val[i];
-      okeys[base + pos] = (unsigned long long)T.key[i];
-      ovals[base + pos] = sv != 0.0 ? sv : -0.0;
-    }
-    cnt += __popc(m);
-  }
-  if (lane == 0) counts[w] = cnt;
-}
-
-__global__ void k_window_compact(const unsigned long long* __restrict__ keys, const double* __restrict__ vals,
-                                 const int* __restrict__ counts, const long long* __restrict__ offs,
-                                 unsigned long long* okeys, double* ovals) {
-  const long long w = blockIdx.x;
-  const int c = counts[w];
-  const long long src = w * kWin, dst = offs[w];
-  for (int i = threadIdx.x; i < c; i += blockDim.x) {
-    okeys[dst + i] = keys[src + i];
-    ovals[dst + i] = vals[src + i];
-  }
-}
-
 // Stable radix sort of the COO (row, col) keys, then one thread per run
 // sums its values in COO position order -> CSR rows of this batch.
 template <typename KT>
 nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64, double* vals, long long coo,
-                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept, bool prereduce,
-                     bool keys_narrow = false) {
+                     long long nrows, Csr& piece, long long& nnz, long long* coo_kept, bool keys_narrow = false) {
   int bits = 1;
   {
     const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
     while (bits < 64 && (1ull << bits) <= maxkey) ++bits;
-  }
-  // ---- window pre-reduction + compaction (deterministic)
-  DevBuf wk, wv, wc, wo;
-  if (prereduce && coo > kWin) {
-    const long long nwin = (coo + kWin - 1) / kWin;
-    CK(wk.alloc(sizeof(unsigned long long) * nwin * kWin, s));
-    CK(wv.alloc(sizeof(double) * nwin * kWin, s));
-    CK(wc.alloc(sizeof(int) * nwin, s));
-    CK(wo.alloc(sizeof(long long) * (nwin + 1), s));
-    {
-      const unsigned g = (unsigned)((nwin + kWinWarps - 1) / kWinWarps);
-      if (bits <= 32) {
-        const int smem = kWinWarps * (int)sizeof(WinTable<unsigned>);
-        CK(cudaFuncSetAttribute(k_window_reduce<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k_window_reduce<unsigned><<<g, 32 * kWinWarps, smem, s>>>(keys64, vals, coo, wk.as<unsigned long long>(),
-                                                                 wv.as<double>(), wc.as<int>());
-      } else {
-        const int smem = kWinWarps * (int)sizeof(WinTable<unsigned long long>);
-        CK(cudaFuncSetAttribute(k_window_reduce<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        k_window_reduce<unsigned long long><<<g, 32 * kWinWarps, smem, s>>>(
-            keys64, vals, coo, wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>());
-      }
-      LAUNCHED();
-    }
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, wc.as<int>(), wo.as<long long>(), (int)nwin, s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, wc.as<int>(), wo.as<long long>(), (int)nwin, s));
-    long long lo;
-    int lc;
-    CK(cudaMemcpyAsync(&lo, wo.as<long long>() + nwin - 1, sizeof lo, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lc, wc.as<int>() + nwin - 1, sizeof lc, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    TRACE("sync 1720");
-    const long long kept = lo + lc;
-    k_window_compact<<<(unsigned)nwin, 256, 0, s>>>(wk.as<unsigned long long>(), wv.as<double>(), wc.as<int>(),
-                                                    wo.as<long long>(), keys64, vals);
-    LAUNCHED();
-    g_launches += 1;
-    coo = kept;
   }
   DevBuf k1, k2, v2;
   KT* keys;
@@ -2686,8 +2521,8 @@ fits:
   Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
   long long nnz = 0;
   long long kept = 0;
-  rc = P.narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false, true)
-                : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, false);
+  rc = P.narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, true)
+                : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept);
   st->coo_reduced += kept;
   if (rc) return rc;
   piece.nnz = nnz;
@@ -3271,7 +3106,7 @@ nlg_status nlg_mass(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc, void*
     rc = narrow ? merge_csr<unsigned>(s, P, keys.as<unsigned long long>(), vals.as<double>(), coo, P.J, piece, nnz,
                                       &kept, false)
                 : merge_csr<unsigned long long>(s, P, keys.as<unsigned long long>(), vals.as<double>(), coo, P.J,
-                                                piece, nnz, &kept, false);
+                                                piece, nnz, &kept);
     if (rc) return rc;
     piece.nnz = nnz;
     pieces.push_back(piece);

@@ -308,121 +308,4 @@ __device__ __forceinline__ void full_identical(const Params& P, const double* kx
   for (int e = 0; e < 9 * NC2; ++e) { h0[e] *= c; h1[e] *= c; }
 }
 
-// ---------------------------------------------------------------------
-// truncated sweep (_engine._sweep :46-185 / _pyengine._sweep :48-152)
-//   MODE 0: outer = root k (to*), inner = l (ti*): kk += W oh_a oh_b S0,
-//           kl -= W oh_a SyQ_b
-//   MODE 1: outer = l, inner = root k: kl -= W oh_b SyP_a, kk += W Syy_ab
-//   MODE 2: identical pair: h0 = kk-half, h1 = second half
-// Returns true if any outer point saw a nonempty truncated region.
-// ---------------------------------------------------------------------
-template <int KID, int MODE>
-__device__ __forceinline__ bool sweep(const Params& P, const double* tox, const double* toy,
-                                      const double* tix, const double* tiy, double rs2, double* kk,
-                                      double* kl, long long& n_eval, long long& n_outer) {
-  using T = KTraits<KID>;
-  constexpr int NC = T::NC, NC2 = T::NC2;
-  const double twoA = twice_area(tox, toy);
-  const double o0 = tix[0], o1 = tiy[0];
-  const double e1x = tix[1] - o0, e1y = tiy[1] - o1, e2x = tix[2] - o0, e2y = tiy[2] - o1;
-  const double idet = 1.0 / cross2(e1x, e2y, e1y, e2x);
-  double px[7], py[7];
-  rule_points(P, tox, toy, px, py);
-  bool nonzero = false;
-#pragma unroll 1
-  for (int p = 0; p < 7; ++p) {
-    const double x0 = px[p], x1 = py[p];
-    Poly poly;
-    truncate_inner(tix, tiy, x0, x1, P.delta, P.ball, poly);
-    const int nv = poly.n;
-    if (nv < 3) continue;
-    nonzero = true;
-    ++n_outer;
-    const double W = c_rule.ow[p] * twoA;
-    double S0[NC2], SyP[3][NC2], SyQ[3][NC2], Syy[3][3][NC2];
-#pragma unroll
-    for (int i = 0; i < NC2; ++i) {
-      S0[i] = 0.0;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        SyP[a][i] = SyQ[a][i] = 0.0;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) Syy[a][b][i] = 0.0;
-      }
-    }
-#pragma unroll 1
-    for (int t = 1; t < nv - 1; ++t) {
-      const double q0x = poly.x[0], q0y = poly.y[0];
-      const double ax = poly.x[t] - q0x, ay = poly.y[t] - q0y;
-      const double bx = poly.x[t + 1] - q0x, by = poly.y[t + 1] - q0y;
-      const double jac2 = cross2(ax, by, ay, bx);
-      if (jac2 <= P.drop2) continue;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        double y0, y1, d0, d1, r2;
-        if (rs2 > 0.0) {  // the diagonal-skip predicate needs the reference's rounding
-          y0 = __dadd_rn(__dadd_rn(q0x, mul(ax, c_rule.ip[q][0])), mul(bx, c_rule.ip[q][1]));
-          y1 = __dadd_rn(__dadd_rn(q0y, mul(ay, c_rule.ip[q][0])), mul(by, c_rule.ip[q][1]));
-          d0 = x0 - y0;
-          d1 = x1 - y1;
-          r2 = sumsq(d0, d1);
-          if (r2 < rs2) continue;
-        } else {
-          y0 = fma(bx, c_rule.ip[q][1], fma(ax, c_rule.ip[q][0], q0x));
-          y1 = fma(by, c_rule.ip[q][1], fma(ay, c_rule.ip[q][0], q0y));
-          d0 = x0 - y0;
-          d1 = x1 - y1;
-          r2 = fma(d0, d0, d1 * d1);
-        }
-        double pv[NC2], qv[NC2];
-        kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
-        ++n_eval;
-        const double wq = c_rule.iw[q] * jac2;
-        const double u0 = y0 - o0, u1 = y1 - o1;
-        const double xi1 = (u0 * e2y - u1 * e2x) * idet;
-        const double xi2 = (e1x * u1 - e1y * u0) * idet;
-        const double h[3] = {1.0 - xi1 - xi2, xi1, xi2};
-#pragma unroll
-        for (int i = 0; i < NC2; ++i) {
-          const double tp = wq * pv[i];
-          const double tq = T::SYM ? tp : wq * qv[i];
-          if (MODE != 1) S0[i] += tp;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            if (MODE != 1) SyQ[a][i] = fma(tq, h[a], SyQ[a][i]);
-            if (MODE != 0) {
-              SyP[a][i] = fma(tp, h[a], SyP[a][i]);
-#pragma unroll
-              for (int b = 0; b < 3; ++b) Syy[a][b][i] = fma(tq, h[a] * h[b], Syy[a][b][i]);
-            }
-          }
-        }
-      }
-    }
-    const double* oh = c_rule.oh[p];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-#pragma unroll
-          for (int d = 0; d < NC; ++d) {
-            const int e = ((a * NC + c) * 3 + b) * NC + d;
-            const int i = c * NC + d;
-            if (MODE == 0) {
-              kk[e] += (W * (oh[a] * oh[b])) * S0[i];
-              kl[e] -= (W * oh[a]) * SyQ[b][i];
-            } else if (MODE == 1) {
-              kl[e] -= (W * oh[b]) * SyP[a][i];
-              kk[e] += W * Syy[a][b][i];
-            } else {
-              kk[e] += (W * (oh[a] * oh[b])) * S0[i] + W * Syy[a][b][i];
-              kl[e] -= (W * oh[a]) * SyQ[b][i] + (W * oh[b]) * SyP[a][i];
-            }
-          }
-  }
-  return nonzero;
-}
-
 }  // namespace nlg

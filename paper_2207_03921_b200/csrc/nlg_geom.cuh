@@ -236,16 +236,4 @@ __device__ __forceinline__ int truncate_inner(const double* tx, const double* ty
   return truncate_inner(make_tri(tx, ty), cx, cy, delta, ball, sx, sy, px, py);
 }
 
-// Small local polygon (for the thread-per-visit paths).
-struct Poly {
-  double x[kMaxPoly], y[kMaxPoly];
-  double sx[kMaxPoly], sy[kMaxPoly];
-  int n;
-};
-
-__device__ __forceinline__ void truncate_inner(const double* tx, const double* ty, double cx, double cy,
-                                               double delta, int ball, Poly& p) {
-  p.n = truncate_inner(tx, ty, cx, cy, delta, ball, p.sx, p.sy, p.x, p.y);
-}
-
 }  // namespace nlg
