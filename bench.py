@@ -280,7 +280,7 @@ def main():
         "all_integration": {"alg_flops": st0["alg_flops"], "ms": integ_ms,
                             "tflops": st0["alg_flops"] / (integ_ms * 1e-3) / 1e12 if integ_ms else 0.0},
         "phase_ms": {k: float(np.mean([s[k] for s in stats])) for k in
-                     ("ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge", "ms_total")},
+                     ("ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge", "ms_merge_stage_r", "ms_total")},
         "merge_hbm": {"coo_entries": st0["coo_entries"], "coo_reduced": st0["coo_reduced"], "nnz": st0["nnz"]},
     }
 

@@ -45,7 +45,7 @@ typedef int32_t nlg_status;
 #define NLG_ERR_NUMERICAL 2 /* maps to NumericalError (nonfinite local contribution) */
 #define NLG_ERR_CUDA 3      /* launch / runtime failure, no device, OOM */
 
-#define NLG_ABI_VERSION 1
+#define NLG_ABI_VERSION 2
 
 /* Kernel ids (kernels.py :57-118 built-ins + 3 = nonsymmetric affine). */
 #define NLG_KERNEL_FRACTIONAL 0  /* c |x-y|^(-2-2s) */
@@ -98,6 +98,7 @@ typedef struct nlg_stats {
   int64_t err_k, err_l; /* first nonfinite pair (lexicographic min), or -1 */
   double ms_prep, ms_candidates, ms_full, ms_partial, ms_singular, ms_merge, ms_total;
   double ms_integrate_kernels; /* full + partial + singular kernel time */
+  double ms_merge_stage_r;     /* per-root reduction part of ms_merge */
 } nlg_stats;
 
 int32_t nlg_abi_version(void);

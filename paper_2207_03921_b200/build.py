@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "nlg.cu")
-DEPS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("nlg_eval.cuh", "nlg_geom.cuh")] + [
+DEPS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("nlg_eval.cuh", "nlg_geom.cuh", "nlg_math.cuh")] + [
     os.path.join(ROOT, "include", "nlg.h")]
 OUT = os.path.join(HERE, "libnlg.so")
 

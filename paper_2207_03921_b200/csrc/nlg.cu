@@ -303,7 +303,11 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     if (!(needAk || needA[l])) return -1;
     return k == l ? 2 : (ns == 2 ? 3 : 4);
   }
-  if (LIGHT) return (needAk || ((el.w & 16) && needA[l])) ? 0 : -1;  // upper bound for the count pass
+  if (LIGHT) {  // upper bounds for the count pass: 0 full, 1 possibly clipped
+    if (!(needAk || ((el.w & 16) && needA[l]))) return -1;
+    const bool full_ub = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
+    return full_ub && !(P.analytic && k == l) ? 0 : 1;
+  }
   const bool full = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
   bool full_lk = full, rej_lk = false;
   if (k != l && (el.w & 16)) {  // root l's view of the same pair
@@ -318,7 +322,8 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     lx[0] = a.x; ly[0] = a.y; lx[1] = b.x; ly[1] = b.y; lx[2] = c.x; ly[2] = c.y;
     tcls = pair_trunc_class(P, kx, ky, xk, yk, ck, rk, lx, ly, cl, rl);
   }
-  const int cat_kl = full || tcls == 2 ? 0 : 1;
+  // (analytic mode: the identical pair keeps its stored blocks on the clipped path)
+  const int cat_kl = (full || tcls == 2) && !(P.analytic && k == l) ? 0 : 1;
   if (tcls == 1) return -1;  // every item empty in both visits: nothing to emit
   bool shared = false;
   if (k != l && (el.w & 16)) {
@@ -389,7 +394,10 @@ __global__ void __launch_bounds__(256, 2) k_candidates(Params P, Grid G, const i
         if (!FILL) {
           if (j < c1) cat = classify<true>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, vis, fl);
           c[C_EPI] += vis;
-          if (cat >= 0) c[cat == 0 ? C_FULL : cat]++;
+          // C_FULL: all records, C_PART: the possibly clipped ones
+          if (cat >= 0) {
+            if (cat <= 1) { c[C_FULL]++; c[C_PART] += cat; } else c[cat]++;
+          }
         } else {
           if (j < c1) cat = classify<false>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, vis, fl);
           nfull += cat == 0;
@@ -435,7 +443,7 @@ __global__ void __launch_bounds__(256, 2) k_candidates(Params P, Grid G, const i
 // per-row cost of a batch attempt that does not fit (batch planning): each
 // root's memory (bytes), record and COO-slot counts go to its first in-range row
 __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, const int* __restrict__ cnt,
-                            double rec_bytes, double sing_bytes, double root_bytes, double rec_slots,
+                            double rec_bytes, double store_bytes, double sing_bytes, double root_bytes, double rec_slots,
                             double sing_slots, unsigned long long* row_cost) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nR) return;
@@ -449,10 +457,11 @@ __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, con
     }
   if (home < 0) home = P.row_lo;
   const long long rec = cnt[(long long)C_FULL * nR + i];
+  const long long stored = P.analytic ? cnt[(long long)C_PART * nR + i] : rec;
   const long long sing = (long long)cnt[(long long)C_SID * nR + i] + cnt[(long long)C_SED * nR + i] +
                          cnt[(long long)C_SVX * nR + i];
   unsigned long long* rc = row_cost + 3 * (home - P.row_lo);
-  atomicAdd(&rc[0], (unsigned long long)(rec * rec_bytes + sing * sing_bytes + root_bytes));
+  atomicAdd(&rc[0], (unsigned long long)(rec * rec_bytes + stored * store_bytes + sing * sing_bytes + root_bytes));
   atomicAdd(&rc[1], (unsigned long long)rec);
   atomicAdd(&rc[2], (unsigned long long)(rec * rec_slots + sing * sing_slots + 9 * P.nc * P.nc));
 }
@@ -525,9 +534,9 @@ struct VisitOut {
   double* kkv;              // [record][side][NKK] own blocks of visit A (k, l) / B (l, k), symmetric: I <= J
   double* klv;              // [record][side][b][NVP] neighbour blocks, column-major and padded:
                             // the 3NC row values of one neighbour dof are contiguous
-  long long nvis;           // records of both lists
-  const int* revpos;        // record -> its side B's block: nvis + revpos[record] (reverse-index order)
-  long long vofs;           // this list's first record index
+  long long a_base;         // side A of list record v -> block a_base + v
+  long long b_base;         // side B -> block b_base + revpos[v] (reverse-index order)
+  const int* revpos;
   long long nlist;
   unsigned long long* counters;
   unsigned long long* errpair;
@@ -557,6 +566,52 @@ __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, lo
     O.klv[slot * B::KLS + B::kl(I, J)] = on ? emit_val(kl[e]) : 0.0;
   }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
+}
+
+__device__ __forceinline__ double4 ld_f4(const double4* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// Per-element factors of the analytic full pairs (Params::analytic).  For a
+// full pair of the constant (f = c) or affine (f(x) = (1 + a x_1) b) kernel
+// the visit (r, n) block of _engine._sweep (:46-185, both sweeps over the
+// whole triangles) is, with A2 = twice the area and f at the 7 rule points,
+//   kk[a,b] = 2 A2_r A2_n sw Phi_r[a,b],   Phi_r[a,b] = sum_p w_p H_pa H_pb f(x_p on r)
+//   kl[a,b] = -2 A2_r whs_a (A2_n psi_n[b]), psi_n[b] = sum_q w_q H_qb f(y_q on n)
+// (sw = sum w, whs_a = sum_p w_p H_pa): the partner enters only through
+// A2_n and A2_n psi_n, so stage R sums those per root / neighbour dof.
+template <int KID>
+__global__ void k_elem_factors(Params P, double4* ft) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P.K) return;
+  double tx[3], ty[3], px[7], py[7];
+  load_tri(P, e, tx, ty);
+  rule_points(P, tx, ty, px, py);
+  double ps[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    const double f = KID == 2 ? P.cst : (1.0 + P.kp0 * px[p]) * P.kp1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ps[a] = fma(c_rule.wh[p][a], f, ps[a]);
+  }
+  const double a2 = twice_area(tx, ty);
+  ft[e] = make_double4(a2 * ps[0], a2 * ps[1], a2 * ps[2], a2);
+}
+
+// Phi_r[a][b] of the root (see k_elem_factors)
+template <int KID>
+__device__ __forceinline__ double root_phi(const Params& P, int r, int a, int b) {
+  double tx[3], ty[3], px[7], py[7];
+  load_tri(P, r, tx, ty);
+  rule_points(P, tx, ty, px, py);
+  double v = 0.0;
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    const double f = KID == 2 ? P.cst : (1.0 + P.kp0 * px[p]) * P.kp1;
+    v = fma(c_rule.whh[p][a * 3 + b], f, v);
+  }
+  return v;
 }
 
 // full records, one thread each: the 7x7 point-pair matrix gives both visits
@@ -600,9 +655,8 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
       ev0 += ne * mult;
       out0 += 14 * mult;
     }
-    const long long vi = O.vofs + v;
-    emit_side<NC>(P, O, vi, emitA, k, l, kkA, klA);
-    emit_side<NC>(P, O, O.nvis + __ldg(&O.revpos[vi]), emitB && k != l, l, k, kkB, klB);
+    emit_side<NC>(P, O, O.a_base + v, emitA, k, l, kkA, klA);
+    emit_side<NC>(P, O, O.b_base + __ldg(&O.revpos[v]), emitB && k != l, l, k, kkB, klB);
   }
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
   warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
@@ -1098,8 +1152,7 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
         const int side = g / C::NSIDE, w = g % C::NSIDE;
         const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
         const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
-        const long long vi = O.vofs + v;
-        const long long slot = side ? O.nvis + __ldg(&O.revpos[vi]) : vi;
+        const long long slot = side ? O.b_base + __ldg(&O.revpos[v]) : O.a_base + v;
         if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
         if (w < C::NKK) {
           O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;  // unique (I <= J) order
@@ -1146,9 +1199,15 @@ struct RootIn {
   const long long* off;
   long long nF;
   const int2* rec;  // full then clipped records
-  const int* rev_start;
-  const int* partB;  // [reverse position] the record's root (side B's partner)
-  long long nvis;
+  // reverse indices (side B by partner root), one per list: per-root ranges
+  // and the record's root at each reverse position
+  const int* rstartF;
+  const int* rstartP;
+  const int* partBF;
+  const int* partBP;
+  // block slots: side A of list record v -> a + v, side B -> b + reverse position
+  long long aF, bF, aP, bP;
+  int analytic;             // full sides carry no blocks: their terms come from ftab
   const double* kkv;  // [side][NKK]
   const double* klv;  // [side][3][NVP]
   const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
@@ -1163,23 +1222,33 @@ struct RootOut {
   long long r_base, r_cap;
   int* overflow;
   unsigned long long* total;  // run entries of all chunks (written by the last one)
+  unsigned long long* errpair;
 };
 
+// A root's record sides in their fixed order: side A of its full records,
+// side B of the full records where it is the partner, then the same two for
+// the clipped list (the reference adds the visits one by one into the root's
+// rows; any fixed order is run-to-run deterministic)
 struct RootSides {
-  long long f0, fn, p0, pn, r0, rn;
-  __device__ __forceinline__ long long n() const { return fn + pn + rn; }
-  // block slot of the root's rs-th side: side A of its own records (full
-  // then clipped list), then side B of the records where it is the partner,
-  // stored contiguously in reverse-index order
+  long long f0, fn, fb0, fbn, p0, pn, pb0, pbn;
+  __device__ __forceinline__ long long n() const { return fn + fbn + pn + pbn; }
+  __device__ __forceinline__ long long nfull() const { return fn + fbn; }
   __device__ __forceinline__ long long slot(const RootIn& I, long long rs) const {
-    if (rs < fn) return f0 + rs;
-    if (rs < fn + pn) return p0 + (rs - fn);
-    return I.nvis + r0 + (rs - fn - pn);
+    if (rs < fn) return I.aF + f0 + rs;
+    rs -= fn;
+    if (rs < fbn) return I.bF + fb0 + rs;
+    rs -= fbn;
+    if (rs < pn) return I.aP + p0 + rs;
+    return I.bP + pb0 + (rs - pn);
   }
   // the other element of that side's pair
   __device__ __forceinline__ int partner(const RootIn& I, long long rs) const {
-    if (rs < fn + pn) return __ldg(&I.rec[slot(I, rs)].y) & kIdMask;
-    return __ldg(&I.partB[r0 + (rs - fn - pn)]);
+    if (rs < fn) return __ldg(&I.rec[f0 + rs].y) & kIdMask;
+    rs -= fn;
+    if (rs < fbn) return __ldg(&I.partBF[fb0 + rs]);
+    rs -= fbn;
+    if (rs < pn) return __ldg(&I.rec[I.nF + p0 + rs].y) & kIdMask;
+    return __ldg(&I.partBP[pb0 + (rs - pn)]);
   }
 };
 
@@ -1187,10 +1256,12 @@ __device__ __forceinline__ RootSides root_sides(const RootIn& I, int i) {
   RootSides R;
   R.f0 = I.off[0 * (long long)(I.nR + 1) + i];
   R.fn = I.cnt[(long long)C_FULL * I.nR + i];
-  R.p0 = I.nF + I.off[1 * (long long)(I.nR + 1) + i];
+  R.fb0 = I.rstartF[i];
+  R.fbn = I.rstartF[i + 1] - R.fb0;
+  R.p0 = I.off[1 * (long long)(I.nR + 1) + i];
   R.pn = I.cnt[(long long)C_PART * I.nR + i];
-  R.r0 = I.rev_start[i];
-  R.rn = I.rev_start[i + 1] - R.r0;
+  R.pb0 = I.rstartP[i];
+  R.pbn = I.rstartP[i + 1] - R.pb0;
   return R;
 }
 
@@ -1214,18 +1285,24 @@ struct RootSmem {
   using Scan = cub::BlockScan<int, kRootThreads>;
   union {
     typename Sort::TempStorage sort;
-    double red[kRootThreads / 32][9 * NC * NC];
+    double red[kRootThreads / 32][9 * NC * NC + 1];
   } u;
   typename Scan::TempStorage scan;
   unsigned last_key[kRootThreads];   // key at each thread's last sorted position
-  double cont[kRootThreads][NV];     // each thread's leading partial run (before its first head)
+  double cont[kRootThreads][NV + 1]; // each thread's leading partial run (before its first head)
   unsigned cont_pres[kRootThreads];
   unsigned char has_head[kRootThreads];
 };
 
-template <int NC>
+// AN: analytic full sides (nc = 1).  Their own-block term is
+// 2 A2_r sw Phi_r * sum A2_n and their neighbour term for row a and dof w is
+// -2 A2_r whs_a * sum (A2_n psi_n[b]) (k_elem_factors): one scalar per item,
+// kept beside the stored columns (bit 31 of the presence mask) and combined
+// at the end of each run.
+template <int NC, bool AN>
 __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootIn I, RootOut O, int key_bits) {
   constexpr int N3 = 3 * NC, E = 9 * NC * NC, NWARP = kRootThreads / 32, NV = N3 * NC, IT = kRootItems;
+  constexpr unsigned PT = 1u << 31;  // presence bit of the analytic scalar
   using SM = RootSmem<NC>;
   extern __shared__ __align__(16) unsigned char root_smem[];
   SM& S = *reinterpret_cast<SM*>(root_smem);
@@ -1244,7 +1321,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
   const int i = I.chunk_root[ch], c = ch - I.chunk_first[i];
   const int k = I.roots[i];
   const RootSides R = root_sides(I, i);
-  const long long n_rs = R.n(), nitems = 3 * n_rs;
+  const long long n_rs = R.n(), nitems = 3 * n_rs, nan_rs = AN ? R.nfull() : 0;
   const int4 dk4 = P.dofs[k];
   const int dka[3] = {dk4.x, dk4.y, dk4.z};
   unsigned inr = 0;  // in-range local rows I = (a, c)
@@ -1254,15 +1331,28 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     const long long row = (long long)NC * dka[r / NC] + r % NC;
     if (row >= P.row_lo && row < P.row_hi) { inr |= 1u << r; ++nr; }
   }
+  const double a2r = AN ? __ldg(&P.ftab[k].w) : 0.0;
   // ---- the root's own block (symmetric, packed), by its first chunk
   if (c == 0) {
     constexpr int NKK = Blk<NC>::NKK;
-    double acc[NKK];
+    double acc[NKK + 1];  // [NKK]: sum of the analytic partners' A2
 #pragma unroll
-    for (int e = 0; e < NKK; ++e) acc[e] = 0.0;
+    for (int e = 0; e <= NKK; ++e) acc[e] = 0.0;
     unsigned fl = 0;  // presence: some side's value is nonzero
+    if (AN) {
+      const double4 fr = ld_f4(P.ftab + k);
+      const bool rbad = nonfinite(fr.x) | nonfinite(fr.y) | nonfinite(fr.z) | nonfinite(fr.w);
+      for (long long rs = t; rs < nan_rs; rs += kRootThreads) {
+        const int n = R.partner(I, rs);
+        const double4 fn = ld_f4(P.ftab + n);
+        acc[NKK] += fn.w;
+        fl |= fn.w != 0.0 ? PT : 0u;
+        report_nonfinite(rbad | nonfinite(fn.x) | nonfinite(fn.y) | nonfinite(fn.z) | nonfinite(fn.w), k, n, P.K,
+                         O.errpair);
+      }
+    }
 #pragma unroll 2
-    for (long long rs = t; rs < n_rs; rs += kRootThreads) {
+    for (long long rs = nan_rs + t; rs < n_rs; rs += kRootThreads) {
       const double* src = I.kkv + R.slot(I, rs) * NKK;
 #pragma unroll
       for (int e = 0; e < NKK; ++e) {
@@ -1272,7 +1362,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
       }
     }
 #pragma unroll
-    for (int e = 0; e < NKK; ++e) {
+    for (int e = 0; e < (AN ? NKK + 1 : NKK); ++e) {
       double v = acc[e];
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1288,7 +1378,18 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
       double v = 0.0;
 #pragma unroll
       for (int w = 0; w < NWARP; ++w) v += S.u.red[w][u];
-      const bool present = I.cnt[(long long)C_KK * I.nR + i] != 0 && ((s_fl >> u) & 1ull);
+      bool pres = (s_fl >> u) & 1ull;
+      if (AN && (s_fl & PT)) {
+        double sa = 0.0, sw = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) sa += S.u.red[w][NKK];
+#pragma unroll
+        for (int p = 0; p < 7; ++p) sw += c_rule.ow[p];
+        const double phi = (2.0 * a2r * sw) * (P.kid == 2 ? root_phi<2>(P, k, rr, cc) : root_phi<3>(P, k, rr, cc));
+        v = fma(phi, sa, v);
+        pres |= phi != 0.0;
+      }
+      const bool present = I.cnt[(long long)C_KK * I.nR + i] != 0 && pres;
       const long long slot = O.kk_base + (long long)i * E + t;
       put_key(P, O.keys, slot,
               present ? coo_key(P, (long long)NC * dka[rr / NC] + rr % NC, (long long)NC * dka[cc / NC] + cc % NC)
@@ -1297,10 +1398,10 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     }
     __syncthreads();
   }
-  // ---- neighbour items of this chunk: (dof base w, value column) sorted by w
+  // ---- neighbour items of this chunk: (dof base w, item position) sorted by w
   const long long c0 = (long long)c * kRootCap;
   const int nval = nr ? (int)min((long long)kRootCap, max(0LL, nitems - c0)) : 0;
-  unsigned key[IT], col[IT];  // col: (record side * 3 + b), the item's value column in klv
+  unsigned key[IT], col[IT];  // col: the item's position in the chunk (item g = c0 + col: side g / 3, dof g % 3)
   int nseg = 0, hb = 0;
   unsigned heads = 0;
   if (nval) {
@@ -1315,7 +1416,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
         const int b = (int)(g - 3 * rs);
         const int4 dn = __ldg(&P.dofs[R.partner(I, rs)]);
         key[q] = (unsigned)(b == 0 ? dn.x : (b == 1 ? dn.y : dn.z));
-        col[q] = (unsigned)(R.slot(I, rs) * 3 + b);
+        col[q] = (unsigned)j;
       }
     }
     typename SM::Sort(S.u.sort).Sort(key, col, 0, key_bits);  // blocked: position t IT + q
@@ -1357,10 +1458,22 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     s_base = excl;
   }
   if (!nval) return;  // block-uniform
+  // analytic row factors -2 A2_r whs_a
+  double fkl[N3];
+#pragma unroll
+  for (int r = 0; r < N3; ++r) {
+    fkl[r] = 0.0;
+    if (AN) {
+      double whs = 0.0;
+#pragma unroll
+      for (int p = 0; p < 7; ++p) whs += c_rule.wh[p][r];
+      fkl[r] = -2.0 * a2r * whs;
+    }
+  }
   // ---- run sums: each thread adds its sorted positions in order; a run that
   // starts in an earlier thread gets this thread's leading piece afterwards
   const int npos = min(IT, max(0, nval - t * IT));
-  double acc[NV];
+  double acc[NV], acc_t = 0.0;
   unsigned pres = 0;
 #pragma unroll
   for (int e = 0; e < NV; ++e) acc[e] = 0.0;
@@ -1373,17 +1486,27 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
 #pragma unroll
       for (int d = 0; d < NC; ++d) {
         const int e = d * N3 + r;
+        double v = acc[e];
+        bool pr = (pres >> e) & 1u;
+        if (AN && (pres & PT)) {
+          v = fma(fkl[r], acc_t, v);
+          pr |= fkl[r] != 0.0;
+        }
         put_key(P, O.keys, pos, (unsigned long long)row * (unsigned long long)P.J + (unsigned long long)NC * w + d);
-        O.vals[pos] = ((pres >> e) & 1u) ? (acc[e] != 0.0 ? acc[e] : -0.0) : 0.0;
+        O.vals[pos] = pr ? (v != 0.0 ? v : -0.0) : 0.0;
         ++pos;
       }
     }
   };
-  // the value columns of this thread's positions, fetched while the block
-  // waits for its output offset
+  // the value columns of this thread's stored positions, fetched while the
+  // block waits for its output offset
 #pragma unroll
   for (int q = 0; q < IT; ++q)
-    if (q < npos) asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + (long long)col[q] * Blk<NC>::NVP));
+    if (q < npos) {
+      const long long g = c0 + col[q], rs = g / 3;
+      if (rs >= nan_rs)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + (R.slot(I, rs) * 3 + (g - 3 * rs)) * Blk<NC>::NVP));
+    }
   __syncthreads();  // s_base, has_head
   const long long base = s_base;
   const bool fits = base + count <= O.r_cap;
@@ -1398,38 +1521,49 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
         } else {  // leading piece of a run begun earlier
 #pragma unroll
           for (int e = 0; e < NV; ++e) S.cont[t][e] = acc[e];
+          S.cont[t][NV] = acc_t;
           S.cont_pres[t] = pres;
         }
         ++seg;
         wseg = key[q];
 #pragma unroll
         for (int e = 0; e < NV; ++e) acc[e] = 0.0;
+        acc_t = 0.0;
         pres = 0;
       }
-      const double* src = I.klv + (long long)col[q] * Blk<NC>::NVP;
+      const long long g = c0 + col[q], rs = g / 3;
+      const int b = (int)(g - 3 * rs);
+      if (AN && rs < nan_rs) {
+        const double4 fn = ld_f4(P.ftab + R.partner(I, rs));
+        const double v = b == 0 ? fn.x : (b == 1 ? fn.y : fn.z);
+        acc_t += v;
+        pres |= v != 0.0 ? PT : 0u;
+      } else {
+        const double* src = I.klv + (R.slot(I, rs) * 3 + b) * Blk<NC>::NVP;
 #pragma unroll
-      for (int e = 0; e < NV; ++e) {  // e = d * N3 + I
-        const double v = __ldg(&src[e]);
-        acc[e] += v;
-        pres |= (__double_as_longlong(v) != 0 ? 1u : 0u) << e;
+        for (int e = 0; e < NV; ++e) {  // e = d * N3 + I
+          const double v = __ldg(&src[e]);
+          acc[e] += v;
+          pres |= (__double_as_longlong(v) != 0 ? 1u : 0u) << e;
+        }
       }
     }
   }
   if (!heads && npos > 0) {  // the whole range continues an earlier run
 #pragma unroll
     for (int e = 0; e < NV; ++e) S.cont[t][e] = acc[e];
+    S.cont[t][NV] = acc_t;
     S.cont_pres[t] = pres;
   }
   __syncthreads();
   if (heads) {  // the last run begun here may continue into the next threads
     const int ntot = (nval + IT - 1) / IT;
     for (int u = t + 1; u < ntot; ++u) {
-      // thread u's leading piece belongs to this run unless u starts with a head
+      // thread u's leading piece belongs to this run (up to its first head)
       const unsigned uh = S.has_head[u];
-      const int upos = u * IT;
-      (void)upos;
 #pragma unroll
       for (int e = 0; e < NV; ++e) acc[e] += S.cont[u][e];
+      acc_t += S.cont[u][NV];
       pres |= S.cont_pres[u];
       if (uh) break;
     }
@@ -1663,7 +1797,7 @@ __global__ void k_seg_starts(const KT* __restrict__ key, long long n, const int*
 template <typename KT>
 __global__ void k_seg_sum(const KT* __restrict__ key, const double* __restrict__ val,
                           const long long* __restrict__ start, long long nseg, long long J, int* present,
-                          int* rowcnt, int* col, double* sum) {
+                          int* segrow, int* col, double* sum) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= nseg) return;
   const long long a = start[s], b = start[s + 1];
@@ -1677,8 +1811,23 @@ __global__ void k_seg_sum(const KT* __restrict__ key, const double* __restrict__
   const unsigned long long kk = (unsigned long long)key[a];
   present[s] = pres;
   col[s] = (int)(kk % (unsigned long long)J);
+  segrow[s] = (int)(kk / (unsigned long long)J);
   sum[s] = acc;
-  if (pres) atomicAdd(&rowcnt[kk / (unsigned long long)J], 1);
+}
+
+// CSR row pointers from the row-sorted segments: indptr[r] = output position
+// of the first segment whose row is >= r (no per-row atomics)
+__global__ void k_seg_indptr(const int* __restrict__ segrow, const long long* __restrict__ pos,
+                             const int* __restrict__ present, long long nseg, long long nrows, long long* indptr) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const int r = segrow[s];
+  const int rp = s ? segrow[s - 1] : -1;
+  for (int rr = rp + 1; rr <= r; ++rr) indptr[rr] = pos[s];
+  if (s == nseg - 1) {
+    const long long end = pos[s] + present[s];
+    for (long long rr = r + 1; rr <= nrows; ++rr) indptr[rr] = end;
+  }
 }
 
 __global__ void k_seg_scatter(const int* __restrict__ present, const long long* __restrict__ pos,
@@ -1816,6 +1965,7 @@ struct nlg_plan {
   int4* dofs = nullptr;
   double2* ctr = nullptr;
   double* rad = nullptr;
+  double4* ftab = nullptr;  // analytic full-pair factors (k_elem_factors)
   double* sing_tab[3][5] = {};
   int sing_n[3] = {0, 0, 0};
   bool prepped = false;
@@ -1897,6 +2047,11 @@ nlg_status prep(nlg_plan* pl) {
   CK(cudaMemcpyAsync(ext.p, init, sizeof init, cudaMemcpyHostToDevice, st));
   k_bounds<<<grid_for(K, 256), 256, 0, st>>>(P, pl->ctr, pl->rad, ext.as<unsigned long long>());
   LAUNCHED();
+  if (P.analytic && K) {
+    if (P.kid == 2) k_elem_factors<2><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab);
+    else k_elem_factors<3><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab);
+    LAUNCHED();
+  }
   unsigned long long h[5];
   CK(cudaMemcpyAsync(h, ext.p, sizeof h, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1981,17 +2136,14 @@ long long alg_flops(const Params& P, const unsigned long long* c, int part) {
 }
 
 template <int KID>
-nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, long long nF, const int2* lp,
-                      long long nP, VisitOut O, cudaEvent_t ev_mid) {
-  O.vofs = 0;
-  O.nlist = nF;
-  if (nF) {
-    k_full<KID><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, O);
+nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2* lp, VisitOut OF, VisitOut O,
+                      cudaEvent_t ev_mid) {
+  const long long nF = OF.nlist, nP = O.nlist;
+  if (nF) {  // (analytic full pairs: none to integrate)
+    k_full<KID><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, OF);
     LAUNCHED();
   }
   CK(cudaEventRecord(ev_mid, pl->stream));
-  O.vofs = nF;
-  O.nlist = nP;
   if (nP) {
     const long long chunks = (nP + 1) / 2;
     const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
@@ -2075,7 +2227,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
   // the sentinel's low `bits` bits are all ones, above every valid key
   const KT* sk = dk.Current();
   const double* sv = dv.Current();
-  DevBuf head, sid, start, present, rowcnt, col, sum, pos;
+  DevBuf head, sid, start, present, segrow, col, sum, pos;
   CK(head.alloc(sizeof(int) * std::max(coo, 1LL), s));
   CK(sid.alloc(sizeof(long long) * (coo + 1), s));
   if (coo) {
@@ -2103,8 +2255,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
   CK(col.alloc(sizeof(int) * std::max(nseg, 1LL), s));
   CK(sum.alloc(sizeof(double) * std::max(nseg, 1LL), s));
   CK(pos.alloc(sizeof(long long) * (nseg + 1), s));
-  CK(rowcnt.alloc(sizeof(int) * (nrows + 1), s));
-  CK(cudaMemsetAsync(rowcnt.p, 0, sizeof(int) * (nrows + 1), s));
+  CK(segrow.alloc(sizeof(int) * std::max(nseg, 1LL), s));
   CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
   nnz = 0;
   if (nseg) {
@@ -2112,7 +2263,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
                                                         start.as<long long>());
     LAUNCHED();
     k_seg_sum<KT><<<grid_for(nseg, 256), 256, 0, s>>>(sk, sv, start.as<long long>(), nseg, P.J, present.as<int>(),
-                                                      rowcnt.as<int>(), col.as<int>(), sum.as<double>());
+                                                      segrow.as<int>(), col.as<int>(), sum.as<double>());
     LAUNCHED();
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
@@ -2131,24 +2282,21 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     k_seg_scatter<<<grid_for(nseg, 256), 256, 0, s>>>(present.as<int>(), pos.as<long long>(), col.as<int>(),
                                                       sum.as<double>(), nseg, piece.indices, piece.data);
     LAUNCHED();
+    k_seg_indptr<<<grid_for(nseg, 256), 256, 0, s>>>(segrow.as<int>(), pos.as<long long>(), present.as<int>(), nseg,
+                                                     nrows, piece.indptr);
+    LAUNCHED();
+    g_launches += 1;
   } else {
     CK(cudaMallocAsync(&piece.indices, sizeof(int), s));
     CK(cudaMallocAsync(&piece.data, sizeof(double), s));
-  }
-  {
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rowcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
-    g_launches += 2;
+    CK(cudaMemsetAsync(piece.indptr, 0, sizeof(long long) * (nrows + 1), s));
   }
   piece.nnz = nnz;
   return NLG_OK;
 }
 
 struct Timing {
-  double prep = 0, cand = 0, full = 0, part = 0, sing = 0, merge = 0;
+  double prep = 0, cand = 0, full = 0, part = 0, sing = 0, merge = 0, stage_r = 0;
 };
 
 // one row batch: returns NLG_OK and appends to `out`, or asks for a split
@@ -2259,6 +2407,8 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     }
   }
   const long long nUB = tot[C_FULL];  // upper bound of full + clipped records
+  // records with stored blocks: all, or (analytic full pairs) the clipped ones
+  const long long nStUB = P.analytic ? tot[C_PART] : nUB;
   const long long nS[3] = {tot[C_SID], tot[C_SED], tot[C_SVX]};
   const int NC = P.nc;
   const long long E = 9LL * NC * NC;
@@ -2269,12 +2419,12 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     const long long coo_ub = (long long)nR * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC +
                              (long long)(kRunFrac * (double)(nUB * 2 * E)) + 1;
     const long long side_bytes = 8LL * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));  // kkv + klv
-    const long long bytes = nUB * 2 * side_bytes + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
+    const long long bytes = nStUB * 2 * side_bytes + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
                             nUB * 24;
-    // 32-bit sort payloads: record sides x 3 (stage R) and COO entries must fit
-    const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB * 6 >= (1LL << 32);
+    // 32-bit sizes: records (reverse-index sort) and COO entries must fit
+    const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB >= (1LL << 31);
     if (too_big && row_hi - row_lo <= P.nc) {
-      if (coo_ub < (1LL << 31) && nUB * 6 < (1LL << 32)) goto fits;  // one vertex's rows: try anyway
+      if (coo_ub < (1LL << 31) && nUB < (1LL << 31)) goto fits;  // one vertex's rows: try anyway
       set_err("a single row needs %lld COO slots", coo_ub);
       return NLG_ERR_CUDA;
     }
@@ -2286,17 +2436,18 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       DevBuf rcost;
       CK(rcost.alloc(sizeof(unsigned long long) * 3 * nrows, s));
       CK(cudaMemsetAsync(rcost.p, 0, sizeof(unsigned long long) * 3 * nrows, s));
-      const double rec_bytes = 16.0 * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36)) + kRunFrac * 2 * E * 32 + 40;
+      const double store_bytes = 16.0 * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));
+      const double rec_bytes = kRunFrac * 2 * E * 32 + 40;
       const double sing_bytes = 36.0 * NC * NC * 32 + 8, root_bytes = E * 32.0 + 64;
       if (nR)
-        k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, sing_bytes,
+        k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, store_bytes, sing_bytes,
                                                       root_bytes, kRunFrac * 2 * E, 36.0 * NC * NC,
                                                       rcost.as<unsigned long long>());
       LAUNCHED();
       std::vector<unsigned long long> hcost((size_t)3 * nrows);
       CK(cudaMemcpyAsync(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      const double lim[3] = {budget > 0 ? 0.7 * (double)budget : 1e300, 0.7 * (double)(1LL << 32) / 6.0,
+      const double lim[3] = {budget > 0 ? 0.7 * (double)budget : 1e300, 0.7 * (double)(1LL << 31),
                              0.7 * (double)(1LL << 31)};
       double acc[3] = {0, 0, 0};
       for (long long r = 0; r < nrows; ++r) {
@@ -2372,37 +2523,46 @@ fits:
     g_launches += 2;
   }
   const long long nvis = nF + nPt;
-  const long long coo = (long long)nR * E + nvis * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
-  // reverse index of side-B records by partner root (stable: record order)
-  DevBuf rkey, rkey2, ritem0, ritem, rstart;
-  CK(rkey.alloc(sizeof(unsigned) * std::max(nvis, 1LL), s));
-  CK(rkey2.alloc(sizeof(unsigned) * std::max(nvis, 1LL), s));
-  CK(ritem0.alloc(sizeof(int) * std::max(nvis, 1LL), s));
-  CK(ritem.alloc(sizeof(int) * std::max(nvis, 1LL), s));
-  CK(rstart.alloc(sizeof(int) * (nR + 1), s));
-  if (nvis) {
-    k_rev_keys<<<grid_for(nvis, 256), 256, 0, s>>>(lf, nvis, inR.as<int>(), nR, rkey.as<unsigned>(), ritem0.as<int>());
+  const long long nst = P.analytic ? nPt : nvis;  // records with stored blocks
+  const long long coo = (long long)nR * E + nst * 2 * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
+  // reverse index of side-B records by partner root, one per list (stable:
+  // list order): per-root ranges, each record's reverse position (its side-B
+  // block goes there) and the record's root at each position
+  DevBuf rstartF, rstartP, revposF, revposP, partBF, partBP;
+  auto reverse_index = [&](const int2* list, long long n, DevBuf& rstart, DevBuf& revpos, DevBuf& partB) -> nlg_status {
+    DevBuf rkey, rkey2, ritem0, ritem;
+    CK(rkey.alloc(sizeof(unsigned) * std::max(n, 1LL), s));
+    CK(rkey2.alloc(sizeof(unsigned) * std::max(n, 1LL), s));
+    CK(ritem0.alloc(sizeof(int) * std::max(n, 1LL), s));
+    CK(ritem.alloc(sizeof(int) * std::max(n, 1LL), s));
+    CK(rstart.alloc(sizeof(int) * (nR + 1), s));
+    CK(revpos.alloc(sizeof(int) * std::max(n, 1LL), s));
+    CK(partB.alloc(sizeof(int) * std::max(n, 1LL), s));
+    if (n) {
+      k_rev_keys<<<grid_for(n, 256), 256, 0, s>>>(list, n, inR.as<int>(), nR, rkey.as<unsigned>(), ritem0.as<int>());
+      LAUNCHED();
+      int rbits = 1;
+      while ((1ll << rbits) <= nR) ++rbits;
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, rkey.as<unsigned>(), rkey2.as<unsigned>(), ritem0.as<int>(),
+                                         ritem.as<int>(), (int)n, 0, rbits, s));
+      DevBuf tmp;
+      CK(tmp.alloc(tb, s));
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, rkey.as<unsigned>(), rkey2.as<unsigned>(), ritem0.as<int>(),
+                                         ritem.as<int>(), (int)n, 0, rbits, s));
+      g_launches += 1 + (rbits + 7) / 8;
+    }
+    k_cell_ranges<<<grid_for(nR + 1, 256), 256, 0, s>>>(rkey2.as<unsigned>(), (int)n, nR, rstart.as<int>());
     LAUNCHED();
-    int rbits = 1;
-    while ((1ll << rbits) <= nR) ++rbits;
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, rkey.as<unsigned>(), rkey2.as<unsigned>(), ritem0.as<int>(),
-                                       ritem.as<int>(), (int)nvis, 0, rbits, s));
-    DevBuf tmp;
-    CK(tmp.alloc(tb, s));
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, rkey.as<unsigned>(), rkey2.as<unsigned>(), ritem0.as<int>(),
-                                       ritem.as<int>(), (int)nvis, 0, rbits, s));
-    g_launches += 1 + (rbits + 7) / 8;
-  }
-  k_cell_ranges<<<grid_for(nR + 1, 256), 256, 0, s>>>(rkey2.as<unsigned>(), (int)nvis, nR, rstart.as<int>());
-  LAUNCHED();
-  DevBuf revpos, partB;  // side-B blocks are stored in reverse-index order (contiguous per root)
-  CK(revpos.alloc(sizeof(int) * std::max(nvis, 1LL), s));
-  CK(partB.alloc(sizeof(int) * std::max(nvis, 1LL), s));
-  if (nvis) {
-    k_rev_pos<<<grid_for(nvis, 256), 256, 0, s>>>(ritem.as<int>(), nvis, lf, revpos.as<int>(), partB.as<int>());
-    LAUNCHED();
-  }
+    if (n) {
+      k_rev_pos<<<grid_for(n, 256), 256, 0, s>>>(ritem.as<int>(), n, list, revpos.as<int>(), partB.as<int>());
+      LAUNCHED();
+    }
+    return NLG_OK;
+  };
+  // (the sort scratch of each index is released at the end of the batch)
+  if (nlg_status r = reverse_index(lf, nF, rstartF, revposF, partBF)) return r;
+  if (nlg_status r = reverse_index(lp, nPt, rstartP, revposP, partBP)) return r;
   CK(cudaEventRecord(ev[1], s));
   // ---- integrate
   const long long nsing_slots = (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
@@ -2412,21 +2572,25 @@ fits:
   CK(keys.alloc(sizeof(unsigned long long) * (r_base + r_cap), s));
   CK(vals.alloc(sizeof(double) * (r_base + r_cap), s));
   const long long nkk = 3LL * NC * (3 * NC + 1) / 2, kls = NC == 1 ? 12 : 36;  // Blk<NC>::NKK, KLS
-  CK(kkv.alloc(sizeof(double) * 2 * nkk * std::max(nvis, 1LL), s));
-  CK(klv.alloc(sizeof(double) * 2 * kls * std::max(nvis, 1LL), s));
+  CK(kkv.alloc(sizeof(double) * 2 * nkk * std::max(nst, 1LL), s));
+  CK(klv.alloc(sizeof(double) * 2 * kls * std::max(nst, 1LL), s));
+  // block slots: [full A | full B | clipped A | clipped B], the full ones
+  // only when they are stored
+  const long long aF = 0, bF = nF, aP = P.analytic ? 0 : 2 * nF, bP = aP + nPt;
   VisitOut O;
   O.kkv = kkv.as<double>();
   O.klv = klv.as<double>();
-  O.nvis = nvis;
-  O.revpos = revpos.as<int>();
   O.counters = d_counters;
   O.errpair = d_err;
+  VisitOut OF = O, OP = O;
+  OF.a_base = aF; OF.b_base = bF; OF.revpos = revposF.as<int>(); OF.nlist = P.analytic ? 0 : nF;
+  OP.a_base = aP; OP.b_base = bP; OP.revpos = revposP.as<int>(); OP.nlist = nPt;
   nlg_status rc = NLG_OK;
   switch (P.kid) {
-    case 0: rc = run_visits<0>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
-    case 1: rc = run_visits<1>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
-    case 2: rc = run_visits<2>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
-    default: rc = run_visits<3>(pl, P, lf, nF, lp, nPt, O, ev[2]); break;
+    case 0: rc = run_visits<0>(pl, P, lf, lp, OF, OP, ev[2]); break;
+    case 1: rc = run_visits<1>(pl, P, lf, lp, OF, OP, ev[2]); break;
+    case 2: rc = run_visits<2>(pl, P, lf, lp, OF, OP, ev[2]); break;
+    default: rc = run_visits<3>(pl, P, lf, lp, OF, OP, ev[2]); break;
   }
   if (rc) return rc;
   CK(cudaEventRecord(ev[3], s));
@@ -2451,9 +2615,12 @@ fits:
     RI.off = off.as<long long>();
     RI.nF = nF;
     RI.rec = lf;
-    RI.partB = partB.as<int>();
-    RI.nvis = nvis;
-    RI.rev_start = rstart.as<int>();
+    RI.rstartF = rstartF.as<int>();
+    RI.rstartP = rstartP.as<int>();
+    RI.partBF = partBF.as<int>();
+    RI.partBP = partBP.as<int>();
+    RI.aF = aF; RI.bF = bF; RI.aP = aP; RI.bP = bP;
+    RI.analytic = P.analytic;
     RI.kkv = O.kkv;
     RI.klv = O.klv;
     DevBuf nch, cfirst, rstate;
@@ -2491,17 +2658,19 @@ fits:
     RO.kk_base = 0;
     RO.r_base = r_base;
     RO.r_cap = r_cap;
+    RO.errpair = d_err;
     int key_bits = 1;
     while ((1LL << key_bits) - 1 < (long long)P.J / NC) ++key_bits;
     if (key_bits > 31) { set_err("dof count too large for the run sort"); return NLG_ERR_CONFIG; }
     if (NC == 1) {
       const int smem = (int)sizeof(RootSmem<1>);
-      CK(cudaFuncSetAttribute(k_root_reduce<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_root_reduce<1><<<(unsigned)max_chunks, kRootThreads, smem, s>>>(P, RI, RO, key_bits);
+      auto kern = P.analytic ? k_root_reduce<1, true> : k_root_reduce<1, false>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<(unsigned)max_chunks, kRootThreads, smem, s>>>(P, RI, RO, key_bits);
     } else {
       const int smem = (int)sizeof(RootSmem<2>);
-      CK(cudaFuncSetAttribute(k_root_reduce<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_root_reduce<2><<<(unsigned)max_chunks, kRootThreads, smem, s>>>(P, RI, RO, key_bits);
+      CK(cudaFuncSetAttribute(k_root_reduce<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_root_reduce<2, false><<<(unsigned)max_chunks, kRootThreads, smem, s>>>(P, RI, RO, key_bits);
     }
     LAUNCHED();
     unsigned long long hst[3];
@@ -2515,6 +2684,7 @@ fits:
     }
     r_total = (long long)hst[2];
   }
+  CK(cudaEventRecord(ev[6], s));
   const long long coo_red = r_base + r_total;
   // ---- sort (row, col) keys (stable: equal keys keep COO position order), sum runs
   const long long nrows = row_hi - row_lo;
@@ -2536,6 +2706,7 @@ fits:
   CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); tm.part += ms;
   CK(cudaEventElapsedTime(&ms, ev[3], ev[4])); tm.sing += ms;
   CK(cudaEventElapsedTime(&ms, ev[4], ev[5])); tm.merge += ms;
+  CK(cudaEventElapsedTime(&ms, ev[4], ev[6])); tm.stage_r += ms;
   st->n_full += nF;
   st->n_partial += nPt;
   st->n_singular += nS[0] + nS[1] + nS[2];
@@ -2699,6 +2870,8 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   P.kp1 = pb->kp1;
   P.J = pb->n_dofs;
   P.dbg = getenv("NLG_DEBUG") ? atoi(getenv("NLG_DEBUG")) : 0;
+  // NLG_NO_ANALYTIC: integrate the full pairs of kid 2 / 3 per record (A/B and tests)
+  P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC");
   Rule7 hr;
   for (int p = 0; p < 7; ++p) {
     hr.op[p][0] = pb->op[2 * p]; hr.op[p][1] = pb->op[2 * p + 1];
@@ -2740,7 +2913,8 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
       cudaMallocAsync(&pl->elem, sizeof(int4) * std::max(K, 1LL), s) ||
       cudaMallocAsync(&pl->dofs, sizeof(int4) * std::max(K, 1LL), s) ||
       cudaMallocAsync(&pl->ctr, sizeof(double2) * std::max(K, 1LL), s) ||
-      cudaMallocAsync(&pl->rad, sizeof(double) * std::max(K, 1LL), s)) {
+      cudaMallocAsync(&pl->rad, sizeof(double) * std::max(K, 1LL), s) ||
+      (P.analytic && cudaMallocAsync(&pl->ftab, sizeof(double4) * std::max(K, 1LL), s))) {
     set_err("device allocation failed");
     return fail(NLG_ERR_CUDA);
   }
@@ -2798,6 +2972,7 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   P.dofs = pl->dofs;
   P.ctr = pl->ctr;
   P.rad = pl->rad;
+  P.ftab = pl->ftab;
   *out = pl;
   return NLG_OK;
 }
@@ -2806,7 +2981,7 @@ void nlg_plan_destroy(nlg_plan* pl) {
   if (!pl) return;
   cudaSetDevice(pl->device);
   cudaStream_t s = pl->stream;
-  void* ptrs[] = {pl->vtx, pl->elem, pl->dofs, pl->ctr, pl->rad, pl->grid_start, pl->grid_items, pl->act};
+  void* ptrs[] = {pl->vtx, pl->elem, pl->dofs, pl->ctr, pl->rad, pl->ftab, pl->grid_start, pl->grid_items, pl->act};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   for (auto& f : pl->sing_tab)
@@ -2923,6 +3098,7 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   st.ms_partial = tm.part;
   st.ms_singular = tm.sing;
   st.ms_merge = tm.merge;
+  st.ms_merge_stage_r = tm.stage_r;
   st.ms_integrate_kernels = tm.full + tm.part + tm.sing;
   st.nnz = nnz;
   st.inner_evals = (long long)(hc[K_EVAL_M0] + hc[K_EVAL_M1] + hc[K_EVAL_M2]);

@@ -43,6 +43,11 @@ struct Params {
   double s, kexp, cst, delta, prer, rskip2, drop2, kp0, kp1;
   long long J, row_lo, row_hi;
   int narrow;  // COO keys of this batch are written as 32-bit (rows x J < 2^32)
+  // full pairs of the constant / affine kernels (kid 2, 3 on the standard
+  // path) factor into per-element terms (ftab): merge stage R forms their
+  // blocks, no per-record storage
+  int analytic;
+  const double4* __restrict__ ftab;  // [K] (A2 psi_0, A2 psi_1, A2 psi_2, A2)
   int dbg;  // NLG_DEBUG bit mask (experiments only; 0 in production)
 };
 
