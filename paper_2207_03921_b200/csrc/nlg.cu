@@ -186,6 +186,16 @@ __global__ void k_cell_ranges(const unsigned* __restrict__ skey, int K, int ncel
   start[c] = lo;
 }
 
+// (dof base, element * 4 + local vertex) of every element corner
+__global__ void k_dof_keys(Params P, unsigned* key, int* val) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= 3LL * P.K) return;
+  const int e = (int)(i / 3), a = (int)(i % 3);
+  const int4 d = P.dofs[e];
+  key[i] = (unsigned)(a == 0 ? d.x : (a == 1 ? d.y : d.z));
+  val[i] = e * 4 + a;
+}
+
 // ---------------------------------------------------------------- batch marking
 __device__ __forceinline__ bool row_in(const Params& P, long long base) {
   // any component row nc*base + c in [row_lo, row_hi)
@@ -499,6 +509,8 @@ __global__ void k_rev_pos(const int* __restrict__ rev_item, long long n, const i
   partB[i] = rec[r].x & kIdMask;
 }
 
+template <typename KT> __host__ __device__ constexpr KT key_sentinel() { return (KT)~(KT)0; }
+
 // ---------------------------------------------------------------- visits
 __device__ __forceinline__ unsigned long long coo_key(const Params& P, long long row, long long col) {
   if (row < P.row_lo || row >= P.row_hi) return kSentinel;
@@ -532,30 +544,38 @@ __device__ __forceinline__ void warp_add_ll(T v, unsigned long long* dst) {
 
 struct VisitOut {
   double* kkv;              // [record][side][NKK] own blocks of visit A (k, l) / B (l, k), symmetric: I <= J
-  double* klv;              // [record][side][b][NVP] neighbour blocks, column-major and padded:
-                            // the 3NC row values of one neighbour dof are contiguous
+  double* klv;              // [record][side][I][NVP] neighbour blocks, row-major and padded
   long long a_base;         // side A of list record v -> block a_base + v
   long long b_base;         // side B -> block b_base + revpos[v] (reverse-index order)
   const int* revpos;
   long long nlist;
   unsigned long long* counters;
   unsigned long long* errpair;
+  unsigned long long* vmax;  // max |value| written (bits of a nonnegative double), for the merge's fixed point
 };
 
+// max of nonnegative doubles (as bit patterns) over the warp, one atomic
+__device__ __forceinline__ void warp_max_abs(double m, unsigned long long* dst) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(m == m ? m : 0.0);
+  for (int o = 16; o; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+  if (lane_id() == 0 && b) atomicMax(dst, b);
+}
+
 // per-record-side block layouts: the own block is symmetric (I <= J, packed
-// in (I <= J) row-major order, presence = value != 0); the neighbour block is stored by
-// neighbour dof b as a 3nc x nc column (d * 3nc + I), padded to 32 B for nc = 1
+// in (I <= J) row-major order, presence = value != 0); the neighbour block is
+// row-major (row I on the root, J = b nc + d on the neighbour), rows padded to
+// 32 B for nc = 1, so one root row of the block is one sector (merge)
 template <int NC> struct Blk {
   static constexpr int N3 = 3 * NC, E = 9 * NC * NC, NKK = N3 * (N3 + 1) / 2;
-  static constexpr int NV = N3 * NC, NVP = NC == 1 ? 4 : NV, KLS = 3 * NVP;
+  static constexpr int NV = N3 * NC, NVP = NC == 1 ? 4 : N3, KLS = N3 * NVP;
   __host__ __device__ static constexpr int sym(int I, int J) { return I * N3 - I * (I - 1) / 2 + (J - I); }
-  __host__ __device__ static constexpr int kl(int I, int J) { return (J / NC) * NVP + (J % NC) * N3 + I; }
+  __host__ __device__ static constexpr int kl(int I, int J) { return I * NVP + J; }
 };
 
 // emit one side of a record: own block -> kkv, neighbour block -> klv
 template <int NC>
 __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, long long slot, bool on,
-                                          int root, int nb, const double* kk, const double* kl) {
+                                          int root, int nb, const double* kk, const double* kl, double& vm) {
   using B = Blk<NC>;
   bool bad = false;
 #pragma unroll
@@ -564,6 +584,7 @@ __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, lo
     if (I <= J) O.kkv[slot * B::NKK + B::sym(I, J)] = on ? kk[e] : 0.0;
     bad |= nonfinite(kk[e]) | nonfinite(kl[e]);
     O.klv[slot * B::KLS + B::kl(I, J)] = on ? emit_val(kl[e]) : 0.0;
+    if (on) vm = fmax(vm, fmax(fabs(kk[e]), fabs(kl[e])));
   }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
 }
@@ -581,22 +602,37 @@ __device__ __forceinline__ double4 ld_f4(const double4* p) {
 //   kl[a,b] = -2 A2_r whs_a (A2_n psi_n[b]), psi_n[b] = sum_q w_q H_qb f(y_q on n)
 // (sw = sum w, whs_a = sum_p w_p H_pa): the partner enters only through
 // A2_n and A2_n psi_n, so stage R sums those per root / neighbour dof.
+// fmax: max |A2|, max |A2 psi_b|, max |Phi_ab| over the elements (bounds of
+// the analytic terms for the merge's fixed-point scale)
 template <int KID>
-__global__ void k_elem_factors(Params P, double4* ft) {
+__global__ void k_elem_factors(Params P, double4* ft, unsigned long long* fbound) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= P.K) return;
-  double tx[3], ty[3], px[7], py[7];
-  load_tri(P, e, tx, ty);
-  rule_points(P, tx, ty, px, py);
-  double ps[3] = {0.0, 0.0, 0.0};
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  if (e < P.K) {
+    double tx[3], ty[3], px[7], py[7];
+    load_tri(P, e, tx, ty);
+    rule_points(P, tx, ty, px, py);
+    double ps[3] = {0.0, 0.0, 0.0}, phi[9];
 #pragma unroll
-  for (int p = 0; p < 7; ++p) {
-    const double f = KID == 2 ? P.cst : (1.0 + P.kp0 * px[p]) * P.kp1;
+    for (int i = 0; i < 9; ++i) phi[i] = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) ps[a] = fma(c_rule.wh[p][a], f, ps[a]);
+    for (int p = 0; p < 7; ++p) {
+      const double f = KID == 2 ? P.cst : (1.0 + P.kp0 * px[p]) * P.kp1;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) ps[a] = fma(c_rule.wh[p][a], f, ps[a]);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) phi[i] = fma(c_rule.whh[p][i], f, phi[i]);
+    }
+    const double a2 = twice_area(tx, ty);
+    ft[e] = make_double4(a2 * ps[0], a2 * ps[1], a2 * ps[2], a2);
+    m0 = fabs(a2);
+    m1 = fmax(fabs(a2 * ps[0]), fmax(fabs(a2 * ps[1]), fabs(a2 * ps[2])));
+#pragma unroll
+    for (int i = 0; i < 9; ++i) m2 = fmax(m2, fabs(phi[i]));
   }
-  const double a2 = twice_area(tx, ty);
-  ft[e] = make_double4(a2 * ps[0], a2 * ps[1], a2 * ps[2], a2);
+  warp_max_abs(m0, &fbound[0]);
+  warp_max_abs(m1, &fbound[1]);
+  warp_max_abs(m2, &fbound[2]);
 }
 
 // Phi_r[a][b] of the root (see k_elem_factors)
@@ -626,6 +662,7 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     __syncthreads();
   }
   long long ev0 = 0, ev2 = 0, out0 = 0, out2 = 0;
+  double vm = 0.0;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < O.nlist;
        v += (long long)gridDim.x * blockDim.x) {
     const int2 pr = list[v];
@@ -655,9 +692,10 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
       ev0 += ne * mult;
       out0 += 14 * mult;
     }
-    emit_side<NC>(P, O, O.a_base + v, emitA, k, l, kkA, klA);
-    emit_side<NC>(P, O, O.b_base + __ldg(&O.revpos[v]), emitB && k != l, l, k, kkB, klB);
+    emit_side<NC>(P, O, O.a_base + v, emitA, k, l, kkA, klA, vm);
+    emit_side<NC>(P, O, O.b_base + __ldg(&O.revpos[v]), emitB && k != l, l, k, kkB, klB, vm);
   }
+  warp_max_abs(vm, O.vmax);
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
   warp_add_ll(ev2, &O.counters[K_EVAL_FULL2]);
   warp_add_ll(out0, &O.counters[K_OUT_FULL0]);
@@ -806,6 +844,7 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   unsigned n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;  // per thread: < 2^32
+  double vmx = 0.0;  // max |value| written
   const int vs = lane >> 4, r = lane & 15;
   if (threadIdx.x == 0) CQ.n[0] = 0;
   if (KID == 0)
@@ -1153,7 +1192,10 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
         const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
         const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
         const long long slot = side ? O.b_base + __ldg(&O.revpos[v]) : O.a_base + v;
-        if (on) report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
+        if (on) {
+          report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
+          vmx = fmax(vmx, fabs(val));
+        }
         if (w < C::NKK) {
           O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;  // unique (I <= J) order
         } else {
@@ -1164,6 +1206,7 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
     }
     __syncwarp();
   }
+  warp_max_abs(vmx, O.vmax);
   warp_add_ll((unsigned long long)n_eval0, &O.counters[K_EVAL_M0]);
   warp_add_ll((unsigned long long)n_out0, &O.counters[K_OUT_M0]);
   warp_add_ll((unsigned long long)n_eval1, &O.counters[K_EVAL_M1]);
@@ -1191,6 +1234,9 @@ constexpr int kRootThreads = 256, kRootItems = 12, kRootCap = kRootThreads * kRo
 // stage-R run entries per record value, for the buffer estimate (cfg2: 0.2);
 // a batch that needs more is split
 constexpr double kRunFrac = 0.35;
+// stage-W CSR entries per record value, for the entry buffer (cfg4 0.012,
+// cfg1-3 0.03); a batch that needs more is split
+constexpr double kEntFrac = 0.08;
 
 struct RootIn {
   const int* roots;
@@ -1208,6 +1254,7 @@ struct RootIn {
   // block slots: side A of list record v -> a + v, side B -> b + reverse position
   long long aF, bF, aP, bP;
   int analytic;             // full sides carry no blocks: their terms come from ftab
+  const int* inR;           // element -> root rank (-1: not a root of the batch)
   const double* kkv;  // [side][NKK]
   const double* klv;  // [side][3][NVP]
   const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
@@ -1505,7 +1552,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     if (q < npos) {
       const long long g = c0 + col[q], rs = g / 3;
       if (rs >= nan_rs)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + (R.slot(I, rs) * 3 + (g - 3 * rs)) * Blk<NC>::NVP));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(I.klv + R.slot(I, rs) * Blk<NC>::KLS + (g - 3 * rs) * NC));
     }
   __syncthreads();  // s_base, has_head
   const long long base = s_base;
@@ -1539,10 +1586,10 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
         acc_t += v;
         pres |= v != 0.0 ? PT : 0u;
       } else {
-        const double* src = I.klv + (R.slot(I, rs) * 3 + b) * Blk<NC>::NVP;
+        const double* src = I.klv + R.slot(I, rs) * Blk<NC>::KLS + b * NC;
 #pragma unroll
-        for (int e = 0; e < NV; ++e) {  // e = d * N3 + I
-          const double v = __ldg(&src[e]);
+        for (int e = 0; e < NV; ++e) {  // e = d * N3 + I: row I, column b nc + d
+          const double v = __ldg(&src[(e % N3) * Blk<NC>::NVP + e / N3]);
           acc[e] += v;
           pres |= (__double_as_longlong(v) != 0 ? 1u : 0u) << e;
         }
@@ -1569,6 +1616,400 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
     }
     if (fits) flush(seg, wseg);
   }
+}
+
+// ---------------------------------------------------------------- row merge
+// Merge stage W (replaces stage R + the global sort when every row fits a
+// shared-memory table): one CTA per dof base d gathers, for its in-range rows
+// NC d + c, every contribution the reference's _merge_triplets
+// (assembly.py:137-173) would sum into them -- the own blocks and neighbour
+// blocks of the record sides of the batch roots incident to d, the analytic
+// full-pair terms and the touching-pair (singular) entries -- into a hash
+// table keyed by the column dof base.  Sums are exact 128-bit fixed point
+// (value x 2^S, S from a bound of every contribution's magnitude), so their
+// result does not depend on the order the threads add them: run-to-run
+// deterministic without a sort.  The table is then radix-sorted by column
+// in shared memory and each row leaves as one sorted CSR row.  A row whose
+// distinct columns outgrow the table is retried with a larger one; beyond
+// the largest, the batch falls back to stage R + the global sort.
+constexpr unsigned kRowEmpty = 0x7fffffffu;
+constexpr int kFixBits = 96;  // bound x 2^S = 2^96: 2^31 contributions of headroom below 2^127
+
+struct RowIn {
+  const int* de_start;
+  const int* de_items;
+  const int* inR;
+  const int* dlist;  // dof bases to process, or nullptr: d_lo + blockIdx.x
+  long long d_lo;
+  int key_bits;      // bits of the largest dof base + 1 (the empty key sorts last)
+  // singular entries sorted by key, and each local row's first position
+  const unsigned long long* skey64;
+  const unsigned* skey32;
+  const double* sval;
+  const long long* sstart;
+  const unsigned long long* vmax;  // max |stored / singular value| of the batch
+  const unsigned long long* fmax;  // plan bounds of the analytic terms (k_elem_factors)
+};
+struct RowOut {
+  int* col;
+  double* val;
+  long long cap;
+  unsigned long long* used;
+  long long* roff;  // per local row: first entry in col / val
+  int* rcnt;        // per local row: entries
+  int* ovf;         // dof bases whose table overflowed
+  unsigned* novf;
+};
+
+struct Fix {  // 128-bit two's complement fixed point
+  unsigned long long lo;
+  long long hi;
+};
+__device__ __forceinline__ Fix fix_of(double v, double scale) {
+  const double t = rint(v * scale);
+  Fix f;
+  if (fabs(t) < 0x1p63) {
+    const long long q = (long long)t;
+    f.lo = (unsigned long long)q;
+    f.hi = q < 0 ? -1 : 0;
+  } else {  // t is a multiple of 2^11 here: the remainder is exact
+    const double hd = floor(t * 0x1p-64);
+    f.hi = (long long)hd;
+    f.lo = (unsigned long long)(t - hd * 0x1p64);
+  }
+  return f;
+}
+__device__ __forceinline__ void fix_add(Fix& a, const Fix& b) {
+  const unsigned long long s = a.lo + b.lo;
+  a.hi += b.hi + (s < a.lo ? 1 : 0);
+  a.lo = s;
+}
+__device__ __forceinline__ double fix_val(const Fix& f, double inv) {
+  return fma((double)f.hi, 0x1p64, (double)f.lo) * inv;
+}
+__device__ __forceinline__ void fix_atomic(unsigned long long* cell, const Fix& b) {
+  if (!b.lo && !b.hi) return;
+  const unsigned long long old = atomicAdd(&cell[0], b.lo);
+  const long long h = b.hi + ((old + b.lo < old) ? 1 : 0);
+  if (h) atomicAdd(&cell[1], (unsigned long long)h);
+}
+__device__ __forceinline__ Fix fix_warp_sum(Fix a) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Fix b;
+    b.lo = __shfl_xor_sync(0xffffffffu, a.lo, o);
+    b.hi = __shfl_xor_sync(0xffffffffu, a.hi, o);
+    fix_add(a, b);
+  }
+  return a;
+}
+
+template <int NC, int CAP, int TH>
+struct RowSmem {
+  using Sort = cub::BlockRadixSort<unsigned, TH, CAP / TH, unsigned>;
+  using Scan = cub::BlockScan<int, TH>;
+  unsigned key[CAP];                      // column dof base (bit 31: present, nc = 1)
+  unsigned pres[NC == 1 ? 1 : CAP];       // nc = 2: presence bit per (c, d) component
+  unsigned long long acc[CAP][NC * NC][2];
+  union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } u;
+  unsigned long long sa[2];  // analytic: sum of the partners' A2 (fixed point)
+  unsigned sa_pres;
+  int used, ovf;
+  long long base[NC];
+};
+
+template <int NC, int CAP, int TH, bool AN>
+__global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, RowOut O) {
+  constexpr int NC2 = NC * NC, N3 = 3 * NC, IT = CAP / TH, NWARP = TH / 32;
+  constexpr int LOG2CAP = CAP == 512 ? 9 : CAP == 1024 ? 10 : CAP == 2048 ? 11 : CAP == 4096 ? 12 : 13;
+  static_assert((1 << LOG2CAP) == CAP, "CAP must be a power of two in [512, 8192]");
+  using SM = RowSmem<NC, CAP, TH>;
+  extern __shared__ __align__(16) unsigned char row_smem[];
+  SM& S = *reinterpret_cast<SM*>(row_smem);
+  const int t = threadIdx.x, lane = lane_id(), warp = t >> 5;
+  const long long d = W.dlist ? (long long)W.dlist[blockIdx.x] : W.d_lo + blockIdx.x;
+  for (int i = t; i < CAP; i += TH) {
+    S.key[i] = kRowEmpty;
+    if (NC > 1) S.pres[i] = 0;
+#pragma unroll
+    for (int e = 0; e < NC2; ++e) S.acc[i][e][0] = S.acc[i][e][1] = 0;
+  }
+  if (t == 0) {
+    S.used = 0;
+    S.ovf = 0;
+    S.sa[0] = S.sa[1] = 0;
+    S.sa_pres = 0;
+  }
+  // fixed-point scale from a bound of every contribution's magnitude
+  double whsmax = 0.0, sw = 0.0;
+#pragma unroll
+  for (int p = 0; p < 7; ++p) sw += c_rule.ow[p];
+  double bound = __longlong_as_double((long long)*W.vmax);
+  double fa2 = 0.0;
+  if (AN) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double wsum = 0.0;
+#pragma unroll
+      for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
+      whsmax = fmax(whsmax, wsum);
+    }
+    fa2 = __longlong_as_double((long long)W.fmax[0]);
+    const double fg = __longlong_as_double((long long)W.fmax[1]);
+    const double fphi = __longlong_as_double((long long)W.fmax[2]);
+    bound = fmax(bound, 2.0 * fa2 * whsmax * fg);
+    bound = fmax(bound, 2.0 * fa2 * sw * fphi * fa2 * 0x1p24);  // own term: A2_r Phi_r x (sum of up to 2^24 A2_n)
+  }
+  const bool bok = bound > 0.0 && bound <= 1e300;
+  const int be = bok ? ilogb(bound) + 1 : 0;
+  const double scale = bok ? ldexp(1.0, kFixBits - be) : 1.0, inv = bok ? ldexp(1.0, be - kFixBits) : 1.0;
+  const int ae = AN && fa2 > 0.0 && fa2 <= 1e300 ? ilogb(fa2) + 1 + 24 : 0;  // sum of A2: its own scale
+  const double ascale = ldexp(1.0, kFixBits - ae), ainv = ldexp(1.0, ae - kFixBits);
+  unsigned inr = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long row = NC * d + c;
+    if (row >= P.row_lo && row < P.row_hi) inr |= 1u << c;
+  }
+  __syncthreads();
+  // slot of column dof base w (inserted if new); -1 once the table overflowed
+  auto slot_of = [&](unsigned w) -> int {
+    unsigned h = (w * 2654435761u) >> (32 - LOG2CAP);
+    for (int probe = 0; probe < CAP; ++probe) {
+      const unsigned kk = *(volatile unsigned*)&S.key[h] & 0x7fffffffu;
+      if (kk == w) return (int)h;
+      if (kk == kRowEmpty) {
+        if (*(volatile int*)&S.ovf) return -1;
+        const unsigned old = atomicCAS(&S.key[h], kRowEmpty, w);
+        if (old == kRowEmpty) {
+          if (atomicAdd(&S.used, 1) >= CAP - CAP / 8) S.ovf = 1;
+          return (int)h;
+        }
+        if ((old & 0x7fffffffu) == w) return (int)h;
+      }
+      h = (h + 1) & (CAP - 1);
+    }
+    S.ovf = 1;
+    return -1;
+  };
+  auto add = [&](unsigned w, int comp, double v, bool pres) {
+    if (!pres || !(v == v) || fabs(v) > 1e300) return;  // absent; nonfinite values are reported elsewhere
+    const int h = slot_of(w);
+    if (h < 0) return;
+    fix_atomic(S.acc[h][comp], fix_of(v, scale));
+    if (NC == 1) atomicOr(&S.key[h], 0x80000000u);
+    else atomicOr(&S.pres[h], 1u << comp);
+  };
+  auto add_fix = [&](unsigned w, int comp, const Fix& f, bool pres) {
+    if (!pres) return;
+    const int h = slot_of(w);
+    if (h < 0) return;
+    fix_atomic(S.acc[h][comp], f);
+    if (NC == 1) atomicOr(&S.key[h], 0x80000000u);
+    else atomicOr(&S.pres[h], 1u << comp);
+  };
+  if (inr) {
+    // ---- the record sides of the batch roots incident to d
+    const int e0 = W.de_start[d], e1 = W.de_start[d + 1];
+    for (int ei = e0; ei < e1; ++ei) {
+      const int it = __ldg(&W.de_items[ei]);
+      const int k = it >> 2, a = it & 3;
+      const int rank = __ldg(&W.inR[k]);
+      if (rank < 0) continue;  // block-uniform
+      const RootSides R = root_sides(I, rank);
+      const long long n_rs = R.n(), nan_rs = AN ? R.nfull() : 0;
+      const int4 dk4 = __ldg(&P.dofs[k]);
+      const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
+      const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
+      double fkl = 0.0;
+      if (AN) {
+        double wsum = 0.0;
+#pragma unroll
+        for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
+        fkl = -2.0 * __ldg(&P.ftab[k].w) * wsum;
+      }
+      Fix own[3][NC2];
+      unsigned opres = 0;  // bit b * NC2 + comp
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int e = 0; e < NC2; ++e) own[b][e].lo = 0, own[b][e].hi = 0;
+      Fix sa{0, 0};
+      bool sapres = false;
+      for (long long rs = t; rs < n_rs; rs += TH) {
+        const int n = R.partner(I, rs);
+        const int4 dn4 = __ldg(&P.dofs[n]);
+        const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
+        if (AN && rs < nan_rs) {
+          const double4 g = ld_f4(P.ftab + n);
+          fix_add(sa, fix_of(g.w, ascale));
+          sapres |= g.w != 0.0;
+          if (inr & 1u) {
+            add(dn[0], 0, fkl * g.x, g.x != 0.0 && fkl != 0.0);
+            add(dn[1], 0, fkl * g.y, g.y != 0.0 && fkl != 0.0);
+            add(dn[2], 0, fkl * g.z, g.z != 0.0 && fkl != 0.0);
+          }
+        } else {
+          const long long slot = R.slot(I, rs);
+          const double* kk = I.kkv + slot * Blk<NC>::NKK;
+          const double* kl = I.klv + slot * Blk<NC>::KLS;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (!((inr >> c) & 1u)) continue;
+            const int Ir = a * NC + c;
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int dd = 0; dd < NC; ++dd) {
+                const int Jc = b * NC + dd;
+                const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
+                const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
+                if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
+                  fix_add(own[b][c * NC + dd], fix_of(vo, scale));
+                  opres |= 1u << (b * NC2 + c * NC + dd);
+                }
+                add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
+              }
+          }
+        }
+      }
+      // own block of (k, a): fixed-point partials -> warp sums -> table
+#pragma unroll
+      for (int o = 16; o; o >>= 1) opres |= __shfl_xor_sync(0xffffffffu, opres, o);
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int e = 0; e < NC2; ++e) {
+          const Fix f = fix_warp_sum(own[b][e]);
+          if (lane == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
+        }
+      if (AN) {
+        const Fix f = fix_warp_sum(sa);
+        const bool sp = __any_sync(0xffffffffu, sapres);
+        if (lane == 0) {
+          fix_atomic(S.sa, f);
+          if (sp) atomicOr(&S.sa_pres, 1u);
+        }
+        __syncthreads();
+        if (t < 3 && own_on && S.sa_pres && (inr & 1u)) {
+          Fix tot;
+          tot.lo = S.sa[0];
+          tot.hi = (long long)S.sa[1];
+          const double sa_d = fix_val(tot, ainv);
+          const double fown = (2.0 * __ldg(&P.ftab[k].w) * sw) *
+                              (P.kid == 2 ? root_phi<2>(P, k, a, t) : root_phi<3>(P, k, a, t));
+          add(dk[t], 0, fown * sa_d, fown != 0.0);
+        }
+        __syncthreads();
+        if (t == 0) S.sa[0] = S.sa[1] = 0, S.sa_pres = 0;
+      }
+    }
+    // ---- touching-pair (singular) entries of the rows
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (!((inr >> c) & 1u)) continue;
+      const long long lr = NC * d + c - P.row_lo;
+      const long long s0 = W.sstart[lr], s1 = W.sstart[lr + 1];
+      for (long long i = s0 + t; i < s1; i += TH) {
+        const unsigned long long key = W.skey64 ? W.skey64[i] : (unsigned long long)W.skey32[i];
+        const long long col = (long long)(key % (unsigned long long)P.J);
+        const double v = W.sval[i];
+        add((unsigned)(col / NC), c * NC + (int)(col % NC), v, __double_as_longlong(v) != 0);
+      }
+    }
+  }
+  __syncthreads();
+  if (S.ovf) {
+    if (t == 0) O.ovf[atomicAdd(O.novf, 1u)] = (int)d;
+    return;
+  }
+  // ---- sort the table by column and write each row
+  unsigned key[IT], sl[IT];
+  const unsigned PAD = (1u << W.key_bits) - 1u;
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    const int i = t * IT + q;
+    const unsigned kk = S.key[i] & 0x7fffffffu;
+    key[q] = kk == kRowEmpty ? PAD : kk;
+    sl[q] = (unsigned)i;
+  }
+  __syncthreads();
+  typename SM::Sort(S.u.sort).Sort(key, sl, 0, W.key_bits);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    if (!((inr >> c) & 1u)) continue;  // block-uniform
+    int cntq = 0;
+#pragma unroll
+    for (int q = 0; q < IT; ++q) {
+      if (key[q] == PAD) continue;
+      const unsigned pm = NC == 1 ? (S.key[sl[q]] >> 31) : (S.pres[sl[q]] >> (c * NC)) & ((1u << NC) - 1u);
+      cntq += __popc(pm);
+    }
+    int pre = 0, tot = 0;
+    typename SM::Scan(S.u.scan).ExclusiveSum(cntq, pre, tot);
+    if (t == 0) {
+      const long long b0 = (long long)atomicAdd(O.used, (unsigned long long)tot);
+      S.base[c] = b0;
+      const long long lr = NC * d + c - P.row_lo;
+      O.roff[lr] = b0;
+      O.rcnt[lr] = tot;
+    }
+    __syncthreads();
+    long long pos = S.base[c] + pre;
+    if (S.base[c] + tot <= O.cap) {
+#pragma unroll
+      for (int q = 0; q < IT; ++q) {
+        if (key[q] == PAD) continue;
+        const int h = (int)sl[q];
+        const unsigned pm = NC == 1 ? (S.key[h] >> 31) : (S.pres[h] >> (c * NC)) & ((1u << NC) - 1u);
+#pragma unroll
+        for (int dd = 0; dd < NC; ++dd) {
+          if (!((pm >> dd) & 1u)) continue;
+          Fix f;
+          f.lo = S.acc[h][c * NC + dd][0];
+          f.hi = (long long)S.acc[h][c * NC + dd][1];
+          O.col[pos] = (int)(NC * key[q] + dd);
+          O.val[pos] = fix_val(f, inv);
+          ++pos;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// CSR of the batch from the per-row entry runs: one warp per row
+__global__ void k_row_gather(const long long* __restrict__ roff, const int* __restrict__ rcnt,
+                             const long long* __restrict__ indptr, long long nrows, const int* __restrict__ col,
+                             const double* __restrict__ val, int* indices, double* data) {
+  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (r >= nrows) return;
+  const long long src = roff[r], dst = indptr[r];
+  const int n = rcnt[r];
+  for (int i = lane_id(); i < n; i += 32) {
+    indices[dst + i] = col[src + i];
+    data[dst + i] = val[src + i];
+  }
+}
+
+// first sorted singular entry of each local row (keys row_local * J + col)
+template <typename KT>
+__global__ void k_row_starts(const KT* __restrict__ key, long long n, long long nrows, long long J, long long* start) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r > nrows) return;
+  const unsigned long long want = (unsigned long long)r * (unsigned long long)J;
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    const KT k = key[mid];
+    const bool less = k != key_sentinel<KT>() && (unsigned long long)k < want;
+    if (less) lo = mid + 1; else hi = mid;
+  }
+  start[r] = lo;
 }
 
 // ---------------------------------------------------------------- singular pairs
@@ -1600,7 +2041,7 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
                                                   long long n, SingRule R,
                                                   unsigned long long* keys, double* vals,
                                                   long long cbase, unsigned long long* counters,
-                                                  unsigned long long* errpair) {
+                                                  unsigned long long* errpair, unsigned long long* vmax) {
   using T = KTraits<KID>;
   constexpr int NC = T::NC, UN = U * NC;
   using A = SingAcc<U, NC, T::SYM>;
@@ -1609,6 +2050,7 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
   __shared__ int sMk[6], sMl[6], sUb[6];
   __shared__ double red[kSingThreads / 32][A::N];
   long long npts = 0;
+  double vm = 0.0;
   for (long long pi = blockIdx.x; pi < n; pi += gridDim.x) {
     const int k = list[pi].x, l = list[pi].y;
     if (threadIdx.x == 0) {
@@ -1755,6 +2197,7 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
       for (int w = 1; w < kSingThreads / 32; ++w) v += red[w][ai];
       v *= sScale;
       report_nonfinite(nonfinite(v), k, l, P.K, errpair);
+      vm = fmax(vm, fabs(v));
       const int m = ii / NC, c = ii % NC, mp = jj / NC, d = jj % NC;
       put_key(P, keys, slot, coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d));
       vals[slot] = emit_val(v);
@@ -1762,10 +2205,10 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
     __syncthreads();
   }
   warp_add_ll(npts, &counters[K_SPTS3 + (U - 3)]);
+  warp_max_abs(vm, vmax);
 }
 
 // ---------------------------------------------------------------- merge
-template <typename KT> __host__ __device__ constexpr KT key_sentinel() { return (KT)~(KT)0; }
 
 // 64-bit COO keys -> 32-bit when (rows x J) fits (fewer bytes per radix pass)
 __global__ void k_narrow_keys(const unsigned long long* __restrict__ in, long long n, unsigned* out) {
@@ -1966,6 +2409,9 @@ struct nlg_plan {
   double2* ctr = nullptr;
   double* rad = nullptr;
   double4* ftab = nullptr;  // analytic full-pair factors (k_elem_factors)
+  unsigned long long* fmax = nullptr;  // [3] bounds of the analytic terms
+  int* de_start = nullptr;  // dof base -> its (element, local vertex) pairs: [J / nc + 1]
+  int* de_items = nullptr;  // element * 4 + local vertex, by dof base
   double* sing_tab[3][5] = {};
   int sing_n[3] = {0, 0, 0};
   bool prepped = false;
@@ -1976,6 +2422,8 @@ struct nlg_plan {
   int* act = nullptr;
   int nact = -1;
   int nbase = 0;
+  int row_cap = 0;  // stage-W table size the last batches needed (start there)
+  bool use_rows = true;  // merge stage W (NLG_MERGE=sort: stage R + global sort)
   size_t arena_used = 0;  // virtual bump offset into the device arena during a call
 };
 
@@ -2047,9 +2495,38 @@ nlg_status prep(nlg_plan* pl) {
   CK(cudaMemcpyAsync(ext.p, init, sizeof init, cudaMemcpyHostToDevice, st));
   k_bounds<<<grid_for(K, 256), 256, 0, st>>>(P, pl->ctr, pl->rad, ext.as<unsigned long long>());
   LAUNCHED();
+  CK(cudaMemsetAsync(pl->fmax, 0, 3 * sizeof(unsigned long long), st));
   if (P.analytic && K) {
-    if (P.kid == 2) k_elem_factors<2><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab);
-    else k_elem_factors<3><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab);
+    if (P.kid == 2) k_elem_factors<2><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab, pl->fmax);
+    else k_elem_factors<3><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab, pl->fmax);
+    LAUNCHED();
+  }
+  {
+    // dof base -> (element, local vertex) incidence, for the row merge
+    const long long nb = P.J / P.nc, n3 = 3LL * K;
+    DevBuf dk, dk2, dv;
+    CK(dk.alloc(sizeof(unsigned) * std::max(n3, 1LL), st));
+    CK(dk2.alloc(sizeof(unsigned) * std::max(n3, 1LL), st));
+    CK(dv.alloc(sizeof(int) * std::max(n3, 1LL), st));
+    if (pl->de_items) cudaFreeAsync(pl->de_items, st);
+    if (pl->de_start) cudaFreeAsync(pl->de_start, st);
+    CK(cudaMallocAsync(&pl->de_items, sizeof(int) * std::max(n3, 1LL), st));
+    CK(cudaMallocAsync(&pl->de_start, sizeof(int) * (nb + 1), st));
+    if (n3) {
+      k_dof_keys<<<grid_for(n3, 256), 256, 0, st>>>(P, dk.as<unsigned>(), dv.as<int>());
+      LAUNCHED();
+      int bits = 1;
+      while ((1ll << bits) <= nb) ++bits;
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk.as<unsigned>(), dk2.as<unsigned>(), dv.as<int>(),
+                                         pl->de_items, (int)n3, 0, bits, st));
+      DevBuf tmp;
+      CK(tmp.alloc(tb, st));
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk.as<unsigned>(), dk2.as<unsigned>(), dv.as<int>(),
+                                         pl->de_items, (int)n3, 0, bits, st));
+      g_launches += 1 + (bits + 7) / 8;
+    }
+    k_cell_ranges<<<grid_for(nb + 1, 256), 256, 0, st>>>(dk2.as<unsigned>(), (int)n3, (int)nb, pl->de_start);
     LAUNCHED();
   }
   unsigned long long h[5];
@@ -2164,7 +2641,7 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
 template <int KID>
 nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const long long* nS,
                         unsigned long long* keys, double* vals, long long cbase,
-                        unsigned long long* counters, unsigned long long* errpair) {
+                        unsigned long long* counters, unsigned long long* errpair, unsigned long long* vmax) {
   constexpr int NC = KTraits<KID>::NC;
   const long long slots = 36LL * NC * NC;
   for (int f = 0; f < 3; ++f) {
@@ -2173,14 +2650,14 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
                pl->sing_tab[f][4], pl->sing_n[f]};
     const unsigned g = (unsigned)std::min<long long>(nS[f], 1 << 20);
     if (f == 0)
-      k_singular<KID, 0, 3><<<g, kSingThreads, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair);
+      k_singular<KID, 0, 3><<<g, kSingThreads, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair, vmax);
     else if (P.is_dg)
       (f == 1 ? k_singular<KID, 1, 6> : k_singular<KID, 2, 6>)<<<g, kSingThreads, 0, pl->stream>>>(
-          P, ls[f], nS[f], R, keys, vals, cbase, counters, errpair);
+          P, ls[f], nS[f], R, keys, vals, cbase, counters, errpair, vmax);
     else if (f == 1)
-      k_singular<KID, 1, 4><<<g, kSingThreads, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair);
+      k_singular<KID, 1, 4><<<g, kSingThreads, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair, vmax);
     else
-      k_singular<KID, 2, 5><<<g, kSingThreads, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair);
+      k_singular<KID, 2, 5><<<g, kSingThreads, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair, vmax);
     LAUNCHED();
     cbase += nS[f] * slots;
   }
@@ -2290,6 +2767,173 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(cudaMallocAsync(&piece.indices, sizeof(int), s));
     CK(cudaMallocAsync(&piece.data, sizeof(double), s));
     CK(cudaMemsetAsync(piece.indptr, 0, sizeof(long long) * (nrows + 1), s));
+  }
+  piece.nnz = nnz;
+  return NLG_OK;
+}
+
+// ---- merge stage W (k_row_asm) for one batch
+template <int NC, int CAP, bool AN>
+cudaError_t launch_rows(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
+                        cudaStream_t s) {
+  constexpr int TH = CAP >= 4096 ? 512 : 256;
+  const int smem = (int)sizeof(RowSmem<NC, CAP, TH>);
+  cudaError_t e = cudaFuncSetAttribute(k_row_asm<NC, CAP, TH, AN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  if (nblk) k_row_asm<NC, CAP, TH, AN><<<(unsigned)nblk, TH, smem, s>>>(P, I, W, O);
+  g_launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rows_cap(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
+                            int cap, cudaStream_t s) {
+  if (P.nc == 2) {
+    switch (cap) {
+      case 512: return launch_rows<2, 512, false>(P, I, W, O, nblk, s);
+      case 1024: return launch_rows<2, 1024, false>(P, I, W, O, nblk, s);
+      default: return launch_rows<2, 2048, false>(P, I, W, O, nblk, s);
+    }
+  }
+  if (P.analytic) {
+    switch (cap) {
+      case 1024: return launch_rows<1, 1024, true>(P, I, W, O, nblk, s);
+      case 2048: return launch_rows<1, 2048, true>(P, I, W, O, nblk, s);
+      case 4096: return launch_rows<1, 4096, true>(P, I, W, O, nblk, s);
+      default: return launch_rows<1, 8192, true>(P, I, W, O, nblk, s);
+    }
+  }
+  switch (cap) {
+    case 1024: return launch_rows<1, 1024, false>(P, I, W, O, nblk, s);
+    case 2048: return launch_rows<1, 2048, false>(P, I, W, O, nblk, s);
+    case 4096: return launch_rows<1, 4096, false>(P, I, W, O, nblk, s);
+    default: return launch_rows<1, 8192, false>(P, I, W, O, nblk, s);
+  }
+}
+
+// Rows [row_lo, row_hi) of the batch through stage W into `piece`.  *fallback:
+// some row outgrew the largest table (use stage R + sort); *need_split: the
+// entry estimate was too small.
+nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* skeys, double* svals, long long nsing,
+                      const unsigned long long* d_vmax, long long ent_cap, Csr& piece, long long& nnz, bool* fallback,
+                      bool* need_split) {
+  cudaStream_t s = pl->stream;
+  const int NC = P.nc;
+  const long long nrows = P.row_hi - P.row_lo;
+  *fallback = *need_split = false;
+  // singular entries sorted by (row, col); each row's first position
+  DevBuf k2, v2, sstart;
+  CK(sstart.alloc(sizeof(long long) * (nrows + 1), s));
+  const void* sk = skeys;
+  const double* sv = svals;
+  int bits = 1;
+  {
+    const unsigned long long maxkey = (unsigned long long)nrows * (unsigned long long)P.J;
+    while (bits < 64 && (1ull << bits) <= maxkey) ++bits;
+  }
+  if (nsing) {
+    CK(k2.alloc((P.narrow ? 4 : 8) * nsing, s));
+    CK(v2.alloc(sizeof(double) * nsing, s));
+    size_t tb = 0;
+    if (P.narrow) {
+      cub::DoubleBuffer<unsigned> dk((unsigned*)skeys, k2.as<unsigned>());
+      cub::DoubleBuffer<double> dv(svals, v2.as<double>());
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nsing, 0, bits, s));
+      DevBuf tmp;
+      CK(tmp.alloc(tb, s));
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, (int)nsing, 0, bits, s));
+      sk = dk.Current();
+      sv = dv.Current();
+    } else {
+      cub::DoubleBuffer<unsigned long long> dk((unsigned long long*)skeys, k2.as<unsigned long long>());
+      cub::DoubleBuffer<double> dv(svals, v2.as<double>());
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nsing, 0, bits, s));
+      DevBuf tmp;
+      CK(tmp.alloc(tb, s));
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, (int)nsing, 0, bits, s));
+      sk = dk.Current();
+      sv = dv.Current();
+    }
+    g_launches += (bits + 7) / 8 + 1;
+  }
+  if (P.narrow)
+    k_row_starts<unsigned><<<grid_for(nrows + 1, 256), 256, 0, s>>>((const unsigned*)sk, nsing, nrows, P.J,
+                                                                    sstart.as<long long>());
+  else
+    k_row_starts<unsigned long long><<<grid_for(nrows + 1, 256), 256, 0, s>>>((const unsigned long long*)sk, nsing,
+                                                                              nrows, P.J, sstart.as<long long>());
+  LAUNCHED();
+  const long long d_lo = P.row_lo / NC, d_hi = (P.row_hi - 1) / NC + 1, nd = std::max(0LL, d_hi - d_lo);
+  DevBuf col, val, roff, rcnt, ovf0, ovf1, st;
+  CK(col.alloc(sizeof(int) * std::max(ent_cap, 1LL), s));
+  CK(val.alloc(sizeof(double) * std::max(ent_cap, 1LL), s));
+  CK(roff.alloc(sizeof(long long) * std::max(nrows, 1LL), s));
+  CK(rcnt.alloc(sizeof(int) * (nrows + 1), s));
+  CK(ovf0.alloc(sizeof(int) * std::max(nd, 1LL), s));
+  CK(ovf1.alloc(sizeof(int) * std::max(nd, 1LL), s));
+  CK(st.alloc(4 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(rcnt.p, 0, sizeof(int) * (nrows + 1), s));
+  CK(cudaMemsetAsync(st.p, 0, 4 * sizeof(unsigned long long), s));
+  RowIn W;
+  W.de_start = pl->de_start;
+  W.de_items = pl->de_items;
+  W.inR = RI.inR;
+  W.dlist = nullptr;
+  W.d_lo = d_lo;
+  W.key_bits = 1;
+  while ((1LL << W.key_bits) - 1 < (long long)P.J / NC) ++W.key_bits;
+  W.skey64 = P.narrow ? nullptr : (const unsigned long long*)sk;
+  W.skey32 = P.narrow ? (const unsigned*)sk : nullptr;
+  W.sval = sv;
+  W.sstart = sstart.as<long long>();
+  W.vmax = d_vmax;
+  W.fmax = pl->fmax;
+  RowOut O;
+  O.col = col.as<int>();
+  O.val = val.as<double>();
+  O.cap = ent_cap;
+  O.used = st.as<unsigned long long>();
+  O.novf = (unsigned*)(st.as<unsigned long long>() + 1);
+  O.roff = roff.as<long long>();
+  O.rcnt = rcnt.as<int>();
+  const int cap_max = NC == 1 ? 8192 : 2048;
+  int cap = std::max(NC == 1 ? 1024 : 512, std::min(pl->row_cap, cap_max));
+  long long nblk = nd;
+  int* lists[2] = {ovf0.as<int>(), ovf1.as<int>()};
+  for (int pass = 0;; ++pass) {
+    O.ovf = lists[pass & 1];
+    CK(launch_rows_cap(P, RI, W, O, nblk, cap, s));
+    unsigned hov = 0;
+    CK(cudaMemcpyAsync(&hov, O.novf, sizeof hov, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    TRACE("row pass");
+    if (!hov) break;
+    if (4LL * hov > nblk) pl->row_cap = std::min(cap * 2, cap_max);  // most rows need more: start there next time
+    if (cap >= cap_max) { *fallback = true; return NLG_OK; }
+    cap *= 2;
+    W.dlist = lists[pass & 1];
+    nblk = hov;
+    CK(cudaMemsetAsync(O.novf, 0, sizeof(unsigned), s));
+  }
+  unsigned long long used = 0;
+  CK(cudaMemcpyAsync(&used, O.used, sizeof used, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if ((long long)used > ent_cap) { *need_split = true; return NLG_OK; }
+  CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
+  {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    g_launches += 1;
+  }
+  nnz = (long long)used;
+  CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
+  CK(cudaMallocAsync(&piece.data, sizeof(double) * std::max(nnz, 1LL), s));
+  if (nrows) {
+    k_row_gather<<<grid_for(nrows * 32, 256), 256, 0, s>>>(roff.as<long long>(), rcnt.as<int>(), piece.indptr, nrows,
+                                                           col.as<int>(), val.as<double>(), piece.indices, piece.data);
+    LAUNCHED();
   }
   piece.nnz = nnz;
   return NLG_OK;
@@ -2568,9 +3212,14 @@ fits:
   const long long nsing_slots = (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC;
   const long long r_base = (long long)nR * E + nsing_slots;
   const long long r_cap = (long long)(kRunFrac * (double)(nvis * 2 * E)) + 1;
-  DevBuf keys, vals, kkv, klv;
-  CK(keys.alloc(sizeof(unsigned long long) * (r_base + r_cap), s));
-  CK(vals.alloc(sizeof(double) * (r_base + r_cap), s));
+  const bool rows_mode = pl->use_rows;
+  DevBuf keys, vals, kkv, klv, vmaxb;
+  // stage W needs the singular slots only; stage R also its run buffer
+  CK(keys.alloc(sizeof(unsigned long long) * (r_base + (rows_mode ? 0 : r_cap)), s));
+  CK(vals.alloc(sizeof(double) * (r_base + (rows_mode ? 0 : r_cap)), s));
+  CK(vmaxb.alloc(sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(vmaxb.p, 0, sizeof(unsigned long long), s));
+  unsigned long long* d_vmax = vmaxb.as<unsigned long long>();
   const long long nkk = 3LL * NC * (3 * NC + 1) / 2, kls = NC == 1 ? 12 : 36;  // Blk<NC>::NKK, KLS
   CK(kkv.alloc(sizeof(double) * 2 * nkk * std::max(nst, 1LL), s));
   CK(klv.alloc(sizeof(double) * 2 * kls * std::max(nst, 1LL), s));
@@ -2582,6 +3231,7 @@ fits:
   O.klv = klv.as<double>();
   O.counters = d_counters;
   O.errpair = d_err;
+  O.vmax = d_vmax;
   VisitOut OF = O, OP = O;
   OF.a_base = aF; OF.b_base = bF; OF.revpos = revposF.as<int>(); OF.nlist = P.analytic ? 0 : nF;
   OP.a_base = aP; OP.b_base = bP; OP.revpos = revposP.as<int>(); OP.nlist = nPt;
@@ -2598,31 +3248,65 @@ fits:
   double* cvals = vals.as<double>();
   const long long sbase = (long long)nR * E;
   switch (P.kid) {
-    case 0: rc = run_singular<0>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
-    case 1: rc = run_singular<1>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
-    case 2: rc = run_singular<2>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
-    default: rc = run_singular<3>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err); break;
+    case 0: rc = run_singular<0>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
+    case 1: rc = run_singular<1>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
+    case 2: rc = run_singular<2>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
+    default: rc = run_singular<3>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
   }
   if (rc) return rc;
   CK(cudaEventRecord(ev[4], s));
   // ---- merge stage R: per-root reduction of the record blocks
+  RootIn RI;
+  RI.roots = roots.as<int>();
+  RI.nR = nR;
+  RI.cnt = cnt.as<int>();
+  RI.off = off.as<long long>();
+  RI.nF = nF;
+  RI.rec = lf;
+  RI.rstartF = rstartF.as<int>();
+  RI.rstartP = rstartP.as<int>();
+  RI.partBF = partBF.as<int>();
+  RI.partBP = partBP.as<int>();
+  RI.aF = aF; RI.bF = bF; RI.aP = aP; RI.bP = bP;
+  RI.analytic = P.analytic;
+  RI.inR = inR.as<int>();
+  RI.kkv = O.kkv;
+  RI.klv = O.klv;
+  const long long nrows = row_hi - row_lo;
+  Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
+  long long nnz = 0;
+  bool merged = false;
+  if (rows_mode) {
+    // ---- merge stage W: per-row fixed-point tables -> CSR rows
+    bool fb = false, ns = false;
+    const long long ent_cap = (long long)(kEntFrac * (double)(nvis * 2 * E)) + nR * E + nsing_slots + 1024;
+    void* sk = P.narrow ? (void*)(reinterpret_cast<unsigned*>(keys.p) + sbase)
+                        : (void*)(keys.as<unsigned long long>() + sbase);
+    rc = merge_rows(pl, P, RI, sk, vals.as<double>() + sbase, nsing_slots, d_vmax, ent_cap, piece, nnz, &fb, &ns);
+    if (rc) return rc;
+    if (ns) {
+      if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
+      set_err("a single row exceeds the entry buffer");
+      return NLG_ERR_CUDA;
+    }
+    merged = !fb;
+    if (fb) {  // stage R + sort: the COO with its run buffer (singular slots carried over)
+      TRACE("stage W fallback");
+      DevBuf k2, v2;
+      CK(k2.alloc(sizeof(unsigned long long) * (r_base + r_cap), s));
+      CK(v2.alloc(sizeof(double) * (r_base + r_cap), s));
+      CK(cudaMemcpyAsync(k2.p, keys.p, (P.narrow ? 4 : 8) * r_base, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(v2.p, vals.p, sizeof(double) * r_base, cudaMemcpyDeviceToDevice, s));
+      std::swap(keys.p, k2.p);
+      std::swap(vals.p, v2.p);
+      std::swap(keys.arena, k2.arena);
+      std::swap(vals.arena, v2.arena);
+      ckeys = keys.as<unsigned long long>();
+      cvals = vals.as<double>();
+    }
+  }
   long long r_total = 0;
-  if (nR) {
-    RootIn RI;
-    RI.roots = roots.as<int>();
-    RI.nR = nR;
-    RI.cnt = cnt.as<int>();
-    RI.off = off.as<long long>();
-    RI.nF = nF;
-    RI.rec = lf;
-    RI.rstartF = rstartF.as<int>();
-    RI.rstartP = rstartP.as<int>();
-    RI.partBF = partBF.as<int>();
-    RI.partBP = partBP.as<int>();
-    RI.aF = aF; RI.bF = bF; RI.aP = aP; RI.bP = bP;
-    RI.analytic = P.analytic;
-    RI.kkv = O.kkv;
-    RI.klv = O.klv;
+  if (nR && !merged) {
     DevBuf nch, cfirst, rstate;
     CK(nch.alloc(sizeof(int) * (nR + 1), s));
     CK(cfirst.alloc(sizeof(int) * (nR + 1), s));
@@ -2685,17 +3369,18 @@ fits:
     r_total = (long long)hst[2];
   }
   CK(cudaEventRecord(ev[6], s));
-  const long long coo_red = r_base + r_total;
-  // ---- sort (row, col) keys (stable: equal keys keep COO position order), sum runs
-  const long long nrows = row_hi - row_lo;
-  Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
-  long long nnz = 0;
-  long long kept = 0;
-  rc = P.narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, true)
-                : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept);
-  st->coo_reduced += kept;
-  if (rc) return rc;
-  piece.nnz = nnz;
+  if (!merged) {
+    const long long coo_red = r_base + r_total;
+    // ---- sort (row, col) keys (stable: equal keys keep COO position order), sum runs
+    long long kept = 0;
+    rc = P.narrow ? merge_csr<unsigned>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept, true)
+                  : merge_csr<unsigned long long>(s, P, ckeys, cvals, coo_red, nrows, piece, nnz, &kept);
+    st->coo_reduced += kept;
+    if (rc) return rc;
+    piece.nnz = nnz;
+  } else {
+    st->coo_reduced += nnz;
+  }
   out.push_back(piece);
   CK(cudaEventRecord(ev[5], s));
   CK(cudaStreamSynchronize(s));
@@ -2872,6 +3557,7 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   P.dbg = getenv("NLG_DEBUG") ? atoi(getenv("NLG_DEBUG")) : 0;
   // NLG_NO_ANALYTIC: integrate the full pairs of kid 2 / 3 per record (A/B and tests)
   P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC");
+  pl->use_rows = !(getenv("NLG_MERGE") && !strcmp(getenv("NLG_MERGE"), "sort"));
   Rule7 hr;
   for (int p = 0; p < 7; ++p) {
     hr.op[p][0] = pb->op[2 * p]; hr.op[p][1] = pb->op[2 * p + 1];
@@ -2914,7 +3600,8 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
       cudaMallocAsync(&pl->dofs, sizeof(int4) * std::max(K, 1LL), s) ||
       cudaMallocAsync(&pl->ctr, sizeof(double2) * std::max(K, 1LL), s) ||
       cudaMallocAsync(&pl->rad, sizeof(double) * std::max(K, 1LL), s) ||
-      (P.analytic && cudaMallocAsync(&pl->ftab, sizeof(double4) * std::max(K, 1LL), s))) {
+      (P.analytic && cudaMallocAsync(&pl->ftab, sizeof(double4) * std::max(K, 1LL), s)) ||
+      cudaMallocAsync(&pl->fmax, 4 * sizeof(unsigned long long), s)) {
     set_err("device allocation failed");
     return fail(NLG_ERR_CUDA);
   }
@@ -2981,7 +3668,8 @@ void nlg_plan_destroy(nlg_plan* pl) {
   if (!pl) return;
   cudaSetDevice(pl->device);
   cudaStream_t s = pl->stream;
-  void* ptrs[] = {pl->vtx, pl->elem, pl->dofs, pl->ctr, pl->rad, pl->ftab, pl->grid_start, pl->grid_items, pl->act};
+  void* ptrs[] = {pl->vtx,        pl->elem,       pl->dofs,     pl->ctr,      pl->rad,     pl->ftab,
+                  pl->fmax,       pl->de_start,   pl->de_items, pl->grid_start, pl->grid_items, pl->act};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   for (auto& f : pl->sing_tab)
