@@ -1633,7 +1633,7 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
 // distinct columns outgrow the table is retried with a larger one; beyond
 // the largest, the batch falls back to stage R + the global sort.
 constexpr unsigned kRowEmpty = 0x7fffffffu;
-constexpr int kFixBits = 96;  // bound x 2^S = 2^96: 2^31 contributions of headroom below 2^127
+constexpr int kFixBits = 72;  // bound x 2^S = 2^72: 2^23 contributions per cell below 2^95
 
 struct RowIn {
   const int* de_start;
@@ -1661,48 +1661,45 @@ struct RowOut {
   unsigned* novf;
 };
 
-struct Fix {  // 128-bit two's complement fixed point
-  unsigned long long lo;
-  long long hi;
-};
-__device__ __forceinline__ Fix fix_of(double v, double scale) {
+// Fixed point: t = rint(v 2^S), |t| < 2^80, summed exactly as a 96-bit two's
+// complement integer (three 32-bit limbs in shared memory, native 32-bit
+// atomics with the carries propagated by the adding thread; __int128 in
+// registers), so a sum does not depend on the order of its terms.
+using fix_t = __int128;
+__device__ __forceinline__ fix_t fix_of(double v, double scale) {
   const double t = rint(v * scale);
-  Fix f;
-  if (fabs(t) < 0x1p63) {
-    const long long q = (long long)t;
-    f.lo = (unsigned long long)q;
-    f.hi = q < 0 ? -1 : 0;
-  } else {  // t is a multiple of 2^11 here: the remainder is exact
-    const double hd = floor(t * 0x1p-64);
-    f.hi = (long long)hd;
-    f.lo = (unsigned long long)(t - hd * 0x1p64);
+  const double hd = floor(t * 0x1p-40);
+  const long long h = __double2ll_rz(hd);
+  const long long l = __double2ll_rz(fma(hd, -0x1p40, t));  // exact: t and hd 2^40 share the grid of t
+  return ((fix_t)h << 40) + (fix_t)l;
+}
+__device__ __forceinline__ double fix_val3(const unsigned* c, double inv) {
+  const double v = fma((double)(int)c[2], 0x1p64, fma((double)c[1], 0x1p32, (double)c[0]));
+  return v * inv;
+}
+__device__ __forceinline__ void fix_atomic(unsigned* c, fix_t x) {
+  unsigned x0 = (unsigned)x, x1 = (unsigned)(x >> 32), x2 = (unsigned)(x >> 64);
+  if (x0) {
+    const unsigned o = atomicAdd(&c[0], x0);
+    if (o + x0 < o && ++x1 == 0) ++x2;
   }
-  return f;
+  if (x1) {
+    const unsigned o = atomicAdd(&c[1], x1);
+    if (o + x1 < o) ++x2;
+  }
+  if (x2) atomicAdd(&c[2], x2);
 }
-__device__ __forceinline__ void fix_add(Fix& a, const Fix& b) {
-  const unsigned long long s = a.lo + b.lo;
-  a.hi += b.hi + (s < a.lo ? 1 : 0);
-  a.lo = s;
-}
-__device__ __forceinline__ double fix_val(const Fix& f, double inv) {
-  return fma((double)f.hi, 0x1p64, (double)f.lo) * inv;
-}
-__device__ __forceinline__ void fix_atomic(unsigned long long* cell, const Fix& b) {
-  if (!b.lo && !b.hi) return;
-  const unsigned long long old = atomicAdd(&cell[0], b.lo);
-  const long long h = b.hi + ((old + b.lo < old) ? 1 : 0);
-  if (h) atomicAdd(&cell[1], (unsigned long long)h);
-}
-__device__ __forceinline__ Fix fix_warp_sum(Fix a) {
+__device__ __forceinline__ fix_t fix_warp_sum(fix_t a) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    Fix b;
-    b.lo = __shfl_xor_sync(0xffffffffu, a.lo, o);
-    b.hi = __shfl_xor_sync(0xffffffffu, a.hi, o);
-    fix_add(a, b);
+    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)a, o);
+    const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(a >> 64), o);
+    a += ((fix_t)hi << 64) | (fix_t)lo;
   }
   return a;
 }
+
+constexpr int kRowGroup = 32;  // incident roots whose analytic own terms are flushed together
 
 template <int NC, int CAP, int TH>
 struct RowSmem {
@@ -1710,12 +1707,12 @@ struct RowSmem {
   using Scan = cub::BlockScan<int, TH>;
   unsigned key[CAP];                      // column dof base (bit 31: present, nc = 1)
   unsigned pres[NC == 1 ? 1 : CAP];       // nc = 2: presence bit per (c, d) component
-  unsigned long long acc[CAP][NC * NC][2];
+  unsigned acc[CAP][NC * NC][3];
   union {
     typename Sort::TempStorage sort;
     typename Scan::TempStorage scan;
   } u;
-  unsigned long long sa[2];  // analytic: sum of the partners' A2 (fixed point)
+  unsigned sa[kRowGroup][3];  // analytic: per incident root, sum of the partners' A2
   unsigned sa_pres;
   int used, ovf;
   long long base[NC];
@@ -1723,24 +1720,24 @@ struct RowSmem {
 
 template <int NC, int CAP, int TH, bool AN>
 __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, RowOut O) {
-  constexpr int NC2 = NC * NC, N3 = 3 * NC, IT = CAP / TH, NWARP = TH / 32;
+  constexpr int NC2 = NC * NC, IT = CAP / TH;
   constexpr int LOG2CAP = CAP == 512 ? 9 : CAP == 1024 ? 10 : CAP == 2048 ? 11 : CAP == 4096 ? 12 : 13;
   static_assert((1 << LOG2CAP) == CAP, "CAP must be a power of two in [512, 8192]");
   using SM = RowSmem<NC, CAP, TH>;
   extern __shared__ __align__(16) unsigned char row_smem[];
   SM& S = *reinterpret_cast<SM*>(row_smem);
-  const int t = threadIdx.x, lane = lane_id(), warp = t >> 5;
+  const int t = threadIdx.x, lane = lane_id();
   const long long d = W.dlist ? (long long)W.dlist[blockIdx.x] : W.d_lo + blockIdx.x;
   for (int i = t; i < CAP; i += TH) {
     S.key[i] = kRowEmpty;
     if (NC > 1) S.pres[i] = 0;
 #pragma unroll
-    for (int e = 0; e < NC2; ++e) S.acc[i][e][0] = S.acc[i][e][1] = 0;
+    for (int e = 0; e < NC2; ++e) S.acc[i][e][0] = S.acc[i][e][1] = S.acc[i][e][2] = 0;
   }
+  for (int i = t; i < kRowGroup * 3; i += TH) (&S.sa[0][0])[i] = 0;
   if (t == 0) {
     S.used = 0;
     S.ovf = 0;
-    S.sa[0] = S.sa[1] = 0;
     S.sa_pres = 0;
   }
   // fixed-point scale from a bound of every contribution's magnitude
@@ -1761,12 +1758,12 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
     const double fg = __longlong_as_double((long long)W.fmax[1]);
     const double fphi = __longlong_as_double((long long)W.fmax[2]);
     bound = fmax(bound, 2.0 * fa2 * whsmax * fg);
-    bound = fmax(bound, 2.0 * fa2 * sw * fphi * fa2 * 0x1p24);  // own term: A2_r Phi_r x (sum of up to 2^24 A2_n)
+    bound = fmax(bound, 2.0 * fa2 * sw * fphi * fa2 * 0x1p14);  // own term: A2_r Phi_r x (sum of up to 2^14 A2_n)
   }
   const bool bok = bound > 0.0 && bound <= 1e300;
   const int be = bok ? ilogb(bound) + 1 : 0;
   const double scale = bok ? ldexp(1.0, kFixBits - be) : 1.0, inv = bok ? ldexp(1.0, be - kFixBits) : 1.0;
-  const int ae = AN && fa2 > 0.0 && fa2 <= 1e300 ? ilogb(fa2) + 1 + 24 : 0;  // sum of A2: its own scale
+  const int ae = AN && fa2 > 0.0 && fa2 <= 1e300 ? ilogb(fa2) + 1 : 0;  // sums of A2: their own scale
   const double ascale = ldexp(1.0, kFixBits - ae), ainv = ldexp(1.0, ae - kFixBits);
   unsigned inr = 0;
 #pragma unroll
@@ -1795,116 +1792,132 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
     S.ovf = 1;
     return -1;
   };
-  auto add = [&](unsigned w, int comp, double v, bool pres) {
-    if (!pres || !(v == v) || fabs(v) > 1e300) return;  // absent; nonfinite values are reported elsewhere
-    const int h = slot_of(w);
-    if (h < 0) return;
-    fix_atomic(S.acc[h][comp], fix_of(v, scale));
-    if (NC == 1) atomicOr(&S.key[h], 0x80000000u);
-    else atomicOr(&S.pres[h], 1u << comp);
+  auto mark = [&](int h, int comp) {
+    if (NC == 1) {
+      if (!(*(volatile unsigned*)&S.key[h] & 0x80000000u)) atomicOr(&S.key[h], 0x80000000u);
+    } else {
+      if (!((*(volatile unsigned*)&S.pres[h] >> comp) & 1u)) atomicOr(&S.pres[h], 1u << comp);
+    }
   };
-  auto add_fix = [&](unsigned w, int comp, const Fix& f, bool pres) {
+  auto add_fix = [&](unsigned w, int comp, fix_t f, bool pres) {
     if (!pres) return;
     const int h = slot_of(w);
     if (h < 0) return;
     fix_atomic(S.acc[h][comp], f);
-    if (NC == 1) atomicOr(&S.key[h], 0x80000000u);
-    else atomicOr(&S.pres[h], 1u << comp);
+    mark(h, comp);
+  };
+  auto add = [&](unsigned w, int comp, double v, bool pres) {
+    if (!pres || !(v == v) || fabs(v) > 1e300) return;  // absent; nonfinite values are reported elsewhere
+    add_fix(w, comp, fix_of(v, scale), true);
   };
   if (inr) {
-    // ---- the record sides of the batch roots incident to d
+    // ---- the record sides of the batch roots incident to d, in groups of
+    // kRowGroup (the analytic own terms need the group's sums of A2)
     const int e0 = W.de_start[d], e1 = W.de_start[d + 1];
-    for (int ei = e0; ei < e1; ++ei) {
-      const int it = __ldg(&W.de_items[ei]);
-      const int k = it >> 2, a = it & 3;
-      const int rank = __ldg(&W.inR[k]);
-      if (rank < 0) continue;  // block-uniform
-      const RootSides R = root_sides(I, rank);
-      const long long n_rs = R.n(), nan_rs = AN ? R.nfull() : 0;
-      const int4 dk4 = __ldg(&P.dofs[k]);
-      const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
-      const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
-      double fkl = 0.0;
-      if (AN) {
-        double wsum = 0.0;
+    for (int g0 = e0; g0 < e1; g0 += kRowGroup) {
+      const int g1 = min(e1, g0 + kRowGroup);
+      for (int ei = g0; ei < g1; ++ei) {
+        const int it = __ldg(&W.de_items[ei]);
+        const int k = it >> 2, a = it & 3;
+        const int rank = __ldg(&W.inR[k]);
+        if (rank < 0) continue;  // block-uniform
+        const RootSides R = root_sides(I, rank);
+        const long long n_rs = R.n(), nan_rs = AN ? R.nfull() : 0;
+        const int4 dk4 = __ldg(&P.dofs[k]);
+        const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
+        const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
+        double fkl = 0.0;
+        if (AN) {
+          double wsum = 0.0;
 #pragma unroll
-        for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
-        fkl = -2.0 * __ldg(&P.ftab[k].w) * wsum;
-      }
-      Fix own[3][NC2];
-      unsigned opres = 0;  // bit b * NC2 + comp
+          for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
+          fkl = -2.0 * __ldg(&P.ftab[k].w) * wsum;
+        }
+        fix_t own[3][NC2];
+        unsigned opres = 0;  // bit b * NC2 + comp
 #pragma unroll
-      for (int b = 0; b < 3; ++b)
+        for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int e = 0; e < NC2; ++e) own[b][e].lo = 0, own[b][e].hi = 0;
-      Fix sa{0, 0};
-      bool sapres = false;
-      for (long long rs = t; rs < n_rs; rs += TH) {
-        const int n = R.partner(I, rs);
-        const int4 dn4 = __ldg(&P.dofs[n]);
-        const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
-        if (AN && rs < nan_rs) {
-          const double4 g = ld_f4(P.ftab + n);
-          fix_add(sa, fix_of(g.w, ascale));
-          sapres |= g.w != 0.0;
-          if (inr & 1u) {
+          for (int e = 0; e < NC2; ++e) own[b][e] = 0;
+        fix_t sa = 0;
+        bool sapres = false;
+        for (long long rs = t; rs < n_rs; rs += TH) {
+          if (*(volatile int*)&S.ovf) break;  // this table is too small: retried with a larger one
+          const int n = R.partner(I, rs);
+          const int4 dn4 = __ldg(&P.dofs[n]);
+          const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
+          if (AN && rs < nan_rs) {
+            const double4 g = ld_f4(P.ftab + n);
+            sa += fix_of(g.w, ascale);
+            sapres |= g.w != 0.0;
             add(dn[0], 0, fkl * g.x, g.x != 0.0 && fkl != 0.0);
             add(dn[1], 0, fkl * g.y, g.y != 0.0 && fkl != 0.0);
             add(dn[2], 0, fkl * g.z, g.z != 0.0 && fkl != 0.0);
-          }
-        } else {
-          const long long slot = R.slot(I, rs);
-          const double* kk = I.kkv + slot * Blk<NC>::NKK;
-          const double* kl = I.klv + slot * Blk<NC>::KLS;
+          } else {
+            const long long slot = R.slot(I, rs);
+            const double* kk = I.kkv + slot * Blk<NC>::NKK;
+            const double* kl = I.klv + slot * Blk<NC>::KLS;
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            if (!((inr >> c) & 1u)) continue;
-            const int Ir = a * NC + c;
+            for (int c = 0; c < NC; ++c) {
+              if (!((inr >> c) & 1u)) continue;
+              const int Ir = a * NC + c;
 #pragma unroll
-            for (int b = 0; b < 3; ++b)
+              for (int b = 0; b < 3; ++b)
 #pragma unroll
-              for (int dd = 0; dd < NC; ++dd) {
-                const int Jc = b * NC + dd;
-                const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
-                const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
-                if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
-                  fix_add(own[b][c * NC + dd], fix_of(vo, scale));
-                  opres |= 1u << (b * NC2 + c * NC + dd);
+                for (int dd = 0; dd < NC; ++dd) {
+                  const int Jc = b * NC + dd;
+                  const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
+                  const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
+                  if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
+                    own[b][c * NC + dd] += fix_of(vo, scale);
+                    opres |= 1u << (b * NC2 + c * NC + dd);
+                  }
+                  add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
                 }
-                add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
-              }
+            }
+          }
+        }
+        // own block of (k, a): fixed-point partials -> warp sums -> table
+#pragma unroll
+        for (int o = 16; o; o >>= 1) opres |= __shfl_xor_sync(0xffffffffu, opres, o);
+        if (opres) {  // warp-uniform
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int e = 0; e < NC2; ++e) {
+              const fix_t f = fix_warp_sum(own[b][e]);
+              if (lane == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
+            }
+        }
+        if (AN) {
+          const fix_t f = fix_warp_sum(sa);
+          const bool sp = __any_sync(0xffffffffu, sapres);
+          if (lane == 0 && sp) {
+            fix_atomic(S.sa[ei - g0], f);
+            atomicOr(&S.sa_pres, 1u << (ei - g0));
           }
         }
       }
-      // own block of (k, a): fixed-point partials -> warp sums -> table
-#pragma unroll
-      for (int o = 16; o; o >>= 1) opres |= __shfl_xor_sync(0xffffffffu, opres, o);
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int e = 0; e < NC2; ++e) {
-          const Fix f = fix_warp_sum(own[b][e]);
-          if (lane == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
-        }
       if (AN) {
-        const Fix f = fix_warp_sum(sa);
-        const bool sp = __any_sync(0xffffffffu, sapres);
-        if (lane == 0) {
-          fix_atomic(S.sa, f);
-          if (sp) atomicOr(&S.sa_pres, 1u);
-        }
+        // analytic own terms of the group's roots: 2 A2_r sw Phi_r[a][b] x sum A2_n
         __syncthreads();
-        if (t < 3 && own_on && S.sa_pres && (inr & 1u)) {
-          Fix tot;
-          tot.lo = S.sa[0];
-          tot.hi = (long long)S.sa[1];
-          const double sa_d = fix_val(tot, ainv);
+        const unsigned sp = S.sa_pres;
+        for (int q = t; q < 3 * (g1 - g0); q += TH) {
+          const int j = q / 3, b = q % 3;
+          if (!((sp >> j) & 1u)) continue;
+          const int it = __ldg(&W.de_items[g0 + j]);
+          const int k = it >> 2, a = it & 3;
+          const int rank = __ldg(&W.inR[k]);
+          if (rank < 0 || I.cnt[(long long)C_KK * I.nR + rank] == 0) continue;
+          const double sa_d = fix_val3(S.sa[j], ainv);
           const double fown = (2.0 * __ldg(&P.ftab[k].w) * sw) *
-                              (P.kid == 2 ? root_phi<2>(P, k, a, t) : root_phi<3>(P, k, a, t));
-          add(dk[t], 0, fown * sa_d, fown != 0.0);
+                              (P.kid == 2 ? root_phi<2>(P, k, a, b) : root_phi<3>(P, k, a, b));
+          const int4 dk4 = __ldg(&P.dofs[k]);
+          add((unsigned)(b == 0 ? dk4.x : (b == 1 ? dk4.y : dk4.z)), 0, fown * sa_d, fown != 0.0);
         }
         __syncthreads();
-        if (t == 0) S.sa[0] = S.sa[1] = 0, S.sa_pres = 0;
+        for (int i = t; i < kRowGroup * 3; i += TH) (&S.sa[0][0])[i] = 0;
+        if (t == 0) S.sa_pres = 0;
       }
     }
     // ---- touching-pair (singular) entries of the rows
@@ -1969,11 +1982,8 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
 #pragma unroll
         for (int dd = 0; dd < NC; ++dd) {
           if (!((pm >> dd) & 1u)) continue;
-          Fix f;
-          f.lo = S.acc[h][c * NC + dd][0];
-          f.hi = (long long)S.acc[h][c * NC + dd][1];
           O.col[pos] = (int)(NC * key[q] + dd);
-          O.val[pos] = fix_val(f, inv);
+          O.val[pos] = fix_val3(S.acc[h][c * NC + dd], inv);
           ++pos;
         }
       }
@@ -2814,8 +2824,8 @@ cudaError_t launch_rows_cap(const Params& P, const RootIn& I, const RowIn& W, co
 // some row outgrew the largest table (use stage R + sort); *need_split: the
 // entry estimate was too small.
 nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* skeys, double* svals, long long nsing,
-                      const unsigned long long* d_vmax, long long ent_cap, Csr& piece, long long& nnz, bool* fallback,
-                      bool* need_split) {
+                      const unsigned long long* d_vmax, long long ent_cap, double cols_est, Csr& piece, long long& nnz,
+                      bool* fallback, bool* need_split) {
   cudaStream_t s = pl->stream;
   const int NC = P.nc;
   const long long nrows = P.row_hi - P.row_lo;
@@ -2896,7 +2906,9 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   O.roff = roff.as<long long>();
   O.rcnt = rcnt.as<int>();
   const int cap_max = NC == 1 ? 8192 : 2048;
-  int cap = std::max(NC == 1 ? 1024 : 512, std::min(pl->row_cap, cap_max));
+  // first table: the plan's last need, or the column estimate at <= 3/4 load
+  int cap = NC == 1 ? 1024 : 512;
+  while (cap < cap_max && (cap < pl->row_cap || 0.75 * cap < cols_est)) cap *= 2;
   long long nblk = nd;
   int* lists[2] = {ovf0.as<int>(), ovf1.as<int>()};
   for (int pass = 0;; ++pass) {
@@ -3282,7 +3294,10 @@ fits:
     const long long ent_cap = (long long)(kEntFrac * (double)(nvis * 2 * E)) + nR * E + nsing_slots + 1024;
     void* sk = P.narrow ? (void*)(reinterpret_cast<unsigned*>(keys.p) + sbase)
                         : (void*)(keys.as<unsigned long long>() + sbase);
-    rc = merge_rows(pl, P, RI, sk, vals.as<double>() + sbase, nsing_slots, d_vmax, ent_cap, piece, nnz, &fb, &ns);
+    // distinct columns of a row ~ half the visits of a root (the partner vertices)
+    const double cols_est = nR ? 0.55 * (double)tot[C_EPI] / (double)nR : 0.0;
+    rc = merge_rows(pl, P, RI, sk, vals.as<double>() + sbase, nsing_slots, d_vmax, ent_cap, cols_est, piece, nnz,
+                    &fb, &ns);
     if (rc) return rc;
     if (ns) {
       if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
