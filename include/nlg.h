@@ -159,6 +159,15 @@ nlg_status nlg_fp64_peak(int32_t device, double *tflops);
 /* Number of kernels this library launched on the calling process so far. */
 int64_t nlg_launch_count(void);
 
+/* nlcsr text tokens (host, replaces the token loops of write_nlcsr,
+ * assembly.py:509-516): v[0..n) as space-separated tokens, Python int() for
+ * the integer arrays and repr(float) for the values, into buf (no trailing
+ * separator).  Returns the length, or -1 if cap is too small (33 bytes per
+ * token always suffice).  threads <= 0: all hardware threads. */
+int64_t nlg_format_f64(const double *v, int64_t n, char *buf, int64_t cap, int32_t threads);
+int64_t nlg_format_i64(const int64_t *v, int64_t n, char *buf, int64_t cap, int32_t threads);
+int64_t nlg_format_i32(const int32_t *v, int64_t n, char *buf, int64_t cap, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,7 @@ from .kernels import (KernelSpec, affine_kernel, constant_kernel, constant_kerne
                       fractional_kernel, peridynamic_kernel)
 from .mesh import (AdjacencyGraph, Label, Mesh, build_adjacency_graph, generate_structured_mesh,
                    grid_mesh, lshape_mesh, perturb)
+from .nlio import read_mesh, read_nlcsr, write_mesh, write_nlcsr, write_nlcsr_blocks
 from .quadrature import Path, QuadratureConfig, dispatch, gauss_legendre, rule_7point, singular_rule
 
 __all__ = [
@@ -19,5 +20,6 @@ __all__ = [
     "fractional_kernel", "peridynamic_kernel",
     "AdjacencyGraph", "Label", "Mesh", "build_adjacency_graph", "generate_structured_mesh",
     "grid_mesh", "lshape_mesh", "perturb",
+    "read_mesh", "read_nlcsr", "write_mesh", "write_nlcsr", "write_nlcsr_blocks",
     "Path", "QuadratureConfig", "dispatch", "gauss_legendre", "rule_7point", "singular_rule",
 ]

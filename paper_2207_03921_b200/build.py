@@ -7,7 +7,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "nlg.cu")
-DEPS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("nlg_eval.cuh", "nlg_geom.cuh", "nlg_math.cuh")] + [
+SRC_IO = os.path.join(HERE, "csrc", "nlg_io.cpp")
+DEPS = [SRC, SRC_IO] + [os.path.join(HERE, "csrc", f) for f in ("nlg_eval.cuh", "nlg_geom.cuh", "nlg_math.cuh")] + [
     os.path.join(ROOT, "include", "nlg.h")]
 OUT = os.path.join(HERE, "libnlg.so")
 
@@ -19,7 +20,7 @@ def build(force=False, verbose=False):
     if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in DEPS):
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", SRC]
+    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", SRC, SRC_IO]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
