@@ -1078,8 +1078,53 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
         const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
         const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
         int ne = 0;
+        bool closed = false;
+        if constexpr (KID == 2 || KID == 3) {
+          // constant / affine kernel: the integrands are polynomials of degree
+          // <= 3 and the 7-point rule (degree 5) integrates them exactly, so the
+          // reference's point sums equal closed-form moments of the
+          // sub-triangle (same quantities, other rounding).  Vertex values of
+          // the inner barycentrics and of Q(y) = (1 + a y_1) b:
+          if (!(rs2 > 0.0)) {
+            closed = true;
+            ne = 7;
+            const double w = jac2 * c_rule.iws;
+            const double f[3] = {z1, z1 + z1a, z1 + z1b}, g[3] = {z2, z2 + z2a, z2 + z2b};
+            const double sf = f[0] + f[1] + f[2], sg = g[0] + g[1] + g[2];
+            const double ff = f[0] * f[0] + f[1] * f[1] + f[2] * f[2], gg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
+            const double fg = f[0] * g[0] + f[1] * g[1] + f[2] * g[2];
+            if constexpr (KID == 2) {  // means: (sum)/3, (sum f_i g_i + sum f sum g)/12
+              const double m0 = w * P.cst;
+              sm[X::mp(0, 0)] = m0;
+              sm[X::mp(1, 0)] = m0 * sf * (1.0 / 3.0);
+              sm[X::mp(2, 0)] = m0 * sg * (1.0 / 3.0);
+              sm[X::mq(3, 0)] = m0 * (ff + sf * sf) * (1.0 / 12.0);
+              sm[X::mq(4, 0)] = m0 * (fg + sf * sg) * (1.0 / 12.0);
+              sm[X::mq(5, 0)] = m0 * (gg + sg * sg) * (1.0 / 12.0);
+            } else {
+              const double tp = w * (1.0 + P.kp0 * x0) * P.kp1;
+              sm[X::mp(0, 0)] = tp;
+              sm[X::mp(1, 0)] = tp * sf * (1.0 / 3.0);
+              sm[X::mp(2, 0)] = tp * sg * (1.0 / 3.0);
+              const double Q[3] = {(1.0 + P.kp0 * q0x) * P.kp1, (1.0 + P.kp0 * (q0x + ax)) * P.kp1,
+                                   (1.0 + P.kp0 * (q0x + bx)) * P.kp1};
+              const double sq = Q[0] + Q[1] + Q[2];
+              const double qf = Q[0] * f[0] + Q[1] * f[1] + Q[2] * f[2], qg = Q[0] * g[0] + Q[1] * g[1] + Q[2] * g[2];
+              const double qff = Q[0] * f[0] * f[0] + Q[1] * f[1] * f[1] + Q[2] * f[2] * f[2];
+              const double qfg = Q[0] * f[0] * g[0] + Q[1] * f[1] * g[1] + Q[2] * f[2] * g[2];
+              const double qgg = Q[0] * g[0] * g[0] + Q[1] * g[1] * g[1] + Q[2] * g[2] * g[2];
+              // mean(a b c) = (sa sb sc + (ab) sc + (ac) sb + (bc) sa + 2 (abc)) / 60
+              sm[X::mq(0, 0)] = w * sq * (1.0 / 3.0);
+              sm[X::mq(1, 0)] = w * (qf + sq * sf) * (1.0 / 12.0);
+              sm[X::mq(2, 0)] = w * (qg + sq * sg) * (1.0 / 12.0);
+              sm[X::mq(3, 0)] = w * (sq * sf * sf + 2.0 * qf * sf + ff * sq + 2.0 * qff) * (1.0 / 60.0);
+              sm[X::mq(4, 0)] = w * (sq * sf * sg + qf * sg + qg * sf + fg * sq + 2.0 * qfg) * (1.0 / 60.0);
+              sm[X::mq(5, 0)] = w * (sq * sg * sg + 2.0 * qg * sg + gg * sq + 2.0 * qgg) * (1.0 / 60.0);
+            }
+          }
+        }
 #pragma unroll 1
-        for (int q = 0; q < 7; ++q) {
+        for (int q = 0; q < (closed ? 0 : 7); ++q) {
           const double i0 = c_rule.ip[q][0], i1 = c_rule.ip[q][1];
           const double y0 = fma(bx, i1, fma(ax, i0, q0x));
           const double y1 = fma(by, i1, fma(ay, i0, q0y));
@@ -2786,7 +2831,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
 template <int NC, int CAP, bool AN>
 cudaError_t launch_rows(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
                         cudaStream_t s) {
-  constexpr int TH = CAP >= 4096 ? 512 : 256;
+  constexpr int TH = CAP >= 4096 ? 1024 : (CAP >= 2048 ? 512 : 256);
   const int smem = (int)sizeof(RowSmem<NC, CAP, TH>);
   cudaError_t e = cudaFuncSetAttribute(k_row_asm<NC, CAP, TH, AN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -3587,6 +3632,8 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
       delete pl;
       return NLG_ERR_CONFIG;
     }
+  hr.iws = 0.0;
+  for (int p = 0; p < 7; ++p) hr.iws += hr.iw[p];
   for (int p = 0; p < 7; ++p)
     for (int a = 0; a < 3; ++a) {
       hr.wh[p][a] = hr.ow[p] * hr.oh[p][a];

@@ -29,6 +29,7 @@ struct Rule7 {
   double op[7][2], ow[7], oh[7][3], ip[7][2], iw[7];
   double wh[7][3];   // w_p * H_pa
   double whh[7][9];  // w_p * H_pa * H_pb
+  double iws;        // sum of the inner weights
 };
 
 struct Params {
