@@ -650,6 +650,32 @@ __device__ __forceinline__ double root_phi(const Params& P, int r, int a, int b)
   return v;
 }
 
+// one side of a peridynamic full record from its unique components
+// (full_pair_peri): own block c2 K, neighbour block -c2 G (side B: G transposed)
+__device__ __forceinline__ void emit_peri(const Params& P, const VisitOut& O, long long slot, bool on, int root,
+                                          int nb, double c2, const double (*K)[3], const double (*G)[3][3],
+                                          bool transpose, double& vm) {
+  using B = Blk<2>;
+  bool bad = false;
+#pragma unroll
+  for (int I = 0; I < 6; ++I)
+#pragma unroll
+    for (int J = 0; J < 6; ++J) {
+      const int a = I >> 1, c = I & 1, b = J >> 1, d = J & 1, u = c + d;
+      if (I <= J) {
+        const double kk = c2 * K[sym3i(a, b)][u];
+        O.kkv[slot * B::NKK + B::sym(I, J)] = on ? kk : 0.0;
+        bad |= nonfinite(kk);
+        if (on) vm = fmax(vm, fabs(kk));
+      }
+      const double kl = -c2 * (transpose ? G[b][a][u] : G[a][b][u]);
+      O.klv[slot * B::KLS + B::kl(I, J)] = on ? emit_val(kl) : 0.0;
+      bad |= nonfinite(kl);
+      if (on) vm = fmax(vm, fabs(kl));
+    }
+  report_nonfinite(on && bad, root, nb, P.K, O.errpair);
+}
+
 // full records, one thread each: the 7x7 point-pair matrix gives both visits
 template <int KID>
 __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__ list, VisitOut O) {
@@ -675,6 +701,21 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     const bool touching = (k == l) || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
                           ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
     const double rs2 = (touching && P.path == 1) ? P.rskip2 : 0.0;
+    if constexpr (KID == 1) {
+      if (k != l) {  // unique components, emitted on the fly (no 36-entry blocks in registers)
+        double lx[3], ly[3], K[6][3], K2[6][3], G[3][3][3];
+        load_tri(P, l, lx, ly);
+        long long ne = 0;
+        full_pair_peri(P, kx, ky, lx, ly, rs2, K, K2, G, ne);
+        const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+        const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
+        ev0 += ne * mult;
+        out0 += 14 * mult;
+        emit_peri(P, O, O.a_base + v, emitA, k, l, c2, K, G, false, vm);
+        emit_peri(P, O, O.b_base + __ldg(&O.revpos[v]), emitB, l, k, c2, K2, G, true, vm);
+        continue;
+      }
+    }
     double kkA[E], klA[E], kkB[E], klB[E];
     if (k == l) {
       // identical pair: both column halves of the reference's B hit k's dofs;
@@ -827,6 +868,60 @@ __device__ __forceinline__ void item_folds(double W, const double* oh, const dou
       F1[C::NKK + I * N3 + J] = -Woh[b] * syp[a][cd];
     }
 }
+
+// The same folds entry by entry (index g of [kk unique | kl]), so the fold
+// phase holds the moment-derived terms only, not two NSIDE-value blocks per
+// lane (nc = 2: 57 + 57); identical arithmetic to item_folds.
+template <int KID>
+struct FoldSrc {
+  using C = ClipCfg<KID>;
+  using X = SumIdx<KID>;
+  static constexpr int NC = C::NC, N3 = 3 * NC, NU = C::NCU;
+  double W, oh[3], Woh[3];
+  double s0[NU], syp[3][NU], syq[3][NU], syy[6][NU];  // by stored component
+  __device__ __forceinline__ FoldSrc(double w, const double* o, const double* s) {
+    W = w;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { oh[a] = o[a]; Woh[a] = w * o[a]; }
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const double p0 = s[X::mp(0, u)], p1 = s[X::mp(1, u)], p2 = s[X::mp(2, u)];
+      const double q0 = s[X::mq(0, u)], q1 = s[X::mq(1, u)], q2 = s[X::mq(2, u)];
+      s0[u] = p0;
+      syp[0][u] = (p0 - p1) - p2; syp[1][u] = p1; syp[2][u] = p2;
+      syq[0][u] = (q0 - q1) - q2; syq[1][u] = q1; syq[2][u] = q2;
+      const double m11 = s[X::mq(3, u)], m12 = s[X::mq(4, u)], m22 = s[X::mq(5, u)];
+      const double s01 = (q1 - m11) - m12, s02 = (q2 - m12) - m22;
+      syy[0][u] = (syq[0][u] - s01) - s02; syy[1][u] = s01; syy[2][u] = s02;
+      syy[3][u] = m11; syy[4][u] = m12; syy[5][u] = m22;
+    }
+  }
+  // row / column of the u-th unique (I <= J) own-block entry, as I * 8 + J
+  struct KKTab {
+    unsigned char ij[C::NKK];
+  };
+  __host__ __device__ static constexpr KKTab kk_tab() {
+    KKTab t{};
+    int u = 0;
+    for (int I = 0; I < N3; ++I)
+      for (int J = I; J < N3; ++J) t.ij[u++] = (unsigned char)(I * 8 + J);
+    return t;
+  }
+  __device__ __forceinline__ void entry(int g, double& f0, double& f1) const {
+    if (g < C::NKK) {
+      constexpr KKTab tab = kk_tab();
+      const int I = tab.ij[g] >> 3, J = tab.ij[g] & 7;
+      const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, u = X::uc(c * NC + d);
+      f0 = (Woh[a] * oh[b]) * s0[u];
+      f1 = W * syy[sym3(a, b)][u];
+    } else {
+      const int e = g - C::NKK, I = e / N3, J = e % N3;
+      const int a = I / NC, c = I % NC, b = J / NC, d = J % NC, u = X::uc(c * NC + d);
+      f0 = -Woh[a] * syq[b][u];
+      f1 = -Woh[b] * syp[a][u];
+    }
+  }
+};
 
 template <int KID, bool SQ>
 __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
@@ -1195,19 +1290,8 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
     const int rk = S.vk[vs], rl = S.vl[vs], rf = S.fl[vs];
     // side A (visit (k, l)) gets the fold of the sweep it calls mode 0 / 1,
     // side B (visit (l, k)) the other one; an identical pair (m = 2) gets both on A
-    double FA[C::NSIDE], FB[C::NSIDE];
-    {
-      double F0[C::NSIDE], F1[C::NSIDE];
-      item_folds<KID>(Wi, ohi, si, F0, F1);
-      const bool m1 = mi == 1, m2 = ivalid && mi == 2;
-#pragma unroll
-      for (int i = 0; i < C::NSIDE; ++i) {
-        const double a0 = ivalid ? (m1 ? F1[i] : F0[i]) : 0.0;
-        const double b0 = ivalid && !m2 ? (m1 ? F0[i] : F1[i]) : 0.0;
-        FA[i] = m2 ? a0 + F1[i] : a0;
-        FB[i] = b0;
-      }
-    }
+    const FoldSrc<KID> fs(Wi, ohi, si);
+    const bool m1 = mi == 1, m2 = ivalid && mi == 2;
     constexpr int NBATCH = (C::NVAL + 31) / 32;  // reduce-scatter batches of 32 values
 #pragma unroll
     for (int bt = 0; bt < NBATCH; ++bt) {
@@ -1215,7 +1299,18 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int g = bt * 32 + i;
-        vals[i] = g < C::NSIDE ? FA[g] : (g < C::NVAL ? FB[g - C::NSIDE] : 0.0);
+        double v = 0.0;
+        if (g < C::NVAL) {
+          double f0, f1;
+          fs.entry(g < C::NSIDE ? g : g - C::NSIDE, f0, f1);
+          if (g < C::NSIDE) {
+            const double a0 = ivalid ? (m1 ? f1 : f0) : 0.0;
+            v = m2 ? a0 + f1 : a0;
+          } else {
+            v = ivalid && !m2 ? (m1 ? f0 : f1) : 0.0;
+          }
+        }
+        vals[i] = v;
       }
       // reduce-scatter over the 16 lanes of the record: lane r keeps [2r, 2r+2)
 #pragma unroll

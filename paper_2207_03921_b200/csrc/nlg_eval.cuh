@@ -255,6 +255,83 @@ __device__ __forceinline__ void full_pair2(const Params& P, const double* kx, co
         }
 }
 
+// full non-identical pair of the peridynamic kernel (kid 1, nc = 2), in the
+// unique components only: the kernel matrix P_pq = c dd^T / |d|^3 is
+// symmetric (u = 00, 01, 11) and even in d, so Q = P, both own blocks are
+// symmetric in (a, b) and (c, d), and klB is the transpose of klA:
+//   K [ab][u] = sum_p whh_p[ab] sum_q w_q P_pq[u]     kkA = c2 K
+//   K2[ab][u] = sum_q whh_q[ab] sum_p w_p P_pq[u]     kkB = c2 K2
+//   G[a][b][u] = sum_pq wh_p[a] wh_q[b] P_pq[u]        klA[(a,c),(b,d)] = -c2 G[a][b][u(c,d)]
+//                                                      klB[(a,c),(b,d)] = -c2 G[b][a][u(c,d)]
+// (ab: 00 01 02 11 12 22).  66 accumulators instead of four 36-entry blocks.
+__device__ __forceinline__ int sym3i(int a, int b) {
+  const int i = a < b ? a : b, j = a < b ? b : a;
+  return i == 0 ? j : (i == 1 ? 2 + j : 5);
+}
+__device__ __forceinline__ void full_pair_peri(const Params& P, const double* kx, const double* ky,
+                                               const double* lx, const double* ly, double rs2, double (*K)[3],
+                                               double (*K2)[3], double (*G)[3][3], long long& n_eval) {
+  double xk[7], yk[7], xl[7], yl[7];
+  rule_points(P, kx, ky, xk, yk);
+  rule_points(P, lx, ly, xl, yl);
+  double colq[7][3];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) K[i][0] = K[i][1] = K[i][2] = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) G[a][b][0] = G[a][b][1] = G[a][b][2] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) colq[q][0] = colq[q][1] = colq[q][2] = 0.0;
+#pragma unroll 1
+  for (int p = 0; p < 7; ++p) {
+    double rp[3] = {0.0, 0.0, 0.0}, g[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) g[b][0] = g[b][1] = g[b][2] = 0.0;
+    const double wp = c_rule.ow[p];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const double d0 = xk[p] - xl[q], d1 = yk[p] - yl[q];
+      const double r2 = sumsq(d0, d1);
+      if (rs2 > 0.0 && r2 < rs2) continue;
+      ++n_eval;
+      const double f = P.cst / (r2 * sqrt(r2));
+      const double pu[3] = {f * d0 * d0, f * d0 * d1, f * d1 * d1};
+      const double wq = c_rule.iw[q];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        rp[u] = fma(wq, pu[u], rp[u]);
+        colq[q][u] = fma(wp, pu[u], colq[q][u]);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) g[b][u] = fma(c_rule.wh[q][b], pu[u], g[b][u]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = a; b < 3; ++b)
+#pragma unroll
+        for (int u = 0; u < 3; ++u) K[sym3i(a, b)][u] = fma(c_rule.whh[p][a * 3 + b], rp[u], K[sym3i(a, b)][u]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int u = 0; u < 3; ++u) G[a][b][u] = fma(c_rule.wh[p][a], g[b][u], G[a][b][u]);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) v = fma(c_rule.whh[q][a * 3 + b], colq[q][u], v);
+        K2[sym3i(a, b)][u] = v;
+      }
+}
+
 // full identical pair (k == l, mode 2): both column halves land on k's dofs;
 // returned as the two halves so the presence test matches the reference's
 // per-triplet `v != 0` (_engine.py:403-424).
