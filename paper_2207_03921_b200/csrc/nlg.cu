@@ -21,6 +21,7 @@
 //             + k_seg_*: deterministic segmented sums -> CSR (replaces
 //             _merge_triplets, assembly.py:137-173)
 #include <cub/cub.cuh>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1973,7 +1974,11 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
           for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
           fkl = -2.0 * __ldg(&P.ftab[k].w) * wsum;
         }
-        fix_t own[3][NC2];
+        // own-block partials in fixed point (nc = 2: in double, summed by each
+        // thread over its sides in a fixed order -- deterministic for a given
+        // CTA size -- and converted once per root, to save registers)
+        using OwnT = std::conditional_t<NC == 2, double, fix_t>;
+        OwnT own[3][NC2];
         unsigned opres = 0;  // bit b * NC2 + comp
 #pragma unroll
         for (int b = 0; b < 3; ++b)
@@ -2009,7 +2014,8 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
                   const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
                   const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
                   if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
-                    own[b][c * NC + dd] += fix_of(vo, scale);
+                    if constexpr (NC == 2) own[b][c * NC + dd] += vo;
+                    else own[b][c * NC + dd] += fix_of(vo, scale);
                     opres |= 1u << (b * NC2 + c * NC + dd);
                   }
                   add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
@@ -2025,7 +2031,10 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
           for (int b = 0; b < 3; ++b)
 #pragma unroll
             for (int e = 0; e < NC2; ++e) {
-              const fix_t f = fix_warp_sum(own[b][e]);
+              fix_t f0;
+              if constexpr (NC == 2) f0 = fix_of(own[b][e], scale);
+              else f0 = own[b][e];
+              const fix_t f = fix_warp_sum(f0);
               if (lane == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
             }
         }
@@ -2926,7 +2935,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
 template <int NC, int CAP, bool AN>
 cudaError_t launch_rows(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
                         cudaStream_t s) {
-  constexpr int TH = CAP >= 4096 ? 1024 : (CAP >= 2048 ? 512 : 128);
+  constexpr int TH = CAP >= 4096 ? 1024 : (CAP >= 2048 ? 512 : (NC == 2 ? 256 : 128));
   const int smem = (int)sizeof(RowSmem<NC, CAP, TH>);
   cudaError_t e = cudaFuncSetAttribute(k_row_asm<NC, CAP, TH, AN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
