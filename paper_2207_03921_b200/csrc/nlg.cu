@@ -314,16 +314,19 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     if (!(needAk || needA[l])) return -1;
     return k == l ? 2 : (ns == 2 ? 3 : 4);
   }
-  if (LIGHT) {  // upper bounds for the count pass: 0 full, 1 possibly clipped
-    if (!(needAk || ((el.w & 16) && needA[l]))) return -1;
-    const bool full_ub = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
-    return full_ub && !(P.analytic && k == l) ? 0 : 1;
-  }
   const bool full = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
   bool full_lk = full, rej_lk = false;
   if (k != l && (el.w & 16)) {  // root l's view of the same pair
     rej_lk = !touching && __dsub_rn(__dsub_rn(dist, rl), rk) > P.prer;
     full_lk = __dadd_rn(__dadd_rn(dist, rl), rk) <= P.delta;
+  }
+  // When both views agree on `full`, both get the same category whatever the
+  // truncation class, so whether the pair is shared -- and then produced by
+  // the smaller root of the batch -- is known before the (costly) class.
+  if (full == full_lk && k != l && (el.w & 16) && !rej_lk && inR[l] >= 0 && l < k) return -1;
+  if (LIGHT) {  // upper bounds for the count pass: 0 full, 1 possibly clipped
+    if (!(needAk || ((el.w & 16) && needA[l]))) return -1;
+    return full && !(P.analytic && k == l) ? 0 : 1;
   }
   // exact truncation class of the pair (symmetric in k, l)
   int tcls = 0;
