@@ -158,7 +158,21 @@ struct Grid {
   int nx, ny, span;
   const int* __restrict__ start;  // [ncell + 1]
   const int* __restrict__ items;  // active element ids sorted by cell
+  // the items' element records, barycentres and radii in the same order
+  // (the candidate scans read them coalesced)
+  const int4* __restrict__ gel;
+  const double2* __restrict__ gctr;
+  const double* __restrict__ grad;
 };
+
+__global__ void k_grid_gather(Params P, const int* __restrict__ items, int n, int4* gel, double2* gctr, double* grad) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int l = items[j];
+  gel[j] = P.elem[l];
+  gctr[j] = P.ctr[l];
+  grad[j] = P.rad[l];
+}
 
 __global__ void k_cell(Params P, Grid G, unsigned* key, int* val) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -297,15 +311,13 @@ template <bool LIGHT>
 __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2 ck, double rk,
                                         const double* kx, const double* ky, const double* xk, const double* yk,
                                         bool needAk, const unsigned char* __restrict__ needA,
-                                        const int* __restrict__ inR, int l, bool& visited, int& flags) {
+                                        const int* __restrict__ inR, int l, int4 el, double2 cl, double rl,
+                                        bool& visited, int& flags) {
   visited = false;
   flags = 0;
-  const int4 el = __ldg(&P.elem[l]);
   const int ns = (ek.x == el.x) + (ek.x == el.y) + (ek.x == el.z) + (ek.y == el.x) + (ek.y == el.y) +
                  (ek.y == el.z) + (ek.z == el.x) + (ek.z == el.y) + (ek.z == el.z);
   const bool touching = (k == l) || ns > 0;
-  const double2 cl = __ldg(&P.ctr[l]);
-  const double rl = __ldg(&P.rad[l]);
   const double dist = sqrt(sumsq(ck.x - cl.x, ck.y - cl.y));
   if (!touching && __dsub_rn(__dsub_rn(dist, rk), rl) > P.prer) return -1;
   visited = true;
@@ -405,15 +417,23 @@ __global__ void __launch_bounds__(256, 2) k_candidates(Params P, Grid G, const i
         int cat = -1, fl = 0;
         bool vis = false;
         const int l = j < c1 ? G.items[j] : 0;
+        int4 el = make_int4(0, 0, 0, 0);
+        double2 cl = make_double2(0.0, 0.0);
+        double rl = 0.0;
+        if (j < c1) {
+          el = G.gel[j];
+          cl = G.gctr[j];
+          rl = G.grad[j];
+        }
         if (!FILL) {
-          if (j < c1) cat = classify<true>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, vis, fl);
+          if (j < c1) cat = classify<true>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, el, cl, rl, vis, fl);
           c[C_EPI] += vis;
           // C_FULL: all records, C_PART: the possibly clipped ones
           if (cat >= 0) {
             if (cat <= 1) { c[C_FULL]++; c[C_PART] += cat; } else c[cat]++;
           }
         } else {
-          if (j < c1) cat = classify<false>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, vis, fl);
+          if (j < c1) cat = classify<false>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, el, cl, rl, vis, fl);
           nfull += cat == 0;
           nclip += cat == 1;
           // lists: 0 = combined (full or clipped), 1..3 = singular families
@@ -2580,6 +2600,9 @@ struct nlg_plan {
   Grid G{};
   int* grid_start = nullptr;
   int* grid_items = nullptr;
+  int4* grid_el = nullptr;
+  double2* grid_ctr = nullptr;
+  double* grid_rad = nullptr;
   // load vector support
   int* act = nullptr;
   int nact = -1;
@@ -2732,6 +2755,19 @@ nlg_status prep(nlg_plan* pl) {
   LAUNCHED();
   G.start = pl->grid_start;
   G.items = pl->grid_items;
+  if (pl->grid_el) cudaFreeAsync(pl->grid_el, st);
+  if (pl->grid_ctr) cudaFreeAsync(pl->grid_ctr, st);
+  if (pl->grid_rad) cudaFreeAsync(pl->grid_rad, st);
+  CK(cudaMallocAsync(&pl->grid_el, sizeof(int4) * std::max(K, 1), st));
+  CK(cudaMallocAsync(&pl->grid_ctr, sizeof(double2) * std::max(K, 1), st));
+  CK(cudaMallocAsync(&pl->grid_rad, sizeof(double) * std::max(K, 1), st));
+  if (K) {
+    k_grid_gather<<<grid_for(K, 256), 256, 0, st>>>(P, pl->grid_items, K, pl->grid_el, pl->grid_ctr, pl->grid_rad);
+    LAUNCHED();
+  }
+  G.gel = pl->grid_el;
+  G.gctr = pl->grid_ctr;
+  G.grad = pl->grid_rad;
   pl->G = G;
   pl->prepped = true;
   return NLG_OK;
@@ -3838,7 +3874,8 @@ void nlg_plan_destroy(nlg_plan* pl) {
   cudaSetDevice(pl->device);
   cudaStream_t s = pl->stream;
   void* ptrs[] = {pl->vtx,        pl->elem,       pl->dofs,     pl->ctr,      pl->rad,     pl->ftab,
-                  pl->fmax,       pl->de_start,   pl->de_items, pl->grid_start, pl->grid_items, pl->act};
+                  pl->fmax,       pl->de_start,   pl->de_items, pl->grid_start, pl->grid_items, pl->act,
+                  pl->grid_el,    pl->grid_ctr,   pl->grid_rad};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   for (auto& f : pl->sing_tab)
