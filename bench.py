@@ -283,6 +283,19 @@ def main():
                      ("ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge", "ms_merge_stage_r", "ms_total")},
         "merge_hbm": {"coo_entries": st0["coo_entries"], "coo_reduced": st0["coo_reduced"], "nnz": st0["nnz"]},
     }
+    # the merge (stage W) against HBM: algorithmic bytes = the stored record
+    # values it reads once (8 B each) + the CSR it writes (12 B per entry);
+    # analytic full pairs read only per-element factors (L2-resident)
+    merge_ms = float(np.mean([s["ms_merge"] for s in stats]))
+    merge_bytes = 8.0 * st0["coo_entries"] + 12.0 * st0["nnz"]
+    hbm_peak = _peaks().get("hbm_gbs")
+    roofline["merge"] = {
+        "bound": "hbm", "alg_bytes": merge_bytes, "ms": merge_ms,
+        "achieved_gbs": merge_bytes / (merge_ms * 1e-3) / 1e9 if merge_ms else None,
+        "peak_gbs": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if hbm_peak else None,
+        "frac": (merge_bytes / (merge_ms * 1e-3) / 1e9) / hbm_peak if (merge_ms and hbm_peak) else None,
+        "note": "shared-memory atomic / latency bound (stage W hash tables), not HBM bound",
+    }
 
     # ---- end to end through the public API (host numpy in, host scipy CSR out)
     e2e = None
