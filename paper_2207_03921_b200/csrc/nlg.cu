@@ -3260,11 +3260,15 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     // kkv + klv per record side, the reduced COO (own blocks, singular slots,
     // stage-R runs at kRunFrac of the record values) with its sort buffers,
     // lists and indices
+    // (stage W needs no run buffer: its COO is the singular slots, its
+    // output the CSR entries at kEntFrac of the record values)
+    const bool rows_plan = pl->use_rows;
     const long long coo_ub = (long long)nR * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC +
-                             (long long)(kRunFrac * (double)(nUB * 2 * E)) + 1;
+                             (rows_plan ? 0LL : (long long)(kRunFrac * (double)(nUB * 2 * E))) + 1;
+    const long long ent_ub = rows_plan ? (long long)(kEntFrac * (double)(nUB * 2 * E)) : 0LL;
     const long long side_bytes = 8LL * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));  // kkv + klv
-    const long long bytes = nStUB * 2 * side_bytes + coo_ub * (16 + 16) + (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 +
-                            nUB * 24;
+    const long long bytes = nStUB * 2 * side_bytes + coo_ub * (16 + 16) + ent_ub * 12 +
+                            (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 + nUB * 24;
     // 32-bit sizes: records (reverse-index sort) and COO entries must fit
     const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB >= (1LL << 31);
     if (too_big && row_hi - row_lo <= P.nc) {
@@ -3281,11 +3285,11 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       CK(rcost.alloc(sizeof(unsigned long long) * 3 * nrows, s));
       CK(cudaMemsetAsync(rcost.p, 0, sizeof(unsigned long long) * 3 * nrows, s));
       const double store_bytes = 16.0 * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));
-      const double rec_bytes = kRunFrac * 2 * E * 32 + 40;
+      const double rec_bytes = (rows_plan ? kEntFrac * 2 * E * 12 : kRunFrac * 2 * E * 32) + 40;
       const double sing_bytes = 36.0 * NC * NC * 32 + 8, root_bytes = E * 32.0 + 64;
       if (nR)
         k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, store_bytes, sing_bytes,
-                                                      root_bytes, kRunFrac * 2 * E, 36.0 * NC * NC,
+                                                      root_bytes, rows_plan ? 0.0 : kRunFrac * 2 * E, 36.0 * NC * NC,
                                                       rcost.as<unsigned long long>());
       LAUNCHED();
       std::vector<unsigned long long> hcost((size_t)3 * nrows);
@@ -3493,6 +3497,10 @@ fits:
       return NLG_ERR_CUDA;
     }
     merged = !fb;
+    if (fb && r_base + r_cap >= (1LL << 31) && row_hi - row_lo > P.nc) {  // stage R's 32-bit sorts
+      *need_split = true;
+      return NLG_OK;
+    }
     if (fb) {  // stage R + sort: the COO with its run buffer (singular slots carried over)
       TRACE("stage W fallback");
       DevBuf k2, v2;
