@@ -700,8 +700,37 @@ __device__ __forceinline__ void emit_peri(const Params& P, const VisitOut& O, lo
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
 }
 
+// one side of a symmetric scalar full record (full_pair_sym1): own block c2 K,
+// neighbour block -c2 G (side B: G transposed)
+__device__ __forceinline__ void emit_sym1(const Params& P, const VisitOut& O, long long slot, bool on, int root,
+                                          int nb, double c2, const double* K, const double (*G)[3], bool transpose,
+                                          double& vm) {
+  using B = Blk<1>;
+  bool bad = false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (a <= b) {
+        const double kk = c2 * K[sym3i(a, b)];
+        O.kkv[slot * B::NKK + B::sym(a, b)] = on ? kk : 0.0;
+        bad |= nonfinite(kk);
+        if (on) vm = fmax(vm, fabs(kk));
+      }
+      const double kl = -c2 * (transpose ? G[b][a] : G[a][b]);
+      O.klv[slot * B::KLS + B::kl(a, b)] = on ? emit_val(kl) : 0.0;
+      bad |= nonfinite(kl);
+      if (on) vm = fmax(vm, fabs(kl));
+    }
+  report_nonfinite(on && bad, root, nb, P.K, O.errpair);
+}
+
 // full records, one thread each: the 7x7 point-pair matrix gives both visits
-template <int KID>
+// MODE 0: every record; kid 0 / 1 run two launches, MODE 1 the records of
+// the unique-component fast path (non-identical; kid 0: no diagonal skip)
+// and MODE 2 the others, so the fast launch does not carry the general
+// path's registers
+template <int KID, int MODE = 0>
 __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   constexpr int E = T::E, NC = T::NC;
@@ -718,6 +747,15 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     const int2 pr = list[v];
     const int k = pr.x, l = pr.y & kIdMask;
     const bool emitA = pr.y & kEmitA, emitB = pr.y & kEmitB;
+    if constexpr (MODE != 0) {  // fast path: non-identical (kid 0: and no diagonal skip, path 1 only)
+      bool fast = k != l;
+      if (KID == 0 && fast && P.path == 1) {
+        const int4 a = __ldg(&P.elem[k]), b = __ldg(&P.elem[l]);
+        fast = !(a.x == b.x || a.x == b.y || a.x == b.z || a.y == b.x || a.y == b.y || a.y == b.z || a.z == b.x ||
+                 a.z == b.y || a.z == b.z);
+      }
+      if (fast != (MODE == 1)) continue;
+    }
     double kx[3], ky[3], lx[3], ly[3];
     load_tri(P, k, kx, ky);
     const int4 ek = __ldg(&P.elem[k]);
@@ -725,7 +763,22 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     const bool touching = (k == l) || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
                           ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
     const double rs2 = (touching && P.path == 1) ? P.rskip2 : 0.0;
-    if constexpr (KID == 1) {
+    if constexpr (KID == 0 && MODE != 2) {
+      if (k != l && !(rs2 > 0.0)) {  // symmetric scalar kernel: unique components
+        double lx[3], ly[3], K[6], K2[6], G[3][3];
+        load_tri(P, l, lx, ly);
+        long long ne = 0;
+        full_pair_sym1(P, kx, ky, lx, ly, K, K2, G, ne, &s_tab);
+        const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+        const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
+        ev0 += ne * mult;
+        out0 += 14 * mult;
+        emit_sym1(P, O, O.a_base + v, emitA, k, l, c2, K, G, false, vm);
+        emit_sym1(P, O, O.b_base + __ldg(&O.revpos[v]), emitB, l, k, c2, K2, G, true, vm);
+        continue;
+      }
+    }
+    if constexpr (KID == 1 && MODE != 2) {
       if (k != l) {  // unique components, emitted on the fly (no 36-entry blocks in registers)
         double lx[3], ly[3], K[6][3], K2[6][3], G[3][3][3];
         load_tri(P, l, lx, ly);
@@ -740,6 +793,9 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
         continue;
       }
     }
+    if constexpr (MODE == 1) {
+      continue;  // (not reached: every MODE 1 record took a fast path)
+    } else {
     double kkA[E], klA[E], kkB[E], klB[E];
     if (k == l) {
       // identical pair: both column halves of the reference's B hit k's dofs;
@@ -759,6 +815,7 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
     }
     emit_side<NC>(P, O, O.a_base + v, emitA, k, l, kkA, klA, vm);
     emit_side<NC>(P, O, O.b_base + __ldg(&O.revpos[v]), emitB && k != l, l, k, kkB, klB, vm);
+    }
   }
   warp_max_abs(vm, O.vmax);
   warp_add_ll(ev0, &O.counters[K_EVAL_FULL0]);
@@ -2815,7 +2872,15 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
                       cudaEvent_t ev_mid) {
   const long long nF = OF.nlist, nP = O.nlist;
   if (nF) {  // (analytic full pairs: none to integrate)
-    k_full<KID><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, OF);
+    // grid-stride: the pow tables are staged into shared memory once per block
+    if constexpr (KID == 0) {
+      const unsigned gf = (unsigned)std::min<long long>(grid_for(nF, 128), 148LL * 32);
+      k_full<KID, 1><<<gf, 128, 0, pl->stream>>>(P, lf, OF);
+      k_full<KID, 2><<<gf, 128, 0, pl->stream>>>(P, lf, OF);
+      g_launches += 1;
+    } else {
+      k_full<KID><<<grid_for(nF, 128), 128, 0, pl->stream>>>(P, lf, OF);
+    }
     LAUNCHED();
   }
   CK(cudaEventRecord(ev_mid, pl->stream));

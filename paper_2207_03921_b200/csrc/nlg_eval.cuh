@@ -332,6 +332,61 @@ __device__ __forceinline__ void full_pair_peri(const Params& P, const double* kx
       }
 }
 
+// full non-identical pair of a symmetric scalar kernel (kid 0): P_pq =
+// kernel(|x_p - y_q|) = Q_pq, so klB = klA^T and both own blocks are
+// symmetric: K[ab] = sum_p whh_p[ab] sum_q w_q P_pq (kkA = c2 K), K2 from the
+// column sums (kkB = c2 K2), G[a][b] = sum_pq wh_p[a] wh_q[b] P_pq
+// (klA = -c2 G, klB = -c2 G^T).  22 accumulators instead of four 9-entry
+// blocks plus the column sums.
+__device__ __forceinline__ void full_pair_sym1(const Params& P, const double* kx, const double* ky,
+                                               const double* lx, const double* ly, double* K, double* K2,
+                                               double (*G)[3], long long& n_eval, const PowTab* tab) {
+  double xk[7], yk[7], xl[7], yl[7];
+  rule_points(P, kx, ky, xk, yk);
+  rule_points(P, lx, ly, xl, yl);
+  double colq[7];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) K[i] = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) G[a][0] = G[a][1] = G[a][2] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) colq[q] = 0.0;
+#pragma unroll 1
+  for (int p = 0; p < 7; ++p) {
+    double rp = 0.0, g[3] = {0.0, 0.0, 0.0};
+    const double wp = c_rule.ow[p];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const double d0 = xk[p] - xl[q], d1 = yk[p] - yl[q];
+      const double r2 = sumsq(d0, d1);
+      double pv[1], qv[1];
+      kval<0, false, true>(P, xk[p], xl[q], d0, d1, r2, pv, qv, tab);
+      rp = fma(c_rule.iw[q], pv[0], rp);
+      colq[q] = fma(wp, pv[0], colq[q]);
+#pragma unroll
+      for (int b = 0; b < 3; ++b) g[b] = fma(c_rule.wh[q][b], pv[0], g[b]);
+    }
+    n_eval += 49 / 7;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = a; b < 3; ++b) K[sym3i(a, b)] = fma(c_rule.whh[p][a * 3 + b], rp, K[sym3i(a, b)]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) G[a][b] = fma(c_rule.wh[p][a], g[b], G[a][b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) v = fma(c_rule.whh[q][a * 3 + b], colq[q], v);
+      K2[sym3i(a, b)] = v;
+    }
+}
+
 // full identical pair (k == l, mode 2): both column halves land on k's dofs;
 // returned as the two halves so the presence test matches the reference's
 // per-triplet `v != 0` (_engine.py:403-424).
