@@ -45,7 +45,7 @@ typedef int32_t nlg_status;
 #define NLG_ERR_NUMERICAL 2 /* maps to NumericalError (nonfinite local contribution) */
 #define NLG_ERR_CUDA 3      /* launch / runtime failure, no device, OOM */
 
-#define NLG_ABI_VERSION 2
+#define NLG_ABI_VERSION 3
 
 /* Kernel ids (kernels.py :57-118 built-ins + 3 = nonsymmetric affine). */
 #define NLG_KERNEL_FRACTIONAL 0  /* c |x-y|^(-2-2s) */
@@ -99,6 +99,8 @@ typedef struct nlg_stats {
   double ms_prep, ms_candidates, ms_full, ms_partial, ms_singular, ms_merge, ms_total;
   double ms_integrate_kernels; /* full + partial + singular kernel time */
   double ms_merge_stage_r;     /* per-root reduction part of ms_merge */
+  int64_t n_row_retries;       /* stage-W rows re-run in a larger table */
+  int64_t n_merge_fallbacks;   /* batches merged by stage R + sort instead of stage W */
 } nlg_stats;
 
 int32_t nlg_abi_version(void);

@@ -49,7 +49,8 @@ class Stats(ctypes.Structure):
         "sing_points", "alg_flops", "alg_flops_full", "alg_flops_partial", "alg_flops_singular", "coo_entries", "coo_reduced", "nnz", "n_batches", "n_replans", "err_k", "err_l")] + [
         (n, ctypes.c_double) for n in (
             "ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge",
-            "ms_total", "ms_integrate_kernels", "ms_merge_stage_r")]
+            "ms_total", "ms_integrate_kernels", "ms_merge_stage_r")] + [
+        (n, ctypes.c_int64) for n in ("n_row_retries", "n_merge_fallbacks")]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -1863,6 +1863,7 @@ struct RowIn {
   const int* dlist;  // dof bases to process, or nullptr: d_lo + blockIdx.x
   long long d_lo;
   int key_bits;      // bits of the largest dof base + 1 (the empty key sorts last)
+  int fill_div;      // tests (NLG_ROW_FILL_DIV): a table overflows at CAP / fill_div columns (0: at 7/8)
   // singular entries sorted by key, and each local row's first position
   const unsigned long long* skey64;
   const unsigned* skey32;
@@ -2003,7 +2004,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
         if (*(volatile int*)&S.ovf) return -1;
         const unsigned old = atomicCAS(&S.key[h], kRowEmpty, w);
         if (old == kRowEmpty) {
-          if (atomicAdd(&S.used, 1) >= CAP - CAP / 8) S.ovf = 1;
+          if (atomicAdd(&S.used, 1) >= (W.fill_div ? CAP / W.fill_div : CAP - CAP / 8)) S.ovf = 1;
           return (int)h;
         }
         if ((old & 0x7fffffffu) == w) return (int)h;
@@ -3078,7 +3079,7 @@ cudaError_t launch_rows_cap(const Params& P, const RootIn& I, const RowIn& W, co
 // entry estimate was too small.
 nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* skeys, double* svals, long long nsing,
                       const unsigned long long* d_vmax, long long ent_cap, double cols_est, Csr& piece, long long& nnz,
-                      bool* fallback, bool* need_split) {
+                      bool* fallback, bool* need_split, long long* retries) {
   cudaStream_t s = pl->stream;
   const int NC = P.nc;
   const long long nrows = P.row_hi - P.row_lo;
@@ -3144,6 +3145,7 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   W.d_lo = d_lo;
   W.key_bits = 1;
   while ((1LL << W.key_bits) - 1 < (long long)P.J / NC) ++W.key_bits;
+  W.fill_div = getenv("NLG_ROW_FILL_DIV") ? atoi(getenv("NLG_ROW_FILL_DIV")) : 0;
   W.skey64 = P.narrow ? nullptr : (const unsigned long long*)sk;
   W.skey32 = P.narrow ? (const unsigned*)sk : nullptr;
   W.sval = sv;
@@ -3172,6 +3174,7 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
     CK(cudaStreamSynchronize(s));
     TRACE("row pass");
     if (!hov) break;
+    *retries += hov;
     if (4LL * hov > nblk) pl->row_cap = std::min(cap * 2, cap_max);  // most rows need more: start there next time
     if (cap >= cap_max) { *fallback = true; return NLG_OK; }
     cap *= 2;
@@ -3553,8 +3556,11 @@ fits:
                         : (void*)(keys.as<unsigned long long>() + sbase);
     // distinct columns of a row ~ half the visits of a root (the partner vertices)
     const double cols_est = nR ? 0.55 * (double)tot[C_EPI] / (double)nR : 0.0;
+    long long retries = 0;
     rc = merge_rows(pl, P, RI, sk, vals.as<double>() + sbase, nsing_slots, d_vmax, ent_cap, cols_est, piece, nnz,
-                    &fb, &ns);
+                    &fb, &ns, &retries);
+    st->n_row_retries += retries;
+    st->n_merge_fallbacks += fb ? 1 : 0;
     if (rc) return rc;
     if (ns) {
       if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
