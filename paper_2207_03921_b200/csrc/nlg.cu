@@ -132,23 +132,39 @@ __global__ void k_convert(const double* __restrict__ vin, const long long* __res
 // (assembly.py:130-134); bbox/rmax over active elements via ordered atomics
 __global__ void k_bounds(Params P, double2* ctr, double* rad, unsigned long long* ext) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= P.K) return;
-  const int4 e = P.elem[k];
-  const double2 a = P.vtx[e.x], b = P.vtx[e.y], c = P.vtx[e.z];
-  const double cx = __dadd_rn(__dadd_rn(a.x, b.x), c.x) / 3.0;
-  const double cy = __dadd_rn(__dadd_rn(a.y, b.y), c.y) / 3.0;
-  const double ra = sqrt(sumsq(a.x - cx, a.y - cy));
-  const double rb = sqrt(sumsq(b.x - cx, b.y - cy));
-  const double rc = sqrt(sumsq(c.x - cx, c.y - cy));
-  const double r = fmax(fmax(ra, rb), rc);
-  ctr[k] = make_double2(cx, cy);
-  rad[k] = r;
-  if ((e.w & 15) != 0) {
-    atomicMin(&ext[0], d2ord(cx));
-    atomicMin(&ext[1], d2ord(cy));
-    atomicMax(&ext[2], d2ord(cx));
-    atomicMax(&ext[3], d2ord(cy));
-    atomicMax(&ext[4], d2ord(r));
+  // bbox / max radius of the active elements: warp reductions, one atomic
+  // per warp and word
+  unsigned long long mn0 = ~0ull, mn1 = ~0ull, mx0 = 0, mx1 = 0, mr = 0;
+  if (k < P.K) {
+    const int4 e = P.elem[k];
+    const double2 a = P.vtx[e.x], b = P.vtx[e.y], c = P.vtx[e.z];
+    const double cx = __dadd_rn(__dadd_rn(a.x, b.x), c.x) / 3.0;
+    const double cy = __dadd_rn(__dadd_rn(a.y, b.y), c.y) / 3.0;
+    const double ra = sqrt(sumsq(a.x - cx, a.y - cy));
+    const double rb = sqrt(sumsq(b.x - cx, b.y - cy));
+    const double rc = sqrt(sumsq(c.x - cx, c.y - cy));
+    const double r = fmax(fmax(ra, rb), rc);
+    ctr[k] = make_double2(cx, cy);
+    rad[k] = r;
+    if ((e.w & 15) != 0) {
+      mn0 = mx0 = d2ord(cx);
+      mn1 = mx1 = d2ord(cy);
+      mr = d2ord(r);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn0 = min(mn0, __shfl_xor_sync(0xffffffffu, mn0, o));
+    mn1 = min(mn1, __shfl_xor_sync(0xffffffffu, mn1, o));
+    mx0 = max(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = max(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+  }
+  if (lane_id() == 0 && mr) {
+    atomicMin(&ext[0], mn0);
+    atomicMin(&ext[1], mn1);
+    atomicMax(&ext[2], mx0);
+    atomicMax(&ext[3], mx1);
+    atomicMax(&ext[4], mr);
   }
 }
 
