@@ -3379,8 +3379,11 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       std::vector<unsigned long long> hcost((size_t)3 * nrows);
       CK(cudaMemcpyAsync(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      const double lim[3] = {budget > 0 ? 0.7 * (double)budget : 1e300, 0.7 * (double)(1LL << 31),
-                             0.7 * (double)(1LL << 31)};
+      // cut fraction of each limit (the halo roots a batch adds are not in
+      // the per-row costs)
+      static const double pf = getenv("NLG_PLAN_FRAC") ? atof(getenv("NLG_PLAN_FRAC")) : 0.55;
+      const double lim[3] = {budget > 0 ? pf * (double)budget : 1e300, pf * (double)(1LL << 31),
+                             pf * (double)(1LL << 31)};
       double acc[3] = {0, 0, 0};
       for (long long r = 0; r < nrows; ++r) {
         const long long row = row_lo + r;
