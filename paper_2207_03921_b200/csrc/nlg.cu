@@ -516,12 +516,53 @@ __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, con
   atomicAdd(&rc[2], (unsigned long long)(rec * rec_slots + sing * sing_slots + 9 * P.nc * P.nc));
 }
 
-struct IsRecord {
-  int want;  // 0 full, 1 clipped
-  __host__ __device__ bool operator()(const int2& r) const {
-    return r.x != -1 && ((r.x & kCatClip) ? 1 : 0) == want;
+
+// sum of the visits (EPI) and count of the roots whose home row is in the batch
+__global__ void k_epi_home(const int* __restrict__ cnt, int nR, unsigned long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long e = 0, r = 0;
+  if (i < nR && cnt[(long long)C_KK * nR + i] == 2) {
+    e = (unsigned long long)cnt[(long long)C_EPI * nR + i];
+    r = 1;
   }
-};
+  for (int o = 16; o; o >>= 1) {
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  if (lane_id() == 0 && r) {
+    atomicAdd(&out[0], e);
+    atomicAdd(&out[1], r);
+  }
+}
+
+// per-root compaction of the fill's records (contiguous at the start of each
+// root's upper-bound range, full and clipped interleaved in candidate order)
+// into the full and clipped lists at the roots' exact offsets: one warp per
+// root, list order preserved
+__global__ void k_split_records(const int2* __restrict__ comb, const long long* __restrict__ ub_off,
+                                const long long* __restrict__ foff, const long long* __restrict__ poff,
+                                const int* __restrict__ cnt, int nR, int2* lf, int2* lp) {
+  const int i = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  if (i >= nR) return;
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  const int n = cnt[(long long)C_FULL * nR + i] + cnt[(long long)C_PART * nR + i];
+  const int2* src = comb + ub_off[i];
+  int2* fd = lf + foff[i];
+  int2* pd = lp + poff[i];
+  int fp = 0, pp = 0;
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int j = j0 + lane;
+    const bool valid = j < n;
+    const int2 r = valid ? src[j] : make_int2(0, 0);
+    const bool clip = valid && (r.x & kCatClip);
+    const unsigned mf = __ballot_sync(0xffffffffu, valid && !clip), mp = __ballot_sync(0xffffffffu, clip);
+    if (valid && !clip) fd[fp + __popc(mf & lt)] = r;
+    if (clip) pd[pp + __popc(mp & lt)] = r;
+    fp += __popc(mf);
+    pp += __popc(mp);
+  }
+}
 
 __global__ void k_rank(const int* __restrict__ roots, int nR, int* inR) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -3182,13 +3223,16 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   while (cap < cap_max && (cap < pl->row_cap || 0.75 * cap < cols_est)) cap *= 2;
   long long nblk = nd;
   int* lists[2] = {ovf0.as<int>(), ovf1.as<int>()};
+  unsigned long long used = 0;
   for (int pass = 0;; ++pass) {
     O.ovf = lists[pass & 1];
     CK(launch_rows_cap(P, RI, W, O, nblk, cap, s));
-    unsigned hov = 0;
-    CK(cudaMemcpyAsync(&hov, O.novf, sizeof hov, cudaMemcpyDeviceToHost, s));
+    unsigned long long hst[2] = {0, 0};  // entries used, overflowed dofs
+    CK(cudaMemcpyAsync(hst, st.p, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     TRACE("row pass");
+    const unsigned hov = (unsigned)hst[1];
+    used = hst[0];
     if (!hov) break;
     *retries += hov;
     if (4LL * hov > nblk) pl->row_cap = std::min(cap * 2, cap_max);  // most rows need more: start there next time
@@ -3198,9 +3242,6 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
     nblk = hov;
     CK(cudaMemsetAsync(O.novf, 0, sizeof(unsigned), s));
   }
-  unsigned long long used = 0;
-  CK(cudaMemcpyAsync(&used, O.used, sizeof used, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
   if ((long long)used > ent_cap) { *need_split = true; return NLG_OK; }
   CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
   {
@@ -3399,24 +3440,19 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     }
   }
 fits:
-  // EPI of the roots whose home is this batch: sum cnt[EPI] where cnt[KK] == 2
-  {
-    std::vector<int> hc((size_t)2 * nR);
-    if (nR) {
-      CK(cudaMemcpyAsync(hc.data(), cnt.as<int>() + (size_t)C_EPI * nR, sizeof(int) * nR, cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(hc.data() + nR, cnt.as<int>() + (size_t)C_KK * nR, sizeof(int) * nR, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      TRACE("sync 1956");
-    }
-    for (int i = 0; i < nR; ++i)
-      if (hc[nR + i] == 2) { st->epi += hc[i]; st->n_roots += 1; }
+  // EPI of the roots whose home is this batch (read with the batch's last
+  // synchronisation, counted only if the batch completes)
+  DevBuf epib;
+  CK(epib.alloc(2 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(epib.p, 0, 2 * sizeof(unsigned long long), s));
+  if (nR) {
+    k_epi_home<<<grid_for(nR, 256), 256, 0, s>>>(cnt.as<int>(), nR, epib.as<unsigned long long>());
+    LAUNCHED();
   }
-  // ---- fill: records into per-root upper-bound ranges, then stable compaction
-  DevBuf comb, lists, nsel;
+  // ---- fill: records into per-root upper-bound ranges, then per-root compaction
+  DevBuf comb, lists;
   CK(comb.alloc(sizeof(int2) * (size_t)std::max(1LL, nUB), s));
-  CK(cudaMemsetAsync(comb.p, 0xff, sizeof(int2) * (size_t)std::max(1LL, nUB), s));
   CK(lists.alloc(sizeof(int2) * (size_t)std::max(1LL, nUB + nS[0] + nS[1] + nS[2]), s));
-  CK(nsel.alloc(sizeof(long long) * 2, s));
   int2* lsing = lists.as<int2>() + nUB;
   int2* ls[3] = {lsing, lsing + nS[0], lsing + nS[0] + nS[1]};
   if (nR) {
@@ -3425,37 +3461,40 @@ fits:
         off.as<long long>(), comb.as<int2>(), ls[0], ls[1], ls[2]);
     LAUNCHED();
   }
-  long long nsel_h[2] = {0, 0};
-  if (nUB) {
-    size_t tb = 0, tb2 = 0;
-    CK(cub::DeviceSelect::If(nullptr, tb, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>(), nUB, IsRecord{0}, s));
-    CK(cub::DeviceSelect::If(nullptr, tb2, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>() + 1, nUB, IsRecord{1}, s));
-    DevBuf tmp;
-    CK(tmp.alloc(std::max(tb, tb2), s));
-    CK(cub::DeviceSelect::If(tmp.p, tb, comb.as<int2>(), lists.as<int2>(), nsel.as<long long>(), nUB, IsRecord{0}, s));
-    CK(cudaMemcpyAsync(nsel_h, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    TRACE("sync 1984");
-    CK(cub::DeviceSelect::If(tmp.p, tb2, comb.as<int2>(), lists.as<int2>() + nsel_h[0], nsel.as<long long>() + 1, nUB,
-                             IsRecord{1}, s));
-    CK(cudaMemcpyAsync(nsel_h + 1, nsel.as<long long>() + 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    TRACE("sync 1988");
-    g_launches += 4;
-  }
-  const long long nF = nsel_h[0], nPt = nsel_h[1];
-  int2* lf = lists.as<int2>();
-  int2* lp = lf + nF;
-  // actual per-root full / clipped counts -> offsets for the own-block reduction
+  // actual per-root full / clipped counts -> list offsets (columns 4, 5 of
+  // off; column 0 still holds the fill's upper-bound offsets), their totals
+  long long nF = 0, nPt = 0;
+  long long* offF = off.as<long long>() + 4 * (size_t)(nR + 1);
+  long long* offP = off.as<long long>() + 5 * (size_t)(nR + 1);
   if (nR) {
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveScan(nullptr, tb, cnt.as<int>(), off.as<long long>(), cub::Sum(), 0LL, nR, s));
     DevBuf tmp;
     CK(tmp.alloc(tb, s));
-    for (int q : {C_FULL, C_PART})
-      CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, cnt.as<int>() + (size_t)q * nR,
-                                        off.as<long long>() + (size_t)q * (nR + 1), cub::Sum(), 0LL, nR, s));
+    CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, cnt.as<int>() + (size_t)C_FULL * nR, offF, cub::Sum(), 0LL, nR, s));
+    CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, cnt.as<int>() + (size_t)C_PART * nR, offP, cub::Sum(), 0LL, nR, s));
     g_launches += 2;
+    long long lo[2];
+    int lc[2];
+    CK(cudaMemcpyAsync(&lo[0], offF + nR - 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lo[1], offP + nR - 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lc[0], cnt.as<int>() + (size_t)C_FULL * nR + nR - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lc[1], cnt.as<int>() + (size_t)C_PART * nR + nR - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    TRACE("sync list totals");
+    nF = lo[0] + lc[0];
+    nPt = lo[1] + lc[1];
+  }
+  int2* lf = lists.as<int2>();
+  int2* lp = lf + nF;
+  if (nR) {
+    k_split_records<<<grid_for((long long)nR * 32, 256), 256, 0, s>>>(comb.as<int2>(), off.as<long long>(), offF, offP,
+                                                                      cnt.as<int>(), nR, lf, lp);
+    LAUNCHED();
+    // the roots' exact offsets where RootSides reads them (columns 0, 1)
+    CK(cudaMemcpyAsync(off.as<long long>(), offF, sizeof(long long) * nR, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(off.as<long long>() + (size_t)(nR + 1), offP, sizeof(long long) * nR,
+                       cudaMemcpyDeviceToDevice, s));
   }
   const long long nvis = nF + nPt;
   const long long nst = P.analytic ? nPt : nvis;  // records with stored blocks
@@ -3684,8 +3723,12 @@ fits:
   }
   out.push_back(piece);
   CK(cudaEventRecord(ev[5], s));
+  unsigned long long hepi[2] = {0, 0};
+  CK(cudaMemcpyAsync(hepi, epib.p, sizeof hepi, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   TRACE("sync 2089");
+  st->epi += (long long)hepi[0];
+  st->n_roots += (long long)hepi[1];
   float ms;
   CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); tm.cand += ms;
   CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); tm.full += ms;
