@@ -1061,6 +1061,52 @@ struct FoldSrc {
   }
 };
 
+// closed-form moments of one fan sub-triangle for the constant / affine
+// kernels (phase 2 of k_clipped): the integrands are polynomials of degree
+// <= 3 and the 7-point rule (degree 5) integrates them exactly, so these are
+// the reference's point sums with other rounding.  (q0, a, b): the
+// sub-triangle; z*: the inner barycentrics at q0 and along a, b; x0: the
+// outer point's first coordinate.
+template <int KID>
+__device__ __forceinline__ void closed_moments(const Params& P, double q0x, double ax, double bx, double jac2,
+                                               double x0, double z1, double z2, double z1a, double z2a, double z1b,
+                                               double z2b, double* sm) {
+  using X = SumIdx<KID>;
+  const double w = jac2 * c_rule.iws;
+  const double f[3] = {z1, z1 + z1a, z1 + z1b}, g[3] = {z2, z2 + z2a, z2 + z2b};
+  const double sf = f[0] + f[1] + f[2], sg = g[0] + g[1] + g[2];
+  const double ff = f[0] * f[0] + f[1] * f[1] + f[2] * f[2], gg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
+  const double fg = f[0] * g[0] + f[1] * g[1] + f[2] * g[2];
+  if constexpr (KID == 2) {  // means: (sum)/3, (sum f_i g_i + sum f sum g)/12
+    const double m0 = w * P.cst;
+    sm[X::mp(0, 0)] = m0;
+    sm[X::mp(1, 0)] = m0 * sf * (1.0 / 3.0);
+    sm[X::mp(2, 0)] = m0 * sg * (1.0 / 3.0);
+    sm[X::mq(3, 0)] = m0 * (ff + sf * sf) * (1.0 / 12.0);
+    sm[X::mq(4, 0)] = m0 * (fg + sf * sg) * (1.0 / 12.0);
+    sm[X::mq(5, 0)] = m0 * (gg + sg * sg) * (1.0 / 12.0);
+  } else {
+    const double tp = w * (1.0 + P.kp0 * x0) * P.kp1;
+    sm[X::mp(0, 0)] = tp;
+    sm[X::mp(1, 0)] = tp * sf * (1.0 / 3.0);
+    sm[X::mp(2, 0)] = tp * sg * (1.0 / 3.0);
+    const double Q[3] = {(1.0 + P.kp0 * q0x) * P.kp1, (1.0 + P.kp0 * (q0x + ax)) * P.kp1,
+                         (1.0 + P.kp0 * (q0x + bx)) * P.kp1};
+    const double sq = Q[0] + Q[1] + Q[2];
+    const double qf = Q[0] * f[0] + Q[1] * f[1] + Q[2] * f[2], qg = Q[0] * g[0] + Q[1] * g[1] + Q[2] * g[2];
+    const double qff = Q[0] * f[0] * f[0] + Q[1] * f[1] * f[1] + Q[2] * f[2] * f[2];
+    const double qfg = Q[0] * f[0] * g[0] + Q[1] * f[1] * g[1] + Q[2] * f[2] * g[2];
+    const double qgg = Q[0] * g[0] * g[0] + Q[1] * g[1] * g[1] + Q[2] * g[2] * g[2];
+    // mean(a b c) = (sa sb sc + (ab) sc + (ac) sb + (bc) sa + 2 (abc)) / 60
+    sm[X::mq(0, 0)] = w * sq * (1.0 / 3.0);
+    sm[X::mq(1, 0)] = w * (qf + sq * sf) * (1.0 / 12.0);
+    sm[X::mq(2, 0)] = w * (qg + sq * sg) * (1.0 / 12.0);
+    sm[X::mq(3, 0)] = w * (sq * sf * sf + 2.0 * qf * sf + ff * sq + 2.0 * qff) * (1.0 / 60.0);
+    sm[X::mq(4, 0)] = w * (sq * sf * sg + qf * sg + qg * sf + fg * sq + 2.0 * qfg) * (1.0 / 60.0);
+    sm[X::mq(5, 0)] = w * (sq * sg * sg + 2.0 * qg * sg + gg * sq + 2.0 * qgg) * (1.0 / 60.0);
+  }
+}
+
 template <int KID, bool SQ>
 __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
@@ -1235,6 +1281,46 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
     }
     __syncthreads();
     par ^= 1;
+    double si[C::NSUM];  // the item's sums over its fan sub-triangles
+#pragma unroll
+    for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
+    if ((KID == 2 || KID == 3) && P.path == 0) {
+      // closed-form moments are cheap: each item's lane sums its own fan
+      // sub-triangles in fan order (no block queue and no rounds; the same
+      // arithmetic in the same order as the queued path)
+      nv = S.nv[lane];
+      if (nv >= 3) {
+        n_out0 += m == 0 ? mult : 0;
+        n_out1 += m == 1 ? mult : 0;
+        n_out2 += m == 2;
+        const double* qx = S.px[lane];
+        const double* qy = S.py[lane];
+        const double* tr = S.tri[vs][m == 1];
+        const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
+        const double q0x = qx[0], q0y = qy[0];
+        const double v0 = q0x - o0, v1 = q0y - o1;
+        const double z1 = (v0 * e2y - v1 * e2x) * idet, z2 = (e1x * v1 - e1y * v0) * idet;
+        const double x0 = S.xo[lane][0];
+        int ne = 0;
+#pragma unroll 1
+        for (int t = 1; t < nv - 1; ++t) {
+          const double ax = qx[t] - q0x, ay = qy[t] - q0y;
+          const double bx = qx[t + 1] - q0x, by = qy[t + 1] - q0y;
+          const double jac2 = cross2(ax, by, ay, bx);
+          if (!(jac2 > P.drop2)) continue;
+          const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
+          const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
+          double sm[C::NSUM];
+          closed_moments<KID>(P, q0x, ax, bx, jac2, x0, z1, z2, z1a, z2a, z1b, z2b, sm);
+#pragma unroll
+          for (int i = 0; i < C::NSUM; ++i) si[i] += sm[i];
+          ne += 7;
+        }
+        n_eval0 += m == 0 ? ne * mult : 0;
+        n_eval1 += m == 1 ? ne * mult : 0;
+        n_eval2 += m == 2 ? ne : 0;
+      }
+    } else {
     // ---------------- phase 1c: fan sub-triangles of each item -> block queue
     unsigned mask = 0;
     nv = S.nv[lane];
@@ -1274,9 +1360,6 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
       const int it = ((int)wib << 5) | lane;
       for (unsigned mm = mask; mm; mm &= mm - 1) CQ.sub[pos++] = (unsigned short)((it << 4) | (__ffs(mm) - 1));
     }
-    double si[C::NSUM];  // and their sums
-#pragma unroll
-    for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
     if (g_trace_dev && threadIdx.x == 0) {
       atomicAdd(&O.counters[K_DBG_SUBTRI], (unsigned long long)total);
       atomicAdd(&O.counters[K_DBG_ROUNDS], (unsigned long long)((total + 127) / 128));
@@ -1321,39 +1404,7 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
           if (!(rs2 > 0.0)) {
             closed = true;
             ne = 7;
-            const double w = jac2 * c_rule.iws;
-            const double f[3] = {z1, z1 + z1a, z1 + z1b}, g[3] = {z2, z2 + z2a, z2 + z2b};
-            const double sf = f[0] + f[1] + f[2], sg = g[0] + g[1] + g[2];
-            const double ff = f[0] * f[0] + f[1] * f[1] + f[2] * f[2], gg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
-            const double fg = f[0] * g[0] + f[1] * g[1] + f[2] * g[2];
-            if constexpr (KID == 2) {  // means: (sum)/3, (sum f_i g_i + sum f sum g)/12
-              const double m0 = w * P.cst;
-              sm[X::mp(0, 0)] = m0;
-              sm[X::mp(1, 0)] = m0 * sf * (1.0 / 3.0);
-              sm[X::mp(2, 0)] = m0 * sg * (1.0 / 3.0);
-              sm[X::mq(3, 0)] = m0 * (ff + sf * sf) * (1.0 / 12.0);
-              sm[X::mq(4, 0)] = m0 * (fg + sf * sg) * (1.0 / 12.0);
-              sm[X::mq(5, 0)] = m0 * (gg + sg * sg) * (1.0 / 12.0);
-            } else {
-              const double tp = w * (1.0 + P.kp0 * x0) * P.kp1;
-              sm[X::mp(0, 0)] = tp;
-              sm[X::mp(1, 0)] = tp * sf * (1.0 / 3.0);
-              sm[X::mp(2, 0)] = tp * sg * (1.0 / 3.0);
-              const double Q[3] = {(1.0 + P.kp0 * q0x) * P.kp1, (1.0 + P.kp0 * (q0x + ax)) * P.kp1,
-                                   (1.0 + P.kp0 * (q0x + bx)) * P.kp1};
-              const double sq = Q[0] + Q[1] + Q[2];
-              const double qf = Q[0] * f[0] + Q[1] * f[1] + Q[2] * f[2], qg = Q[0] * g[0] + Q[1] * g[1] + Q[2] * g[2];
-              const double qff = Q[0] * f[0] * f[0] + Q[1] * f[1] * f[1] + Q[2] * f[2] * f[2];
-              const double qfg = Q[0] * f[0] * g[0] + Q[1] * f[1] * g[1] + Q[2] * f[2] * g[2];
-              const double qgg = Q[0] * g[0] * g[0] + Q[1] * g[1] * g[1] + Q[2] * g[2] * g[2];
-              // mean(a b c) = (sa sb sc + (ab) sc + (ac) sb + (bc) sa + 2 (abc)) / 60
-              sm[X::mq(0, 0)] = w * sq * (1.0 / 3.0);
-              sm[X::mq(1, 0)] = w * (qf + sq * sf) * (1.0 / 12.0);
-              sm[X::mq(2, 0)] = w * (qg + sq * sg) * (1.0 / 12.0);
-              sm[X::mq(3, 0)] = w * (sq * sf * sf + 2.0 * qf * sf + ff * sq + 2.0 * qff) * (1.0 / 60.0);
-              sm[X::mq(4, 0)] = w * (sq * sf * sg + qf * sg + qg * sf + fg * sq + 2.0 * qfg) * (1.0 / 60.0);
-              sm[X::mq(5, 0)] = w * (sq * sg * sg + 2.0 * qg * sg + gg * sq + 2.0 * qgg) * (1.0 / 60.0);
-            }
+            closed_moments<KID>(P, q0x, ax, bx, jac2, x0, z1, z2, z1a, z2a, z1b, z2b, sm);
           }
         }
 #pragma unroll 1
@@ -1414,6 +1465,7 @@ __global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(
       __syncthreads();
     }
     __syncthreads();
+    }
     // ---------------- phase 3: fold into both visits, reduce over the record's lanes
     const int pmy = S.pm[lane];
     const bool ivalid = !(pmy & 0x80);
