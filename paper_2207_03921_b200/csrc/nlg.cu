@@ -1108,7 +1108,7 @@ __device__ __forceinline__ void closed_moments(const Params& P, double q0x, doub
 }
 
 template <int KID, bool SQ>
-__global__ void __launch_bounds__(128, KTraits<KID>::NC == 2 ? 5 : 6) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
+__global__ void __launch_bounds__(128, KID == 1 ? 4 : (KID == 0 ? 6 : 5)) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
   using X = SumIdx<KID>;
