@@ -386,7 +386,7 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
 constexpr int kCatClip = 1 << 30;
 
 template <bool FILL>
-__global__ void __launch_bounds__(256, 2) k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
+__global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
                              const unsigned char* __restrict__ needA, const int* __restrict__ inR,
                              int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ comb,
                              int2* __restrict__ ls0, int2* __restrict__ ls1, int2* __restrict__ ls2) {
