@@ -3149,7 +3149,7 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
 template <int NC, int CAP, bool AN>
 cudaError_t launch_rows(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
                         cudaStream_t s) {
-  constexpr int TH = CAP >= 4096 ? 1024 : (CAP >= 2048 ? 512 : (NC == 2 ? 256 : 128));
+  constexpr int TH = CAP >= 4096 ? 1024 : (CAP >= 2048 || NC == 2 ? 512 : 128);
   const int smem = (int)sizeof(RowSmem<NC, CAP, TH>);
   cudaError_t e = cudaFuncSetAttribute(k_row_asm<NC, CAP, TH, AN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
