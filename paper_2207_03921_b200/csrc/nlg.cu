@@ -389,12 +389,14 @@ template <bool FILL>
 __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const int* __restrict__ roots, int nR,
                              const unsigned char* __restrict__ needA, const int* __restrict__ inR,
                              int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ comb,
-                             int2* __restrict__ ls0, int2* __restrict__ ls1, int2* __restrict__ ls2) {
+                             int2* __restrict__ ls0, int2* __restrict__ ls1, int2* __restrict__ ls2,
+                             int stride = 1) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  for (int i = warp; i < nR; i += nwarps) {
+  for (long long i0 = (long long)warp * stride; i0 < nR; i0 += (long long)nwarps * stride) {
+    const int i = (int)i0;
     const int k = roots[i];
     const int4 ek = P.elem[k];
     const double2 ck = P.ctr[k];
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
 // root's memory (bytes), record and COO-slot counts go to its first in-range row
 __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, const int* __restrict__ cnt,
                             double rec_bytes, double store_bytes, double sing_bytes, double root_bytes, double rec_slots,
-                            double sing_slots, unsigned long long* row_cost) {
+                            double sing_slots, unsigned long long* row_cost, double scale = 1.0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nR) return;
   const int4 d = P.dofs[roots[i]];
@@ -511,9 +513,9 @@ __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, con
   const long long sing = (long long)cnt[(long long)C_SID * nR + i] + cnt[(long long)C_SED * nR + i] +
                          cnt[(long long)C_SVX * nR + i];
   unsigned long long* rc = row_cost + 3 * (home - P.row_lo);
-  atomicAdd(&rc[0], (unsigned long long)(rec * rec_bytes + stored * store_bytes + sing * sing_bytes + root_bytes));
-  atomicAdd(&rc[1], (unsigned long long)rec);
-  atomicAdd(&rc[2], (unsigned long long)(rec * rec_slots + sing * sing_slots + 9 * P.nc * P.nc));
+  atomicAdd(&rc[0], (unsigned long long)(scale * (rec * rec_bytes + stored * store_bytes + sing * sing_bytes + root_bytes)));
+  atomicAdd(&rc[1], (unsigned long long)(scale * rec));
+  atomicAdd(&rc[2], (unsigned long long)(scale * (rec * rec_slots + sing * sing_slots + 9 * P.nc * P.nc)));
 }
 
 
@@ -3321,7 +3323,7 @@ struct Timing {
 };
 
 // one row batch: returns NLG_OK and appends to `out`, or asks for a split
-nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget,
+nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget, bool allow_sample,
                      std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
                      unsigned long long* d_counters, unsigned long long* d_err, bool* need_split,
                      std::vector<long long>* cuts) {
@@ -3388,10 +3390,16 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
   CK(cnt.alloc(sizeof(int) * (size_t)kCnt * std::max(nR, 1), s));
   CK(off.alloc(sizeof(long long) * 6 * (size_t)(nR + 1), s));
   const int cand_blocks = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
+  // a first attempt over very many roots counts a 1/16 sample of them: if
+  // the extrapolation does not fit, the cuts are planned from it; if it
+  // does, the exact count follows
+  int stride = allow_sample && nR > (1 << 18) ? 16 : 1;
+count_pass:
+  if (stride > 1) CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (size_t)kCnt * nR, s));
   if (nR) {
     k_candidates<false><<<std::max(cand_blocks, 1), 256, 0, s>>>(
         P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), inR.as<int>(), cnt.as<int>(), nullptr,
-        nullptr, nullptr, nullptr, nullptr);
+        nullptr, nullptr, nullptr, nullptr, stride);
     LAUNCHED();
   }
   {
@@ -3426,6 +3434,8 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       CK(cudaMemcpyAsync(off.as<long long>() + (size_t)q * (nR + 1) + nR, &tot[q], sizeof(long long),
                          cudaMemcpyHostToDevice, s));
     }
+    // (the totals are stored before they are scaled: a sampled count only plans)
+    for (int q = 0; q < 6; ++q) tot[q] *= stride;
   }
   const long long nUB = tot[C_FULL];  // upper bound of full + clipped records
   // records with stored blocks: all, or (analytic full pairs) the clipped ones
@@ -3448,6 +3458,10 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
                             (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 + nUB * 24;
     // 32-bit sizes: records (reverse-index sort) and COO entries must fit
     const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB >= (1LL << 31);
+    if (stride > 1 && !too_big) {  // the sample says it fits: count exactly
+      stride = 1;
+      goto count_pass;
+    }
     if (too_big && row_hi - row_lo <= P.nc) {
       if (coo_ub < (1LL << 31) && nUB < (1LL << 31)) goto fits;  // one vertex's rows: try anyway
       set_err("a single row needs %lld COO slots", coo_ub);
@@ -3467,7 +3481,7 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
       if (nR)
         k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, store_bytes, sing_bytes,
                                                       root_bytes, rows_plan ? 0.0 : kRunFrac * 2 * E, 36.0 * NC * NC,
-                                                      rcost.as<unsigned long long>());
+                                                      rcost.as<unsigned long long>(), (double)stride);
       LAUNCHED();
       std::vector<unsigned long long> hcost((size_t)3 * nrows);
       CK(cudaMemcpyAsync(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, cudaMemcpyDeviceToHost, s));
@@ -4141,7 +4155,8 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     todo.pop_back();
     bool split = false;
     std::vector<long long> cuts;
-    rc = run_batch(pl, rg.first, rg.second, budget, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
+    const bool first_attempt = st.n_batches == 0 && st.n_replans == 0;
+    rc = run_batch(pl, rg.first, rg.second, budget, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
                    derr.as<unsigned long long>(), &split, &cuts);
     if (rc) break;
     if (split) {
