@@ -2467,8 +2467,15 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
     constexpr bool HALF = FAM == 0 && T::SYM;
     const int m4 = R.n / 6;  // points per half sector (identical family: 6 blocks)
     const int npts_eval = HALF ? R.n / 2 : R.n;
+    // (HALF: point ii0 of the evaluated halves is i = (ii0 / m4) 2 m4 + ii0 % m4,
+    // the quotient and remainder tracked incrementally instead of divided)
+    int hq = HALF ? (int)threadIdx.x / m4 : 0, hr = HALF ? (int)threadIdx.x % m4 : 0;
     for (int ii0 = threadIdx.x; ii0 < npts_eval; ii0 += blockDim.x) {
-      const int i = HALF ? (ii0 / m4) * 2 * m4 + (ii0 % m4) : ii0;
+      const int i = HALF ? hq * 2 * m4 + hr : ii0;
+      if (HALF) {
+        hr += blockDim.x;
+        while (hr >= m4) { hr -= m4; ++hq; }
+      }
       const double xs0 = __ldg(&R.xs[2 * i]), xs1 = __ldg(&R.xs[2 * i + 1]);
       const double ys0 = __ldg(&R.ys[2 * i]), ys1 = __ldg(&R.ys[2 * i + 1]);
       const double x0 = __dadd_rn(__dadd_rn(t0x, mul(e1kx, xs0)), mul(e2kx, xs1));
