@@ -137,8 +137,10 @@ def run_reference(args, cfg, ws, rank):
     from oracle import oracle
     oracle.build()
     vals = []
+    # each step a bounded sample; the whole run stays within ~2-3 minutes
+    per_step = min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps))
     for i in range(args.warmup + args.steps):
-        v, sample, dt, epi = cpu_reference(cfg, args.ref_seconds, threads)
+        v, sample, dt, epi = cpu_reference(cfg, per_step, threads)
         if i >= args.warmup:
             vals.append((v, dt))
     value = float(np.mean([v for v, _ in vals]))
