@@ -927,14 +927,18 @@ struct ClipWarp {
   int vk[2], vl[2], fl[2];  // per record slot
   int4 ek[2], el[2];        // element records (vertices, label) of the slot's record
 };
-constexpr int kClipWarps = 4;
+// warps per k_clipped block: the fractional kernel's expensive points want
+// small blocks (6 per SM); the others gain from larger clip / fan queues
+template <int KID> __host__ __device__ constexpr int clip_warps() { return KID == 0 ? 4 : 8; }
+constexpr int kClipWarps = 4;  // (trace statistics only)
 template <int KID>
 struct ClipBlock {  // block-wide work queues
   int n[2];                                 // clip queue length, by chunk parity (reset one chunk ahead)
-  int wtot[kClipWarps];                     // sub-triangles per warp
-  unsigned char item[32 * kClipWarps];      // clip queue: (warp << 5) | lane
-  unsigned short sub[32 * kClipWarps * 7];  // sub-triangle queue: (item << 4) | t, item-major
-  double tile[32 * kClipWarps][ClipCfg<KID>::NSUM + 1];  // one round's sub-triangle sums (padded rows)
+  static constexpr int NW = clip_warps<KID>();
+  int wtot[NW];                             // sub-triangles per warp
+  unsigned char item[32 * NW];              // clip queue: (warp << 5) | lane
+  unsigned short sub[32 * NW * 7];          // sub-triangle queue: (item << 4) | t, item-major
+  double tile[32 * NW][ClipCfg<KID>::NSUM + 1];  // one round's sub-triangle sums (padded rows)
   PowTab tab;                                            // pow_tab tables (fractional kernel)
 };
 
@@ -1110,7 +1114,7 @@ __device__ __forceinline__ void closed_moments(const Params& P, double q0x, doub
 }
 
 template <int KID, bool SQ>
-__global__ void __launch_bounds__(128, KID == 1 ? 4 : (KID == 0 ? 6 : 5)) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
+__global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID == 1 ? 2 : 3)) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
   using X = SumIdx<KID>;
@@ -1118,6 +1122,7 @@ __global__ void __launch_bounds__(128, KID == 1 ? 4 : (KID == 0 ? 6 : 5)) k_clip
   extern __shared__ __align__(16) unsigned char clip_smem[];
   using CW = ClipWarp<KID, SQ>;
   CW* SW = reinterpret_cast<CW*>(clip_smem);
+  constexpr int kClipWarps = clip_warps<KID>();
   ClipBlock<KID>& CQ = *reinterpret_cast<ClipBlock<KID>*>(clip_smem + kClipWarps * sizeof(CW));
   CW& S = SW[threadIdx.x >> 5];
   const int lane = lane_id();
@@ -3005,15 +3010,16 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
   CK(cudaEventRecord(ev_mid, pl->stream));
   if (nP) {
     const long long chunks = (nP + 1) / 2;
-    const unsigned g = (unsigned)std::min<long long>((chunks + 3) / 4, 148LL * 64);
+    constexpr int NWB = clip_warps<KID>();
+    const unsigned g = (unsigned)std::min<long long>((chunks + NWB - 1) / NWB, 148LL * 256 / NWB);
     if (P.ball == 2) {
-      const int smem = kClipWarps * (int)sizeof(ClipWarp<KID, true>) + (int)sizeof(ClipBlock<KID>);
+      const int smem = NWB * (int)sizeof(ClipWarp<KID, true>) + (int)sizeof(ClipBlock<KID>);
       CK(cudaFuncSetAttribute(k_clipped<KID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_clipped<KID, true><<<g, 128, smem, pl->stream>>>(P, lp, O);
+      k_clipped<KID, true><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
     } else {
-      const int smem = kClipWarps * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
+      const int smem = NWB * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
       CK(cudaFuncSetAttribute(k_clipped<KID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_clipped<KID, false><<<g, 128, smem, pl->stream>>>(P, lp, O);
+      k_clipped<KID, false><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
     }
     LAUNCHED();
   }
