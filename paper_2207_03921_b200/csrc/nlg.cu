@@ -929,7 +929,7 @@ struct ClipWarp {
 };
 // warps per k_clipped block: the fractional kernel's expensive points want
 // small blocks (6 per SM); the others gain from larger clip / fan queues
-template <int KID> __host__ __device__ constexpr int clip_warps() { return KID == 0 ? 4 : 8; }
+template <int KID> __host__ __device__ constexpr int clip_warps() { return KID == 0 || KID == 2 ? 4 : 8; }
 constexpr int kClipWarps = 4;  // (trace statistics only)
 template <int KID>
 struct ClipBlock {  // block-wide work queues
@@ -1114,7 +1114,7 @@ __device__ __forceinline__ void closed_moments(const Params& P, double q0x, doub
 }
 
 template <int KID, bool SQ>
-__global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID == 1 ? 2 : 3)) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
+__global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID == 1 ? 2 : (KID == 2 ? 5 : 3))) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
   using X = SumIdx<KID>;
