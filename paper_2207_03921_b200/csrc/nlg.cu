@@ -3712,8 +3712,14 @@ fits:
     if (fb) {  // stage R + sort: the COO with its run buffer (singular slots carried over)
       TRACE("stage W fallback");
       DevBuf k2, v2;
-      CK(k2.alloc(sizeof(unsigned long long) * (r_base + r_cap), s));
-      CK(v2.alloc(sizeof(double) * (r_base + r_cap), s));
+      if (k2.alloc(sizeof(unsigned long long) * (r_base + r_cap), s) != cudaSuccess ||
+          v2.alloc(sizeof(double) * (r_base + r_cap), s) != cudaSuccess) {
+        // the batch was planned for stage W; its stage-R buffer does not fit: split
+        cudaGetLastError();
+        if (row_hi - row_lo > P.nc) { *need_split = true; return NLG_OK; }
+        set_err("stage-R fallback buffer for one row does not fit");
+        return NLG_ERR_CUDA;
+      }
       CK(cudaMemcpyAsync(k2.p, keys.p, (P.narrow ? 4 : 8) * r_base, cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(v2.p, vals.p, sizeof(double) * r_base, cudaMemcpyDeviceToDevice, s));
       std::swap(keys.p, k2.p);
