@@ -284,7 +284,8 @@ def main():
         "phase_ms": {k: float(np.mean([s[k] for s in stats])) for k in
                      ("ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge", "ms_merge_stage_r", "ms_total")},
         "merge_hbm": {"coo_entries": st0["coo_entries"], "coo_reduced": st0["coo_reduced"], "nnz": st0["nnz"]},
-        "batches": {"n": st0["n_batches"], "replans": st0["n_replans"]},
+        "batches": {"n": st0["n_batches"], "replans": st0["n_replans"], "row_retries": st0["n_row_retries"],
+                    "merge_fallbacks": st0["n_merge_fallbacks"]},
     }
     # the merge (stage W) against HBM: algorithmic bytes = the stored record
     # values it reads once (8 B each) + the CSR it writes (12 B per entry);
