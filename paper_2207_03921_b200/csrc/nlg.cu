@@ -1995,8 +1995,11 @@ struct RowOut {
   unsigned long long* used;
   long long* roff;  // per local row: first entry in col / val
   int* rcnt;        // per local row: entries
+  long long* roff2; // per local row: the second run (columns >= the row's dof base, split rows)
+  int* rcnt2;
   int* ovf;         // dof bases whose table overflowed
   unsigned* novf;
+  int split;        // 0: all columns; 1 / 2: only column bases < / >= d (rows too wide for one table)
 };
 
 // Fixed point: t = rint(v 2^S), |t| < 2^80, summed exactly as a 96-bit two's
@@ -2139,6 +2142,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   };
   auto add_fix = [&](unsigned w, int comp, fix_t f, bool pres) {
     if (!pres) return;
+    if (O.split && ((w < (unsigned)d) != (O.split == 1))) return;  // the other half's column
     const int h = slot_of(w);
     if (h < 0) return;
     fix_atomic(S.acc[h][comp], f);
@@ -2314,8 +2318,13 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
       const long long b0 = (long long)atomicAdd(O.used, (unsigned long long)tot);
       S.base[c] = b0;
       const long long lr = NC * d + c - P.row_lo;
-      O.roff[lr] = b0;
-      O.rcnt[lr] = tot;
+      if (O.split == 2) {
+        O.roff2[lr] = b0;
+        O.rcnt2[lr] = tot;
+      } else {
+        O.roff[lr] = b0;
+        O.rcnt[lr] = tot;
+      }
     }
     __syncthreads();
     long long pos = S.base[c] + pre;
@@ -2338,8 +2347,18 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   }
 }
 
+__global__ void k_add_int(int* a, const int* __restrict__ b, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] += b[i];
+}
+__global__ void k_sub_int(int* a, const int* __restrict__ b, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] -= b[i];
+}
+
 // CSR of the batch from the per-row entry runs: one warp per row
 __global__ void k_row_gather(const long long* __restrict__ roff, const int* __restrict__ rcnt,
+                             const long long* __restrict__ roff2, const int* __restrict__ rcnt2,
                              const long long* __restrict__ indptr, long long nrows, const int* __restrict__ col,
                              const double* __restrict__ val, int* indices, double* data) {
   const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -2349,6 +2368,13 @@ __global__ void k_row_gather(const long long* __restrict__ roff, const int* __re
   for (int i = lane_id(); i < n; i += 32) {
     indices[dst + i] = col[src + i];
     data[dst + i] = val[src + i];
+  }
+  // split rows: the columns >= the row's dof base follow (both runs sorted)
+  const long long src2 = roff2[r];
+  const int n2 = rcnt2[r];
+  for (int i = lane_id(); i < n2; i += 32) {
+    indices[dst + n + i] = col[src2 + i];
+    data[dst + n + i] = val[src2 + i];
   }
 }
 
@@ -3251,11 +3277,14 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
                                                                               nrows, P.J, sstart.as<long long>());
   LAUNCHED();
   const long long d_lo = P.row_lo / NC, d_hi = (P.row_hi - 1) / NC + 1, nd = std::max(0LL, d_hi - d_lo);
-  DevBuf col, val, roff, rcnt, ovf0, ovf1, st;
+  DevBuf col, val, roff, rcnt, roff2, rcnt2, ovf0, ovf1, st;
   CK(col.alloc(sizeof(int) * std::max(ent_cap, 1LL), s));
   CK(val.alloc(sizeof(double) * std::max(ent_cap, 1LL), s));
   CK(roff.alloc(sizeof(long long) * std::max(nrows, 1LL), s));
   CK(rcnt.alloc(sizeof(int) * (nrows + 1), s));
+  CK(roff2.alloc(sizeof(long long) * std::max(nrows, 1LL), s));
+  CK(rcnt2.alloc(sizeof(int) * (nrows + 1), s));
+  CK(cudaMemsetAsync(rcnt2.p, 0, sizeof(int) * (nrows + 1), s));
   CK(ovf0.alloc(sizeof(int) * std::max(nd, 1LL), s));
   CK(ovf1.alloc(sizeof(int) * std::max(nd, 1LL), s));
   CK(st.alloc(4 * sizeof(unsigned long long), s));
@@ -3284,6 +3313,9 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   O.novf = (unsigned*)(st.as<unsigned long long>() + 1);
   O.roff = roff.as<long long>();
   O.rcnt = rcnt.as<int>();
+  O.roff2 = roff2.as<long long>();
+  O.rcnt2 = rcnt2.as<int>();
+  O.split = 0;
   const int cap_max = NC == 1 ? 8192 : 2048;
   // first table: the plan's last need, or the column estimate at <= 3/4 load
   int cap = NC == 1 ? 1024 : 512;
@@ -3303,7 +3335,24 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
     if (!hov) break;
     *retries += hov;
     if (4LL * hov > nblk) pl->row_cap = std::min(cap * 2, cap_max);  // most rows need more: start there next time
-    if (cap >= cap_max) { *fallback = true; return NLG_OK; }
+    if (cap >= cap_max) {
+      // rows too wide for the largest table: their columns below / from the
+      // row's own dof base in two passes (two sorted runs per row); a half
+      // that still overflows sends the batch to stage R + sort
+      W.dlist = lists[pass & 1];
+      for (int half = 1; half <= 2; ++half) {
+        O.split = half;
+        O.ovf = lists[(pass + 1) & 1];
+        CK(cudaMemsetAsync(O.novf, 0, sizeof(unsigned), s));
+        CK(launch_rows_cap(P, RI, W, O, hov, cap, s));
+        unsigned long long h2[2] = {0, 0};
+        CK(cudaMemcpyAsync(h2, st.p, sizeof h2, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        used = h2[0];
+        if (h2[1]) { *fallback = true; return NLG_OK; }
+      }
+      break;
+    }
     cap *= 2;
     W.dlist = lists[pass & 1];
     nblk = hov;
@@ -3311,6 +3360,10 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   }
   if ((long long)used > ent_cap) { *need_split = true; return NLG_OK; }
   CK(cudaMallocAsync(&piece.indptr, sizeof(long long) * (nrows + 1), s));
+  if (O.split) {  // split rows: both runs count
+    k_add_int<<<grid_for(nrows + 1, 256), 256, 0, s>>>(rcnt.as<int>(), rcnt2.as<int>(), nrows + 1);
+    LAUNCHED();
+  }
   {
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
@@ -3319,12 +3372,17 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
     CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
     g_launches += 1;
   }
+  if (O.split) {  // the gather needs the first run's own length back
+    k_sub_int<<<grid_for(nrows + 1, 256), 256, 0, s>>>(rcnt.as<int>(), rcnt2.as<int>(), nrows + 1);
+    LAUNCHED();
+  }
   nnz = (long long)used;
   CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
   CK(cudaMallocAsync(&piece.data, sizeof(double) * std::max(nnz, 1LL), s));
   if (nrows) {
-    k_row_gather<<<grid_for(nrows * 32, 256), 256, 0, s>>>(roff.as<long long>(), rcnt.as<int>(), piece.indptr, nrows,
-                                                           col.as<int>(), val.as<double>(), piece.indices, piece.data);
+    k_row_gather<<<grid_for(nrows * 32, 256), 256, 0, s>>>(roff.as<long long>(), rcnt.as<int>(), roff2.as<long long>(),
+                                                           rcnt2.as<int>(), piece.indptr, nrows, col.as<int>(),
+                                                           val.as<double>(), piece.indices, piece.data);
     LAUNCHED();
   }
   piece.nnz = nnz;

@@ -82,6 +82,21 @@ def test_analytic_full_pairs_match_integrated(name):
     _agree(_assemble(c), _assemble(c, {"NLG_NO_ANALYTIC": "1"}), c.matrix)
 
 
+@pytest.mark.parametrize("name", ["cfg1_approxcaps", "lshape16_affine"])
+def test_stage_w_column_split_rows(name):
+    """Rows too wide for the largest table run as two column halves (below /
+    from the row's own dof base): a limit just under the widest rows forces
+    it without any fallback."""
+    c = Case(name)
+    a = _assemble(c, {"NLG_MERGE": "sort"})
+    widest = int(np.diff(a.indptr).max())
+    div = str(8192 // max(1, widest - 4))  # the largest table holds fewer columns than the widest rows
+    st = {}
+    b = _assemble(c, {"NLG_ROW_FILL_DIV": div}, stats=st)
+    assert st["n_merge_fallbacks"] == 0 and st["n_row_retries"] > 0
+    _agree(a, b, c.matrix)
+
+
 def test_stage_w_deterministic_across_table_sizes():
     """Fixed-point sums are exact: the same row summed in a larger table
     (after a retry) gives bitwise the same values."""
