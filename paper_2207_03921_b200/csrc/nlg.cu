@@ -2059,7 +2059,7 @@ struct RowSmem {
   long long base[NC];
 };
 
-template <int NC, int CAP, int TH, bool AN>
+template <int NC, int CAP, int TH, bool AN, bool SPL = false>
 __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, RowOut O) {
   constexpr int NC2 = NC * NC, IT = CAP / TH;
   constexpr int LOG2CAP = CAP == 512 ? 9 : CAP == 1024 ? 10 : CAP == 2048 ? 11 : CAP == 4096 ? 12 : 13;
@@ -2142,7 +2142,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   };
   auto add_fix = [&](unsigned w, int comp, fix_t f, bool pres) {
     if (!pres) return;
-    if (O.split && ((w < (unsigned)d) != (O.split == 1))) return;  // the other half's column
+    if (SPL && ((w < (unsigned)d) != (O.split == 1))) return;  // the other half's column
     const int h = slot_of(w);
     if (h < 0) return;
     fix_atomic(S.acc[h][comp], f);
@@ -3187,16 +3187,25 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
 }
 
 // ---- merge stage W (k_row_asm) for one batch
-template <int NC, int CAP, bool AN>
+template <int NC, int CAP, bool AN, bool SPL = false>
 cudaError_t launch_rows(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
                         cudaStream_t s) {
   constexpr int TH = CAP >= 4096 ? 1024 : (CAP >= 2048 || NC == 2 ? 512 : 128);
   const int smem = (int)sizeof(RowSmem<NC, CAP, TH>);
-  cudaError_t e = cudaFuncSetAttribute(k_row_asm<NC, CAP, TH, AN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(k_row_asm<NC, CAP, TH, AN, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  if (nblk) k_row_asm<NC, CAP, TH, AN><<<(unsigned)nblk, TH, smem, s>>>(P, I, W, O);
+  if (nblk) k_row_asm<NC, CAP, TH, AN, SPL><<<(unsigned)nblk, TH, smem, s>>>(P, I, W, O);
   g_launches += 1;
   return cudaGetLastError();
+}
+
+// the column-half passes of rows wider than the largest table
+cudaError_t launch_rows_split(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
+                              cudaStream_t s) {
+  if (P.nc == 2) return launch_rows<2, 2048, false, true>(P, I, W, O, nblk, s);
+  if (P.analytic) return launch_rows<1, 8192, true, true>(P, I, W, O, nblk, s);
+  return launch_rows<1, 8192, false, true>(P, I, W, O, nblk, s);
 }
 
 cudaError_t launch_rows_cap(const Params& P, const RootIn& I, const RowIn& W, const RowOut& O, long long nblk,
@@ -3344,7 +3353,7 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
         O.split = half;
         O.ovf = lists[(pass + 1) & 1];
         CK(cudaMemsetAsync(O.novf, 0, sizeof(unsigned), s));
-        CK(launch_rows_cap(P, RI, W, O, hov, cap, s));
+        CK(launch_rows_split(P, RI, W, O, hov, s));
         unsigned long long h2[2] = {0, 0};
         CK(cudaMemcpyAsync(h2, st.p, sizeof h2, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
