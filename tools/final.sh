@@ -1,5 +1,5 @@
 # final round evidence: tests, smoke, bench lines of all configs, reference arm, launch list, ncu of the dominant kernel
-T=r01j
+T=r01k
 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/gputests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/gputests.log
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 timeout 600 python bench.py > gpurun_out/default.json 2> gpurun_out/default.err; echo "default rc=$?"; python tools/show.py gpurun_out/default.json 2>/dev/null | head -2
