@@ -1,15 +1,19 @@
 """Benchmark: full nonlocal stiffness assembly (fp64) on B200 vs the CPU path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+    python bench.py --config 4 --emulate-shards 8     # config 4 on one GPU, rank by rank
 
-A step is one complete assembly of BASELINE config C (default 2: N=128,
-fractional s=0.4, approxcaps, singular path) from mesh
-arrays resident in HBM to the CSR resident in HBM: element bounds, grid
-hash, candidate search, pair integration, touching-pair tensor rules, sort
-and segmented reduction.  ``value`` = evaluated element-pair integrals
-(EPI) / second over the whole job.  ``e2e`` repeats the step
-through the public drop-in API ``bfs_assemble`` with host numpy inputs and
-a host scipy CSR out (H2D and D2H inside the timed region).
+A step is one complete assembly of BASELINE config C from mesh arrays
+resident in HBM to the CSR resident in HBM: element bounds, grid hash,
+candidate search, pair integration, touching-pair tensor rules and the row
+merge into CSR.  The default is config 5 (the N=512 jittered L-shape with
+the nonsymmetric kernel, 4.87e9 EPI): the largest configuration whose CSR
+fits one GPU (config 4's ~266 GB CSR does not; ``--emulate-shards 8`` times
+its eight row shards one after the other on one GPU instead).  ``value`` =
+evaluated element-pair integrals (EPI) / second over the whole
+job.  ``e2e`` repeats the step through the public drop-in API
+``bfs_assemble`` with host numpy inputs and a host scipy CSR out (H2D and
+D2H inside the timed region).
 
 Under torchrun each rank owns a contiguous CSR row range (owner computes;
 no collective on the data path) and the time is the max over ranks.
@@ -105,12 +109,24 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_reference(cfg, budget_s, threads):
+def cpu_path_label(cfg, kernel=None):
+    """What the CPU oracle restates for this config's kernel (the reference's
+    own path for it)."""
+    kid = int((kernel or cfg.kernel).builtin_id)
+    if kid == 3:
+        return ("C restatement (oracle/, bit-identical) of the reference's interpreted engine "
+                "(_pyengine, the only reference path for the nonsymmetric kernel) + _merge_triplets")
+    return "C restatement (oracle/, bit-identical) of the reference's numba engine (_engine._chunk) + _merge_triplets"
+
+
+def cpu_reference(cfg, budget_s, threads, kernel=None):
     """The reference algorithm (oracle port, bit-identical) on a bounded band
-    of outer elements: returns EPI/s, the sample description and seconds."""
+    of outer elements: returns EPI/s, the sample description and seconds.
+    ``kernel`` replaces the config's kernel (the symmetric-constant proxy of
+    config 5)."""
     from oracle import oracle
     from paper_2207_03921_b200.problem import marshal
-    inp = marshal(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
+    inp = marshal(cfg.mesh, cfg.adjacency, kernel or cfg.kernel, cfg.ansatz, cfg.quad)
     op = oracle.OracleProblem(inp, cfg.adjacency)
     K = cfg.mesh.n_elements
     mid = K // 2
@@ -128,6 +144,23 @@ def cpu_reference(cfg, budget_s, threads):
     r = op.run(*op.spans(lo, min(K, lo + n2)), nthreads=threads)
     dt = time.perf_counter() - t0
     return r["epi"] / dt, f"outer elements [{lo}, {lo + n2}) of {K} (64-root spans, BFS, merge)", dt, r["epi"]
+
+
+def cpu_baselines(cfg, budget_s, threads):
+    """cpu_baseline of the line: the reference's path for the config's kernel
+    on a bounded sample; config 5 adds the compiled-engine proxy (symmetric
+    constant kernel on the same mesh), both labelled."""
+    v, sample, dt, _ = cpu_reference(cfg, budget_s, threads)
+    out = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample, "seconds": dt,
+           "path": cpu_path_label(cfg), "cpu_model": cpu_model()}
+    if int(cfg.kernel.builtin_id) == 3:
+        from paper_2207_03921_b200.kernels import constant_kernel
+        proxy = constant_kernel(cfg.kernel.delta, cfg.kernel.ball)
+        pv, psample, pdt, _ = cpu_reference(cfg, budget_s / 2, threads, kernel=proxy)
+        out["proxy"] = {"value": pv, "unit": UNIT, "cores": threads, "sample": psample, "seconds": pdt,
+                        "path": cpu_path_label(cfg, proxy) + "; symmetric constant kernel (id 2) on the same mesh",
+                        "note": "the reference's compiled engine cannot evaluate the nonsymmetric kernel"}
+    return out
 
 
 def run_reference(args, cfg, ws, rank):
@@ -151,26 +184,41 @@ def run_reference(args, cfg, ws, rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded mesh)",
         "config": {**cfg.describe(), "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "path": cpu_path_label(cfg), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 
-_KERNEL_OF_PHASE = {"pair_full": "k_full", "pair_clipped": "k_clipped", "touching_singular": "k_singular"}
+def merge_alg_bytes(cfg, inp, st):
+    """Algorithmic HBM bytes of the merge (stage W, k_row_asm) per assembly:
+    every stored record-side block read once (own block NKK + neighbour block
+    9 nc^2 values of 8 B: 6 + 9 = 15 for nc = 1), the touching-pair COO
+    (16 B per slot), the record lists (8 B per record), the per-element
+    tables once (element, dofs, analytic factors: 64 B per element) and the
+    CSR written (int32 column + f64 value per entry, int64 row pointers)."""
+    nc = inp.nc
+    nkk, nkl = 3 * nc * (3 * nc + 1) // 2, 9 * nc * nc
+    analytic = inp.kernel_id in (2, 3) and inp.path_touch == 0 and nc == 1
+    stored = st["n_partial"] + (0 if analytic else st["n_full"])
+    blocks = 2 * stored * (nkk + nkl) * 8
+    sing = st["n_singular"] * 36 * nc * nc * 16
+    lists = (st["n_full"] + st["n_partial"]) * 8
+    tables = inp.elements.shape[0] * 64
+    csr = st["nnz"] * 12 + (inp.n_dofs + 1) * 8
+    return {"stored_blocks": blocks, "singular_coo": sing, "record_lists": lists, "element_tables": tables,
+            "csr_out": csr, "total": float(blocks + sing + lists + tables + csr)}
 
 
-def _ncu_traffic(phase, config):
-    """DRAM bytes (read + write) per launch of the dominant kernel, from the
-    newest committed `ncu --set full` summary of config 2 (profiles/); None
-    for other configs or when no summary exists."""
+def _ncu_traffic(kernel, config):
+    """DRAM bytes (read + write) per launch of ``kernel`` from the newest
+    committed `ncu --set full` summary of this config (profiles/
+    r*_<kernel>_cfg<C>_ncu_summary.txt); (None, None) when none exists."""
     import glob
     import re
-    if config != 2:
-        return None, None
-    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                          f"r*_{_KERNEL_OF_PHASE[phase]}_ncu_summary.txt")))
+    here = os.path.dirname(os.path.abspath(__file__))
+    files = sorted(glob.glob(os.path.join(here, "profiles", f"r*_{kernel}_cfg{config}_ncu_summary.txt")))
     if not files:
         return None, None
     txt = open(files[-1]).read()
@@ -181,18 +229,96 @@ def _ncu_traffic(phase, config):
         if not m:
             return None, None
         total += float(m.group(1)) * scale.get(m.group(2), 1)
-    return total, os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))
+    return total, os.path.relpath(files[-1], here)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_emulated_shards(args, cfg):
+    """Every rank's row shard of the config, one after the other on this GPU
+    (owner computes: each shard evaluates the outer elements reaching its
+    rows, no collective).  T1 = sum of the shard times is the full 1-GPU
+    assembly (streamed by shard; config 4's whole CSR does not fit one GPU),
+    max_r T_r the W-GPU time.  Each shard's CSR gets a device checksum."""
+    import torch
+    from paper_2207_03921_b200 import _native, shard
+    from paper_2207_03921_b200.assembly import DevicePlan
+    from paper_2207_03921_b200.problem import marshal
+    torch.cuda.set_device(0)
+    inp = marshal(cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
+    W = args.emulate_shards
+    plan = DevicePlan(inp, device=0, on_device=True)
+    weights = shard.row_weights(plan, cfg.mesh, cfg.ansatz)
+    cuts = shard.row_partition(inp.n_dofs, inp.nc, W, weights)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda:0")
+    launches0 = _native.launch_count()
+    shards = []
+    with ClockSampler(0) as clk:
+        for r in range(W):
+            lo, hi = cuts[r], cuts[r + 1]
+            for _ in range(args.warmup if r == 0 else 1):
+                plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
+            times, epi = [], 0
+            for i in range(args.steps):
+                flush.fill_(float(i))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                ip, ix, dv, st = plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+                epi = st["epi"]
+            nnz = int(st["nnz"])
+            chk = {"nnz": nnz, "sum_data": float(dv[:nnz].sum().item()),
+                   "sum_abs_data": float(dv[:nnz].abs().sum().item()),
+                   "sum_indices": int(ix[:nnz].to(torch.int64).sum().item())}
+            shards.append({"rank": r, "rows": [lo, hi], "ms": float(np.mean(times)), "epi": int(epi),
+                           "batches": st["n_batches"], "checksum": chk,
+                           "phase_ms": {k: st[k] for k in ("ms_candidates", "ms_partial", "ms_merge")}})
+            print(json.dumps({"shard": shards[-1]}), file=sys.stderr, flush=True)
+    t1 = sum(x["ms"] for x in shards)
+    tmax = max(x["ms"] for x in shards)
+    epi = sum(x["epi"] for x in shards)
+    line = {
+        "metric": METRIC, "value": epi / (t1 * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t1, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded mesh, SURVEY.md App. A)",
+        "config": {**cfg.describe(), "epi": epi, "rows": "all, as %d row shards run one after the other" % W,
+                   "parallelism": f"{W} emulated row shards on 1 GPU", "l2": "flushed between steps (512 MB write)",
+                   "inputs": "mesh arrays resident in HBM", "output": "each shard's CSR resident in HBM in turn"},
+        "assembly_ms": t1,
+        "projected": {"n_gpus": W, "max_rank_ms": tmax, "efficiency": t1 / (W * tmax),
+                      "note": "T1 / (W max_r T_r): per-rank work measured on one GPU; no collective on the data path"},
+        "shards": shards, "gpu_launches": int(_native.launch_count() - launches0), "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    plan.close()
+
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--emulate-shards", type=int, default=0, metavar="W",
+                    help="single GPU: time the row shards of all W ranks one after the other (config 4: the "
+                         "1-GPU full-assembly time T1 = their sum, and the projected W-GPU efficiency "
+                         "T1 / (W max_r T_r))")
     ap.add_argument("--emulate-shard", default=None, metavar="R/W",
                     help="single GPU: time only the rows rank R of W would own (a per-rank projection "
                          "for meshes whose CSR does not fit one GPU, e.g. config 4)")
@@ -203,6 +329,9 @@ def main():
     cfg = configs.build(args.config)
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)
+        return
+    if args.emulate_shards:
+        run_emulated_shards(args, cfg)
         return
 
     import torch
@@ -222,8 +351,9 @@ def main():
     srank, sws = rank, ws
     if args.emulate_shard and ws == 1:
         srank, sws = (int(x) for x in args.emulate_shard.split("/"))
-    lo, hi = shard.my_rows(J, inp.nc, srank, sws, shard.vertex_work(cfg.mesh, cfg.ansatz))
     plan = DevicePlan(inp, device=local, on_device=True)  # mesh arrays resident in HBM
+    # rows balanced by EPI prefix sums, from the device's count pass
+    lo, hi = (0, J) if sws == 1 else shard.my_rows(J, inp.nc, srank, sws, shard.row_weights(plan))
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")  # > 126 MB L2
 
     def barrier():
@@ -262,43 +392,45 @@ def main():
     ms_per_step = t_total / args.steps
     value = epi_total / (ms_per_step * 1e-3)
 
-    # ---- roofline of the dominant integration kernel (live CUDA-event phase times)
+    # ---- roofline: every timed phase against its bound; the top-level line
+    # is the dominant (longest) phase's kernel
     st0 = stats[-1]
-    phases = {"pair_full": ("ms_full", "alg_flops_full"), "pair_clipped": ("ms_partial", "alg_flops_partial"),
-              "touching_singular": ("ms_singular", "alg_flops_singular")}
-    avg = {k: float(np.mean([s[v[0]] for s in stats])) for k, v in phases.items()}
-    dom = max(avg, key=avg.get)
+    phase_avg = {k: float(np.mean([s[k] for s in stats])) for k in
+                 ("ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge", "ms_merge_stage_r",
+                  "ms_total")}
     peak_fp64 = _native.fp64_peak_tflops(local)
-    dom_ms = avg[dom]
-    dom_flops = st0[phases[dom][1]]
-    achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
-    integ_ms = float(np.mean([s["ms_integrate_kernels"] for s in stats]))
-    traffic, traffic_src = _ncu_traffic(dom, args.config)
+    hbm_peak = _peaks().get("hbm_gbs")
+    phases = {}
+    for name, ms_key, fl_key in (("k_full", "ms_full", "alg_flops_full"), ("k_clipped", "ms_partial", "alg_flops_partial"),
+                                 ("k_singular", "ms_singular", "alg_flops_singular")):
+        ms = phase_avg[ms_key]
+        ach = st0[fl_key] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+        phases[name] = {"bound": "fp64", "ms": ms, "alg_flops": st0[fl_key], "achieved": ach, "peak": peak_fp64,
+                        "unit": "TFLOP/s", "frac": ach / peak_fp64 if peak_fp64 else None}
+    mb = merge_alg_bytes(cfg, inp, st0)
+    ms = phase_avg["ms_merge"]
+    phases["k_row_asm"] = {"bound": "hbm", "ms": ms, "alg_bytes": mb["total"], "bytes_model": mb,
+                           "achieved": mb["total"] / (ms * 1e-3) / 1e9 if ms else None, "peak": hbm_peak,
+                           "unit": "GB/s", "frac": (mb["total"] / (ms * 1e-3) / 1e9) / hbm_peak if (ms and hbm_peak) else None}
+    phases["k_candidates"] = {"bound": "l2/latency", "ms": phase_avg["ms_candidates"],
+                              "note": "grid scan + exact reject/full/truncation-class tests per candidate (two passes)"}
+    dom = max(phases, key=lambda k: phases[k]["ms"])
+    top = phases[dom] if phases[dom].get("frac") is not None else phases["k_clipped"]
+    dom_name = dom if phases[dom].get("frac") is not None else "k_clipped"
+    traffic, traffic_src = _ncu_traffic(dom_name, args.config)
     roofline = {
-        "bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
-        "frac": achieved / peak_fp64 if peak_fp64 else None, "traffic": traffic, "traffic_source": traffic_src,
-        "peak_source": "measured DFMA microbenchmark (nlg_fp64_peak) on this GPU, this run",
-        "alg_flops_per_launch": dom_flops, "kernel_ms": dom_ms,
-        "all_integration": {"alg_flops": st0["alg_flops"], "ms": integ_ms,
-                            "tflops": st0["alg_flops"] / (integ_ms * 1e-3) / 1e12 if integ_ms else 0.0},
-        "phase_ms": {k: float(np.mean([s[k] for s in stats])) for k in
-                     ("ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge", "ms_merge_stage_r", "ms_total")},
-        "merge_hbm": {"coo_entries": st0["coo_entries"], "coo_reduced": st0["coo_reduced"], "nnz": st0["nnz"]},
+        "bound": top["bound"], "kernel": dom_name, "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
+        "frac": top["frac"], "traffic": traffic, "traffic_source": traffic_src,
+        "peak_source": ("measured DFMA microbenchmark (nlg_fp64_peak) on this GPU, this run" if top["bound"] == "fp64"
+                        else "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"),
+        "kernel_ms": top["ms"], "share_of_step": top["ms"] / ms_per_step if ms_per_step else None,
+        "dominant_phase": dom,
+        "phases": phases,
+        "all_integration": {"alg_flops": st0["alg_flops"], "ms": float(np.mean([s["ms_integrate_kernels"] for s in stats])),
+                            "note": "reference-algorithmic flops (SURVEY 8d) of all integration kernels"},
+        "phase_ms": phase_avg,
         "batches": {"n": st0["n_batches"], "replans": st0["n_replans"], "row_retries": st0["n_row_retries"],
                     "merge_fallbacks": st0["n_merge_fallbacks"]},
-    }
-    # the merge (stage W) against HBM: algorithmic bytes = the stored record
-    # values it reads once (8 B each) + the CSR it writes (12 B per entry);
-    # analytic full pairs read only per-element factors (L2-resident)
-    merge_ms = float(np.mean([s["ms_merge"] for s in stats]))
-    merge_bytes = 8.0 * st0["coo_entries"] + 12.0 * st0["nnz"]
-    hbm_peak = _peaks().get("hbm_gbs")
-    roofline["merge"] = {
-        "bound": "hbm", "alg_bytes": merge_bytes, "ms": merge_ms,
-        "achieved_gbs": merge_bytes / (merge_ms * 1e-3) / 1e9 if merge_ms else None,
-        "peak_gbs": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if hbm_peak else None,
-        "frac": (merge_bytes / (merge_ms * 1e-3) / 1e9) / hbm_peak if (merge_ms and hbm_peak) else None,
-        "note": "shared-memory atomic / latency bound (stage W hash tables), not HBM bound",
     }
 
     # ---- end to end through the public API (host numpy in, host scipy CSR out)
@@ -326,10 +458,7 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        threads = len(os.sched_getaffinity(0))
-        v, sample, dt, _ = cpu_reference(cfg, args.ref_seconds, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
-               "seconds": dt}
+        cpu = cpu_baselines(cfg, args.ref_seconds, len(os.sched_getaffinity(0)))
 
     if rank == 0:
         line = {

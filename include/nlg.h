@@ -45,7 +45,7 @@ typedef int32_t nlg_status;
 #define NLG_ERR_NUMERICAL 2 /* maps to NumericalError (nonfinite local contribution) */
 #define NLG_ERR_CUDA 3      /* launch / runtime failure, no device, OOM */
 
-#define NLG_ABI_VERSION 3
+#define NLG_ABI_VERSION 4
 
 /* Kernel ids (kernels.py :57-118 built-ins + 3 = nonsymmetric affine). */
 #define NLG_KERNEL_FRACTIONAL 0  /* c |x-y|^(-2-2s) */
@@ -101,6 +101,7 @@ typedef struct nlg_stats {
   double ms_merge_stage_r;     /* per-root reduction part of ms_merge */
   int64_t n_row_retries;       /* stage-W rows re-run in a larger table */
   int64_t n_merge_fallbacks;   /* batches merged by stage R + sort instead of stage W */
+  int64_t err_self_k;          /* smallest root whose own (k, k) visit was nonfinite, or -1 */
 } nlg_stats;
 
 int32_t nlg_abi_version(void);
@@ -155,8 +156,20 @@ nlg_status nlg_mass(nlg_plan *plan, int32_t out_on_host, nlg_alloc_fn alloc, voi
 nlg_status nlg_cg(int32_t device, int64_t n, const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *b, double *x, double rtol, int32_t maxit, int32_t *iters, double *relres);
 
+/* Work estimate per dof base for balancing row shards across GPUs: for
+ * every dof base, the summed EPI (visits passing the reject test) of the
+ * outer elements incident to it, from the device's candidate count pass;
+ * written to the host array work[n_dofs / nc].  Deterministic (integer sums). */
+nlg_status nlg_row_work(nlg_plan *plan, int64_t *work);
+
 /* DFMA throughput microbenchmark on `device` (the FP64 roofline denominator). */
 nlg_status nlg_fp64_peak(int32_t device, double *tflops);
+
+/* Row ranges of the batches the last nlg_assemble on this plan ran, in row
+ * order: writes min(n, cap) pairs (lo, hi) into ranges[2 * cap] and returns
+ * n (the batch count), or -1 for a null plan.  Diagnostics / tests: parity at
+ * the batch cuts, where each batch re-evaluates its halo roots. */
+int64_t nlg_last_batches(const nlg_plan *plan, int64_t *ranges, int64_t cap);
 
 /* Number of kernels this library launched on the calling process so far. */
 int64_t nlg_launch_count(void);

@@ -91,6 +91,8 @@ def lib():
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
         L.orc_clip_square.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_count_visits.argtypes = [ctypes.POINTER(_Prob), ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                       ctypes.c_void_p]
         L.orc_assemble_load.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 4 + [
             ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 5
         _lib = L
@@ -195,6 +197,15 @@ class OracleProblem:
             return out
         finally:
             L.orc_result_free(res)
+
+    def count_visits(self, k0=0, k1=None, nthreads=0):
+        """Per-root EPI (visits passing _visit_pair's reject test, the
+        reference's brute traversal) of the roots [k0, k1); 0 for non-outer."""
+        K = self.inp.elements.shape[0]
+        k1 = K if k1 is None else k1
+        vis = np.zeros(max(k1 - k0, 1), dtype=np.int64)
+        lib().orc_count_visits(ctypes.byref(self.pb), int(k0), int(k1), int(nthreads), _p(vis))
+        return vis[:k1 - k0]
 
     def matrix(self, **kw):
         r = self.run(**kw)

@@ -50,7 +50,7 @@ class Stats(ctypes.Structure):
         (n, ctypes.c_double) for n in (
             "ms_prep", "ms_candidates", "ms_full", "ms_partial", "ms_singular", "ms_merge",
             "ms_total", "ms_integrate_kernels", "ms_merge_stage_r")] + [
-        (n, ctypes.c_int64) for n in ("n_row_retries", "n_merge_fallbacks")]
+        (n, ctypes.c_int64) for n in ("n_row_retries", "n_merge_fallbacks", "err_self_k")]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -78,8 +78,10 @@ SIGNATURES = {
     "nlg_cg": (ctypes.c_int32, [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]),
+    "nlg_row_work": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_void_p]),
     "nlg_fp64_peak": (ctypes.c_int32, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "nlg_launch_count": (ctypes.c_int64, []),
+    "nlg_last_batches": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]),
     "nlg_format_f64": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                         ctypes.c_int32]),
     "nlg_format_i64": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,

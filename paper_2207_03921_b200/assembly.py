@@ -26,7 +26,7 @@ import numpy as np
 from scipy import sparse
 
 from . import _native
-from .errors import ConfigurationError, DeviceError
+from .errors import ConfigurationError, DeviceError, NumericalError
 from .mesh import Label
 from .problem import AssemblyInputs, marshal, quad_arrays
 from .quadrature import QuadratureConfig
@@ -154,7 +154,8 @@ class DevicePlan:
     def __del__(self):
         self.close()
 
-    def assemble(self, row_lo=0, row_hi=None, out_on_host=True, mem_budget=0, reuse_output=False):
+    def assemble(self, row_lo=0, row_hi=None, out_on_host=True, mem_budget=0, reuse_output=False,
+                 traversal="brute"):
         """CSR rows [row_lo, row_hi): (indptr int64, indices int32, data f64, stats dict).
 
         ``reuse_output`` (device outputs only) recycles the previous call's
@@ -173,10 +174,33 @@ class DevicePlan:
         st = _native.Stats()
         rc = self.lib.nlg_assemble(self.handle, int(row_lo), int(row_hi), 1 if out_on_host else 0,
                                    sink.callback, None, int(mem_budget), ctypes.byref(st))
+        if rc == _native.NLG_ERR_NUMERICAL and st.err_k >= 0:
+            # the reference raises for the first failing visit of its smallest
+            # failing root (spans in order, assembly.py:285-288): partners
+            # ascending under "brute"; under "bfs" the root's own pair is
+            # visited first (_engine.py:545-560)
+            k, l = int(st.err_k), int(st.err_l)
+            if traversal == "bfs" and st.err_self_k == k:
+                l = k
+            raise NumericalError(f"nonfinite local contribution for element pair ({k}, {l})")
         _native.check(rc, "nlg_assemble")
         nnz = st.nnz
         return (sink.array(0, np.int64, row_hi - row_lo + 1), sink.array(1, np.int32, nnz),
                 sink.array(2, np.float64, nnz), st.as_dict())
+
+    def row_work(self):
+        """Per-dof-base EPI of the incident outer elements (int64[J / nc]):
+        the weights of the EPI-balanced shard partition (shard.row_weights)."""
+        w = np.zeros(max(self.inp.n_dofs // self.inp.nc, 1), dtype=np.int64)
+        _native.check(self.lib.nlg_row_work(self.handle, _ptr(w)), "nlg_row_work")
+        return w[:self.inp.n_dofs // self.inp.nc]
+
+    def last_batches(self):
+        """Row ranges [(lo, hi), ...] of the batches the last assemble() ran."""
+        n = int(self.lib.nlg_last_batches(self.handle, None, 0))
+        buf = np.zeros(2 * max(n, 1), dtype=np.int64)
+        self.lib.nlg_last_batches(self.handle, _ptr(buf), n)
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n)]
 
     def load_points(self):
         sink = _native.OutputSink(True, self.device)
@@ -241,7 +265,8 @@ def bfs_assemble(mesh, adjacency, kernel, ansatz, quad=None, n_threads=1, rows="
     lo, hi = (0, J) if row_range is None else (int(row_range[0]), int(row_range[1]))
     plan = DevicePlan(inp, device=device)
     try:
-        indptr, indices, data, st = plan.assemble(lo, hi, out_on_host=True, mem_budget=mem_budget)
+        indptr, indices, data, st = plan.assemble(lo, hi, out_on_host=True, mem_budget=mem_budget,
+                                                  traversal=traversal)
     finally:
         plan.close()
     if stats is not None:

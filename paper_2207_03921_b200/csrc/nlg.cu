@@ -519,6 +519,18 @@ __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, con
 }
 
 
+// per dof base: the EPI of every outer root incident to it (shard balancing)
+__global__ void k_base_work(Params P, const int* __restrict__ roots, int nR, const int* __restrict__ cnt,
+                            unsigned long long* work) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nR) return;
+  const int4 d = P.dofs[roots[i]];
+  const unsigned long long e = (unsigned long long)cnt[(long long)C_EPI * nR + i];
+  atomicAdd(&work[d.x], e);
+  atomicAdd(&work[d.y], e);
+  atomicAdd(&work[d.z], e);
+}
+
 // sum of the visits (EPI) and count of the roots whose home row is in the batch
 __global__ void k_epi_home(const int* __restrict__ cnt, int nR, unsigned long long* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -614,8 +626,16 @@ __device__ __forceinline__ double emit_val(double v) { return v != 0.0 ? v : 0.0
 __device__ __forceinline__ bool nonfinite(double v) {
   return ((unsigned long long)__double_as_longlong(v) & 0x7ff0000000000000ull) == 0x7ff0000000000000ull;
 }
+// errpair[0]: lexicographically smallest (root, partner) -- the reference's
+// first failing visit under "brute" traversal (roots ascending, partners
+// ascending, _engine.py:483-490); errpair[1]: smallest root whose visit of
+// itself failed -- under "bfs" the root's own pair is its first visit
+// (_engine.py:545-560), so the host reports (k, k) when k == errpair[1]
 __device__ __forceinline__ void report_nonfinite(bool bad, int k, int l, int K, unsigned long long* errpair) {
-  if (bad) atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
+  if (bad) {
+    atomicMin(errpair, (unsigned long long)k * (unsigned long long)K + l);
+    if (k == l) atomicMin(errpair + 1, (unsigned long long)k);
+  }
 }
 
 
@@ -2817,6 +2837,7 @@ struct nlg_plan {
   int row_cap = 0;  // stage-W table size the last batches needed (start there)
   bool use_rows = true;  // merge stage W (NLG_MERGE=sort: stage R + global sort)
   size_t arena_used = 0;  // virtual bump offset into the device arena during a call
+  std::vector<long long> last_batches;  // row ranges (lo, hi) of the last nlg_assemble's batches
 };
 
 namespace {
@@ -3994,6 +4015,16 @@ int32_t nlg_abi_version(void) { return NLG_ABI_VERSION; }
 const char* nlg_last_error(void) { return g_err.c_str(); }
 int64_t nlg_launch_count(void) { return g_launches.load(); }
 
+int64_t nlg_last_batches(const nlg_plan* pl, int64_t* ranges, int64_t cap) {
+  if (!pl) return -1;
+  const int64_t n = (int64_t)pl->last_batches.size() / 2;
+  for (int64_t i = 0; i < std::min(n, cap); ++i) {
+    ranges[2 * i] = pl->last_batches[2 * i];
+    ranges[2 * i + 1] = pl->last_batches[2 * i + 1];
+  }
+  return n;
+}
+
 nlg_status nlg_device_count(int32_t* count) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -4052,7 +4083,10 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   P.J = pb->n_dofs;
   P.dbg = getenv("NLG_DEBUG") ? atoi(getenv("NLG_DEBUG")) : 0;
   // NLG_NO_ANALYTIC: integrate the full pairs of kid 2 / 3 per record (A/B and tests)
-  P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC");
+  // (nonfinite kernel parameters: every pair is integrated per record, so the
+  // failing visit is detected and named -- the analytic sums carry no check)
+  P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC") &&
+               std::isfinite(P.cst) && std::isfinite(P.kp0) && std::isfinite(P.kp1);
   pl->use_rows = !(getenv("NLG_MERGE") && !strcmp(getenv("NLG_MERGE"), "sort"));
   Rule7 hr;
   for (int p = 0; p < 7; ++p) {
@@ -4227,9 +4261,9 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   CK(cudaEventRecord(e1, s));
   DevBuf dctr, derr;
   CK(dctr.alloc(sizeof(unsigned long long) * K_NCOUNTERS, s));
-  CK(derr.alloc(sizeof(unsigned long long), s));
+  CK(derr.alloc(2 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(dctr.p, 0, sizeof(unsigned long long) * K_NCOUNTERS, s));
-  CK(cudaMemsetAsync(derr.p, 0xff, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(derr.p, 0xff, 2 * sizeof(unsigned long long), s));
   std::vector<Csr> pieces;
   Counters ctr{};
   Timing tm;
@@ -4265,14 +4299,21 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     return rc;
   }
   TRACE("batches done");
+  pl->last_batches.clear();
+  for (const Csr& c : pieces) {
+    pl->last_batches.push_back(c.row_lo);
+    pl->last_batches.push_back(c.row_hi);
+  }
   // pieces are produced in ascending row order (ranges are popped low-first)
   long long nnz = 0;
   rc = emit_pieces(pl, ds, pieces, row_lo, row_hi, out_on_host, alloc, user, e2, &nnz);
   if (rc) return rc;
-  unsigned long long hc[K_NCOUNTERS], herr;
+  unsigned long long hc[K_NCOUNTERS], herr, herr2[2];
   CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&herr, derr.p, sizeof herr, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(herr2, derr.p, sizeof herr2, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  herr = herr2[0];
+  st.err_self_k = herr2[1] == ~0ull ? -1 : (long long)herr2[1];
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   st.ms_prep = ms;
@@ -4477,6 +4518,66 @@ nlg_status nlg_mass(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc, void*
   }
   long long nnz = 0;
   return emit_pieces(pl, ds, pieces, 0, P.J, out_on_host, alloc, user, nullptr, &nnz);
+}
+
+nlg_status nlg_row_work(nlg_plan* pl, int64_t* work) {
+  if (!pl || !work) { set_err("null plan or output"); return NLG_ERR_CONFIG; }
+  CK(cudaSetDevice(pl->device));
+  DeviceScratch& ds = g_scratch[pl->device];
+  std::lock_guard<std::mutex> scratch_lock(ds.mu);
+  pl->arena_used = 0;
+  cudaStream_t s = pl->stream;
+  pl->prepped = false;
+  if (nlg_status rc = prep(pl)) return rc;
+  Params P = pl->P;
+  P.row_lo = 0;
+  P.row_hi = P.J;
+  const int K = P.K;
+  const long long nb = P.J / P.nc;
+  DevBuf needA, rflag, roots, nroots, inR, idx, cnt, wk;
+  CK(needA.alloc(K, s));
+  CK(rflag.alloc(sizeof(int) * K, s));
+  CK(roots.alloc(sizeof(int) * K, s));
+  CK(nroots.alloc(sizeof(int), s));
+  CK(inR.alloc(sizeof(int) * K, s));
+  CK(idx.alloc(sizeof(int) * K, s));
+  CK(wk.alloc(sizeof(unsigned long long) * std::max(nb, 1LL), s));
+  CK(cudaMemsetAsync(wk.p, 0, sizeof(unsigned long long) * std::max(nb, 1LL), s));
+  int nR = 0;
+  if (K) {
+    k_mark_a<<<grid_for(K, 256), 256, 0, s>>>(P, needA.as<unsigned char>());
+    LAUNCHED();
+    k_mark_roots<<<grid_for(K, 256), 256, 0, s>>>(P, needA.as<unsigned char>(), nullptr, rflag.as<int>());
+    LAUNCHED();
+    k_iota<<<grid_for(K, 256), 256, 0, s>>>(idx.as<int>(), K);
+    LAUNCHED();
+    size_t tb = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, idx.as<int>(), rflag.as<int>(), roots.as<int>(), nroots.as<int>(), K, s));
+    DevBuf tmp;
+    CK(tmp.alloc(tb, s));
+    CK(cub::DeviceSelect::Flagged(tmp.p, tb, idx.as<int>(), rflag.as<int>(), roots.as<int>(), nroots.as<int>(), K, s));
+    g_launches += 1;
+    CK(cudaMemcpyAsync(&nR, nroots.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  if (nR) {
+    CK(cudaMemsetAsync(inR.p, 0xff, sizeof(int) * K, s));
+    k_rank<<<grid_for(nR, 256), 256, 0, s>>>(roots.as<int>(), nR, inR.as<int>());
+    LAUNCHED();
+    CK(cnt.alloc(sizeof(int) * (size_t)kCnt * nR, s));
+    const int cand_blocks = (int)std::min<long long>((nR * 32LL + 255) / 256, 148 * 16);
+    k_candidates<false><<<std::max(cand_blocks, 1), 256, 0, s>>>(P, pl->G, roots.as<int>(), nR,
+                                                                 needA.as<unsigned char>(), inR.as<int>(),
+                                                                 cnt.as<int>(), nullptr, nullptr, nullptr, nullptr,
+                                                                 nullptr, 1);
+    LAUNCHED();
+    k_base_work<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(),
+                                                  wk.as<unsigned long long>());
+    LAUNCHED();
+  }
+  CK(cudaMemcpyAsync(work, wk.p, sizeof(unsigned long long) * nb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return NLG_OK;
 }
 
 nlg_status nlg_fp64_peak(int32_t device, double* tflops) {

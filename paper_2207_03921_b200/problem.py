@@ -15,7 +15,6 @@ import numpy as np
 
 from .errors import ConfigurationError
 from .geometry import BALL_IDS, PairClass
-from .kernels import KernelSpec
 from .mesh import Label
 from .quadrature import PATH_CODES, SINGULAR_KINDS, QuadratureConfig, dispatch, singular_rule
 
@@ -70,10 +69,26 @@ def quad_arrays(quad):
     return op, ow, oh, ip, iw
 
 
+KERNEL_FIELDS = ("delta", "s", "n", "symmetric", "ball", "builtin_id", "scale")
+
+
+def is_kernel_spec(kernel):
+    """A kernel description by its fields, not its class: this package's
+    :class:`~.kernels.KernelSpec` and the reference's
+    ``nlfem.kernels.KernelSpec`` (kernels.py:21-54) both qualify, so a caller
+    that swaps only the assembly import keeps its kernel objects."""
+    return all(hasattr(kernel, f) for f in KERNEL_FIELDS)
+
+
+def kernel_params(kernel):
+    """Extra parameters of a parametrised built-in (id 3: (alpha, c))."""
+    return tuple(getattr(kernel, "params", ()) or ())
+
+
 def validate(mesh, adjacency, kernel, ansatz, quad, n_threads, rows, traversal):
     if quad is None:
         quad = QuadratureConfig()
-    if not isinstance(kernel, KernelSpec):
+    if not is_kernel_spec(kernel):
         raise ConfigurationError("kernel must be a KernelSpec")
     if kernel.n != ansatz.n:
         raise ConfigurationError(
@@ -98,13 +113,15 @@ def marshal(mesh, adjacency, kernel, ansatz, quad=None, n_threads=1, rows="all",
         raise ConfigurationError(
             "the B200 assembly evaluates built-in kernels only (builtin_id 0-3); a Python "
             "callable kernel cannot run on the device and there is no CPU fallback")
-    if kernel.builtin_id == 3 and len(kernel.params) != 2:
+    if kernel.builtin_id > 3:
+        raise ConfigurationError(f"unknown built-in kernel id {kernel.builtin_id}")
+    if kernel.builtin_id == 3 and len(kernel_params(kernel)) != 2:
         raise ConfigurationError("kernel id 3 needs params (alpha, c)")
     labels = mesh.labels
     outer = labels == Label.DOMAIN if rows == "domain" else labels != Label.INACTIVE
     op, ow, oh, ip, iw = quad_arrays(quad)
     h = mesh.h
-    kp = tuple(kernel.params) + (0.0, 0.0)
+    kp = kernel_params(kernel) + (0.0, 0.0)
     return AssemblyInputs(
         vertices=np.ascontiguousarray(mesh.vertices, dtype=np.float64),
         elements=np.ascontiguousarray(mesh.elements, dtype=np.int64),

@@ -7,13 +7,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+REFERENCE = "/root/reference/pkg/src"
+# In the build container the reference is importable as `nlfem` (a drop-in
+# user's environment): the package's exceptions then subclass nlfem.errors.
+# The GPU box has no reference tree; the package stands alone there.
+if os.path.isdir(REFERENCE) and REFERENCE not in sys.path:
+    sys.path.append(REFERENCE)
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libnlg.so")
     config.addinivalue_line("markers", "slow: long-running parity case")
-
-
-REFERENCE = "/root/reference/pkg/src"
 
 
 @pytest.fixture(scope="session")

@@ -46,3 +46,32 @@ def test_cg_deterministic_and_dirichlet_data():
     assert np.all(u1[~sysm.free_mask] == 0.25)
     r = sysm.matrix @ u1 - b
     assert np.linalg.norm(r[sysm.free_mask]) <= 1e-10 * np.linalg.norm(b[sysm.free_mask])
+
+
+def test_table2_fractional_convergence_study():
+    """SURVEY 8f row 1 / SPEC.md:459-499: the paper's Table 2 study (fractional
+    CG, s = 0.5, delta = 0.2, nocaps, Omega = (0, 0.5)^2, n_div 5..40, free
+    dofs 16 / 81 / 361 / 1521 as in the table): assembly, load and Dirichlet
+    solve on the GPU, L2 error of the manufactured solution over Omega~.
+
+    * rates within 0.3 of Table 2's {2.13, 2.01, 2.01} (PAPER.md:684-689);
+    * errors equal (1e-6 relative: CG vs a direct solve) to the same study
+      run with the CPU oracle + scipy spsolve (pinned values below).  The
+      paper does not define its error norm; ours (the
+      7-point rule on |u_h - u|^2 over Omega~) is a constant factor ~4 above
+      the tabulated values at every level, with the same rates.
+    """
+    from paper_2207_03921_b200 import fractional_kernel
+    from paper_2207_03921_b200.manufactured import problem_fractional
+    from paper_2207_03921_b200.solve import run_study
+    rows = run_study(lambda: fractional_kernel(0.5, 0.2), problem_fractional(), [5, 10, 20, 40])
+    for r in rows:
+        assert r["cg_relres"] <= 1e-10
+    assert [r["dof"] for r in rows] == [16, 81, 361, 1521]
+    errs = [r["l2_error"] for r in rows]
+    rates = [r["rate"] for r in rows[1:]]
+    for got, want in zip(rates, (2.13, 2.01, 2.01)):
+        assert abs(got - want) <= 0.3, (rates, errs)
+    oracle_errs = (0.002723214856838669, 0.0006639707327425461, 0.00016612007113837868, 4.1585564860848426e-05)
+    for got, want in zip(errs, oracle_errs):
+        assert abs(got - want) <= 1e-6 * want, (errs, oracle_errs)
