@@ -171,6 +171,7 @@ __global__ void k_bounds(Params P, double2* ctr, double* rad, unsigned long long
 struct Grid {
   double ox, oy, cs;
   double reach;  // candidate radius around a barycentre: prer + 2 r_max (widened)
+  double rmax;   // largest element radius
   int nx, ny, span;
   const int* __restrict__ start;  // [ncell + 1]
   const int* __restrict__ items;  // active element ids sorted by cell
@@ -179,15 +180,27 @@ struct Grid {
   const int4* __restrict__ gel;
   const double2* __restrict__ gctr;
   const double* __restrict__ grad;
+  const double4* __restrict__ gft;  // analytic: (A2 psi_0, A2 psi_1, A2 psi_2, A2) in scan order
+  const int4* __restrict__ gdof;    // analytic: dof bases in scan order
+  // analytic: the dof bases (columns) on the same cells, by their position
+  const int* __restrict__ cstart;   // [ncell + 1]
+  const int* __restrict__ cid;      // dof base of each slot
+  const double4* __restrict__ cpos; // (x, y, H, H present): H = sum over the incident active elements n of
+                                    // A2_n psi_n[corner], the column's factor when all its elements are full partners
 };
 
-__global__ void k_grid_gather(Params P, const int* __restrict__ items, int n, int4* gel, double2* gctr, double* grad) {
+__global__ void k_grid_gather(Params P, const int* __restrict__ items, int n, int4* gel, double2* gctr, double* grad,
+                              double4* gft, int4* gdof) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int l = items[j];
   gel[j] = P.elem[l];
   gctr[j] = P.ctr[l];
   grad[j] = P.rad[l];
+  if (gft) {  // analytic: the partners' factors and dofs in scan order
+    gft[j] = P.ftab[l];
+    gdof[j] = P.dofs[l];
+  }
 }
 
 __global__ void k_cell(Params P, Grid G, unsigned* key, int* val) {
@@ -204,6 +217,46 @@ __global__ void k_cell(Params P, Grid G, unsigned* key, int* val) {
   }
   key[k] = cell;
   val[k] = k;
+}
+
+// analytic rows: each dof base's position (a corner of an incident element),
+// its factor H (sum over the incident active elements, fixed order) and cell
+__global__ void k_col_keys(Params P, Grid G, const int* __restrict__ de_start, const int* __restrict__ de_items,
+                           int nb, unsigned* key, int* val, double4* cpos) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  double h = 0.0, px = 0.0, py = 0.0;
+  bool any = false, pres = false;
+  for (int i = de_start[b]; i < de_start[b + 1]; ++i) {
+    const int it = de_items[i], n = it >> 2, a = it & 3;
+    const int4 el = P.elem[n];
+    if (!any) {
+      const double2 v = P.vtx[a == 0 ? el.x : (a == 1 ? el.y : el.z)];
+      px = v.x;
+      py = v.y;
+      any = true;
+    }
+    if ((el.w & 15) == 0) continue;
+    const double4 f = P.ftab[n];
+    const double fa = a == 0 ? f.x : (a == 1 ? f.y : f.z);
+    h += fa;
+    pres |= fa != 0.0;
+  }
+  unsigned cell = (unsigned)(G.nx * G.ny);
+  if (any) {
+    int ix = (int)floor((px - G.ox) / G.cs), iy = (int)floor((py - G.oy) / G.cs);
+    ix = min(max(ix, 0), G.nx - 1);
+    iy = min(max(iy, 0), G.ny - 1);
+    cell = (unsigned)(iy * G.nx + ix);
+  }
+  key[b] = cell;
+  val[b] = b;
+  cpos[b] = make_double4(px, py, h, pres ? 1.0 : 0.0);
+}
+
+__global__ void k_col_gather(const int* __restrict__ ids, int n, const double4* __restrict__ cpos_by_id, double4* cpos) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) cpos[j] = cpos_by_id[ids[j]];
 }
 
 __global__ void k_cell_ranges(const unsigned* __restrict__ skey, int K, int ncell, int* start) {
@@ -280,81 +333,225 @@ constexpr int kEmitA = 1 << 30;
 constexpr int kEmitB = (int)(1u << 31);
 constexpr int kIdMask = (1 << 30) - 1;
 
+constexpr int kFixBits = 62;  // bound x 2^S = 2^62: a term is one int64, 2^33 terms per cell below 2^95
+// Fixed point: t = rint(v 2^S), |t| <= 2^62, summed exactly as a 96-bit two's
+// complement integer (three 32-bit limbs in shared memory -- native 32-bit
+// atomics; 64-bit shared atomics are CAS loops -- with the carries propagated
+// by the adding thread; __int128 in registers), so a sum does not depend on
+// the order of its terms.
+using fix_t = __int128;
+__device__ __forceinline__ fix_t fix_of(double v, double scale) { return (fix_t)__double2ll_rn(v * scale); }
+__device__ __forceinline__ double fix_val3(const unsigned* c, double inv) {
+  const double v = fma((double)(int)c[2], 0x1p64, fma((double)c[1], 0x1p32, (double)c[0]));
+  return v * inv;
+}
+__device__ __forceinline__ void fix_atomic(unsigned* c, fix_t x) {
+  unsigned x0 = (unsigned)x, x1 = (unsigned)(x >> 32), x2 = (unsigned)(x >> 64);
+  if (x0) {
+    const unsigned o = atomicAdd(&c[0], x0);
+    if (o + x0 < o && ++x1 == 0) ++x2;
+  }
+  if (x1) {
+    const unsigned o = atomicAdd(&c[1], x1);
+    if (o + x1 < o) ++x2;
+  }
+  if (x2) atomicAdd(&c[2], x2);
+}
+__device__ __forceinline__ fix_t fix_warp_sum(fix_t a) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)a, o);
+    const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(a >> 64), o);
+    a += ((fix_t)hi << 64) | (fix_t)lo;
+  }
+  return a;
+}
+
+// The 7 rule points of a triangle (reference arithmetic, as rule_points).
+__device__ __forceinline__ void tri_points(const double* tx, const double* ty, double* px, double* py) {
+  const double e1x = tx[1] - tx[0], e2x = tx[2] - tx[0], e1y = ty[1] - ty[0], e2y = ty[2] - ty[0];
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    px[p] = __dadd_rn(__dadd_rn(tx[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+    py[p] = __dadd_rn(__dadd_rn(ty[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+  }
+}
+
+// Every vertex of l inside the widened ball of every outer point of k, and
+// vice versa: both sweeps' clips return the whole inner triangle
+// (_geom_scalar.py:53-66).  Symmetric in (k, l); exact reference predicates.
+__device__ __forceinline__ bool pair_all_in(const Params& P, const double* kx, const double* ky, const double* xk,
+                                            const double* yk, const double* lx, const double* ly, const double* xl,
+                                            const double* yl) {
+  const double rad = mul(P.delta, 1.0 + kBallTieRel);
+  const double r2 = mul(rad, rad);
+  // The rule points are convex combinations of the vertices, and the
+  // distance to a point is convex: the 9 vertex-vertex distances decide the
+  // 42 reference tests except within a relative 1e-10 of the radius (the
+  // rule points' rounding is ~1e-16).  Only such near-ties run the exact tests.
+  {
+    const double hi = r2 * (1.0 + 1e-10), lo = r2 * (1.0 - 1e-10);
+    bool clear = true;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double d2 = sumsq(lx[i] - kx[a], ly[i] - ky[a]);
+        if (d2 > hi) return false;
+        clear = clear && d2 < lo;
+      }
+    if (clear) return true;
+  }
+  // the vertex points (p = 1..3) first: a pair that fails usually fails there
+#pragma unroll 1
+  for (int q = 0; q < 7; ++q) {
+    const int p = q < 6 ? q + 1 : 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (__dsub_rn(sumsq(lx[i] - xk[p], ly[i] - yk[p]), r2) > 0.0) return false;
+      if (__dsub_rn(sumsq(kx[i] - xl[p], ky[i] - yl[p]), r2) > 0.0) return false;
+    }
+  }
+  return true;
+}
+
 // Per-item truncation class of a clipped pair, with the reference's exact
 // predicates: every inner vertex inside the widened ball of every outer
 // point (the clip returns the triangle itself, _geom_scalar.py:53-66) or the
 // inner element's bounding disk beyond the ball by a margin no rounding can
 // bridge (the clip is empty).  Returns 2 if all 14 items are "inside", 1 if
 // all are empty, 0 otherwise.
-__device__ __forceinline__ int pair_trunc_class(const Params& P, const double* kx, const double* ky,
+__device__ __noinline__ int pair_trunc_class(const Params& P, const double* kx, const double* ky,
                                                 const double* xk, const double* yk, double2 ck, double rk,
                                                 const double* lx, const double* ly, double2 cl, double rl) {
-  const double rad = mul(P.delta, 1.0 + kBallTieRel);
-  const double r2 = mul(rad, rad);
+  if (P.ball == 2) return 0;
+  double xl[7], yl[7];
+  tri_points(lx, ly, xl, yl);
+  if (pair_all_in(P, kx, ky, xk, yk, lx, ly, xl, yl)) return 2;
   const double far2k = (P.delta * (1.0 + 1e-6) + rk) * (P.delta * (1.0 + 1e-6) + rk);
   const double far2l = (P.delta * (1.0 + 1e-6) + rl) * (P.delta * (1.0 + 1e-6) + rl);
-  double xl[7], yl[7];
   {
-    const double e1x = lx[1] - lx[0], e2x = lx[2] - lx[0], e1y = ly[1] - ly[0], e2y = ly[2] - ly[0];
-#pragma unroll
-    for (int p = 0; p < 7; ++p) {
-      xl[p] = __dadd_rn(__dadd_rn(lx[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
-      yl[p] = __dadd_rn(__dadd_rn(ly[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
-    }
+    // every rule point of k lies within r_k of c_k (and of l within r_l of
+    // c_l): the barycentre distance decides "all far" outside a band of width
+    // 2 max(r_k, r_l) (margins 1e-9 relative cover the roundings)
+    const double d2 = (cl.x - ck.x) * (cl.x - ck.x) + (cl.y - ck.y) * (cl.y - ck.y);
+    const double fo = P.delta * (1.0 + 1e-6) + rl + rk, fi = P.delta * (1.0 + 1e-6) + rl - rk;
+    const double gi = P.delta * (1.0 + 1e-6) + rk - rl;
+    if (d2 > fo * fo * (1.0 + 1e-9)) return 1;
+    if ((fi > 0.0 && d2 < fi * fi * (1.0 - 1e-9)) || (gi > 0.0 && d2 < gi * gi * (1.0 - 1e-9))) return 0;
   }
-  bool all_in = true, all_far = true;
+  bool all_far = true;
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
     // outer point on k, inner l / outer point on l, inner k
     const double dkx = cl.x - xk[p], dky = cl.y - yk[p];
     const double dlx = ck.x - xl[p], dly = ck.y - yl[p];
     all_far = all_far && dkx * dkx + dky * dky > far2l && dlx * dlx + dly * dly > far2k;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      all_in = all_in && __dsub_rn(sumsq(lx[i] - xk[p], ly[i] - yk[p]), r2) <= 0.0 &&
-               __dsub_rn(sumsq(kx[i] - xl[p], ky[i] - yl[p]), r2) <= 0.0;
-    }
   }
-  return P.ball == 2 ? 0 : (all_in ? 2 : (all_far ? 1 : 0));
+  return all_far ? 1 : 0;
 }
+
+// pair_all_in of root k (vertices, rule points) and element el, out of line
+// (rare: only pairs within the ball's rim reach it)
+__device__ __noinline__ bool pair_all_in_el(const Params& P, const double* kx, const double* ky, const double* xk,
+                                            const double* yk, int4 el) {
+  double lx[3], ly[3], xl[7], yl[7];
+  const double2 v0 = __ldg(&P.vtx[el.x]), v1 = __ldg(&P.vtx[el.y]), v2 = __ldg(&P.vtx[el.z]);
+  lx[0] = v0.x; ly[0] = v0.y; lx[1] = v1.x; ly[1] = v1.y; lx[2] = v2.x; ly[2] = v2.y;
+  tri_points(lx, ly, xl, yl);
+  return pair_all_in(P, kx, ky, xk, yk, lx, ly, xl, yl);
+}
+
+// Distance predicates of a visit in the reference's operand order
+// (_engine.py:219-227): reject  (dist - r_root) - r_nb > prer  and
+// full  (dist + r_root) + r_nb <= delta, with dist = sqrt(d2).  Pairs far
+// from either threshold are decided from d2 alone -- a relative margin of
+// 1e-12 dwarfs every rounding of the thresholds -- so the square root (and
+// the exact test) only runs in thin shells around them.
+struct VisitDist {
+  double d2, dist;
+  __device__ __forceinline__ explicit VisitDist(double d2_) : d2(d2_), dist(-1.0) {}
+  __device__ __forceinline__ double get() {
+    if (dist < 0.0) dist = sqrt(d2);
+    return dist;
+  }
+  // (get() - a) - b > t
+  __device__ __forceinline__ bool reject(double a, double b, double t) {
+    const double th = t + a + b, eta = 1e-12 * th;
+    if (d2 > (th + eta) * (th + eta)) return true;
+    if (d2 < (th - eta) * (th - eta)) return false;
+    return __dsub_rn(__dsub_rn(get(), a), b) > t;
+  }
+  // (get() + a) + b <= t
+  __device__ __forceinline__ bool within(double a, double b, double t) {
+    const double th = t - a - b, eta = 1e-12 * (t + a + b);
+    if (th - eta > 0.0 && d2 < (th - eta) * (th - eta)) return true;
+    if (th + eta <= 0.0 || d2 > (th + eta) * (th + eta)) return false;
+    return __dadd_rn(__dadd_rn(get(), a), b) <= t;
+  }
+};
 
 //  -1 none here, 0 full record, 1 clipped record, 2/3/4 singular id/edge/vertex.
 // *visited: the reference would count the visit (k, l) (EPI); *flags: record sides.
 // Clipped pairs whose every sweep item is untruncated take the full path (same
 // arithmetic: the fan of the untruncated triangle is the triangle); pairs
 // whose every item is empty contribute nothing and produce no record.
+// Analytic mode (P.analytic): a visit of category 0 ("full", by distance or
+// by truncation class) has no record at all -- the row merge enumerates such
+// visits itself (k_row_asm) -- and *an reports it (the fill pass sums the
+// partners' areas of the root's own block).
 template <bool LIGHT>
 __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2 ck, double rk,
                                         const double* kx, const double* ky, const double* xk, const double* yk,
                                         bool needAk, const unsigned char* __restrict__ needA,
                                         const int* __restrict__ inR, int l, int4 el, double2 cl, double rl,
-                                        bool& visited, int& flags) {
+                                        bool& visited, int& flags, bool& an) {
   visited = false;
   flags = 0;
-  const int ns = (ek.x == el.x) + (ek.x == el.y) + (ek.x == el.z) + (ek.y == el.x) + (ek.y == el.y) +
-                 (ek.y == el.z) + (ek.z == el.x) + (ek.z == el.y) + (ek.z == el.z);
+  an = false;
+  VisitDist D(sumsq(ck.x - cl.x, ck.y - cl.y));
+  // a shared vertex lies within r of both barycentres: dist <= r_k + r_l
+  const double rs = (rk + rl) * (1.0 + 1e-9);
+  const int ns = D.d2 > rs * rs ? 0
+                                : (ek.x == el.x) + (ek.x == el.y) + (ek.x == el.z) + (ek.y == el.x) + (ek.y == el.y) +
+                                      (ek.y == el.z) + (ek.z == el.x) + (ek.z == el.y) + (ek.z == el.z);
   const bool touching = (k == l) || ns > 0;
-  const double dist = sqrt(sumsq(ck.x - cl.x, ck.y - cl.y));
-  if (!touching && __dsub_rn(__dsub_rn(dist, rk), rl) > P.prer) return -1;
+  if (!touching && D.reject(rk, rl, P.prer)) return -1;
   visited = true;
   if (touching && P.path == 2) {
     if (l != k && (el.w & 16) && l < k) return -1;  // owned by the smaller root (_engine.py:233)
     if (!(needAk || needA[l])) return -1;
     return k == l ? 2 : (ns == 2 ? 3 : 4);
   }
-  const bool full = __dadd_rn(__dadd_rn(dist, rk), rl) <= P.delta;
+  const bool full = D.within(rk, rl, P.delta);
+  const bool lroot = k != l && (el.w & 16);
   bool full_lk = full, rej_lk = false;
-  if (k != l && (el.w & 16)) {  // root l's view of the same pair
-    rej_lk = !touching && __dsub_rn(__dsub_rn(dist, rl), rk) > P.prer;
-    full_lk = __dadd_rn(__dadd_rn(dist, rl), rk) <= P.delta;
+  if (lroot) {  // root l's view of the same pair
+    rej_lk = !touching && D.reject(rl, rk, P.prer);
+    full_lk = D.within(rl, rk, P.delta);
+  }
+  if (P.analytic) {
+    // records only for category-1 visits; category 0 = full or all-inside
+    if (k == l) {
+      if (LIGHT) return needAk ? 1 : -1;
+    } else if (full) {
+      an = true;  // (a clipped visit (l, k) is root l's own record)
+      return -1;
+    } else if (LIGHT) {
+      // an upper bound: possibly clipped, and not the shared record root l makes
+      if (!full_lk && lroot && !rej_lk && l < k && inR[l] >= 0) return -1;
+      if (!(needAk || (lroot && needA[l]))) return -1;
+      return 1;
+    }
   }
   // When both views agree on `full`, both get the same category whatever the
   // truncation class, so whether the pair is shared -- and then produced by
   // the smaller root of the batch -- is known before the (costly) class.
-  if (full == full_lk && k != l && (el.w & 16) && !rej_lk && inR[l] >= 0 && l < k) return -1;
+  const bool l_makes = full == full_lk && lroot && !rej_lk && l < k && inR[l] >= 0;
+  if (l_makes && !P.analytic) return -1;
   if (LIGHT) {  // upper bounds for the count pass: 0 full, 1 possibly clipped
-    if (!(needAk || ((el.w & 16) && needA[l]))) return -1;
-    return full && !(P.analytic && k == l) ? 0 : 1;
+    if (!(needAk || (lroot && needA[l]))) return -1;
+    return full ? 0 : 1;
   }
   // exact truncation class of the pair (symmetric in k, l)
   int tcls = 0;
@@ -366,9 +563,16 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
   }
   // (analytic mode: the identical pair keeps its stored blocks on the clipped path)
   const int cat_kl = (full || tcls == 2) && !(P.analytic && k == l) ? 0 : 1;
+  if (P.analytic) {
+    if (cat_kl == 0) {
+      an = true;
+      return -1;
+    }
+    if (l_makes) return -1;
+  }
   if (tcls == 1) return -1;  // every item empty in both visits: nothing to emit
   bool shared = false;
-  if (k != l && (el.w & 16)) {
+  if (lroot) {
     const int cat_lk = full_lk || tcls == 2 ? 0 : 1;
     shared = !rej_lk && cat_lk == cat_kl;
   }
@@ -390,7 +594,7 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
                              const unsigned char* __restrict__ needA, const int* __restrict__ inR,
                              int* __restrict__ cnt, const long long* __restrict__ off, int2* __restrict__ comb,
                              int2* __restrict__ ls0, int2* __restrict__ ls1, int2* __restrict__ ls2,
-                             int stride = 1) {
+                             int stride = 1, double* __restrict__ own_a2 = nullptr) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
@@ -420,6 +624,9 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
       for (int j = 1; j < 4; ++j) base[j] = off[(long long)(C_SID + j - 1) * (nR + 1) + i];
     }
     int nfull = 0, nclip = 0;
+    // analytic fill: sum of the category-0 partners' areas A2 (per lane in
+    // scan order, then a fixed tree: the same for every batch containing k)
+    double own = 0.0;
     for (int yy = max(iy - G.span, 0); yy <= min(iy + G.span, G.ny - 1); ++yy) {
       const double ylo = G.oy + yy * G.cs, yhi = ylo + G.cs;
       const double dy = ck.y < ylo ? ylo - ck.y : (ck.y > yhi ? ck.y - yhi : 0.0);
@@ -433,25 +640,27 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
       for (int j0 = c0; j0 < c1; j0 += 32) {
         const int j = j0 + lane;
         int cat = -1, fl = 0;
-        bool vis = false;
+        bool vis = false, an = false;
         const int l = j < c1 ? G.items[j] : 0;
         int4 el = make_int4(0, 0, 0, 0);
         double2 cl = make_double2(0.0, 0.0);
-        double rl = 0.0;
+        double rl = 0.0, a2l = 0.0;
         if (j < c1) {
           el = G.gel[j];
           cl = G.gctr[j];
           rl = G.grad[j];
+          if (FILL && P.analytic) a2l = __ldg(&G.gft[j].w);
         }
         if (!FILL) {
-          if (j < c1) cat = classify<true>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, el, cl, rl, vis, fl);
+          if (j < c1) cat = classify<true>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, el, cl, rl, vis, fl, an);
           c[C_EPI] += vis;
           // C_FULL: all records, C_PART: the possibly clipped ones
           if (cat >= 0) {
             if (cat <= 1) { c[C_FULL]++; c[C_PART] += cat; } else c[cat]++;
           }
         } else {
-          if (j < c1) cat = classify<false>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, el, cl, rl, vis, fl);
+          if (j < c1) cat = classify<false>(P, k, ek, ck, rk, kx, ky, xk, yk, needAk, needA, inR, l, el, cl, rl, vis, fl, an);
+          if (an) own += a2l;
           nfull += cat == 0;
           nclip += cat == 1;
           // lists: 0 = combined (full or clipped), 1..3 = singular families
@@ -484,9 +693,12 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
         nfull += __shfl_xor_sync(0xffffffffu, nfull, o);
         nclip += __shfl_xor_sync(0xffffffffu, nclip, o);
       }
+      if (P.analytic)
+        for (int o = 16; o; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
       if (lane == 0) {
         cnt[(long long)C_FULL * nR + i] = nfull;
         cnt[(long long)C_PART * nR + i] = nclip;
+        if (P.analytic) own_a2[i] = own;
       }
     }
   }
@@ -496,7 +708,7 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
 // root's memory (bytes), record and COO-slot counts go to its first in-range row
 __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, const int* __restrict__ cnt,
                             double rec_bytes, double store_bytes, double sing_bytes, double root_bytes, double rec_slots,
-                            double sing_slots, unsigned long long* row_cost, double scale = 1.0) {
+                            double sing_slots, unsigned long long* row_cost, double scale, double epi_bytes) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nR) return;
   const int4 d = P.dofs[roots[i]];
@@ -513,7 +725,9 @@ __global__ void k_root_cost(Params P, const int* __restrict__ roots, int nR, con
   const long long sing = (long long)cnt[(long long)C_SID * nR + i] + cnt[(long long)C_SED * nR + i] +
                          cnt[(long long)C_SVX * nR + i];
   unsigned long long* rc = row_cost + 3 * (home - P.row_lo);
-  atomicAdd(&rc[0], (unsigned long long)(scale * (rec * rec_bytes + stored * store_bytes + sing * sing_bytes + root_bytes)));
+  const long long epi = cnt[(long long)C_EPI * nR + i];
+  atomicAdd(&rc[0], (unsigned long long)(scale * (rec * rec_bytes + stored * store_bytes + sing * sing_bytes + root_bytes +
+                                                  epi * epi_bytes)));
   atomicAdd(&rc[1], (unsigned long long)(scale * rec));
   atomicAdd(&rc[2], (unsigned long long)(scale * (rec * rec_slots + sing * sing_slots + 9 * P.nc * P.nc)));
 }
@@ -1133,7 +1347,9 @@ __device__ __forceinline__ void closed_moments(const Params& P, double q0x, doub
   }
 }
 
-template <int KID, bool SQ>
+// WL: warp-local clipping (no block queue, no block barriers) -- the
+// closed-form path of the constant / affine kernels only
+template <int KID, bool SQ, bool WL = false>
 __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID == 1 ? 2 : (KID == 2 ? 5 : 3))) k_clipped(Params P, const int2* __restrict__ list, VisitOut O) {
   using T = KTraits<KID>;
   using C = ClipCfg<KID>;
@@ -1280,6 +1496,23 @@ __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID ==
     }
     S.pm[lane] = (unsigned char)(p | (m << 4) | (valid ? 0 : 0x80));
     S.nv[lane] = (unsigned char)nv;
+    if constexpr (WL) {
+      // ---------------- phase 1b (warp-local): each lane clips its own item;
+      // no block barrier, the warps run independently
+      __syncwarp();
+      if (need_clip) {
+        const double* tv = S.tv[vs][m == 1];
+        const Tri Tq{tv[0], tv[1], tv[2], tv[3], tv[4], tv[5]};
+        int nvq;
+        if constexpr (SQ)
+          nvq = truncate_inner(Tq, S.xo[lane][0], S.xo[lane][1], P.delta, P.ball, S.sx[lane], S.sy[lane], S.px[lane],
+                               S.py[lane]);
+        else
+          nvq = truncate_inner_inplace(Tq, S.xo[lane][0], S.xo[lane][1], P.delta, P.ball, S.px[lane], S.py[lane]);
+        S.nv[lane] = (unsigned char)nvq;
+      }
+      __syncwarp();
+    } else {
     {
       const unsigned qm = __ballot_sync(0xffffffffu, need_clip);
       int qb = 0;
@@ -1307,6 +1540,7 @@ __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID ==
       }
     }
     __syncthreads();
+    }
     par ^= 1;
     double si[C::NSUM];  // the item's sums over its fan sub-triangles
 #pragma unroll
@@ -1595,6 +1829,18 @@ constexpr double kRunFrac = 0.35;
 // cfg1-3 0.03); a batch that needs more is split
 constexpr double kEntFrac = 0.08;
 
+// CSR entries of a batch's rows: a row holds about 0.47 nc x the EPI of a
+// root (the partner vertices), so kEntPerEpi leaves headroom; records alone
+// under-count in analytic mode, where most visits have none
+constexpr double kEntPerEpi = 0.75;
+inline long long ent_estimate(const Params& P, long long n_records, long long epi, long long nR) {
+  const double E = 9.0 * P.nc * P.nc;
+  const double by_rec = kEntFrac * (double)n_records * 2.0 * E;
+  const double epi_avg = nR ? (double)epi / (double)nR : 0.0;
+  const double by_epi = (double)(P.row_hi - P.row_lo) * (kEntPerEpi * P.nc * epi_avg + 64.0);
+  return (long long)std::max(by_rec, by_epi);
+}
+
 struct RootIn {
   const int* roots;
   int nR;
@@ -1616,6 +1862,7 @@ struct RootIn {
   const double* klv;  // [side][3][NVP]
   const int* chunk_first;  // [nR + 1], chunk_first[nR] = number of chunks
   const int* chunk_root;   // [chunks] root rank of each chunk
+  const double* own_a2;    // analytic: [nR] sum of the category-0 partners' A2
 };
 struct RootOut {
   unsigned* ticket;
@@ -1990,7 +2237,6 @@ __global__ void __launch_bounds__(kRootThreads, 3) k_root_reduce(Params P, RootI
 // distinct columns outgrow the table is retried with a larger one; beyond
 // the largest, the batch falls back to stage R + the global sort.
 constexpr unsigned kRowEmpty = 0x7fffffffu;
-constexpr int kFixBits = 72;  // bound x 2^S = 2^72: 2^23 contributions per cell below 2^95
 
 struct RowIn {
   const int* de_start;
@@ -2007,6 +2253,7 @@ struct RowIn {
   const long long* sstart;
   const unsigned long long* vmax;  // max |stored / singular value| of the batch
   const unsigned long long* fmax;  // plan bounds of the analytic terms (k_elem_factors)
+  Grid G;                          // analytic rows enumerate their category-0 partners
 };
 struct RowOut {
   int* col;
@@ -2022,45 +2269,20 @@ struct RowOut {
   int split;        // 0: all columns; 1 / 2: only column bases < / >= d (rows too wide for one table)
 };
 
-// Fixed point: t = rint(v 2^S), |t| < 2^80, summed exactly as a 96-bit two's
-// complement integer (three 32-bit limbs in shared memory, native 32-bit
-// atomics with the carries propagated by the adding thread; __int128 in
-// registers), so a sum does not depend on the order of its terms.
-using fix_t = __int128;
-__device__ __forceinline__ fix_t fix_of(double v, double scale) {
-  const double t = rint(v * scale);
-  const double hd = floor(t * 0x1p-40);
-  const long long h = __double2ll_rz(hd);
-  const long long l = __double2ll_rz(fma(hd, -0x1p40, t));  // exact: t and hd 2^40 share the grid of t
-  return ((fix_t)h << 40) + (fix_t)l;
-}
-__device__ __forceinline__ double fix_val3(const unsigned* c, double inv) {
-  const double v = fma((double)(int)c[2], 0x1p64, fma((double)c[1], 0x1p32, (double)c[0]));
-  return v * inv;
-}
-__device__ __forceinline__ void fix_atomic(unsigned* c, fix_t x) {
-  unsigned x0 = (unsigned)x, x1 = (unsigned)(x >> 32), x2 = (unsigned)(x >> 64);
-  if (x0) {
-    const unsigned o = atomicAdd(&c[0], x0);
-    if (o + x0 < o && ++x1 == 0) ++x2;
-  }
-  if (x1) {
-    const unsigned o = atomicAdd(&c[1], x1);
-    if (o + x1 < o) ++x2;
-  }
-  if (x2) atomicAdd(&c[2], x2);
-}
-__device__ __forceinline__ fix_t fix_warp_sum(fix_t a) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)a, o);
-    const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(a >> 64), o);
-    a += ((fix_t)hi << 64) | (fix_t)lo;
-  }
-  return a;
-}
-
-constexpr int kRowGroup = 32;  // incident roots whose analytic own terms are flushed together
+// Analytic rows (kid 2 / 3 on the standard path): the category-0 visits of
+// the incident roots have no records.  The row's CTA enumerates the grid
+// around its dof, and for each candidate element n sums the incident roots'
+// row factors over the visits (k, n) of category 0 (exact reference
+// predicates): one table add per column of n instead of one per visit.
+constexpr int kMaxInc = 8;    // incident roots of a dof per enumeration pass
+constexpr int kMaxRowsG = 16; // grid cell rows of one enumeration
+constexpr int kRimCap = 8192; // queued rim candidates of one enumeration (beyond: handled in place)
+struct IncRoot {
+  double cx, cy, r;
+  double kx[3], ky[3], xk[7], yk[7];
+  double fkl;     // -2 A2_k sum_p w_p H_pa: the visit's neighbour-block row factor
+  int k;          // element, -1: not a root of the batch
+};
 
 template <int NC, int CAP, int TH>
 struct RowSmem {
@@ -2073,8 +2295,13 @@ struct RowSmem {
     typename Sort::TempStorage sort;
     typename Scan::TempStorage scan;
   } u;
-  unsigned sa[kRowGroup][3];  // analytic: per incident root, sum of the partners' A2
-  unsigned sa_pres;
+  IncRoot inc[kMaxInc];
+  int gr0[kMaxRowsG], gr1[kMaxRowsG], gpre[kMaxRowsG + 1];  // candidate ranges of the enumeration
+  int ngr;
+  double gvx, gvy, grmax, gsum_all;  // the dof's vertex, largest incident radius, sum of all row factors
+  int gpres_all;
+  int nrim;
+  int rimq[kRimCap];                  // candidates near the rim of the group's balls (scan slots)
   int used, ovf;
   long long base[NC];
 };
@@ -2087,7 +2314,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   using SM = RowSmem<NC, CAP, TH>;
   extern __shared__ __align__(16) unsigned char row_smem[];
   SM& S = *reinterpret_cast<SM*>(row_smem);
-  const int t = threadIdx.x, lane = lane_id();
+  const int t = threadIdx.x;
   const long long d = W.dlist ? (long long)W.dlist[blockIdx.x] : W.d_lo + blockIdx.x;
   for (int i = t; i < CAP; i += TH) {
     S.key[i] = kRowEmpty;
@@ -2095,11 +2322,9 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
 #pragma unroll
     for (int e = 0; e < NC2; ++e) S.acc[i][e][0] = S.acc[i][e][1] = S.acc[i][e][2] = 0;
   }
-  for (int i = t; i < kRowGroup * 3; i += TH) (&S.sa[0][0])[i] = 0;
   if (t == 0) {
     S.used = 0;
     S.ovf = 0;
-    S.sa_pres = 0;
   }
   // fixed-point scale from a bound of every contribution's magnitude
   double whsmax = 0.0, sw = 0.0;
@@ -2118,14 +2343,13 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
     fa2 = __longlong_as_double((long long)W.fmax[0]);
     const double fg = __longlong_as_double((long long)W.fmax[1]);
     const double fphi = __longlong_as_double((long long)W.fmax[2]);
-    bound = fmax(bound, 2.0 * fa2 * whsmax * fg);
-    bound = fmax(bound, 2.0 * fa2 * sw * fphi * fa2 * 0x1p14);  // own term: A2_r Phi_r x (sum of up to 2^14 A2_n)
+    // neighbour terms: up to kMaxInc roots' factors per column of a partner
+    bound = fmax(bound, 2.0 * fa2 * whsmax * fg * kMaxInc);
+    bound = fmax(bound, 2.0 * fa2 * sw * fphi * fa2 * 0x1p17);  // own term: A2_r Phi_r x (sum of up to 2^17 A2_n)
   }
   const bool bok = bound > 0.0 && bound <= 1e300;
   const int be = bok ? ilogb(bound) + 1 : 0;
   const double scale = bok ? ldexp(1.0, kFixBits - be) : 1.0, inv = bok ? ldexp(1.0, be - kFixBits) : 1.0;
-  const int ae = AN && fa2 > 0.0 && fa2 <= 1e300 ? ilogb(fa2) + 1 : 0;  // sums of A2: their own scale
-  const double ascale = ldexp(1.0, kFixBits - ae), ainv = ldexp(1.0, ae - kFixBits);
   unsigned inr = 0;
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -2173,121 +2397,243 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
     add_fix(w, comp, fix_of(v, scale), true);
   };
   if (inr) {
-    // ---- the record sides of the batch roots incident to d, in groups of
-    // kRowGroup (the analytic own terms need the group's sums of A2)
+    // ---- the stored record sides of the batch roots incident to d
+    // (analytic mode: the clipped sides only; category-0 visits follow below)
     const int e0 = W.de_start[d], e1 = W.de_start[d + 1];
-    for (int g0 = e0; g0 < e1; g0 += kRowGroup) {
-      const int g1 = min(e1, g0 + kRowGroup);
-      for (int ei = g0; ei < g1; ++ei) {
-        const int it = __ldg(&W.de_items[ei]);
-        const int k = it >> 2, a = it & 3;
-        const int rank = __ldg(&W.inR[k]);
-        if (rank < 0) continue;  // block-uniform
-        const RootSides R = root_sides(I, rank);
-        const long long n_rs = R.n(), nan_rs = AN ? R.nfull() : 0;
-        const int4 dk4 = __ldg(&P.dofs[k]);
-        const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
-        const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
-        double fkl = 0.0;
-        if (AN) {
-          double wsum = 0.0;
+    for (int ei = e0; ei < ((P.dbg & 4) ? e0 : e1); ++ei) {  // (NLG_DEBUG & 4: timing experiments)
+      const int it = __ldg(&W.de_items[ei]);
+      const int k = it >> 2, a = it & 3;
+      const int rank = __ldg(&W.inR[k]);
+      if (rank < 0) continue;  // block-uniform
+      const RootSides R = root_sides(I, rank);
+      const long long n_rs = R.n();
+      const int4 dk4 = __ldg(&P.dofs[k]);
+      const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
+      const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
+      // own-block partials in fixed point (nc = 2: in double, summed by each
+      // thread over its sides in a fixed order -- deterministic for a given
+      // CTA size -- and converted once per root, to save registers)
+      using OwnT = std::conditional_t<NC == 2, double, fix_t>;
+      OwnT own[3][NC2];
+      unsigned opres = 0;  // bit b * NC2 + comp
 #pragma unroll
-          for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
-          fkl = -2.0 * __ldg(&P.ftab[k].w) * wsum;
-        }
-        // own-block partials in fixed point (nc = 2: in double, summed by each
-        // thread over its sides in a fixed order -- deterministic for a given
-        // CTA size -- and converted once per root, to save registers)
-        using OwnT = std::conditional_t<NC == 2, double, fix_t>;
-        OwnT own[3][NC2];
-        unsigned opres = 0;  // bit b * NC2 + comp
+      for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
+        for (int e = 0; e < NC2; ++e) own[b][e] = 0;
+      for (long long rs = t; rs < n_rs; rs += TH) {
+        if (*(volatile int*)&S.ovf) break;  // this table is too small: retried with a larger one
+        const int n = R.partner(I, rs);
+        const int4 dn4 = __ldg(&P.dofs[n]);
+        const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
+        const long long slot = R.slot(I, rs);
+        const double* kk = I.kkv + slot * Blk<NC>::NKK;
+        const double* kl = I.klv + slot * Blk<NC>::KLS;
 #pragma unroll
-          for (int e = 0; e < NC2; ++e) own[b][e] = 0;
-        fix_t sa = 0;
-        bool sapres = false;
-        for (long long rs = t; rs < n_rs; rs += TH) {
-          if (*(volatile int*)&S.ovf) break;  // this table is too small: retried with a larger one
-          const int n = R.partner(I, rs);
-          const int4 dn4 = __ldg(&P.dofs[n]);
-          const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
-          if (AN && rs < nan_rs) {
-            const double4 g = ld_f4(P.ftab + n);
-            sa += fix_of(g.w, ascale);
-            sapres |= g.w != 0.0;
-            add(dn[0], 0, fkl * g.x, g.x != 0.0 && fkl != 0.0);
-            add(dn[1], 0, fkl * g.y, g.y != 0.0 && fkl != 0.0);
-            add(dn[2], 0, fkl * g.z, g.z != 0.0 && fkl != 0.0);
-          } else {
-            const long long slot = R.slot(I, rs);
-            const double* kk = I.kkv + slot * Blk<NC>::NKK;
-            const double* kl = I.klv + slot * Blk<NC>::KLS;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              if (!((inr >> c) & 1u)) continue;
-              const int Ir = a * NC + c;
-#pragma unroll
-              for (int b = 0; b < 3; ++b)
-#pragma unroll
-                for (int dd = 0; dd < NC; ++dd) {
-                  const int Jc = b * NC + dd;
-                  const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
-                  const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
-                  if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
-                    if constexpr (NC == 2) own[b][c * NC + dd] += vo;
-                    else own[b][c * NC + dd] += fix_of(vo, scale);
-                    opres |= 1u << (b * NC2 + c * NC + dd);
-                  }
-                  add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
-                }
-            }
-          }
-        }
-        // own block of (k, a): fixed-point partials -> warp sums -> table
-#pragma unroll
-        for (int o = 16; o; o >>= 1) opres |= __shfl_xor_sync(0xffffffffu, opres, o);
-        if (opres) {  // warp-uniform
+        for (int c = 0; c < NC; ++c) {
+          if (!((inr >> c) & 1u)) continue;
+          const int Ir = a * NC + c;
 #pragma unroll
           for (int b = 0; b < 3; ++b)
 #pragma unroll
-            for (int e = 0; e < NC2; ++e) {
-              fix_t f0;
-              if constexpr (NC == 2) f0 = fix_of(own[b][e], scale);
-              else f0 = own[b][e];
-              const fix_t f = fix_warp_sum(f0);
-              if (lane == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
+            for (int dd = 0; dd < NC; ++dd) {
+              const int Jc = b * NC + dd;
+              const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
+              const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
+              if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
+                if constexpr (NC == 2) own[b][c * NC + dd] += vo;
+                else own[b][c * NC + dd] += fix_of(vo, scale);
+                opres |= 1u << (b * NC2 + c * NC + dd);
+              }
+              add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
             }
         }
-        if (AN) {
-          const fix_t f = fix_warp_sum(sa);
-          const bool sp = __any_sync(0xffffffffu, sapres);
-          if (lane == 0 && sp) {
-            fix_atomic(S.sa[ei - g0], f);
-            atomicOr(&S.sa_pres, 1u << (ei - g0));
+      }
+      // own block of (k, a): fixed-point partials -> warp sums -> table
+#pragma unroll
+      for (int o = 16; o; o >>= 1) opres |= __shfl_xor_sync(0xffffffffu, opres, o);
+      if (opres) {  // warp-uniform
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int e = 0; e < NC2; ++e) {
+            fix_t f0;
+            if constexpr (NC == 2) f0 = fix_of(own[b][e], scale);
+            else f0 = own[b][e];
+            const fix_t f = fix_warp_sum(f0);
+            if ((t & 31) == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
           }
+      }
+      if (AN && t < 3 && own_on) {
+        // analytic own terms: 2 A2_k sw Phi_k[a][b] x (sum of the category-0
+        // partners' A2, summed exactly by the candidate fill pass)
+        const double sa_d = __ldg(&I.own_a2[rank]);
+        if (sa_d != 0.0) {
+          const double fown = (2.0 * __ldg(&P.ftab[k].w) * sw) *
+                              (P.kid == 2 ? root_phi<2>(P, k, a, t) : root_phi<3>(P, k, a, t));
+          add(dk[t], 0, fown * sa_d, fown != 0.0);
         }
       }
-      if (AN) {
-        // analytic own terms of the group's roots: 2 A2_r sw Phi_r[a][b] x sum A2_n
+    }
+    if constexpr (AN) {
+      // ---- category-0 visits of the incident roots, by enumeration
+      for (int g0 = e0; g0 < ((P.dbg & 8) ? e0 : e1); g0 += kMaxInc) {
+        const int ng = min(e1 - g0, kMaxInc);
         __syncthreads();
-        const unsigned sp = S.sa_pres;
-        for (int q = t; q < 3 * (g1 - g0); q += TH) {
-          const int j = q / 3, b = q % 3;
-          if (!((sp >> j) & 1u)) continue;
-          const int it = __ldg(&W.de_items[g0 + j]);
+        if (t < ng) {
+          IncRoot& Rt = S.inc[t];
+          const int it = __ldg(&W.de_items[g0 + t]);
           const int k = it >> 2, a = it & 3;
           const int rank = __ldg(&W.inR[k]);
-          if (rank < 0 || I.cnt[(long long)C_KK * I.nR + rank] == 0) continue;
-          const double sa_d = fix_val3(S.sa[j], ainv);
-          const double fown = (2.0 * __ldg(&P.ftab[k].w) * sw) *
-                              (P.kid == 2 ? root_phi<2>(P, k, a, b) : root_phi<3>(P, k, a, b));
-          const int4 dk4 = __ldg(&P.dofs[k]);
-          add((unsigned)(b == 0 ? dk4.x : (b == 1 ? dk4.y : dk4.z)), 0, fown * sa_d, fown != 0.0);
+          Rt.k = rank >= 0 && I.cnt[(long long)C_KK * I.nR + rank] != 0 ? k : -1;
+          const double2 ck = __ldg(&P.ctr[k]);
+          Rt.cx = ck.x;
+          Rt.cy = ck.y;
+          Rt.r = __ldg(&P.rad[k]);
+          load_tri(P, k, Rt.kx, Rt.ky);
+          tri_points(Rt.kx, Rt.ky, Rt.xk, Rt.yk);
+          double wsum = 0.0;
+#pragma unroll
+          for (int p = 0; p < 7; ++p) wsum += c_rule.wh[p][a];
+          Rt.fkl = -2.0 * __ldg(&P.ftab[k].w) * wsum;
         }
         __syncthreads();
-        for (int i = t; i < kRowGroup * 3; i += TH) (&S.sa[0][0])[i] = 0;
-        if (t == 0) S.sa_pres = 0;
+        if (t == 0) {
+          // the vertex of d (corner a of the first incident element): every
+          // incident root's barycentre lies within its radius of it
+          {
+            const int it = __ldg(&W.de_items[g0]);
+            const int4 e4 = __ldg(&P.elem[it >> 2]);
+            const int a0 = it & 3;
+            const double2 v = __ldg(&P.vtx[a0 == 0 ? e4.x : (a0 == 1 ? e4.y : e4.z)]);
+            S.gvx = v.x;
+            S.gvy = v.y;
+            double rm = 0.0, gs = 0.0;
+            int gp = 0;
+            for (int i = 0; i < ng; ++i) {
+              if (S.inc[i].k < 0) continue;
+              rm = fmax(rm, S.inc[i].r);
+              gs += S.inc[i].fkl;
+              gp |= S.inc[i].fkl != 0.0;
+            }
+            S.grmax = rm;
+            S.gsum_all = gs;
+            S.gpres_all = gp;
+          }
+          // column-grid cell rows within the reach of any contribution:
+          // |x_c - v| <= delta (1 + 1e-9) + r_max(group) + 2 r_max
+          const double cx = S.gvx, cy = S.gvy, R = P.delta * (1.0 + 1e-9) + S.grmax + 2.0 * W.G.rmax;
+          int iy = (int)floor((cy - W.G.oy) / W.G.cs);
+          iy = min(max(iy, 0), W.G.ny - 1);
+          const int span = (int)ceil(R / W.G.cs);
+          int n = 0, tot = 0;
+          for (int yy = max(iy - span, 0); yy <= min(iy + span, W.G.ny - 1) && n < kMaxRowsG; ++yy) {
+            const double ylo = W.G.oy + yy * W.G.cs, yhi = ylo + W.G.cs;
+            const double dy = cy < ylo ? ylo - cy : (cy > yhi ? cy - yhi : 0.0);
+            if (dy > R) continue;
+            const double hw = sqrt(R * R - dy * dy);
+            const int x0 = max((int)floor((cx - hw - W.G.ox) / W.G.cs), 0);
+            const int x1 = min((int)floor((cx + hw - W.G.ox) / W.G.cs), W.G.nx - 1);
+            if (x0 > x1) continue;
+            S.gr0[n] = W.G.cstart[yy * W.G.nx + x0];
+            S.gr1[n] = W.G.cstart[yy * W.G.nx + x1 + 1];
+            S.gpre[n] = tot;
+            tot += S.gr1[n] - S.gr0[n];
+            ++n;
+          }
+          S.gpre[n] = tot;
+          S.ngr = n;
+          S.nrim = 0;
+        }
+        __syncthreads();
+        const int ngr = S.ngr, tot = S.gpre[ngr];
+        const double tc2 = (P.delta * (1.0 + 1e-9)) * (P.delta * (1.0 + 1e-9));  // beyond: neither full nor all-inside
+        const double gvx = S.gvx, gvy = S.gvy, grm = S.grmax, gsum_all = S.gsum_all;
+        const bool gpres_all = S.gpres_all != 0;
+        const double geta = 1e-12 * (P.delta + 4.0 * W.G.rmax);
+        // element level: every visit (k, n) of the group full when
+        // |v - c_n| + 2 r_max(group) + r_n <= delta - margin (|c_k - v| <= r_k);
+        // none full or all-inside when |v - c_n| > delta (1 + 1e-9) + r_max(group)
+        const double eout = P.delta * (1.0 + 1e-9) + grm, eout2 = eout * eout;
+        // column level (|c_n - x_c| <= r_n for each element n at column c):
+        // every element of the column deep, and none of them in the group
+        // (those contain v, so lie within 2 r_max of it)
+        const double cin = P.delta - 2.0 * grm - 2.0 * W.G.rmax - geta, cin2 = cin > 0.0 ? cin * cin : -1.0;
+        const double cnear = 2.0 * W.G.rmax * (1.0 + 1e-9), cnear2 = cnear * cnear;
+        const double cout = eout + W.G.rmax * (1.0 + 1e-9), cout2 = cout * cout;
+        // G(n) = sum of the row factors of the group's category-0 visits (k, n)
+        auto elem_g = [&](int n, double& gs) -> bool {
+          const int4 el = __ldg(&P.elem[n]);
+          if ((el.w & 15) == 0) return false;  // inactive: no visit
+          const double2 cl = __ldg(&P.ctr[n]);
+          const double rl = __ldg(&P.rad[n]);
+          const double dv2 = sumsq(gvx - cl.x, gvy - cl.y);
+          if (dv2 > eout2) return false;
+          const double gin = P.delta - 2.0 * grm - rl - geta;
+          bool deep = gin > 0.0 && dv2 < gin * gin;
+          for (int i = 0; i < ng && deep; ++i) deep = S.inc[i].k != n;
+          if (deep) {
+            gs = gsum_all;
+            return gpres_all;
+          }
+          double g = 0.0;
+          bool pres = false;
+#pragma unroll 1
+          for (int i = 0; i < ng; ++i) {
+            const IncRoot& Rt = S.inc[i];
+            if (Rt.k < 0 || Rt.k == n) continue;
+            VisitDist D(sumsq(Rt.cx - cl.x, Rt.cy - cl.y));
+            if (D.d2 > tc2) continue;
+            bool cat0 = D.within(Rt.r, rl, P.delta);
+            if (!cat0 && P.ball != 2) cat0 = pair_all_in_el(P, Rt.kx, Rt.ky, Rt.xk, Rt.yk, el);
+            if (cat0) {
+              g += Rt.fkl;
+              pres |= Rt.fkl != 0.0;
+            }
+          }
+          gs = g;
+          return pres;
+        };
+        // a column near the rim: its elements one by one (incidence order)
+        auto rim_col = [&](int c) {
+          double v = 0.0;
+          bool pres = false;
+          for (int e = __ldg(&W.de_start[c]); e < __ldg(&W.de_start[c + 1]); ++e) {
+            const int it = __ldg(&W.de_items[e]);
+            const int n = it >> 2, a = it & 3;
+            double gs = 0.0;
+            if (!elem_g(n, gs)) continue;
+            const double4 f = ld_f4(P.ftab + n);
+            const double fa = a == 0 ? f.x : (a == 1 ? f.y : f.z);
+            v += gs * fa;
+            pres |= fa != 0.0;
+          }
+          add((unsigned)c, 0, v, pres);
+        };
+        // phase A: every column -- beyond (skip), deep (all its elements full
+        // partners of every group root: gsum_all x H) or near the rim / the
+        // group (queued for phase B, which runs the element tests densely)
+        for (int q = t; q < tot; q += TH) {
+          if (*(volatile int*)&S.ovf) break;
+          int r = 0;
+          while (q >= S.gpre[r + 1]) ++r;
+          const int jv = S.gr0[r] + (q - S.gpre[r]);
+          const double4 cp = ld_f4(W.G.cpos + jv);
+          const double dc2 = sumsq(gvx - cp.x, gvy - cp.y);
+          if (dc2 > cout2) continue;
+          if (dc2 < cin2 && dc2 > cnear2) {
+            add((unsigned)__ldg(&W.G.cid[jv]), 0, gsum_all * cp.z, gpres_all && cp.w != 0.0);
+          } else {
+            const int slot = atomicAdd(&S.nrim, 1);
+            if (slot < kRimCap) S.rimq[slot] = jv;
+            else rim_col(__ldg(&W.G.cid[jv]));  // (queue full: in place)
+          }
+        }
+        __syncthreads();
+        const int nrim = min(S.nrim, kRimCap);
+        for (int q = t; q < nrim; q += TH) {
+          if (*(volatile int*)&S.ovf) break;
+          rim_col(__ldg(&W.G.cid[S.rimq[q]]));
+        }
       }
     }
     // ---- touching-pair (singular) entries of the rows
@@ -2309,6 +2655,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
     if (t == 0) O.ovf[atomicAdd(O.novf, 1u)] = (int)d;
     return;
   }
+  if (P.dbg & 16) return;  // (timing experiments)
   // ---- sort the table by column and write each row
   unsigned key[IT], sl[IT];
   const unsigned PAD = (1u << W.key_bits) - 1u;
@@ -2830,6 +3177,11 @@ struct nlg_plan {
   int4* grid_el = nullptr;
   double2* grid_ctr = nullptr;
   double* grid_rad = nullptr;
+  double4* grid_ft = nullptr;
+  int4* grid_dof = nullptr;
+  int* col_start = nullptr;   // analytic: column grid
+  int* col_id = nullptr;
+  double4* col_pos = nullptr;
   // load vector support
   int* act = nullptr;
   int nact = -1;
@@ -2955,6 +3307,7 @@ nlg_status prep(nlg_plan* pl) {
   Grid G;
   G.ox = ox; G.oy = oy; G.cs = cs;
   G.reach = reach;
+  G.rmax = rmax;
   G.span = (int)ceil(reach / cs);
   G.nx = (int)floor(ext_x / cs) + 1;
   G.ny = (int)floor(ext_y / cs) + 1;
@@ -2990,12 +3343,55 @@ nlg_status prep(nlg_plan* pl) {
   CK(cudaMallocAsync(&pl->grid_ctr, sizeof(double2) * std::max(K, 1), st));
   CK(cudaMallocAsync(&pl->grid_rad, sizeof(double) * std::max(K, 1), st));
   if (K) {
-    k_grid_gather<<<grid_for(K, 256), 256, 0, st>>>(P, pl->grid_items, K, pl->grid_el, pl->grid_ctr, pl->grid_rad);
+    if (P.analytic && !pl->grid_ft) {
+      CK(cudaMallocAsync(&pl->grid_ft, sizeof(double4) * K, st));
+      CK(cudaMallocAsync(&pl->grid_dof, sizeof(int4) * K, st));
+    }
+    k_grid_gather<<<grid_for(K, 256), 256, 0, st>>>(P, pl->grid_items, K, pl->grid_el, pl->grid_ctr, pl->grid_rad,
+                                                     P.analytic ? pl->grid_ft : nullptr, pl->grid_dof);
     LAUNCHED();
   }
   G.gel = pl->grid_el;
   G.gctr = pl->grid_ctr;
   G.grad = pl->grid_rad;
+  G.gft = P.analytic ? pl->grid_ft : nullptr;
+  G.gdof = P.analytic ? pl->grid_dof : nullptr;
+  G.cstart = nullptr;
+  G.cid = nullptr;
+  G.cpos = nullptr;
+  if (P.analytic) {
+    const int nb = (int)(P.J / P.nc);
+    DevBuf ck, ck2, cv, cp;
+    CK(ck.alloc(sizeof(unsigned) * std::max(nb, 1), st));
+    CK(ck2.alloc(sizeof(unsigned) * std::max(nb, 1), st));
+    CK(cv.alloc(sizeof(int) * std::max(nb, 1), st));
+    CK(cp.alloc(sizeof(double4) * std::max(nb, 1), st));
+    if (!pl->col_start) {
+      CK(cudaMallocAsync(&pl->col_start, sizeof(int) * (ncell + 1), st));
+      CK(cudaMallocAsync(&pl->col_id, sizeof(int) * std::max(nb, 1), st));
+      CK(cudaMallocAsync(&pl->col_pos, sizeof(double4) * std::max(nb, 1), st));
+    }
+    if (nb) {
+      k_col_keys<<<grid_for(nb, 256), 256, 0, st>>>(P, G, pl->de_start, pl->de_items, nb, ck.as<unsigned>(),
+                                                    cv.as<int>(), cp.as<double4>());
+      LAUNCHED();
+      size_t tb2 = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, ck.as<unsigned>(), ck2.as<unsigned>(), cv.as<int>(), pl->col_id,
+                                         nb, 0, bits, st));
+      DevBuf tmp2;
+      CK(tmp2.alloc(tb2, st));
+      CK(cub::DeviceRadixSort::SortPairs(tmp2.p, tb2, ck.as<unsigned>(), ck2.as<unsigned>(), cv.as<int>(), pl->col_id,
+                                         nb, 0, bits, st));
+      g_launches += 4;
+      k_col_gather<<<grid_for(nb, 256), 256, 0, st>>>(pl->col_id, nb, cp.as<double4>(), pl->col_pos);
+      LAUNCHED();
+    }
+    k_cell_ranges<<<grid_for(ncell + 1, 256), 256, 0, st>>>(ck2.as<unsigned>(), nb, ncell, pl->col_start);
+    LAUNCHED();
+    G.cstart = pl->col_start;
+    G.cid = pl->col_id;
+    G.cpos = pl->col_pos;
+  }
   pl->G = G;
   pl->prepped = true;
   return NLG_OK;
@@ -3059,10 +3455,17 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
     const long long chunks = (nP + 1) / 2;
     constexpr int NWB = clip_warps<KID>();
     const unsigned g = (unsigned)std::min<long long>((chunks + NWB - 1) / NWB, 148LL * 256 / NWB);
+    // warp-local clipping for the closed-form kernels (NLG_CLIP_WL=0: block queue)
+    static const bool wl_env = !(getenv("NLG_CLIP_WL") && atoi(getenv("NLG_CLIP_WL")) == 0);
+    const bool wl = (KID == 2 || KID == 3) && P.path == 0 && wl_env;
     if (P.ball == 2) {
       const int smem = NWB * (int)sizeof(ClipWarp<KID, true>) + (int)sizeof(ClipBlock<KID>);
       CK(cudaFuncSetAttribute(k_clipped<KID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       k_clipped<KID, true><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
+    } else if (wl) {
+      const int smem = NWB * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
+      CK(cudaFuncSetAttribute(k_clipped<KID, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_clipped<KID, false, true><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
     } else {
       const int smem = NWB * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
       CK(cudaFuncSetAttribute(k_clipped<KID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -3335,6 +3738,7 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   W.sstart = sstart.as<long long>();
   W.vmax = d_vmax;
   W.fmax = pl->fmax;
+  W.G = pl->G;
   RowOut O;
   O.col = col.as<int>();
   O.val = val.as<double>();
@@ -3427,11 +3831,13 @@ struct Timing {
 nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget, bool allow_sample,
                      std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
                      unsigned long long* d_counters, unsigned long long* d_err, bool* need_split,
-                     std::vector<long long>* cuts) {
+                     std::vector<long long>* cuts, bool no_analytic, bool* analytic_fallback) {
   *need_split = false;
+  *analytic_fallback = false;
   cuts->clear();
   ArenaScope arena_scope(pl);
   Params P = pl->P;
+  if (no_analytic) P.analytic = 0;  // (a retried batch: every pair integrated per record)
   P.row_lo = row_lo;
   P.row_hi = row_hi;
   P.narrow = (unsigned long long)(row_hi - row_lo) * (unsigned long long)P.J < 0xffffffffull;
@@ -3553,7 +3959,7 @@ count_pass:
     const bool rows_plan = pl->use_rows;
     const long long coo_ub = (long long)nR * E + (nS[0] + nS[1] + nS[2]) * 36LL * NC * NC +
                              (rows_plan ? 0LL : (long long)(kRunFrac * (double)(nUB * 2 * E))) + 1;
-    const long long ent_ub = rows_plan ? (long long)(kEntFrac * (double)(nUB * 2 * E)) : 0LL;
+    const long long ent_ub = rows_plan ? ent_estimate(P, nUB, tot[C_EPI], nR) : 0LL;
     const long long side_bytes = 8LL * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));  // kkv + klv
     const long long bytes = nStUB * 2 * side_bytes + coo_ub * (16 + 16) + ent_ub * 12 +
                             (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 + nUB * 24;
@@ -3582,7 +3988,8 @@ count_pass:
       if (nR)
         k_root_cost<<<grid_for(nR, 256), 256, 0, s>>>(P, roots.as<int>(), nR, cnt.as<int>(), rec_bytes, store_bytes, sing_bytes,
                                                       root_bytes, rows_plan ? 0.0 : kRunFrac * 2 * E, 36.0 * NC * NC,
-                                                      rcost.as<unsigned long long>(), (double)stride);
+                                                      rcost.as<unsigned long long>(), (double)stride,
+                                                      rows_plan ? kEntPerEpi * 0.5 * NC * 12.0 : 0.0);
       LAUNCHED();
       std::vector<unsigned long long> hcost((size_t)3 * nrows);
       CK(cudaMemcpyAsync(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, cudaMemcpyDeviceToHost, s));
@@ -3617,7 +4024,8 @@ fits:
     LAUNCHED();
   }
   // ---- fill: records into per-root upper-bound ranges, then per-root compaction
-  DevBuf comb, lists;
+  DevBuf comb, lists, own_a2;
+  CK(own_a2.alloc(sizeof(double) * (size_t)std::max(nR, 1), s));  // analytic: per-root partner areas
   CK(comb.alloc(sizeof(int2) * (size_t)std::max(1LL, nUB), s));
   CK(lists.alloc(sizeof(int2) * (size_t)std::max(1LL, nUB + nS[0] + nS[1] + nS[2]), s));
   int2* lsing = lists.as<int2>() + nUB;
@@ -3625,7 +4033,7 @@ fits:
   if (nR) {
     k_candidates<true><<<std::max(cand_blocks, 1), 256, 0, s>>>(
         P, pl->G, roots.as<int>(), nR, needA.as<unsigned char>(), inR.as<int>(), cnt.as<int>(),
-        off.as<long long>(), comb.as<int2>(), ls[0], ls[1], ls[2]);
+        off.as<long long>(), comb.as<int2>(), ls[0], ls[1], ls[2], 1, own_a2.as<double>());
     LAUNCHED();
   }
   // actual per-root full / clipped counts -> list offsets (columns 4, 5 of
@@ -3768,6 +4176,7 @@ fits:
   RI.analytic = P.analytic;
   RI.inR = inR.as<int>();
   RI.kkv = O.kkv;
+  RI.own_a2 = own_a2.as<double>();
   RI.klv = O.klv;
   const long long nrows = row_hi - row_lo;
   Csr piece{row_lo, row_hi, 0, nullptr, nullptr, nullptr};
@@ -3776,7 +4185,7 @@ fits:
   if (rows_mode) {
     // ---- merge stage W: per-row fixed-point tables -> CSR rows
     bool fb = false, ns = false;
-    const long long ent_cap = (long long)(kEntFrac * (double)(nvis * 2 * E)) + nR * E + nsing_slots + 1024;
+    const long long ent_cap = ent_estimate(P, nvis, tot[C_EPI], nR) + nR * E + nsing_slots + 1024;
     void* sk = P.narrow ? (void*)(reinterpret_cast<unsigned*>(keys.p) + sbase)
                         : (void*)(keys.as<unsigned long long>() + sbase);
     // distinct columns of a row ~ half the visits of a root (the partner vertices)
@@ -3795,6 +4204,12 @@ fits:
     merged = !fb;
     if (fb && r_base + r_cap >= (1LL << 31) && row_hi - row_lo > P.nc) {  // stage R's 32-bit sorts
       *need_split = true;
+      return NLG_OK;
+    }
+    if (fb && P.analytic) {
+      // stage R needs every visit's record: the batch runs again without the
+      // analytic enumeration (full pairs integrated per record)
+      *analytic_fallback = true;
       return NLG_OK;
     }
     if (fb) {  // stage R + sort: the COO with its run buffer (singular slots carried over)
@@ -4085,9 +4500,11 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   // NLG_NO_ANALYTIC: integrate the full pairs of kid 2 / 3 per record (A/B and tests)
   // (nonfinite kernel parameters: every pair is integrated per record, so the
   // failing visit is detected and named -- the analytic sums carry no check)
-  P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC") &&
-               std::isfinite(P.cst) && std::isfinite(P.kp0) && std::isfinite(P.kp1);
   pl->use_rows = !(getenv("NLG_MERGE") && !strcmp(getenv("NLG_MERGE"), "sort"));
+  // (the analytic visits are enumerated by the stage-W row merge: stage R
+  // integrates every pair per record)
+  P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC") &&
+               std::isfinite(P.cst) && std::isfinite(P.kp0) && std::isfinite(P.kp1) && pl->use_rows;
   Rule7 hr;
   for (int p = 0; p < 7; ++p) {
     hr.op[p][0] = pb->op[2 * p]; hr.op[p][1] = pb->op[2 * p + 1];
@@ -4202,7 +4619,8 @@ void nlg_plan_destroy(nlg_plan* pl) {
   cudaStream_t s = pl->stream;
   void* ptrs[] = {pl->vtx,        pl->elem,       pl->dofs,     pl->ctr,      pl->rad,     pl->ftab,
                   pl->fmax,       pl->de_start,   pl->de_items, pl->grid_start, pl->grid_items, pl->act,
-                  pl->grid_el,    pl->grid_ctr,   pl->grid_rad};
+                  pl->grid_el,    pl->grid_ctr,   pl->grid_rad, pl->grid_ft, pl->grid_dof,
+                  pl->col_start,  pl->col_id,     pl->col_pos};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   for (auto& f : pl->sing_tab)
@@ -4268,17 +4686,26 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   Counters ctr{};
   Timing tm;
   // row batches: a work list of ranges, split in halves when over budget
-  std::vector<std::pair<long long, long long>> todo;
-  if (row_hi > row_lo) todo.push_back({row_lo, row_hi});
+  struct Range {
+    long long first, second;
+    bool plain;  // without the analytic enumeration (after a stage-W overflow)
+  };
+  std::vector<Range> todo;
+  if (row_hi > row_lo) todo.push_back({row_lo, row_hi, false});
   while (!todo.empty()) {
     auto rg = todo.back();
     todo.pop_back();
-    bool split = false;
+    bool split = false, an_fb = false;
     std::vector<long long> cuts;
     const bool first_attempt = st.n_batches == 0 && st.n_replans == 0;
     rc = run_batch(pl, rg.first, rg.second, budget, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
-                   derr.as<unsigned long long>(), &split, &cuts);
+                   derr.as<unsigned long long>(), &split, &cuts, rg.plain, &an_fb);
     if (rc) break;
+    if (an_fb) {
+      todo.push_back({rg.first, rg.second, true});
+      st.n_replans += 1;
+      continue;
+    }
     if (split) {
       if (cuts.empty()) cuts.push_back(rg.first + (rg.second - rg.first) / (2 * pl->P.nc) * pl->P.nc);
       if (cuts.front() <= rg.first) cuts.front() = rg.first + pl->P.nc;
@@ -4286,11 +4713,11 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
       long long hi = rg.second;
       for (size_t c = cuts.size(); c-- > 0;) {
         if (cuts[c] > rg.first && cuts[c] < hi) {
-          todo.push_back({cuts[c], hi});
+          todo.push_back({cuts[c], hi, rg.plain});
           hi = cuts[c];
         }
       }
-      todo.push_back({rg.first, hi});
+      todo.push_back({rg.first, hi, rg.plain});
       st.n_replans += 1;
     }
   }
