@@ -333,14 +333,22 @@ constexpr int kEmitA = 1 << 30;
 constexpr int kEmitB = (int)(1u << 31);
 constexpr int kIdMask = (1 << 30) - 1;
 
-constexpr int kFixBits = 62;  // bound x 2^S = 2^62: a term is one int64, 2^33 terms per cell below 2^95
-// Fixed point: t = rint(v 2^S), |t| <= 2^62, summed exactly as a 96-bit two's
+constexpr int kFixBits = 72;  // bound x 2^S = 2^72: 2^23 contributions per cell below 2^95
+// Fixed point: t = rint(v 2^S), |t| <= 2^72, summed exactly as a 96-bit two's
 // complement integer (three 32-bit limbs in shared memory -- native 32-bit
 // atomics; 64-bit shared atomics are CAS loops -- with the carries propagated
 // by the adding thread; __int128 in registers), so a sum does not depend on
-// the order of its terms.
+// the order of its terms.  (The bound can exceed the largest term by a few
+// powers of two -- the analytic own terms -- so the resolution 2^-72 of the
+// bound keeps ~2^-60 of every row's entries.)
 using fix_t = __int128;
-__device__ __forceinline__ fix_t fix_of(double v, double scale) { return (fix_t)__double2ll_rn(v * scale); }
+__device__ __forceinline__ fix_t fix_of(double v, double scale) {
+  const double t = rint(v * scale);
+  const double hd = floor(t * 0x1p-40);
+  const long long h = __double2ll_rz(hd);
+  const long long l = __double2ll_rz(fma(hd, -0x1p40, t));  // exact: t and hd 2^40 share the grid of t
+  return ((fix_t)h << 40) + (fix_t)l;
+}
 __device__ __forceinline__ double fix_val3(const unsigned* c, double inv) {
   const double v = fma((double)(int)c[2], 0x1p64, fma((double)c[1], 0x1p32, (double)c[0]));
   return v * inv;
@@ -415,31 +423,49 @@ __device__ __forceinline__ bool pair_all_in(const Params& P, const double* kx, c
   return true;
 }
 
-// Per-item truncation class of a clipped pair, with the reference's exact
-// predicates: every inner vertex inside the widened ball of every outer
-// point (the clip returns the triangle itself, _geom_scalar.py:53-66) or the
-// inner element's bounding disk beyond the ball by a margin no rounding can
-// bridge (the clip is empty).  Returns 2 if all 14 items are "inside", 1 if
-// all are empty, 0 otherwise.
-__device__ __noinline__ int pair_trunc_class(const Params& P, const double* kx, const double* ky,
-                                                const double* xk, const double* yk, double2 ck, double rk,
-                                                const double* lx, const double* ly, double2 cl, double rl) {
-  if (P.ball == 2) return 0;
+// Truncation class of a clipped pair, in two parts with the reference's
+// exact predicates: "inside" -- every inner vertex inside the widened ball of
+// every outer point, both ways (the clips return the triangles themselves,
+// _geom_scalar.py:53-66) -- and "far" -- the inner element's bounding disk
+// beyond the ball of every outer point by a margin no rounding can bridge
+// (every clip is empty).  Out of line: only pairs near the ball's rim get here.
+__device__ __noinline__ bool pair_inside(const Params& P, const double* kx, const double* ky, const double* xk,
+                                         const double* yk, const double* lx, const double* ly) {
+  if (P.ball == 2) return false;
+  const double rad = mul(P.delta, 1.0 + kBallTieRel);
+  const double r2 = mul(rad, rad), hi = r2 * (1.0 + 1e-10), lo = r2 * (1.0 - 1e-10);
+  bool clear = true;  // (see pair_all_in: the vertex distances decide all but near-ties)
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double d2 = sumsq(lx[i] - kx[a], ly[i] - ky[a]);
+      if (d2 > hi) return false;
+      clear = clear && d2 < lo;
+    }
+  if (clear) return true;
   double xl[7], yl[7];
   tri_points(lx, ly, xl, yl);
-  if (pair_all_in(P, kx, ky, xk, yk, lx, ly, xl, yl)) return 2;
-  const double far2k = (P.delta * (1.0 + 1e-6) + rk) * (P.delta * (1.0 + 1e-6) + rk);
-  const double far2l = (P.delta * (1.0 + 1e-6) + rl) * (P.delta * (1.0 + 1e-6) + rl);
+  return pair_all_in(P, kx, ky, xk, yk, lx, ly, xl, yl);
+}
+
+__device__ __noinline__ bool pair_far(const Params& P, const double* xk, const double* yk, double2 ck, double rk,
+                                      const double* lx, const double* ly, double2 cl, double rl) {
+  if (P.ball == 2) return false;
   {
     // every rule point of k lies within r_k of c_k (and of l within r_l of
     // c_l): the barycentre distance decides "all far" outside a band of width
-    // 2 max(r_k, r_l) (margins 1e-9 relative cover the roundings)
+    // 2 min(r_k, r_l) (margins 1e-9 relative cover the roundings)
     const double d2 = (cl.x - ck.x) * (cl.x - ck.x) + (cl.y - ck.y) * (cl.y - ck.y);
     const double fo = P.delta * (1.0 + 1e-6) + rl + rk, fi = P.delta * (1.0 + 1e-6) + rl - rk;
     const double gi = P.delta * (1.0 + 1e-6) + rk - rl;
-    if (d2 > fo * fo * (1.0 + 1e-9)) return 1;
-    if ((fi > 0.0 && d2 < fi * fi * (1.0 - 1e-9)) || (gi > 0.0 && d2 < gi * gi * (1.0 - 1e-9))) return 0;
+    if (d2 > fo * fo * (1.0 + 1e-9)) return true;
+    if ((fi > 0.0 && d2 < fi * fi * (1.0 - 1e-9)) || (gi > 0.0 && d2 < gi * gi * (1.0 - 1e-9))) return false;
   }
+  const double far2k = (P.delta * (1.0 + 1e-6) + rk) * (P.delta * (1.0 + 1e-6) + rk);
+  const double far2l = (P.delta * (1.0 + 1e-6) + rl) * (P.delta * (1.0 + 1e-6) + rl);
+  double xl[7], yl[7];
+  tri_points(lx, ly, xl, yl);
   bool all_far = true;
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
@@ -448,7 +474,7 @@ __device__ __noinline__ int pair_trunc_class(const Params& P, const double* kx, 
     const double dlx = ck.x - xl[p], dly = ck.y - yl[p];
     all_far = all_far && dkx * dkx + dky * dky > far2l && dlx * dlx + dly * dly > far2k;
   }
-  return all_far ? 1 : 0;
+  return all_far;
 }
 
 // pair_all_in of root k (vertices, rule points) and element el, out of line
@@ -553,16 +579,18 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     if (!(needAk || (lroot && needA[l]))) return -1;
     return full ? 0 : 1;
   }
-  // exact truncation class of the pair (symmetric in k, l)
-  int tcls = 0;
-  if (k != l && (!full || !full_lk)) {
-    double lx[3], ly[3];
+  // exact truncation class of the pair (symmetric in k, l): "inside" now,
+  // "far" only if this root would make the record
+  const bool lgeom = k != l && (!full || !full_lk) && P.ball != 2;
+  double lx[3], ly[3];
+  bool tin = false;
+  if (lgeom) {
     const double2 a = __ldg(&P.vtx[el.x]), b = __ldg(&P.vtx[el.y]), c = __ldg(&P.vtx[el.z]);
     lx[0] = a.x; ly[0] = a.y; lx[1] = b.x; ly[1] = b.y; lx[2] = c.x; ly[2] = c.y;
-    tcls = pair_trunc_class(P, kx, ky, xk, yk, ck, rk, lx, ly, cl, rl);
+    tin = pair_inside(P, kx, ky, xk, yk, lx, ly);
   }
   // (analytic mode: the identical pair keeps its stored blocks on the clipped path)
-  const int cat_kl = (full || tcls == 2) && !(P.analytic && k == l) ? 0 : 1;
+  const int cat_kl = (full || tin) && !(P.analytic && k == l) ? 0 : 1;
   if (P.analytic) {
     if (cat_kl == 0) {
       an = true;
@@ -570,10 +598,11 @@ __device__ __forceinline__ int classify(const Params& P, int k, int4 ek, double2
     }
     if (l_makes) return -1;
   }
-  if (tcls == 1) return -1;  // every item empty in both visits: nothing to emit
+  // every item empty in both visits: nothing to emit
+  if (lgeom && !tin && pair_far(P, xk, yk, ck, rk, lx, ly, cl, rl)) return -1;
   bool shared = false;
   if (lroot) {
-    const int cat_lk = full_lk || tcls == 2 ? 0 : 1;
+    const int cat_lk = full_lk || tin ? 0 : 1;
     shared = !rej_lk && cat_lk == cat_kl;
   }
   if (shared && inR[l] >= 0 && l < k) return -1;  // root l produces the record
@@ -668,7 +697,18 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const unsigned m = __ballot_sync(0xffffffffu, q0 == q);
-            if (q0 == q) lists[q][base[q] + __popc(m & lt)] = make_int2(k | (cat == 1 ? kCatClip : 0), l | fl);
+            if (q0 == q) {
+              // canonical orientation: a pair record is always (smaller,
+              // larger) element -- its blocks are then computed identically
+              // whichever root (and batch, and GPU) produces it, and the row
+              // split cannot change a value.  A root's own visit of a smaller
+              // partner becomes the record's side B.
+              int2 rec = make_int2(k | (cat == 1 ? kCatClip : 0), l | fl);
+              if (q == 0 && l < k)
+                rec = make_int2(l | (cat == 1 ? kCatClip : 0),
+                                k | ((fl & kEmitA) ? kEmitB : 0) | ((fl & kEmitB) ? kEmitA : 0));
+              lists[q][base[q] + __popc(m & lt)] = rec;
+            }
             base[q] += __popc(m);
           }
         }
@@ -869,7 +909,16 @@ struct VisitOut {
   unsigned long long* counters;
   unsigned long long* errpair;
   unsigned long long* vmax;  // max |value| written (bits of a nonnegative double), for the merge's fixed point
+  unsigned long long* emax;  // [K] per element: max |value| of the emitted sides of its visits (root), as bits
 };
+
+// A root's bound for the merge's fixed-point scale: the largest |value| of
+// its emitted record sides.  A root's sides are the same whichever batch
+// evaluates it, so the scale of each row -- from its incident elements'
+// bounds -- and with it every sum does not depend on the row split.
+__device__ __forceinline__ void elem_bound(unsigned long long* emax, int e, double m) {
+  if (m > 0.0 && m <= 1e300) atomicMax(&emax[e], (unsigned long long)__double_as_longlong(m));
+}
 
 // max of nonnegative doubles (as bit patterns) over the warp, one atomic
 __device__ __forceinline__ void warp_max_abs(double m, unsigned long long* dst) {
@@ -895,15 +944,18 @@ __device__ __forceinline__ void emit_side(const Params& P, const VisitOut& O, lo
                                           int root, int nb, const double* kk, const double* kl, double& vm) {
   using B = Blk<NC>;
   bool bad = false;
+  double sm = 0.0;
 #pragma unroll
   for (int e = 0; e < B::E; ++e) {
     const int I = e / B::N3, J = e % B::N3;
     if (I <= J) O.kkv[slot * B::NKK + B::sym(I, J)] = on ? kk[e] : 0.0;
     bad |= nonfinite(kk[e]) | nonfinite(kl[e]);
     O.klv[slot * B::KLS + B::kl(I, J)] = on ? emit_val(kl[e]) : 0.0;
-    if (on) vm = fmax(vm, fmax(fabs(kk[e]), fabs(kl[e])));
+    if (on) sm = fmax(sm, fmax(fabs(kk[e]), fabs(kl[e])));
   }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
+  vm = fmax(vm, sm);
+  if (on) elem_bound(O.emax, root, sm);
 }
 
 __device__ __forceinline__ double4 ld_f4(const double4* p) {
@@ -974,6 +1026,7 @@ __device__ __forceinline__ void emit_peri(const Params& P, const VisitOut& O, lo
                                           bool transpose, double& vm) {
   using B = Blk<2>;
   bool bad = false;
+  double sm = 0.0;
 #pragma unroll
   for (int I = 0; I < 6; ++I)
 #pragma unroll
@@ -983,14 +1036,16 @@ __device__ __forceinline__ void emit_peri(const Params& P, const VisitOut& O, lo
         const double kk = c2 * K[sym3i(a, b)][u];
         O.kkv[slot * B::NKK + B::sym(I, J)] = on ? kk : 0.0;
         bad |= nonfinite(kk);
-        if (on) vm = fmax(vm, fabs(kk));
+        if (on) sm = fmax(sm, fabs(kk));
       }
       const double kl = -c2 * (transpose ? G[b][a][u] : G[a][b][u]);
       O.klv[slot * B::KLS + B::kl(I, J)] = on ? emit_val(kl) : 0.0;
       bad |= nonfinite(kl);
-      if (on) vm = fmax(vm, fabs(kl));
+      if (on) sm = fmax(sm, fabs(kl));
     }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
+  vm = fmax(vm, sm);
+  if (on) elem_bound(O.emax, root, sm);
 }
 
 // one side of a symmetric scalar full record (full_pair_sym1): own block c2 K,
@@ -1000,6 +1055,7 @@ __device__ __forceinline__ void emit_sym1(const Params& P, const VisitOut& O, lo
                                           double& vm) {
   using B = Blk<1>;
   bool bad = false;
+  double sm = 0.0;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -1008,14 +1064,16 @@ __device__ __forceinline__ void emit_sym1(const Params& P, const VisitOut& O, lo
         const double kk = c2 * K[sym3i(a, b)];
         O.kkv[slot * B::NKK + B::sym(a, b)] = on ? kk : 0.0;
         bad |= nonfinite(kk);
-        if (on) vm = fmax(vm, fabs(kk));
+        if (on) sm = fmax(sm, fabs(kk));
       }
       const double kl = -c2 * (transpose ? G[b][a] : G[a][b]);
       O.klv[slot * B::KLS + B::kl(a, b)] = on ? emit_val(kl) : 0.0;
       bad |= nonfinite(kl);
-      if (on) vm = fmax(vm, fabs(kl));
+      if (on) sm = fmax(sm, fabs(kl));
     }
   report_nonfinite(on && bad, root, nb, P.K, O.errpair);
+  vm = fmax(vm, sm);
+  if (on) elem_bound(O.emax, root, sm);
 }
 
 // full records, one thread each: the 7x7 point-pair matrix gives both visits
@@ -1744,6 +1802,7 @@ __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID ==
     const FoldSrc<KID> fs(Wi, ohi, si);
     const bool m1 = mi == 1, m2 = ivalid && mi == 2;
     constexpr int NBATCH = (C::NVAL + 31) / 32;  // reduce-scatter batches of 32 values
+    double smA = 0.0, smB = 0.0;  // the sides' largest |value| (the roots' merge bounds)
 #pragma unroll
     for (int bt = 0; bt < NBATCH; ++bt) {
       double vals[32];
@@ -1786,6 +1845,8 @@ __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID ==
         if (on) {
           report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
           vmx = fmax(vmx, fabs(val));
+          if (side == 0) smA = fmax(smA, fabs(val));
+          else smB = fmax(smB, fabs(val));
         }
         if (w < C::NKK) {
           O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;  // unique (I <= J) order
@@ -1793,6 +1854,287 @@ __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID ==
           const int e = w - C::NKK, I = e / N3, J = e % N3;
           O.klv[slot * Blk<NC>::KLS + Blk<NC>::kl(I, J)] = on ? emit_val(val) : 0.0;
         }
+      }
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {  // within the record's 16 lanes
+      smA = fmax(smA, __shfl_xor_sync(0xffffffffu, smA, o));
+      smB = fmax(smB, __shfl_xor_sync(0xffffffffu, smB, o));
+    }
+    if (r == 0 && vok) {
+      elem_bound(O.emax, rk, smA);
+      elem_bound(O.emax, rl, smB);
+    }
+    __syncwarp();
+  }
+  warp_max_abs(vmx, O.vmax);
+  warp_add_ll((unsigned long long)n_eval0, &O.counters[K_EVAL_M0]);
+  warp_add_ll((unsigned long long)n_out0, &O.counters[K_OUT_M0]);
+  warp_add_ll((unsigned long long)n_eval1, &O.counters[K_EVAL_M1]);
+  warp_add_ll((unsigned long long)n_out1, &O.counters[K_OUT_M1]);
+  warp_add_ll((unsigned long long)n_eval2, &O.counters[K_EVAL_M2]);
+  warp_add_ll((unsigned long long)n_out2, &O.counters[K_OUT_M2]);
+}
+
+// ---------------------------------------------------------------------
+// Clipped records of the constant / affine kernels on the standard path
+// (closed-form sub-triangle moments): one warp works alone on four records
+// per round -- 56 sweep items in 64 slots, two per lane -- with a warp-local
+// clip queue, so the ~30 items that need clipping run on ~30 of the 32 lanes
+// and no warp ever waits for another (no block barriers).  Same predicates,
+// same arithmetic in the same order as k_clipped's closed-form path.
+// Slot s: record s >> 4 of the round, item s & 15 (sweep m, outer point p).
+// ---------------------------------------------------------------------
+template <int KID>
+struct CfWarp {
+  double px[64][kMaxPoly], py[64][kMaxPoly];
+  double xo[64][2];
+  double W[64];
+  double tri[4][2][7];  // [record][inner side]: o.x o.y e1x e1y e2x e2y idet
+  double tv[4][2][6];   // [record][inner side]: the inner triangle's vertices x0 x1 x2 y0 y1 y2
+  unsigned char pm[64];
+  unsigned char nv[64];
+  unsigned char q[64];  // clip queue (slots)
+  int vk[4], vl[4], fl[4];
+  int4 ek[4], el[4];
+};
+template <int KID, int NWB, int MINB>
+__global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const int2* __restrict__ list, VisitOut O) {
+  static_assert(KID == 2 || KID == 3, "closed-form path: constant / affine kernels");
+  using C = ClipCfg<KID>;
+  constexpr int NC = 1, N3 = 3;
+  extern __shared__ __align__(16) unsigned char cf_smem[];
+  CfWarp<KID>& S = reinterpret_cast<CfWarp<KID>*>(cf_smem)[threadIdx.x >> 5];
+  const int lane = lane_id();
+  const long long nround = (O.nlist + 3) / 4;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  unsigned n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;
+  double vmx = 0.0;
+  const int r = lane & 15, vs = lane >> 4;
+  // software pipeline: lane r < 4 fetches record r of the next round
+  int2 pnext = make_int2(0, 0);
+  int4 eknext = make_int4(0, 0, 0, 0), elnext = eknext;
+  auto fetch = [&](long long rdn) {
+    if (lane < 4) {
+      const long long v = rdn * 4 + lane;
+      if (rdn < nround && v < O.nlist) {
+        pnext = list[v];
+        eknext = __ldg(&P.elem[pnext.x & kIdMask]);
+        elnext = __ldg(&P.elem[pnext.y & kIdMask]);
+      }
+    }
+  };
+  fetch(w0);
+  for (long long rd = w0; rd < nround; rd += nw) {
+    // ---- the round's four records and their element records
+    if (lane < 4 && rd * 4 + lane < O.nlist) {
+      S.vk[lane] = pnext.x & kIdMask;
+      S.vl[lane] = pnext.y & kIdMask;
+      S.fl[lane] = pnext.y & ~kIdMask;
+      S.ek[lane] = eknext;
+      S.el[lane] = elnext;
+    }
+    __syncwarp();
+    fetch(rd + nw);
+    // ---- classify both slots of the lane; queue the ones that need a clip
+    int qn = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rec = vs + 2 * h, sl = lane + 32 * h;
+      const long long v = rd * 4 + rec;
+      bool valid = v < O.nlist && r < 14;
+      const int k = valid ? S.vk[rec] : 0, l = valid ? S.vl[rec] : 0;
+      int m = r >= 7 ? 1 : 0;
+      const int p = r % 7;
+      if (valid && k == l) {
+        if (m == 1) valid = false;
+        m = 2;
+      }
+      bool need_clip = false;
+      int nv = 0;
+      if (valid) {
+        const int4 ek = S.ek[rec], el = S.el[rec];
+        double ox[3], oy[3], ix[3], iy[3];
+        {
+          const int4 eo = m == 1 ? el : ek, ei = m == 1 ? ek : el;
+          const double2 a0 = __ldg(&P.vtx[eo.x]), a1 = __ldg(&P.vtx[eo.y]), a2 = __ldg(&P.vtx[eo.z]);
+          const double2 b0 = __ldg(&P.vtx[ei.x]), b1 = __ldg(&P.vtx[ei.y]), b2 = __ldg(&P.vtx[ei.z]);
+          ox[0] = a0.x; oy[0] = a0.y; ox[1] = a1.x; oy[1] = a1.y; ox[2] = a2.x; oy[2] = a2.y;
+          ix[0] = b0.x; iy[0] = b0.y; ix[1] = b1.x; iy[1] = b1.y; ix[2] = b2.x; iy[2] = b2.y;
+        }
+        const double e1x = ox[1] - ox[0], e2x = ox[2] - ox[0], e1y = oy[1] - oy[0], e2y = oy[2] - oy[0];
+        const double x0 = __dadd_rn(__dadd_rn(ox[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+        const double x1 = __dadd_rn(__dadd_rn(oy[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+        const int inner_el = m == 1 ? k : l;
+        const double2 ci = __ldg(&P.ctr[inner_el]);
+        const double reach = P.delta * (1.0 + 1e-6) + __ldg(&P.rad[inner_el]);
+        const double dcx = ci.x - x0, dcy = ci.y - x1;
+        const bool far = P.ball != 2 && dcx * dcx + dcy * dcy > reach * reach;
+        if (!far) {
+          bool inside = P.ball != 2;
+          if (inside) {
+            const double rad = mul(P.delta, 1.0 + kBallTieRel), r2b = mul(rad, rad);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) inside = inside && __dsub_rn(sumsq(ix[i] - x0, iy[i] - x1), r2b) <= 0.0;
+          }
+          if (inside) {
+            double* qx = S.px[sl];
+            double* qy = S.py[sl];
+            const double dtol = mul(kDedupRel, P.delta);
+            unsigned fdummy = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) push_dedup(qx, qy, fdummy, nv, ix[i], iy[i], false, dtol, true);
+            if (nv >= 2 && fabs(qx[0] - qx[nv - 1]) <= dtol && fabs(qy[0] - qy[nv - 1]) <= dtol) --nv;
+          } else {
+            need_clip = true;
+          }
+        }
+        S.xo[sl][0] = x0;
+        S.xo[sl][1] = x1;
+        S.W[sl] = c_rule.ow[p] * twice_area(ox, oy);
+        if (p == 0) {  // the record's inner triangle of this sweep, for the hat functions
+          double* tr = S.tri[rec][m == 1];
+          tr[0] = ix[0]; tr[1] = iy[0];
+          tr[2] = ix[1] - ix[0]; tr[3] = iy[1] - iy[0];
+          tr[4] = ix[2] - ix[0]; tr[5] = iy[2] - iy[0];
+          tr[6] = 1.0 / cross2(tr[2], tr[5], tr[3], tr[4]);
+          double* tv = S.tv[rec][m == 1];
+          tv[0] = ix[0]; tv[1] = ix[1]; tv[2] = ix[2];
+          tv[3] = iy[0]; tv[4] = iy[1]; tv[5] = iy[2];
+        }
+      }
+      S.pm[sl] = (unsigned char)(p | (m << 4) | (valid ? 0 : 0x80));
+      S.nv[sl] = (unsigned char)nv;
+      const unsigned qm = __ballot_sync(0xffffffffu, need_clip);
+      if (need_clip) S.q[qn + __popc(qm & ((1u << lane) - 1u))] = (unsigned char)sl;
+      qn += __popc(qm);
+    }
+    __syncwarp();
+    // ---- the queued clips on consecutive lanes
+#pragma unroll 1
+    for (int qi = lane; qi < qn; qi += 32) {
+      const int sl = S.q[qi];
+      const int mj = (S.pm[sl] >> 4) & 3;
+      const double* tv = S.tv[sl >> 4][mj == 1];
+      const Tri Tq{tv[0], tv[1], tv[2], tv[3], tv[4], tv[5]};
+      S.nv[sl] = (unsigned char)truncate_inner_inplace(Tq, S.xo[sl][0], S.xo[sl][1], P.delta, P.ball, S.px[sl],
+                                                       S.py[sl]);
+    }
+    __syncwarp();
+    // ---- per slot: closed-form fan sums, then fold and reduce two records
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int rec = vs + 2 * h, sl = lane + 32 * h;
+      const long long v = rd * 4 + rec;
+      const bool vok = v < O.nlist;
+      const int pmy = S.pm[sl];
+      const bool ivalid = !(pmy & 0x80);
+      const int mi = (pmy >> 4) & 3, pi = pmy & 15;
+      const int rf = vok ? S.fl[rec] : 0, rk = vok ? S.vk[rec] : 0, rl = vok ? S.vl[rec] : 0;
+      const int mult = ((rf & kEmitA) ? 1 : 0) + ((rf & kEmitB) ? 1 : 0);
+      double si[C::NSUM];
+#pragma unroll
+      for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
+      const int nv = S.nv[sl];
+      if (ivalid && nv >= 3) {
+        n_out0 += mi == 0 ? mult : 0;
+        n_out1 += mi == 1 ? mult : 0;
+        n_out2 += mi == 2;
+        const double* qx = S.px[sl];
+        const double* qy = S.py[sl];
+        const double* tr = S.tri[rec][mi == 1];
+        const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
+        const double q0x = qx[0], q0y = qy[0];
+        const double v0 = q0x - o0, v1 = q0y - o1;
+        const double z1 = (v0 * e2y - v1 * e2x) * idet, z2 = (e1x * v1 - e1y * v0) * idet;
+        const double x0 = S.xo[sl][0];
+        int ne = 0;
+#pragma unroll 1
+        for (int t = 1; t < nv - 1; ++t) {
+          const double ax = qx[t] - q0x, ay = qy[t] - q0y;
+          const double bx = qx[t + 1] - q0x, by = qy[t + 1] - q0y;
+          const double jac2 = cross2(ax, by, ay, bx);
+          if (!(jac2 > P.drop2)) continue;
+          const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
+          const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
+          double sm[C::NSUM];
+          closed_moments<KID>(P, q0x, ax, bx, jac2, x0, z1, z2, z1a, z2a, z1b, z2b, sm);
+#pragma unroll
+          for (int i = 0; i < C::NSUM; ++i) si[i] += sm[i];
+          ne += 7;
+        }
+        n_eval0 += mi == 0 ? ne * mult : 0;
+        n_eval1 += mi == 1 ? ne * mult : 0;
+        n_eval2 += mi == 2 ? ne : 0;
+      }
+      // fold into both visits, reduce-scatter over the record's 16 lanes
+      const double Wi = ivalid ? S.W[sl] : 0.0;
+      const double* ohi = c_rule.oh[pi];
+      const FoldSrc<KID> fs(Wi, ohi, si);
+      const bool m1 = mi == 1, m2 = ivalid && mi == 2;
+      constexpr int NBATCH = (C::NVAL + 31) / 32;
+      double smA = 0.0, smB = 0.0;  // the sides' largest |value| (the roots' merge bounds)
+#pragma unroll
+      for (int bt = 0; bt < NBATCH; ++bt) {
+        double vals[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int g = bt * 32 + i;
+          double val = 0.0;
+          if (g < C::NVAL) {
+            double f0, f1;
+            fs.entry(g < C::NSIDE ? g : g - C::NSIDE, f0, f1);
+            if (g < C::NSIDE) {
+              const double a0 = ivalid ? (m1 ? f1 : f0) : 0.0;
+              val = m2 ? a0 + f1 : a0;
+            } else {
+              val = ivalid && !m2 ? (m1 ? f0 : f1) : 0.0;
+            }
+          }
+          vals[i] = val;
+        }
+#pragma unroll
+        for (int off = 8, half = 16; off >= 1; off >>= 1, half >>= 1) {
+          const bool upper = lane & off;
+#pragma unroll
+          for (int i = 0; i < half; ++i) {
+            const double send = upper ? vals[i] : vals[i + half];
+            const double keep = upper ? vals[i + half] : vals[i];
+            vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
+        }
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int g = bt * 32 + r * 2 + h2;
+          if (!vok || g >= C::NVAL) continue;
+          const double val = vals[h2];
+          const int side = g / C::NSIDE, w = g % C::NSIDE;
+          const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
+          const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
+          const long long slot = side ? O.b_base + __ldg(&O.revpos[v]) : O.a_base + v;
+          if (on) {
+            report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
+            vmx = fmax(vmx, fabs(val));
+            if (side == 0) smA = fmax(smA, fabs(val));
+            else smB = fmax(smB, fabs(val));
+          }
+          if (w < C::NKK) {
+            O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;
+          } else {
+            const int e = w - C::NKK, I = e / N3, J = e % N3;
+            O.klv[slot * Blk<NC>::KLS + Blk<NC>::kl(I, J)] = on ? emit_val(val) : 0.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 8; o; o >>= 1) {  // within the record's 16 lanes
+        smA = fmax(smA, __shfl_xor_sync(0xffffffffu, smA, o));
+        smB = fmax(smB, __shfl_xor_sync(0xffffffffu, smB, o));
+      }
+      if (r == 0 && vok) {
+        elem_bound(O.emax, rk, smA);
+        elem_bound(O.emax, rl, smB);
       }
     }
     __syncwarp();
@@ -2251,7 +2593,8 @@ struct RowIn {
   const unsigned* skey32;
   const double* sval;
   const long long* sstart;
-  const unsigned long long* vmax;  // max |stored / singular value| of the batch
+  const unsigned long long* vmax;  // max |stored / singular value| of the batch (stage R)
+  const unsigned long long* emax;  // [K] per element: max |value| of its roots' emitted sides
   const unsigned long long* fmax;  // plan bounds of the analytic terms (k_elem_factors)
   Grid G;                          // analytic rows enumerate their category-0 partners
 };
@@ -2298,6 +2641,7 @@ struct RowSmem {
   IncRoot inc[kMaxInc];
   int gr0[kMaxRowsG], gr1[kMaxRowsG], gpre[kMaxRowsG + 1];  // candidate ranges of the enumeration
   int ngr;
+  unsigned long long bnd;  // the row's bound (incident elements' emitted values)
   double gvx, gvy, grmax, gsum_all;  // the dof's vertex, largest incident radius, sum of all row factors
   int gpres_all;
   int nrim;
@@ -2330,7 +2674,16 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   double whsmax = 0.0, sw = 0.0;
 #pragma unroll
   for (int p = 0; p < 7; ++p) sw += c_rule.ow[p];
-  double bound = __longlong_as_double((long long)*W.vmax);
+  // the row's bound: its incident elements' (every contribution to row d
+  // comes from a visit or touching pair of an element containing d)
+  if (t < 32) {
+    unsigned long long b = 0;
+    for (int i = W.de_start[d] + t; i < W.de_start[d + 1]; i += 32) b = max(b, W.emax[W.de_items[i] >> 2]);
+    for (int o = 16; o; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (t == 0) S.bnd = b;
+  }
+  __syncthreads();
+  double bound = __longlong_as_double((long long)S.bnd);
   double fa2 = 0.0;
   if (AN) {
 #pragma unroll
@@ -2358,6 +2711,9 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   }
   __syncthreads();
   // slot of column dof base w (inserted if new); -1 once the table overflowed
+  // (nc = 1: a key is inserted with its presence bit -- only present
+  // contributions reach the table)
+  constexpr unsigned kIns = NC == 1 ? 0x80000000u : 0u;
   auto slot_of = [&](unsigned w) -> int {
     unsigned h = (w * 2654435761u) >> (32 - LOG2CAP);
     for (int probe = 0; probe < CAP; ++probe) {
@@ -2365,7 +2721,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
       if (kk == w) return (int)h;
       if (kk == kRowEmpty) {
         if (*(volatile int*)&S.ovf) return -1;
-        const unsigned old = atomicCAS(&S.key[h], kRowEmpty, w);
+        const unsigned old = atomicCAS(&S.key[h], kRowEmpty, w | kIns);
         if (old == kRowEmpty) {
           if (atomicAdd(&S.used, 1) >= (W.fill_div ? CAP / W.fill_div : CAP - CAP / 8)) S.ovf = 1;
           return (int)h;
@@ -2379,7 +2735,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   };
   auto mark = [&](int h, int comp) {
     if (NC == 1) {
-      if (!(*(volatile unsigned*)&S.key[h] & 0x80000000u)) atomicOr(&S.key[h], 0x80000000u);
+      // (set at insertion)
     } else {
       if (!((*(volatile unsigned*)&S.pres[h] >> comp) & 1u)) atomicOr(&S.pres[h], 1u << comp);
     }
@@ -2410,11 +2766,9 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
       const int4 dk4 = __ldg(&P.dofs[k]);
       const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
       const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
-      // own-block partials in fixed point (nc = 2: in double, summed by each
-      // thread over its sides in a fixed order -- deterministic for a given
-      // CTA size -- and converted once per root, to save registers)
-      using OwnT = std::conditional_t<NC == 2, double, fix_t>;
-      OwnT own[3][NC2];
+      // own-block partials in fixed point: exact, so neither the CTA size
+      // nor the order of the sides (which depends on the batch) matters
+      fix_t own[3][NC2];
       unsigned opres = 0;  // bit b * NC2 + comp
 #pragma unroll
       for (int b = 0; b < 3; ++b)
@@ -2440,8 +2794,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
               const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
               const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
               if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
-                if constexpr (NC == 2) own[b][c * NC + dd] += vo;
-                else own[b][c * NC + dd] += fix_of(vo, scale);
+                own[b][c * NC + dd] += fix_of(vo, scale);
                 opres |= 1u << (b * NC2 + c * NC + dd);
               }
               add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
@@ -2456,10 +2809,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
         for (int b = 0; b < 3; ++b)
 #pragma unroll
           for (int e = 0; e < NC2; ++e) {
-            fix_t f0;
-            if constexpr (NC == 2) f0 = fix_of(own[b][e], scale);
-            else f0 = own[b][e];
-            const fix_t f = fix_warp_sum(f0);
+            const fix_t f = fix_warp_sum(own[b][e]);
             if ((t & 31) == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
           }
       }
@@ -2790,12 +3140,14 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
                                                   long long n, SingRule R,
                                                   unsigned long long* keys, double* vals,
                                                   long long cbase, unsigned long long* counters,
-                                                  unsigned long long* errpair, unsigned long long* vmax) {
+                                                  unsigned long long* errpair, unsigned long long* vmax,
+                                                  unsigned long long* emax) {
   using T = KTraits<KID>;
   constexpr int NC = T::NC, UN = U * NC;
   using A = SingAcc<U, NC, T::SYM>;
   constexpr int SLOTS = 36 * NC * NC;
   __shared__ double sTA[3][2], sTB[3][2], sScale;
+  __shared__ double sPm[kSingThreads / 32];  // the pair's largest |entry| (the elements' merge bounds)
   __shared__ int sMk[6], sMl[6], sUb[6];
   __shared__ double red[kSingThreads / 32][A::N];
   long long npts = 0;
@@ -2939,6 +3291,7 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
       if (lane_id() == 0) red[threadIdx.x >> 5][i] = v;
     }
     __syncthreads();
+    double pm = 0.0;
     for (int s = threadIdx.x; s < SLOTS; s += blockDim.x) {
       const long long slot = cbase + pi * SLOTS + s;
       const int ii = s / (6 * NC), jj = s % (6 * NC);
@@ -2954,9 +3307,19 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
       v *= sScale;
       report_nonfinite(nonfinite(v), k, l, P.K, errpair);
       vm = fmax(vm, fabs(v));
+      pm = fmax(pm, fabs(v));
       const int m = ii / NC, c = ii % NC, mp = jj / NC, d = jj % NC;
       put_key(P, keys, slot, coo_key(P, (long long)NC * sUb[m] + c, (long long)NC * sUb[mp] + d));
       vals[slot] = emit_val(v);
+    }
+    for (int o = 16; o; o >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+    if (lane_id() == 0) sPm[threadIdx.x >> 5] = pm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < kSingThreads / 32; ++w) m = fmax(m, sPm[w]);
+      elem_bound(emax, k, m);  // every row of the pair's block is a row of k or of l
+      if (l != k) elem_bound(emax, l, m);
     }
     __syncthreads();
   }
@@ -3157,6 +3520,7 @@ inline unsigned grid_for(long long n, int bs) {
 struct nlg_plan {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cstream = nullptr;  // host outputs: batch CSR pieces copied to pinned staging while later batches run
   Params P{};
   // owned device arrays
   double2* vtx = nullptr;
@@ -3204,6 +3568,7 @@ struct DeviceScratch {
   size_t cap = 0, peak = 0;
   char* pinned = nullptr;
   size_t pinned_cap = 0;
+  long long pin_nnz = 0;  // staging layout: data[pin_nnz] | indices[pin_nnz] | indptr (grows with the outputs seen)
 };
 DeviceScratch g_scratch[64];
 
@@ -3402,6 +3767,7 @@ struct Csr {  // one batch's rows
   long long* indptr;
   int* indices;
   double* data;
+  long long staged = -1;  // host outputs: entry offset of its copy in the pinned staging (-1: not staged)
 };
 
 struct Counters {
@@ -3463,9 +3829,26 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
       CK(cudaFuncSetAttribute(k_clipped<KID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       k_clipped<KID, true><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
     } else if (wl) {
-      const int smem = NWB * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
-      CK(cudaFuncSetAttribute(k_clipped<KID, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_clipped<KID, false, true><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
+      if constexpr (KID == 2 || KID == 3) {
+        // four records per warp round, warp-local clip queue (k_clipped_cf);
+        // NLG_CLIP_WL = 1..4 picks the block shape (A/B experiments)
+        static const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 3;
+        const long long rounds = (nP + 3) / 4;
+        auto launch = [&](auto kern, int nwb) -> cudaError_t {
+          const int smem = nwb * (int)sizeof(CfWarp<KID>);
+          const unsigned gcf = (unsigned)std::min<long long>((rounds + nwb - 1) / nwb, 148LL * 64);
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          if (e != cudaSuccess) return e;
+          kern<<<gcf, 32 * nwb, smem, pl->stream>>>(P, lp, O);
+          return cudaGetLastError();
+        };
+        switch (var) {
+          case 1: CK(launch(k_clipped_cf<KID, 4, 4>, 4)); break;
+          case 2: CK(launch(k_clipped_cf<KID, 4, 5>, 4)); break;
+          case 4: CK(launch(k_clipped_cf<KID, 8, 3>, 8)); break;
+          default: CK(launch(k_clipped_cf<KID, 8, 2>, 8)); break;  // measured best on config 5
+        }
+      }
     } else {
       const int smem = NWB * (int)sizeof(ClipWarp<KID, false>) + (int)sizeof(ClipBlock<KID>);
       CK(cudaFuncSetAttribute(k_clipped<KID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -3479,7 +3862,8 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
 template <int KID>
 nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const long long* nS,
                         unsigned long long* keys, double* vals, long long cbase,
-                        unsigned long long* counters, unsigned long long* errpair, unsigned long long* vmax) {
+                        unsigned long long* counters, unsigned long long* errpair, unsigned long long* vmax,
+                        unsigned long long* emax) {
   constexpr int NC = KTraits<KID>::NC;
   const long long slots = 36LL * NC * NC;
   for (int f = 0; f < 3; ++f) {
@@ -3488,14 +3872,14 @@ nlg_status run_singular(nlg_plan* pl, const Params& P, int2* const* ls, const lo
                pl->sing_tab[f][4], pl->sing_n[f]};
     const unsigned g = (unsigned)std::min<long long>(nS[f], 1 << 20);
     if (f == 0)
-      k_singular<KID, 0, 3><<<g, kSingThreads, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair, vmax);
+      k_singular<KID, 0, 3><<<g, kSingThreads, 0, pl->stream>>>(P, ls[0], nS[0], R, keys, vals, cbase, counters, errpair, vmax, emax);
     else if (P.is_dg)
       (f == 1 ? k_singular<KID, 1, 6> : k_singular<KID, 2, 6>)<<<g, kSingThreads, 0, pl->stream>>>(
-          P, ls[f], nS[f], R, keys, vals, cbase, counters, errpair, vmax);
+          P, ls[f], nS[f], R, keys, vals, cbase, counters, errpair, vmax, emax);
     else if (f == 1)
-      k_singular<KID, 1, 4><<<g, kSingThreads, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair, vmax);
+      k_singular<KID, 1, 4><<<g, kSingThreads, 0, pl->stream>>>(P, ls[1], nS[1], R, keys, vals, cbase, counters, errpair, vmax, emax);
     else
-      k_singular<KID, 2, 5><<<g, kSingThreads, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair, vmax);
+      k_singular<KID, 2, 5><<<g, kSingThreads, 0, pl->stream>>>(P, ls[2], nS[2], R, keys, vals, cbase, counters, errpair, vmax, emax);
     LAUNCHED();
     cbase += nS[f] * slots;
   }
@@ -3661,7 +4045,8 @@ cudaError_t launch_rows_cap(const Params& P, const RootIn& I, const RowIn& W, co
 // some row outgrew the largest table (use stage R + sort); *need_split: the
 // entry estimate was too small.
 nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* skeys, double* svals, long long nsing,
-                      const unsigned long long* d_vmax, long long ent_cap, double cols_est, Csr& piece, long long& nnz,
+                      const unsigned long long* d_vmax, const unsigned long long* d_emax, long long ent_cap,
+                      double cols_est, Csr& piece, long long& nnz,
                       bool* fallback, bool* need_split, long long* retries) {
   cudaStream_t s = pl->stream;
   const int NC = P.nc;
@@ -3737,6 +4122,7 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   W.sval = sv;
   W.sstart = sstart.as<long long>();
   W.vmax = d_vmax;
+  W.emax = d_emax;
   W.fmax = pl->fmax;
   W.G = pl->G;
   RowOut O;
@@ -4124,6 +4510,9 @@ fits:
   CK(vals.alloc(sizeof(double) * (r_base + (rows_mode ? 0 : r_cap)), s));
   CK(vmaxb.alloc(sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(vmaxb.p, 0, sizeof(unsigned long long), s));
+  DevBuf emaxb;  // per-element bounds of the emitted values (the merge's per-row fixed-point scale)
+  CK(emaxb.alloc(sizeof(unsigned long long) * std::max(K, 1), s));
+  CK(cudaMemsetAsync(emaxb.p, 0, sizeof(unsigned long long) * std::max(K, 1), s));
   unsigned long long* d_vmax = vmaxb.as<unsigned long long>();
   const long long nkk = 3LL * NC * (3 * NC + 1) / 2, kls = NC == 1 ? 12 : 36;  // Blk<NC>::NKK, KLS
   CK(kkv.alloc(sizeof(double) * 2 * nkk * std::max(nst, 1LL), s));
@@ -4137,6 +4526,7 @@ fits:
   O.counters = d_counters;
   O.errpair = d_err;
   O.vmax = d_vmax;
+  O.emax = emaxb.as<unsigned long long>();
   VisitOut OF = O, OP = O;
   OF.a_base = aF; OF.b_base = bF; OF.revpos = revposF.as<int>(); OF.nlist = P.analytic ? 0 : nF;
   OP.a_base = aP; OP.b_base = bP; OP.revpos = revposP.as<int>(); OP.nlist = nPt;
@@ -4153,10 +4543,10 @@ fits:
   double* cvals = vals.as<double>();
   const long long sbase = (long long)nR * E;
   switch (P.kid) {
-    case 0: rc = run_singular<0>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
-    case 1: rc = run_singular<1>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
-    case 2: rc = run_singular<2>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
-    default: rc = run_singular<3>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax); break;
+    case 0: rc = run_singular<0>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax, emaxb.as<unsigned long long>()); break;
+    case 1: rc = run_singular<1>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax, emaxb.as<unsigned long long>()); break;
+    case 2: rc = run_singular<2>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax, emaxb.as<unsigned long long>()); break;
+    default: rc = run_singular<3>(pl, P, ls, nS, ckeys, cvals, sbase, d_counters, d_err, d_vmax, emaxb.as<unsigned long long>()); break;
   }
   if (rc) return rc;
   CK(cudaEventRecord(ev[4], s));
@@ -4191,7 +4581,8 @@ fits:
     // distinct columns of a row ~ half the visits of a root (the partner vertices)
     const double cols_est = nR ? 0.55 * (double)tot[C_EPI] / (double)nR : 0.0;
     long long retries = 0;
-    rc = merge_rows(pl, P, RI, sk, vals.as<double>() + sbase, nsing_slots, d_vmax, ent_cap, cols_est, piece, nnz,
+    rc = merge_rows(pl, P, RI, sk, vals.as<double>() + sbase, nsing_slots, d_vmax, emaxb.as<unsigned long long>(),
+                    ent_cap, cols_est, piece, nnz,
                     &fb, &ns, &retries);
     st->n_row_retries += retries;
     st->n_merge_fallbacks += fb ? 1 : 0;
@@ -4333,11 +4724,66 @@ fits:
   return NLG_OK;
 }
 
+// Host outputs: pinned staging of [data | indices | indptr] with room for
+// `nnz_cap` entries; a batch's piece is copied there on the plan's copy
+// stream as soon as the batch is merged, while the next batch computes.
+struct Stager {
+  nlg_plan* pl = nullptr;
+  DeviceScratch* ds = nullptr;
+  long long nnz_cap = 0, used = 0;
+  bool on = false;
+  double* dat() const { return (double*)ds->pinned; }
+  int* idx() const { return (int*)(ds->pinned + 8 * nnz_cap); }
+  long long* ptr() const { return (long long*)(ds->pinned + ((12 * nnz_cap + 15) & ~15LL)); }
+  static size_t bytes(long long nnz, long long nrows) { return ((12 * (size_t)nnz + 15) & ~(size_t)15) + 8 * (nrows + 1); }
+  void begin(nlg_plan* p, DeviceScratch* d, long long nrows) {
+    pl = p;
+    ds = d;
+    nnz_cap = 0;
+    used = 0;
+    on = false;
+    if (!p->cstream || !d->pin_nnz) return;
+    // the staging of the largest output seen so far (grown at the end of a call)
+    if (d->pinned_cap < bytes(d->pin_nnz, nrows)) {
+      if (d->pinned) cudaFreeHost(d->pinned);
+      d->pinned = nullptr;
+      d->pinned_cap = 0;
+      if (cudaHostAlloc((void**)&d->pinned, bytes(d->pin_nnz, nrows), cudaHostAllocPortable) == cudaSuccess)
+        d->pinned_cap = bytes(d->pin_nnz, nrows);
+      else
+        cudaGetLastError();
+    }
+    if (!d->pinned) return;
+    nnz_cap = d->pin_nnz;
+    on = true;
+  }
+  // queue the D2H of a finished piece (its buffers stay alive until emit)
+  nlg_status stage(Csr& c) {
+    if (!on || used + c.nnz > nnz_cap) {
+      on = false;  // out of room: the rest (and everything) is copied at the end
+      return NLG_OK;
+    }
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, pl->stream));
+    CK(cudaStreamWaitEvent(pl->cstream, ev, 0));
+    cudaEventDestroy(ev);
+    if (c.nnz) {
+      CK(cudaMemcpyAsync(dat() + used, c.data, sizeof(double) * c.nnz, cudaMemcpyDeviceToHost, pl->cstream));
+      CK(cudaMemcpyAsync(idx() + used, c.indices, sizeof(int) * c.nnz, cudaMemcpyDeviceToHost, pl->cstream));
+    }
+    c.staged = used;
+    used += c.nnz;
+    return NLG_OK;
+  }
+};
+
 // Concatenate row-ordered CSR pieces into the caller's buffers (alloc which
 // = 0 indptr, 1 indices, 2 data), on the host through pinned staging and a
 // threaded copy when out_on_host; frees the pieces.
 nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces, long long row_lo, long long row_hi,
-                       int out_on_host, nlg_alloc_fn alloc, void* user, cudaEvent_t e_done, long long* nnz_out) {
+                       int out_on_host, nlg_alloc_fn alloc, void* user, cudaEvent_t e_done, long long* nnz_out,
+                       Stager& stg) {
   cudaStream_t s = pl->stream;
   long long nnz = 0;
   for (auto& p : pieces) nnz += p.nnz;
@@ -4351,24 +4797,31 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
   long long* o_ptr = u_ptr;
   int* o_idx = u_idx;
   double* o_dat = u_dat;
-  const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
-               b_ptr = sizeof(long long) * (nrows + 1);
-  const size_t b_all = b_dat + ((b_idx + 15) & ~(size_t)15) + b_ptr;
+  bool all_staged = false;
+  stg.pl = pl;
+  stg.ds = &ds;
   if (out_on_host) {
-    if (ds.pinned_cap < b_all) {
-      if (ds.pinned) cudaFreeHost(ds.pinned);
-      ds.pinned = nullptr;
-      ds.pinned_cap = 0;
-      if (cudaHostAlloc((void**)&ds.pinned, b_all + b_all / 8, cudaHostAllocPortable) == cudaSuccess)
-        ds.pinned_cap = b_all + b_all / 8;
-      else
-        cudaGetLastError();
+    all_staged = stg.on;
+    for (auto& p : pieces) all_staged = all_staged && p.staged >= 0;
+    if (!all_staged) {
+      // (first call, or the output outgrew the staging): one staging of this size
+      if (pl->cstream) CK(cudaStreamSynchronize(pl->cstream));
+      if (ds.pinned_cap < Stager::bytes(nnz, nrows)) {
+        if (ds.pinned) cudaFreeHost(ds.pinned);
+        ds.pinned = nullptr;
+        ds.pinned_cap = 0;
+        const size_t want = Stager::bytes(nnz + nnz / 8, nrows);
+        if (cudaHostAlloc((void**)&ds.pinned, want, cudaHostAllocPortable) == cudaSuccess) ds.pinned_cap = want;
+        else cudaGetLastError();
+      }
+      stg.nnz_cap = nnz;
     }
     if (ds.pinned) {
-      o_dat = (double*)ds.pinned;
-      o_idx = (int*)(ds.pinned + b_dat);
-      o_ptr = (long long*)(ds.pinned + b_dat + ((b_idx + 15) & ~(size_t)15));
+      o_dat = stg.dat();
+      o_idx = stg.idx();
+      o_ptr = stg.ptr();
     }
+    ds.pin_nnz = std::max(ds.pin_nnz, nnz + nnz / 8);  // the next call stages batch by batch
   }
   DevBuf ptrbuf;
   CK(ptrbuf.alloc(sizeof(long long) * (nrows + 1), s));
@@ -4381,7 +4834,7 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
     }
     CK(cudaMemcpyAsync(ptrbuf.as<long long>() + (p.row_lo - row_lo), p.indptr, sizeof(long long) * (nr + 1),
                        cudaMemcpyDeviceToDevice, s));
-    if (p.nnz) {
+    if (p.nnz && !(all_staged && ds.pinned && o_dat == stg.dat())) {
       CK(cudaMemcpyAsync(o_idx + run, p.indices, sizeof(int) * p.nnz, cudaMemcpyDefault, s));
       CK(cudaMemcpyAsync(o_dat + run, p.data, sizeof(double) * p.nnz, cudaMemcpyDefault, s));
     }
@@ -4392,7 +4845,10 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
   if (e_done) CK(cudaEventRecord(e_done, s));
   TRACE("outputs queued");
   CK(cudaStreamSynchronize(s));
+  if (pl->cstream) CK(cudaStreamSynchronize(pl->cstream));
   TRACE("outputs synced");
+  const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
+               b_ptr = sizeof(long long) * (nrows + 1);
   if (out_on_host && o_dat != u_dat) {  // pinned staging -> caller buffers
     struct Part { void* dst; const void* src; size_t n; };
     const Part parts[3] = {{u_dat, o_dat, b_dat}, {u_idx, o_idx, b_idx}, {u_ptr, o_ptr, b_ptr}};
@@ -4469,6 +4925,10 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   nlg_plan* pl = new nlg_plan();
   pl->device = device;
   pl->stream = (cudaStream_t)stream;
+  if (cudaStreamCreateWithFlags(&pl->cstream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    pl->cstream = nullptr;
+  }
   cudaStream_t s = pl->stream;
   {
     cudaMemPool_t pool;
@@ -4627,6 +5087,7 @@ void nlg_plan_destroy(nlg_plan* pl) {
     for (double* p : f)
       if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
+  if (pl->cstream) cudaStreamDestroy(pl->cstream);
   delete pl;
 }
 
@@ -4683,6 +5144,8 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   CK(cudaMemsetAsync(dctr.p, 0, sizeof(unsigned long long) * K_NCOUNTERS, s));
   CK(cudaMemsetAsync(derr.p, 0xff, 2 * sizeof(unsigned long long), s));
   std::vector<Csr> pieces;
+  Stager stg;
+  if (out_on_host) stg.begin(pl, &ds, row_hi - row_lo);
   Counters ctr{};
   Timing tm;
   // row batches: a work list of ranges, split in halves when over budget
@@ -4698,9 +5161,14 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     bool split = false, an_fb = false;
     std::vector<long long> cuts;
     const bool first_attempt = st.n_batches == 0 && st.n_replans == 0;
+    const size_t npieces = pieces.size();
     rc = run_batch(pl, rg.first, rg.second, budget, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
                    derr.as<unsigned long long>(), &split, &cuts, rg.plain, &an_fb);
     if (rc) break;
+    if (out_on_host && pieces.size() > npieces) {
+      rc = stg.stage(pieces.back());
+      if (rc) break;
+    }
     if (an_fb) {
       todo.push_back({rg.first, rg.second, true});
       st.n_replans += 1;
@@ -4733,7 +5201,7 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   }
   // pieces are produced in ascending row order (ranges are popped low-first)
   long long nnz = 0;
-  rc = emit_pieces(pl, ds, pieces, row_lo, row_hi, out_on_host, alloc, user, e2, &nnz);
+  rc = emit_pieces(pl, ds, pieces, row_lo, row_hi, out_on_host, alloc, user, e2, &nnz, stg);
   if (rc) return rc;
   unsigned long long hc[K_NCOUNTERS], herr, herr2[2];
   CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
@@ -4944,7 +5412,8 @@ nlg_status nlg_mass(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc, void*
     pieces.push_back(piece);
   }
   long long nnz = 0;
-  return emit_pieces(pl, ds, pieces, 0, P.J, out_on_host, alloc, user, nullptr, &nnz);
+  Stager none;
+  return emit_pieces(pl, ds, pieces, 0, P.J, out_on_host, alloc, user, nullptr, &nnz, none);
 }
 
 nlg_status nlg_row_work(nlg_plan* pl, int64_t* work) {

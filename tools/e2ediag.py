@@ -5,9 +5,9 @@ import numpy as np
 from paper_2207_03921_b200 import configs, bfs_assemble
 from paper_2207_03921_b200.assembly import DevicePlan, csr_from_parts
 from paper_2207_03921_b200.problem import marshal
-cfg = configs.build(2)
+cfg = configs.build(int(sys.argv[1]) if len(sys.argv) > 1 else 5)
 adj = cfg.adjacency
-for i in range(4):
+for i in range(3):
     t = [time.perf_counter()]
     inp = marshal(cfg.mesh, adj, cfg.kernel, cfg.ansatz, cfg.quad); t.append(time.perf_counter())
     plan = DevicePlan(inp); t.append(time.perf_counter())
