@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
               // split cannot change a value.  A root's own visit of a smaller
               // partner becomes the record's side B.
               int2 rec = make_int2(k | (cat == 1 ? kCatClip : 0), l | fl);
-              if (q == 0 && l < k)
+              if (q == 0 && l < k && !(P.dbg & 32))  // (NLG_DEBUG & 32: A/B only)
                 rec = make_int2(l | (cat == 1 ? kCatClip : 0),
                                 k | ((fl & kEmitA) ? kEmitB : 0) | ((fl & kEmitB) ? kEmitA : 0));
               lists[q][base[q] + __popc(m & lt)] = rec;
@@ -917,7 +917,11 @@ struct VisitOut {
 // evaluates it, so the scale of each row -- from its incident elements'
 // bounds -- and with it every sum does not depend on the row split.
 __device__ __forceinline__ void elem_bound(unsigned long long* emax, int e, double m) {
-  if (m > 0.0 && m <= 1e300) atomicMax(&emax[e], (unsigned long long)__double_as_longlong(m));
+  if (!(m > 0.0 && m <= 1e300)) return;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+  // a root's records are processed side by side: read first, so that only
+  // a new maximum (rare after the first records) pays for the atomic
+  if (b > __ldcg(&emax[e])) atomicMax(&emax[e], b);
 }
 
 // max of nonnegative doubles (as bit patterns) over the warp, one atomic
@@ -976,7 +980,7 @@ __device__ __forceinline__ double4 ld_f4(const double4* p) {
 template <int KID>
 __global__ void k_elem_factors(Params P, double4* ft, unsigned long long* fbound) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
   if (e < P.K) {
     double tx[3], ty[3], px[7], py[7];
     load_tri(P, e, tx, ty);
@@ -987,6 +991,7 @@ __global__ void k_elem_factors(Params P, double4* ft, unsigned long long* fbound
 #pragma unroll
     for (int p = 0; p < 7; ++p) {
       const double f = KID == 2 ? P.cst : (1.0 + P.kp0 * px[p]) * P.kp1;
+      m3 = fmax(m3, fabs(f));  // (f is affine: its extremes on a triangle are at vertices, rule points 1-3)
 #pragma unroll
       for (int a = 0; a < 3; ++a) ps[a] = fma(c_rule.wh[p][a], f, ps[a]);
 #pragma unroll
@@ -1002,6 +1007,7 @@ __global__ void k_elem_factors(Params P, double4* ft, unsigned long long* fbound
   warp_max_abs(m0, &fbound[0]);
   warp_max_abs(m1, &fbound[1]);
   warp_max_abs(m2, &fbound[2]);
+  warp_max_abs(m3, &fbound[3]);
 }
 
 // Phi_r[a][b] of the root (see k_elem_factors)
@@ -2127,14 +2133,16 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
           }
         }
       }
+      if (!P.analytic) {  // (analytic rows: a plan bound covers the clipped values)
 #pragma unroll
-      for (int o = 8; o; o >>= 1) {  // within the record's 16 lanes
-        smA = fmax(smA, __shfl_xor_sync(0xffffffffu, smA, o));
-        smB = fmax(smB, __shfl_xor_sync(0xffffffffu, smB, o));
-      }
-      if (r == 0 && vok) {
-        elem_bound(O.emax, rk, smA);
-        elem_bound(O.emax, rl, smB);
+        for (int o = 8; o; o >>= 1) {  // within the record's 16 lanes
+          smA = fmax(smA, __shfl_xor_sync(0xffffffffu, smA, o));
+          smB = fmax(smB, __shfl_xor_sync(0xffffffffu, smB, o));
+        }
+        if (r == 0 && vok) {
+          elem_bound(O.emax, rk, smA);
+          elem_bound(O.emax, rl, smB);
+        }
       }
     }
     __syncwarp();
@@ -2697,8 +2705,14 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
     const double fg = __longlong_as_double((long long)W.fmax[1]);
     const double fphi = __longlong_as_double((long long)W.fmax[2]);
     // neighbour terms: up to kMaxInc roots' factors per column of a partner
-    bound = fmax(bound, 2.0 * fa2 * whsmax * fg * kMaxInc);
+    const double fabsmax = __longlong_as_double((long long)W.fmax[3]);
+    // neighbour terms: up to kMaxInc roots' factors x a column's factor H
+    // (up to 64 incident elements)
+    bound = fmax(bound, 2.0 * fa2 * whsmax * fg * kMaxInc * 64.0);
     bound = fmax(bound, 2.0 * fa2 * sw * fphi * fa2 * 0x1p17);  // own term: A2_r Phi_r x (sum of up to 2^17 A2_n)
+    // a clipped record side's entries: sums over the outer points (weights
+    // sw A2) of integrals of |f| x hats over part of the inner triangle
+    bound = fmax(bound, 8.0 * sw * fa2 * fa2 * fabsmax);
   }
   const bool bok = bound > 0.0 && bound <= 1e300;
   const int be = bok ? ilogb(bound) + 1 : 0;
@@ -3529,7 +3543,7 @@ struct nlg_plan {
   double2* ctr = nullptr;
   double* rad = nullptr;
   double4* ftab = nullptr;  // analytic full-pair factors (k_elem_factors)
-  unsigned long long* fmax = nullptr;  // [3] bounds of the analytic terms
+  unsigned long long* fmax = nullptr;  // [4] bounds of the analytic terms (max |A2|, |A2 psi|, |Phi|, |f|)
   int* de_start = nullptr;  // dof base -> its (element, local vertex) pairs: [J / nc + 1]
   int* de_items = nullptr;  // element * 4 + local vertex, by dof base
   double* sing_tab[3][5] = {};
@@ -3625,7 +3639,7 @@ nlg_status prep(nlg_plan* pl) {
   CK(cudaMemcpyAsync(ext.p, init, sizeof init, cudaMemcpyHostToDevice, st));
   k_bounds<<<grid_for(K, 256), 256, 0, st>>>(P, pl->ctr, pl->rad, ext.as<unsigned long long>());
   LAUNCHED();
-  CK(cudaMemsetAsync(pl->fmax, 0, 3 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(pl->fmax, 0, 4 * sizeof(unsigned long long), st));
   if (P.analytic && K) {
     if (P.kid == 2) k_elem_factors<2><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab, pl->fmax);
     else k_elem_factors<3><<<grid_for(K, 256), 256, 0, st>>>(P, pl->ftab, pl->fmax);
