@@ -156,6 +156,20 @@ nlg_status nlg_mass(nlg_plan *plan, int32_t out_on_host, nlg_alloc_fn alloc, voi
 nlg_status nlg_cg(int32_t device, int64_t n, const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *b, double *x, double rtol, int32_t maxit, int32_t *iters, double *relres);
 
+/* Local stiffness blocks of n ORDERED element pairs (the reference's
+ * local_contribution, assembly.py:327-448): pairs[2i], pairs[2i+1] = (k, l).
+ * Block i is written row-major with stride 6 nc into blocks[i][6nc][6nc]; its
+ * size (dims[i] x dims[i]) and its global dofs (dofs[i][0..dims[i])) say
+ * which part is used:
+ *   - the regularizing path's touching pairs: the union-basis block of one
+ *     ordered pair (U nc, U = 3 / 4 / 5, or 6 for DG), from the tensor rules;
+ *   - every other pair: the 4-term block over (k's 3 nc dofs, l's 3 nc dofs),
+ *     the inner element retriangulated against each outer point's ball.
+ * Host arrays.  NLG_ERR_CONFIG for a pair out of range, NLG_ERR_NUMERICAL
+ * for a nonfinite block. */
+nlg_status nlg_local_blocks(nlg_plan *plan, int64_t n, const int64_t *pairs, double *blocks, int64_t *dofs,
+                            int32_t *dims);
+
 /* Work estimate per dof base for balancing row shards across GPUs: for
  * every dof base, the summed EPI (visits passing the reject test) of the
  * outer elements incident to it, from the device's candidate count pass;

@@ -1,8 +1,8 @@
 """B200-native nonlocal FE stiffness assembly (drop-in for nlfem's
 bfs_assemble / assemble_load hot path, arXiv 2207.03921)."""
 
-from .assembly import (AnsatzSpace, DevicePlan, SparseSystem, assemble_load, assemble_mass, bfs_assemble,
-                       build_ansatz)
+from .assembly import (AnsatzSpace, DevicePlan, LocalStiffness, SparseSystem, assemble_load, assemble_mass,
+                       bfs_assemble, build_ansatz, local_contribution)
 from .errors import ConfigurationError, DeviceError, MeshFormatError, NumericalError
 from .geometry import BALL_IDS, BALL_KINDS, PairClass, classify_pair
 from .kernels import (KernelSpec, affine_kernel, constant_kernel, constant_kernel_infinity,
@@ -13,7 +13,8 @@ from .nlio import read_mesh, read_nlcsr, write_mesh, write_nlcsr, write_nlcsr_bl
 from .quadrature import Path, QuadratureConfig, dispatch, gauss_legendre, rule_7point, singular_rule
 
 __all__ = [
-    "AnsatzSpace", "DevicePlan", "SparseSystem", "assemble_load", "assemble_mass", "bfs_assemble", "build_ansatz",
+    "AnsatzSpace", "DevicePlan", "LocalStiffness", "SparseSystem", "assemble_load", "assemble_mass", "bfs_assemble",
+    "build_ansatz", "local_contribution",
     "ConfigurationError", "DeviceError", "MeshFormatError", "NumericalError",
     "BALL_IDS", "BALL_KINDS", "PairClass", "classify_pair",
     "KernelSpec", "affine_kernel", "constant_kernel", "constant_kernel_infinity",

@@ -79,6 +79,8 @@ SIGNATURES = {
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]),
     "nlg_row_work": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_void_p]),
+    "nlg_local_blocks": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p]),
     "nlg_fp64_peak": (ctypes.c_int32, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "nlg_launch_count": (ctypes.c_int64, []),
     "nlg_last_batches": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]),

@@ -67,6 +67,16 @@ def build_ansatz(mesh, kind="cg", n=1):
 
 
 @dataclass(frozen=True)
+class LocalStiffness:
+    """Dense local block with the global dofs its rows and columns hit
+    (assembly.py:111-120); dofs may repeat for CG touching pairs."""
+
+    block: np.ndarray
+    rows: np.ndarray
+    cols: np.ndarray
+
+
+@dataclass(frozen=True)
 class SparseSystem:
     """Stiffness matrix over all dofs (CSR, sorted columns) plus the free mask."""
 
@@ -195,6 +205,24 @@ class DevicePlan:
         _native.check(self.lib.nlg_row_work(self.handle, _ptr(w)), "nlg_row_work")
         return w[:self.inp.n_dofs // self.inp.nc]
 
+    def local_blocks(self, pairs):
+        """[LocalStiffness] of the ordered element pairs (k, l), computed on the
+        device (nlg_local_blocks; the reference's local_contribution)."""
+        pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1, 2))
+        n = pairs.shape[0]
+        nb = 6 * self.inp.nc
+        blocks = np.zeros((max(n, 1), nb, nb))
+        dofs = np.zeros((max(n, 1), nb), dtype=np.int64)
+        dims = np.zeros(max(n, 1), dtype=np.int32)
+        _native.check(self.lib.nlg_local_blocks(self.handle, n, _ptr(pairs), _ptr(blocks), _ptr(dofs), _ptr(dims)),
+                      "nlg_local_blocks")
+        out = []
+        for i in range(n):
+            d = int(dims[i])
+            out.append(LocalStiffness(block=blocks[i, :d, :d].copy(), rows=dofs[i, :d].copy(),
+                                      cols=dofs[i, :d].copy()))
+        return out
+
     def last_batches(self):
         """Row ranges [(lo, hi), ...] of the batches the last assemble() ran."""
         n = int(self.lib.nlg_last_batches(self.handle, None, 0))
@@ -275,6 +303,32 @@ def bfs_assemble(mesh, adjacency, kernel, ansatz, quad=None, n_threads=1, rows="
     return SparseSystem(matrix=matrix, free_mask=ansatz.free_mask.copy())
 
 
+def local_contribution(k, l, kernel, ansatz, quad, geometry, *, device=0):
+    """Local stiffness block of the ordered element pair (k, l), on the GPU.
+
+    Same contract as the reference (assembly.py:327-448): all four terms of
+    the pair ordered as (outer, inner) = (k, l), the inner element
+    retriangulated against the ball of each outer quadrature point; touching
+    pairs on the regularizing path over the full pair domain in the union
+    basis (one ordered pair's worth).  Rows and columns list the affected
+    global dofs.  ``geometry`` is the mesh.
+    """
+    if quad is None:
+        quad = QuadratureConfig()
+    K = geometry.n_elements
+    if kernel.n != ansatz.n:
+        raise ConfigurationError(
+            f"kernel has {kernel.n} output component(s) but the ansatz has {ansatz.n}")
+    inp = marshal(geometry, None, kernel, ansatz, quad)
+    if not (0 <= k < K and 0 <= l < K):
+        raise ConfigurationError(f"element pair ({k}, {l}) out of range for {K} elements")
+    plan = DevicePlan(inp, device=device)
+    try:
+        return plan.local_blocks([(k, l)])[0]
+    finally:
+        plan.close()
+
+
 def _dummy_inputs(mesh, ansatz, quad):
     """Mesh-only plan inputs for the load vector (no kernel involved)."""
     from .kernels import constant_kernel, peridynamic_kernel
@@ -320,5 +374,6 @@ def assemble_mass(mesh, ansatz, *, device=0):
     return csr_from_parts(indptr, indices, data, J, J, canonical=True)
 
 
-__all__ = ["AnsatzSpace", "build_ansatz", "SparseSystem", "bfs_assemble", "assemble_load", "assemble_mass",
+__all__ = ["AnsatzSpace", "build_ansatz", "SparseSystem", "LocalStiffness", "bfs_assemble", "assemble_load",
+           "assemble_mass", "local_contribution",
            "DevicePlan", "csr_from_parts", "quad_arrays"]

@@ -2156,6 +2156,120 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
   warp_add_ll((unsigned long long)n_out2, &O.counters[K_OUT_M2]);
 }
 
+// ---------------------------------------------------------------------
+// local_contribution (assembly.py:327-448): the 4-term block of the ORDERED
+// pair (k, l) -- outer points on k, the inner element l retriangulated
+// against the ball of each -- as a dense (6 nc) x (6 nc) block over the
+// dofs (k's, l's).  One warp per pair, lane p < 7 = outer point p: clip,
+// fan, 7 inner points (kernel values, no closed forms), barycentric moments
+// and the two folds of the item; the 7 items are summed in order p = 0..6.
+// (The touching pairs of the regularizing path go through k_singular.)
+template <int KID>
+__global__ void k_pair_local(Params P, const int2* __restrict__ pairs, int n, double* __restrict__ out,
+                             unsigned long long* errpair) {
+  using T = KTraits<KID>;
+  using C = ClipCfg<KID>;
+  using X = SumIdx<KID>;
+  constexpr int NC = T::NC, NC2 = T::NC2, N3 = 3 * NC, NB = 6 * NC;
+  __shared__ double sF[7][2 * C::NSIDE];
+  const int lane = threadIdx.x;
+  for (int pi = blockIdx.x; pi < n; pi += gridDim.x) {
+    const int k = pairs[pi].x, l = pairs[pi].y;
+    if (lane < 7) {
+      const int p = lane;
+      double kx[3], ky[3], lx[3], ly[3];
+      load_tri(P, k, kx, ky);
+      load_tri(P, l, lx, ly);
+      const int4 ek = __ldg(&P.elem[k]), el = __ldg(&P.elem[l]);
+      const bool touching = k == l || ek.x == el.x || ek.x == el.y || ek.x == el.z || ek.y == el.x ||
+                            ek.y == el.y || ek.y == el.z || ek.z == el.x || ek.z == el.y || ek.z == el.z;
+      const double rs2 = (touching && P.path == 1) ? P.rskip2 : 0.0;
+      const double e1x = kx[1] - kx[0], e2x = kx[2] - kx[0], e1y = ky[1] - ky[0], e2y = ky[2] - ky[0];
+      const double x0 = __dadd_rn(__dadd_rn(kx[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+      const double x1 = __dadd_rn(__dadd_rn(ky[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+      double qx[kMaxPoly], qy[kMaxPoly], sx[kMaxPoly], sy[kMaxPoly];
+      const int nv = truncate_inner(lx, ly, x0, x1, P.delta, P.ball, sx, sy, qx, qy);
+      // the inner element's frame (hat functions)
+      const double o0 = lx[0], o1 = ly[0], f1x = lx[1] - lx[0], f1y = ly[1] - ly[0], f2x = lx[2] - lx[0],
+                   f2y = ly[2] - ly[0];
+      const double idet = 1.0 / cross2(f1x, f2y, f1y, f2x);
+      double si[C::NSUM];
+#pragma unroll
+      for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
+      for (int t = 1; t < nv - 1; ++t) {
+        const double q0x = qx[0], q0y = qy[0];
+        const double ax = qx[t] - q0x, ay = qy[t] - q0y, bx = qx[t + 1] - q0x, by = qy[t + 1] - q0y;
+        const double jac2 = cross2(ax, by, ay, bx);
+        if (!(jac2 > P.drop2)) continue;
+        const double v0 = q0x - o0, v1 = q0y - o1;
+        const double z1 = (v0 * f2y - v1 * f2x) * idet, z2 = (f1x * v1 - f1y * v0) * idet;
+        const double z1a = (ax * f2y - ay * f2x) * idet, z2a = (f1x * ay - f1y * ax) * idet;
+        const double z1b = (bx * f2y - by * f2x) * idet, z2b = (f1x * by - f1y * bx) * idet;
+        for (int q = 0; q < 7; ++q) {
+          const double i0 = c_rule.ip[q][0], i1 = c_rule.ip[q][1];
+          const double y0 = fma(bx, i1, fma(ax, i0, q0x)), y1 = fma(by, i1, fma(ay, i0, q0y));
+          const double d0 = x0 - y0, d1 = x1 - y1;
+          const double r2 = fma(d0, d0, d1 * d1);
+          if (rs2 > 0.0) {  // the diagonal-skip predicate in the reference's rounding
+            const double ey0 = __dadd_rn(__dadd_rn(q0x, mul(ax, i0)), mul(bx, i1));
+            const double ey1 = __dadd_rn(__dadd_rn(q0y, mul(ay, i0)), mul(by, i1));
+            if (sumsq(x0 - ey0, x1 - ey1) < rs2) continue;
+          }
+          double pv[NC2], qv[NC2];
+          kval<KID>(P, x0, y0, d0, d1, r2, pv, qv);
+          const double wq = c_rule.iw[q] * jac2;
+          const double xi1 = fma(i1, z1b, fma(i0, z1a, z1)), xi2 = fma(i1, z2b, fma(i0, z2a, z2));
+#pragma unroll
+          for (int i = 0; i < C::NCU; ++i) {
+            const double tp = wq * pv[X::ucd(i)];
+            const double tq = T::SYM ? tp : wq * qv[X::ucd(i)];
+            const double g1 = tq * xi1, g2 = tq * xi2;
+            si[X::mp(0, i)] += tp;
+            if (T::SYM) {
+              si[X::mp(1, i)] += g1;
+              si[X::mp(2, i)] += g2;
+            } else {
+              si[X::mp(1, i)] = fma(tp, xi1, si[X::mp(1, i)]);
+              si[X::mp(2, i)] = fma(tp, xi2, si[X::mp(2, i)]);
+              si[X::mq(0, i)] += tq;
+              si[X::mq(1, i)] += g1;
+              si[X::mq(2, i)] += g2;
+            }
+            si[X::mq(3, i)] = fma(g1, xi1, si[X::mq(3, i)]);
+            si[X::mq(4, i)] = fma(g1, xi2, si[X::mq(4, i)]);
+            si[X::mq(5, i)] = fma(g2, xi2, si[X::mq(5, i)]);
+          }
+        }
+      }
+      const double W = c_rule.ow[p] * twice_area(kx, ky);
+      item_folds<KID>(W, c_rule.oh[p], si, &sF[p][0], &sF[p][C::NSIDE]);
+    }
+    __syncwarp();
+    // sum the items in order and lay out the dense block: rows / columns are
+    // (k's 3 nc dofs, l's 3 nc dofs); F0 -> the k rows, F1 -> the l rows
+    double* B = out + (long long)pi * NB * NB;
+    for (int e = lane; e < NB * NB; e += 32) {
+      const int R = e / NB, Cc = e % NB;
+      const bool rk = R < N3, ck = Cc < N3;
+      const int I = rk ? R : R - N3, J = ck ? Cc : Cc - N3;
+      double v = 0.0;
+      int g = -1;
+      if (rk == ck) {  // own part: the symmetric kk of F0 (k rows) / F1 (l rows)
+        const int a = min(I, J), b = max(I, J);
+        g = a * N3 - a * (a - 1) / 2 + (b - a);
+      } else {
+        g = C::NKK + I * N3 + J;
+      }
+      const int off = rk ? 0 : C::NSIDE;
+#pragma unroll 1
+      for (int p = 0; p < 7; ++p) v += sF[p][off + g];
+      B[e] = v;
+      report_nonfinite(nonfinite(v), k, l, P.K, errpair);
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- per-root reduction
 // Merge stage R.  A root's contributions are the blocks of its record sides:
 // side A of the records it owns (full list, then clipped list) and side B of
@@ -5487,6 +5601,151 @@ nlg_status nlg_row_work(nlg_plan* pl, int64_t* work) {
   }
   CK(cudaMemcpyAsync(work, wk.p, sizeof(unsigned long long) * nb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return NLG_OK;
+}
+
+nlg_status nlg_local_blocks(nlg_plan* pl, int64_t n, const int64_t* pairs, double* blocks, int64_t* dofs,
+                            int32_t* dims) {
+  if (!pl || n < 0 || (n && (!pairs || !blocks || !dofs || !dims))) { set_err("null plan or output"); return NLG_ERR_CONFIG; }
+  const Params& P0 = pl->P;
+  const int K = P0.K, NC = P0.nc, NB = 6 * NC;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t k = pairs[2 * i], l = pairs[2 * i + 1];
+    if (k < 0 || k >= K || l < 0 || l >= K) {
+      set_err("element pair (%lld, %lld) out of range for %d elements", (long long)k, (long long)l, K);
+      return NLG_ERR_CONFIG;
+    }
+  }
+  if (!n) return NLG_OK;
+  CK(cudaSetDevice(pl->device));
+  DeviceScratch& ds = g_scratch[pl->device];
+  std::lock_guard<std::mutex> scratch_lock(ds.mu);
+  cudaStream_t s = pl->stream;
+  Params P = P0;
+  P.row_lo = 0;
+  P.row_hi = P.J;
+  P.narrow = 0;
+  std::vector<int4> el(K), dof(K);
+  CK(cudaMemcpyAsync(el.data(), pl->elem, sizeof(int4) * K, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(dof.data(), pl->dofs, sizeof(int4) * K, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // the regularizing path's touching pairs use the tensor rules (k_singular,
+  // per family), every other pair the retriangulated sweep (k_pair_local)
+  std::vector<int2> loc, sing[3];
+  std::vector<int64_t> iloc, ising[3];
+  for (int64_t i = 0; i < n; ++i) {
+    const int k = (int)pairs[2 * i], l = (int)pairs[2 * i + 1];
+    const int ea[3] = {el[k].x, el[k].y, el[k].z}, eb[3] = {el[l].x, el[l].y, el[l].z};
+    int ns = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) ns += ea[a] == eb[b];
+    const bool touching = k == l || ns > 0;
+    if (touching && P.path == 2) {
+      const int f = k == l ? 0 : (ns == 2 ? 1 : 2);
+      sing[f].push_back(make_int2(k, l));
+      ising[f].push_back(i);
+    } else {
+      loc.push_back(make_int2(k, l));
+      iloc.push_back(i);
+    }
+  }
+  DevBuf dpairs, dout, derr, dctr, dvmax, demax;
+  CK(derr.alloc(2 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(derr.p, 0xff, 2 * sizeof(unsigned long long), s));
+  CK(dctr.alloc(sizeof(unsigned long long) * K_NCOUNTERS, s));
+  CK(cudaMemsetAsync(dctr.p, 0, sizeof(unsigned long long) * K_NCOUNTERS, s));
+  CK(dvmax.alloc(sizeof(unsigned long long), s));
+  CK(demax.alloc(sizeof(unsigned long long) * K, s));
+  CK(cudaMemsetAsync(demax.p, 0, sizeof(unsigned long long) * K, s));
+  std::vector<double> hloc((size_t)loc.size() * NB * NB);
+  if (!loc.empty()) {
+    CK(dpairs.alloc(sizeof(int2) * loc.size(), s));
+    CK(dout.alloc(sizeof(double) * hloc.size(), s));
+    CK(cudaMemcpyAsync(dpairs.p, loc.data(), sizeof(int2) * loc.size(), cudaMemcpyHostToDevice, s));
+    const unsigned g = (unsigned)std::min<size_t>(loc.size(), 1 << 16);
+    auto* e = derr.as<unsigned long long>();
+    switch (P.kid) {
+      case 0: k_pair_local<0><<<g, 32, 0, s>>>(P, dpairs.as<int2>(), (int)loc.size(), dout.as<double>(), e); break;
+      case 1: k_pair_local<1><<<g, 32, 0, s>>>(P, dpairs.as<int2>(), (int)loc.size(), dout.as<double>(), e); break;
+      case 2: k_pair_local<2><<<g, 32, 0, s>>>(P, dpairs.as<int2>(), (int)loc.size(), dout.as<double>(), e); break;
+      default: k_pair_local<3><<<g, 32, 0, s>>>(P, dpairs.as<int2>(), (int)loc.size(), dout.as<double>(), e); break;
+    }
+    LAUNCHED();
+    CK(cudaMemcpyAsync(hloc.data(), dout.p, sizeof(double) * hloc.size(), cudaMemcpyDeviceToHost, s));
+  }
+  const long long slots = 36LL * NC * NC;
+  const long long nsg = (long long)(sing[0].size() + sing[1].size() + sing[2].size());
+  std::vector<unsigned long long> hkey((size_t)nsg * slots);
+  std::vector<double> hval((size_t)nsg * slots);
+  if (nsg) {
+    DevBuf dls, dkeys, dvals;
+    CK(dls.alloc(sizeof(int2) * nsg, s));
+    CK(dkeys.alloc(sizeof(unsigned long long) * nsg * slots, s));
+    CK(dvals.alloc(sizeof(double) * nsg * slots, s));
+    int2* ls[3];
+    long long nS[3], o = 0;
+    for (int f = 0; f < 3; ++f) {
+      ls[f] = dls.as<int2>() + o;
+      nS[f] = (long long)sing[f].size();
+      if (nS[f]) CK(cudaMemcpyAsync(ls[f], sing[f].data(), sizeof(int2) * nS[f], cudaMemcpyHostToDevice, s));
+      o += nS[f];
+    }
+    nlg_status rc;
+    auto* kk = dkeys.as<unsigned long long>();
+    auto* ctr = dctr.as<unsigned long long>();
+    auto* e = derr.as<unsigned long long>();
+    auto* vm = dvmax.as<unsigned long long>();
+    auto* em = demax.as<unsigned long long>();
+    switch (P.kid) {
+      case 0: rc = run_singular<0>(pl, P, ls, nS, kk, dvals.as<double>(), 0, ctr, e, vm, em); break;
+      case 1: rc = run_singular<1>(pl, P, ls, nS, kk, dvals.as<double>(), 0, ctr, e, vm, em); break;
+      case 2: rc = run_singular<2>(pl, P, ls, nS, kk, dvals.as<double>(), 0, ctr, e, vm, em); break;
+      default: rc = run_singular<3>(pl, P, ls, nS, kk, dvals.as<double>(), 0, ctr, e, vm, em); break;
+    }
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(hkey.data(), dkeys.p, sizeof(unsigned long long) * hkey.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hval.data(), dvals.p, sizeof(double) * hval.size(), cudaMemcpyDeviceToHost, s));
+  }
+  unsigned long long herr[2];
+  CK(cudaMemcpyAsync(herr, derr.p, sizeof herr, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // outputs: each pair's block row-major with stride NB, its dofs, its size
+  for (size_t j = 0; j < loc.size(); ++j) {
+    const int64_t i = iloc[j];
+    memcpy(blocks + i * NB * NB, hloc.data() + j * NB * NB, sizeof(double) * NB * NB);
+    const int4 dk = dof[loc[j].x], dl = dof[loc[j].y];
+    const int da[3] = {dk.x, dk.y, dk.z}, db[3] = {dl.x, dl.y, dl.z};
+    for (int a = 0; a < 3; ++a)
+      for (int c = 0; c < NC; ++c) {
+        dofs[i * NB + a * NC + c] = (int64_t)NC * da[a] + c;
+        dofs[i * NB + 3 * NC + a * NC + c] = (int64_t)NC * db[a] + c;
+      }
+    dims[i] = NB;
+  }
+  long long o = 0;
+  for (int f = 0; f < 3; ++f)
+    for (size_t j = 0; j < sing[f].size(); ++j, ++o) {
+      const int64_t i = ising[f][j];
+      const bool same = sing[f][j].x == sing[f][j].y;
+      double* B = blocks + i * NB * NB;
+      for (int e = 0; e < NB * NB; ++e) B[e] = 0.0;
+      int dim = 0;
+      for (long long q = 0; q < slots; ++q) {
+        const unsigned long long key = hkey[o * slots + q];
+        if (key == kSentinel) continue;
+        const int ii = (int)(q / (6 * NC)), jj = (int)(q % (6 * NC));
+        // (the engine's unordered-pair block is twice one ordered pair's)
+        B[ii * NB + jj] = same ? hval[o * slots + q] : 0.5 * hval[o * slots + q];
+        dofs[i * NB + ii] = (int64_t)(key / (unsigned long long)P.J);
+        dim = std::max(dim, ii + 1);
+      }
+      dims[i] = dim;
+    }
+  if (herr[0] != ~0ull) {
+    set_err("nonfinite local contribution for element pair (%lld, %lld)", (long long)(herr[0] / (unsigned long long)K),
+            (long long)(herr[0] % (unsigned long long)K));
+    return NLG_ERR_NUMERICAL;
+  }
   return NLG_OK;
 }
 
