@@ -23,7 +23,9 @@ FUNCS = {
 
 
 def names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    """The whole-assembly fixtures (local_*.npz hold per-pair blocks)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("local_"))
 
 
 def kernel_from_spec(k):
