@@ -3714,7 +3714,7 @@ struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-o
       // allocation, so arena_peak is the true cumulative peak even when the
       // arena is absent or too small (the next call grows it once)
       DeviceScratch& ds = g_scratch[pl->device];
-      const size_t off = pl->arena_used;
+      const size_t off = pl->arena_used, peak0 = ds.peak;
       pl->arena_used += n;
       ds.peak = std::max(ds.peak, pl->arena_used);
       if (ds.arena && off + n <= ds.cap) {
@@ -3722,6 +3722,13 @@ struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-o
         arena = true;
         return cudaSuccess;
       }
+      const cudaError_t e = cudaMallocAsync(&p, n, st);
+      if (e != cudaSuccess) {  // a buffer that did not fit is not part of the peak to grow to
+        pl->arena_used = off;
+        ds.peak = peak0;
+        p = nullptr;
+      }
+      return e;
     }
     return cudaMallocAsync(&p, n, st);
   }
@@ -4061,10 +4068,10 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     k_seg_heads<KT><<<grid_for(coo, 256), 256, 0, s>>>(sk, coo, head.as<int>());
     LAUNCHED();
     size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, tb, head.as<int>(), sid.as<long long>(), cub::Sum(), 0LL, (int)coo, s));
     DevBuf tmp;
     CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.as<int>(), sid.as<long long>(), (int)coo, s));
+    CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, head.as<int>(), sid.as<long long>(), cub::Sum(), 0LL, (int)coo, s));
     g_launches += 1;
   }
   long long nseg = 0;
@@ -4093,10 +4100,10 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
                                                       segrow.as<int>(), col.as<int>(), sum.as<double>());
     LAUNCHED();
     size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, tb, present.as<int>(), pos.as<long long>(), cub::Sum(), 0LL, (int)nseg, s));
     DevBuf tmp;
     CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, present.as<int>(), pos.as<long long>(), (int)nseg, s));
+    CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, present.as<int>(), pos.as<long long>(), cub::Sum(), 0LL, (int)nseg, s));
     long long lpos;
     int lpres;
     CK(cudaMemcpyAsync(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, cudaMemcpyDeviceToHost, s));
@@ -4314,10 +4321,10 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
   }
   {
     size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, tb, rcnt.as<int>(), piece.indptr, cub::Sum(), 0LL, (int)(nrows + 1), s));
     DevBuf tmp;
     CK(tmp.alloc(tb, s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rcnt.as<int>(), piece.indptr, (int)(nrows + 1), s));
+    CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, rcnt.as<int>(), piece.indptr, cub::Sum(), 0LL, (int)(nrows + 1), s));
     g_launches += 1;
   }
   if (O.split) {  // the gather needs the first run's own length back

@@ -82,15 +82,19 @@ def test_analytic_full_pairs_match_integrated(name):
     _agree(_assemble(c), _assemble(c, {"NLG_NO_ANALYTIC": "1"}), c.matrix)
 
 
-@pytest.mark.parametrize("name", ["cfg1_approxcaps", "lshape16_affine"])
+@pytest.mark.parametrize("name", ["cfg1_approxcaps", "lshape16_affine", "peri_nocaps_avoid"])
 def test_stage_w_column_split_rows(name):
     """Rows too wide for the largest table run as two column halves (below /
     from the row's own dof base): a limit just under the widest rows forces
-    it without any fallback."""
+    it without any fallback.  The peridynamic case runs the nc = 2 split
+    kernel (tables keyed by column dof base, 2048 slots at most)."""
     c = Case(name)
     a = _assemble(c, {"NLG_MERGE": "sort"})
     widest = int(np.diff(a.indptr).max())
-    div = str(8192 // max(1, widest - 4))  # the largest table holds fewer columns than the widest rows
+    if name.startswith("peri"):  # keys are column dof bases: widest / 2 of them per row
+        div = str(2048 // max(1, widest // 2 - 2))
+    else:
+        div = str(8192 // max(1, widest - 4))  # the largest table holds fewer columns than the widest rows
     st = {}
     b = _assemble(c, {"NLG_ROW_FILL_DIV": div}, stats=st)
     assert st["n_merge_fallbacks"] == 0 and st["n_row_retries"] > 0

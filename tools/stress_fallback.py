@@ -1,5 +1,6 @@
 """Stress: rows with more distinct columns than the largest stage-W table
-(constant kernel, delta/h ~ 48) -> stage-R fallback; compare with NLG_MERGE=sort."""
+(constant kernel, delta/h ~ 48).  These now run as two column halves in
+stage W (no stage-R fallback); the result is compared with NLG_MERGE=sort."""
 import os, sys, time
 sys.path.insert(0, ".")
 import numpy as np
