@@ -448,6 +448,7 @@ def main():
             if i:
                 times.append(dt)
             d2h = (hi - lo + 1) * 8 + sysm.matrix.nnz * 12  # int64 indptr, int32 indices, f64 data
+            del sysm  # (its page-locked block goes back to the pool for the next step)
         tl = float(np.mean(times))
         if dist is not None:
             t = torch.tensor([tl], dtype=torch.float64, device=f"cuda:{local}")

@@ -45,7 +45,7 @@ typedef int32_t nlg_status;
 #define NLG_ERR_NUMERICAL 2 /* maps to NumericalError (nonfinite local contribution) */
 #define NLG_ERR_CUDA 3      /* launch / runtime failure, no device, OOM */
 
-#define NLG_ABI_VERSION 4
+#define NLG_ABI_VERSION 5
 
 /* Kernel ids (kernels.py :57-118 built-ins + 3 = nonsymmetric affine). */
 #define NLG_KERNEL_FRACTIONAL 0  /* c |x-y|^(-2-2s) */
@@ -75,7 +75,8 @@ typedef struct nlg_problem {
 typedef struct nlg_plan nlg_plan;
 
 /* Allocator for outputs. which: 0 = indptr (int64), 1 = indices (int32),
- * 2 = data (float64), 3 = load vector (float64), 4 = points (float64). */
+ * 2 = data (float64), 3 = load vector (float64), 4 = points (float64),
+ * 5 = page-locked host block (nlg_assemble_pinned). */
 typedef void *(*nlg_alloc_fn)(void *user, int64_t nbytes, int32_t which);
 
 /* Counters and phase times of one nlg_assemble call. */
@@ -126,6 +127,30 @@ void nlg_plan_destroy(nlg_plan *plan);
 nlg_status nlg_assemble(nlg_plan *plan, int64_t row_lo, int64_t row_hi, int32_t out_on_host,
                         nlg_alloc_fn alloc, void *alloc_user, int64_t mem_budget_bytes,
                         nlg_stats *stats);
+
+/* Host CSR without the final host copy.  block_alloc(user, nbytes, 5) must
+ * return a PAGE-LOCKED host block of at least nbytes (nlg_pinned_alloc, or
+ * the caller's own cudaHostAlloc / registered memory).  The library copies
+ * each batch's rows into it while the next batch computes and leaves the CSR
+ * there: out->arena is the block used, and indptr (int64[row_hi-row_lo+1]),
+ * indices (int32[nnz]), data (float64[nnz]) start at the byte offsets
+ * out->off_*.  The callback runs once when the output size is known from an
+ * earlier call on the same problem and row range (the size then carries 1/8
+ * headroom), else at the end with the exact size; a second time if the
+ * first block proved too small -- the caller recycles any block other than
+ * out->arena.  Replaces the (data, indices, indptr) arrays the reference
+ * builds at assembly.py:294-296 when the consumer is on the host. */
+typedef struct nlg_host_csr {
+  void *arena;
+  int64_t nnz;
+  int64_t off_indptr, off_indices, off_data;
+} nlg_host_csr;
+nlg_status nlg_assemble_pinned(nlg_plan *plan, int64_t row_lo, int64_t row_hi, nlg_alloc_fn block_alloc,
+                               void *alloc_user, int64_t mem_budget_bytes, nlg_stats *stats,
+                               nlg_host_csr *out);
+/* Page-locked host memory for nlg_assemble_pinned (cudaHostAlloc / cudaFreeHost). */
+void *nlg_pinned_alloc(int64_t nbytes);
+void nlg_pinned_free(void *p);
 
 /* Physical outer quadrature points of the active elements, [K_act][n_outer][2]
  * (assembly.py:463-469), written through alloc (which = 4). */

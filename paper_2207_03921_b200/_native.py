@@ -58,6 +58,12 @@ class Stats(ctypes.Structure):
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32)
 
+
+class HostCsr(ctypes.Structure):
+    _fields_ = [("arena", ctypes.c_void_p), ("nnz", ctypes.c_int64), ("off_indptr", ctypes.c_int64),
+                ("off_indices", ctypes.c_int64), ("off_data", ctypes.c_int64)]
+
+
 # symbols of include/nlg.h, with (restype, argtypes)
 SIGNATURES = {
     "nlg_abi_version": (ctypes.c_int32, []),
@@ -68,6 +74,11 @@ SIGNATURES = {
     "nlg_plan_destroy": (None, [ctypes.c_void_p]),
     "nlg_assemble": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                       ALLOC_FN, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(Stats)]),
+    "nlg_assemble_pinned": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ALLOC_FN,
+                                             ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(Stats),
+                                             ctypes.POINTER(HostCsr)]),
+    "nlg_pinned_alloc": (ctypes.c_void_p, [ctypes.c_int64]),
+    "nlg_pinned_free": (None, [ctypes.c_void_p]),
     "nlg_load_points": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_int32, ALLOC_FN, ctypes.c_void_p,
                                          ctypes.POINTER(ctypes.c_int64)]),
     "nlg_load": (ctypes.c_int32, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
@@ -186,3 +197,110 @@ class OutputSink:
         import torch
         tdt = {np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}[np.dtype(dtype).type]
         return buf.view(tdt)[:count]
+
+
+class PinnedPool:
+    """Page-locked host blocks for host-resident CSR outputs (nlg_assemble_pinned).
+
+    Pinning memory costs ~0.2 s per GB, so blocks are recycled: a block goes
+    back to the pool when the last numpy view of it is collected, and the
+    next assembly of a similar size takes it again.  At most ``keep`` free
+    blocks (NLG_PINNED_KEEP, default 2) stay pinned; the rest are released.
+    """
+
+    _GRAIN = 1 << 26  # 64 MiB: similar sizes share a block
+
+    def __init__(self):
+        self._free = []  # (capacity, address)
+        self._mu = threading.Lock()
+        self.keep = int(os.environ.get("NLG_PINNED_KEEP", "2"))
+        self.n_alloc = 0
+
+    def take(self, nbytes):
+        """(address, capacity) of a block of at least nbytes, or (None, 0)."""
+        need = max(int(nbytes), 1)
+        with self._mu:
+            fit = [b for b in self._free if need <= b[0] <= 2 * need + self._GRAIN]
+            if fit:
+                blk = min(fit)
+                self._free.remove(blk)
+                return blk[1], blk[0]
+        cap = (need + self._GRAIN - 1) // self._GRAIN * self._GRAIN
+        addr = load_library().nlg_pinned_alloc(cap)
+        if not addr:
+            self.trim(0)  # release what is pooled and retry once
+            addr = load_library().nlg_pinned_alloc(cap)
+            if not addr:
+                return None, 0
+        self.n_alloc += 1
+        return int(addr), cap
+
+    def give(self, addr, cap):
+        with self._mu:
+            self._free.append((cap, addr))
+        self.trim(self.keep)
+
+    def trim(self, keep):
+        with self._mu:
+            self._free.sort()
+            drop, self._free = self._free[:max(len(self._free) - keep, 0)], self._free[max(len(self._free) - keep, 0):]
+        lib = _lib
+        for _, addr in drop:
+            if lib is not None:
+                lib.nlg_pinned_free(ctypes.c_void_p(addr))
+
+    def view(self, addr, cap):
+        """uint8 numpy array over the block; the block returns to the pool
+        when the array and every view of it are gone."""
+        import weakref
+        raw = (ctypes.c_ubyte * cap).from_address(addr)
+        weakref.finalize(raw, self.give, addr, cap)
+        return np.frombuffer(raw, dtype=np.uint8)
+
+
+PINNED = PinnedPool()
+
+
+class PinnedSink:
+    """Block callback of nlg_assemble_pinned: hands out pooled page-locked
+    blocks and turns the one the library used into the CSR arrays."""
+
+    def __init__(self):
+        self.blocks = []  # (address, capacity) handed out during this call
+        self._cb = ALLOC_FN(self._alloc)
+
+    def _alloc(self, user, nbytes, which):
+        try:
+            addr, cap = PINNED.take(nbytes)
+            if addr is None:
+                return None
+            self.blocks.append((addr, cap))
+            return addr
+        except Exception:  # noqa: BLE001 -- NULL makes the library fail cleanly
+            return None
+
+    @property
+    def callback(self):
+        return self._cb
+
+    def release(self, keep_addr=None):
+        """Blocks not holding the result go back to the pool; the result's (address, capacity)."""
+        kept = None
+        for addr, cap in self.blocks:
+            if keep_addr is not None and addr == keep_addr and kept is None:
+                kept = (addr, cap)
+            else:
+                PINNED.give(addr, cap)
+        self.blocks = []
+        return kept
+
+    def arrays(self, out, n_rows):
+        kept = self.release(out.arena)
+        if kept is None:
+            raise DeviceError("nlg_assemble_pinned returned a block this sink did not hand out")
+        buf = PINNED.view(*kept)
+        nnz = int(out.nnz)
+        indptr = buf[out.off_indptr:out.off_indptr + 8 * (n_rows + 1)].view(np.int64)
+        indices = buf[out.off_indices:out.off_indices + 4 * nnz].view(np.int32)
+        data = buf[out.off_data:out.off_data + 8 * nnz].view(np.float64)
+        return indptr, indices, data

@@ -20,6 +20,7 @@ Differences a caller can observe:
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -182,8 +183,19 @@ class DevicePlan:
         else:
             sink = _native.OutputSink(out_on_host, self.device)
         st = _native.Stats()
-        rc = self.lib.nlg_assemble(self.handle, int(row_lo), int(row_hi), 1 if out_on_host else 0,
-                                   sink.callback, None, int(mem_budget), ctypes.byref(st))
+        pinned = out_on_host and not os.environ.get("NLG_NO_PINNED_OUTPUT")
+        if pinned:
+            # host CSR: each batch's rows land in a pooled page-locked block
+            # while the next batch computes; the arrays are views of the block
+            sink = _native.PinnedSink()
+            hcsr = _native.HostCsr()
+            rc = self.lib.nlg_assemble_pinned(self.handle, int(row_lo), int(row_hi), sink.callback, None,
+                                              int(mem_budget), ctypes.byref(st), ctypes.byref(hcsr))
+            if rc != _native.NLG_OK:
+                sink.release()
+        else:
+            rc = self.lib.nlg_assemble(self.handle, int(row_lo), int(row_hi), 1 if out_on_host else 0,
+                                       sink.callback, None, int(mem_budget), ctypes.byref(st))
         if rc == _native.NLG_ERR_NUMERICAL and st.err_k >= 0:
             # the reference raises for the first failing visit of its smallest
             # failing root (spans in order, assembly.py:285-288): partners
@@ -195,6 +207,8 @@ class DevicePlan:
             raise NumericalError(f"nonfinite local contribution for element pair ({k}, {l})")
         _native.check(rc, "nlg_assemble")
         nnz = st.nnz
+        if pinned:
+            return (*sink.arrays(hcsr, row_hi - row_lo), st.as_dict())
         return (sink.array(0, np.int64, row_hi - row_lo + 1), sink.array(1, np.int32, nnz),
                 sink.array(2, np.float64, nnz), st.as_dict())
 

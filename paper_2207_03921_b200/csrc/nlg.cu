@@ -2740,7 +2740,7 @@ struct RowOut {
 // row factors over the visits (k, n) of category 0 (exact reference
 // predicates): one table add per column of n instead of one per visit.
 constexpr int kMaxInc = 8;    // incident roots of a dof per enumeration pass
-constexpr int kMaxRowsG = 16; // grid cell rows of one enumeration
+constexpr int kMaxRowsG = 48; // grid cell rows of one enumeration (grid pitch >= reach / 16)
 constexpr int kRimCap = 8192; // queued rim candidates of one enumeration (beyond: handled in place)
 struct IncRoot {
   double cx, cy, r;
@@ -2761,7 +2761,8 @@ struct RowSmem {
     typename Scan::TempStorage scan;
   } u;
   IncRoot inc[kMaxInc];
-  int gr0[kMaxRowsG], gr1[kMaxRowsG], gpre[kMaxRowsG + 1];  // candidate ranges of the enumeration
+  int gr0[kMaxRowsG], gr1[kMaxRowsG], gpre[kMaxRowsG + 1];  // column ranges of the enumeration
+  int er0[kMaxRowsG], epre[kMaxRowsG + 1];                  // element ranges of the same cell rows
   int ngr;
   unsigned long long bnd;  // the row's bound (incident elements' emitted values)
   double gvx, gvy, grmax, gsum_all;  // the dof's vertex, largest incident radius, sum of all row factors
@@ -3003,7 +3004,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
           int iy = (int)floor((cy - W.G.oy) / W.G.cs);
           iy = min(max(iy, 0), W.G.ny - 1);
           const int span = (int)ceil(R / W.G.cs);
-          int n = 0, tot = 0;
+          int n = 0, tot = 0, etot = 0;
           for (int yy = max(iy - span, 0); yy <= min(iy + span, W.G.ny - 1) && n < kMaxRowsG; ++yy) {
             const double ylo = W.G.oy + yy * W.G.cs, yhi = ylo + W.G.cs;
             const double dy = cy < ylo ? ylo - cy : (cy > yhi ? cy - yhi : 0.0);
@@ -3016,9 +3017,13 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
             S.gr1[n] = W.G.cstart[yy * W.G.nx + x1 + 1];
             S.gpre[n] = tot;
             tot += S.gr1[n] - S.gr0[n];
+            S.er0[n] = W.G.start[yy * W.G.nx + x0];
+            S.epre[n] = etot;
+            etot += W.G.start[yy * W.G.nx + x1 + 1] - S.er0[n];
             ++n;
           }
           S.gpre[n] = tot;
+          S.epre[n] = etot;
           S.ngr = n;
           S.nrim = 0;
         }
@@ -3037,15 +3042,8 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
         // (those contain v, so lie within 2 r_max of it)
         const double cin = P.delta - 2.0 * grm - 2.0 * W.G.rmax - geta, cin2 = cin > 0.0 ? cin * cin : -1.0;
         const double cnear = 2.0 * W.G.rmax * (1.0 + 1e-9), cnear2 = cnear * cnear;
-        const double cout = eout + W.G.rmax * (1.0 + 1e-9), cout2 = cout * cout;
         // G(n) = sum of the row factors of the group's category-0 visits (k, n)
-        auto elem_g = [&](int n, double& gs) -> bool {
-          const int4 el = __ldg(&P.elem[n]);
-          if ((el.w & 15) == 0) return false;  // inactive: no visit
-          const double2 cl = __ldg(&P.ctr[n]);
-          const double rl = __ldg(&P.rad[n]);
-          const double dv2 = sumsq(gvx - cl.x, gvy - cl.y);
-          if (dv2 > eout2) return false;
+        auto elem_g = [&](int n, int4 el, double2 cl, double rl, double dv2, double& gs) -> bool {
           const double gin = P.delta - 2.0 * grm - rl - geta;
           bool deep = gin > 0.0 && dv2 < gin * gin;
           for (int i = 0; i < ng && deep; ++i) deep = S.inc[i].k != n;
@@ -3071,46 +3069,65 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
           gs = g;
           return pres;
         };
-        // a column near the rim: its elements one by one (incidence order)
-        auto rim_col = [&](int c) {
-          double v = 0.0;
-          bool pres = false;
-          for (int e = __ldg(&W.de_start[c]); e < __ldg(&W.de_start[c + 1]); ++e) {
-            const int it = __ldg(&W.de_items[e]);
-            const int n = it >> 2, a = it & 3;
-            double gs = 0.0;
-            if (!elem_g(n, gs)) continue;
-            const double4 f = ld_f4(P.ftab + n);
-            const double fa = a == 0 ? f.x : (a == 1 ? f.y : f.z);
-            v += gs * fa;
-            pres |= fa != 0.0;
+        // a column is "deep" when every element at it is a full partner of
+        // every group root, and none of them is in the group: one term
+        // gsum_all x H.  The same expression decides it for a column of phase A
+        // and for an element's corner in phase B (same vertex coordinates).
+        auto col_deep = [&](double dc2) -> bool { return dc2 < cin2 && dc2 > cnear2; };
+        // an element with a corner at a column that is not deep: G(n) once,
+        // then one term per such corner
+        auto rim_elem = [&](int j) {
+          const int4 el = W.G.gel[j];
+          const double2 cl = W.G.gctr[j];
+          const double rl = W.G.grad[j];
+          double gs = 0.0;
+          if (!elem_g(__ldg(&W.G.items[j]), el, cl, rl, sumsq(gvx - cl.x, gvy - cl.y), gs)) return;
+          const double4 f = ld_f4(W.G.gft + j);
+          const int4 dn = __ldg(&W.G.gdof[j]);
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const double2 v = __ldg(&P.vtx[b == 0 ? el.x : (b == 1 ? el.y : el.z)]);
+            if (col_deep(sumsq(gvx - v.x, gvy - v.y))) continue;
+            const double fb = b == 0 ? f.x : (b == 1 ? f.y : f.z);
+            add((unsigned)(b == 0 ? dn.x : (b == 1 ? dn.y : dn.z)), 0, gs * fb, fb != 0.0);
           }
-          add((unsigned)c, 0, v, pres);
         };
-        // phase A: every column -- beyond (skip), deep (all its elements full
-        // partners of every group root: gsum_all x H) or near the rim / the
-        // group (queued for phase B, which runs the element tests densely)
+        // phase A: every deep column (all its elements full partners of every
+        // group root): gsum_all x H
         for (int q = t; q < tot; q += TH) {
           if (*(volatile int*)&S.ovf) break;
           int r = 0;
           while (q >= S.gpre[r + 1]) ++r;
           const int jv = S.gr0[r] + (q - S.gpre[r]);
           const double4 cp = ld_f4(W.G.cpos + jv);
-          const double dc2 = sumsq(gvx - cp.x, gvy - cp.y);
-          if (dc2 > cout2) continue;
-          if (dc2 < cin2 && dc2 > cnear2) {
+          if (col_deep(sumsq(gvx - cp.x, gvy - cp.y)))
             add((unsigned)__ldg(&W.G.cid[jv]), 0, gsum_all * cp.z, gpres_all && cp.w != 0.0);
-          } else {
-            const int slot = atomicAdd(&S.nrim, 1);
-            if (slot < kRimCap) S.rimq[slot] = jv;
-            else rim_col(__ldg(&W.G.cid[jv]));  // (queue full: in place)
-          }
+        }
+        // phase B: the elements with a corner at another column, queued so
+        // their pair tests run densely.  An element whose corners (within r_n
+        // of its barycentre) all lie strictly between the two radii has only
+        // deep columns; one beyond eout has no category-0 visit.
+        const int etot = S.epre[ngr];
+        for (int q = t; q < etot; q += TH) {
+          if (*(volatile int*)&S.ovf) break;
+          int r = 0;
+          while (q >= S.epre[r + 1]) ++r;
+          const int j = S.er0[r] + (q - S.epre[r]);
+          const double2 cl = W.G.gctr[j];
+          const double rl = W.G.grad[j] * (1.0 + 1e-9) + 1e-9 * P.delta;
+          const double dv2 = sumsq(gvx - cl.x, gvy - cl.y);
+          if (dv2 > eout2) continue;
+          const double hi = cin - rl, lo = cnear + rl;
+          if (hi > 0.0 && dv2 < hi * hi && dv2 > lo * lo) continue;
+          const int slot = atomicAdd(&S.nrim, 1);
+          if (slot < kRimCap) S.rimq[slot] = j;
+          else rim_elem(j);  // (queue full: in place)
         }
         __syncthreads();
         const int nrim = min(S.nrim, kRimCap);
         for (int q = t; q < nrim; q += TH) {
           if (*(volatile int*)&S.ovf) break;
-          rim_col(__ldg(&W.G.cid[S.rimq[q]]));
+          rim_elem(S.rimq[q]);
         }
       }
     }
@@ -3697,8 +3714,19 @@ struct DeviceScratch {
   char* pinned = nullptr;
   size_t pinned_cap = 0;
   long long pin_nnz = 0;  // staging layout: data[pin_nnz] | indices[pin_nnz] | indptr (grows with the outputs seen)
+  unsigned long long pin_sig = 0;  // problem / row range the hint was measured on (caller-provided arenas)
+  // small device -> host readbacks (counts, totals) go through mapped pinned
+  // memory written by a kernel, not through the copy engine: a 4-byte
+  // cudaMemcpy would queue behind the bulk D2H of the previous batch's CSR
+  // (same engine) and stall the host for the whole copy
+  char* rb_host = nullptr;
+  char* rb_dev = nullptr;
+  size_t rb_used = 0;
+  struct RbPending { void* dst; size_t off, n; };
+  std::vector<RbPending> rb_pending;
 };
 DeviceScratch g_scratch[64];
+constexpr size_t kRbCap = 1 << 20;
 
 thread_local nlg_plan* g_arena_plan = nullptr;  // plan whose device arena backs DevBuf
 
@@ -3800,7 +3828,10 @@ nlg_status prep(nlg_plan* pl) {
   double ox = ord2d(h[0]), oy = ord2d(h[1]), mx = ord2d(h[2]), my = ord2d(h[3]), rmax = ord2d(h[4]);
   if (h[2] == 0ull) { ox = oy = mx = my = 0.0; rmax = 0.0; }  // no active element
   const double reach = (P.prer + 2.0 * rmax) * (1.0 + 1e-9) + 1e-300;
-  double cs = 0.5 * reach;
+  // pitch: reach / 6 (the scanned cell rows hug the disk: ~1.5x its area; reach / 2 scanned ~2.4x);
+  // NLG_GRID_DIV: A/B (the row merge holds <= kMaxRowsG cell rows)
+  static const int grid_div = getenv("NLG_GRID_DIV") ? std::min(16, std::max(1, atoi(getenv("NLG_GRID_DIV")))) : 6;
+  double cs = reach / grid_div;
   // keep the cell count bounded (tiny horizons on huge meshes)
   const double ext_x = mx - ox, ext_y = my - oy;
   while ((ext_x / cs + 1.0) * (ext_y / cs + 1.0) > 6.0e7) cs *= 2.0;
@@ -3895,6 +3926,43 @@ nlg_status prep(nlg_plan* pl) {
   pl->G = G;
   pl->prepped = true;
   return NLG_OK;
+}
+
+__global__ void k_readback(unsigned* __restrict__ dst, const unsigned* __restrict__ src, int nwords) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+// Queue a small device -> host read on stream s; the value lands in `dst`
+// at the next rb_sync(s).  (Larger or unaligned reads use the copy engine.)
+cudaError_t rb_read(void* dst, const void* src, size_t n, cudaStream_t s) {
+  if (!g_arena_plan) return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s);
+  DeviceScratch& ds = g_scratch[g_arena_plan->device];
+  if (!ds.rb_host) {
+    if (cudaHostAlloc((void**)&ds.rb_host, kRbCap, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&ds.rb_dev, ds.rb_host, 0) != cudaSuccess) {
+      cudaGetLastError();
+      if (ds.rb_host) cudaFreeHost(ds.rb_host);
+      ds.rb_host = ds.rb_dev = nullptr;
+    }
+  }
+  if (!ds.rb_host || (n & 3) || ((uintptr_t)src & 3) || ds.rb_used + n > kRbCap)
+    return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s);
+  if (!n) return cudaSuccess;
+  const int nw = (int)(n / 4);
+  k_readback<<<std::min(64, (nw + 255) / 256), 256, 0, s>>>((unsigned*)(ds.rb_dev + ds.rb_used), (const unsigned*)src, nw);
+  g_launches += 1;
+  ds.rb_pending.push_back({dst, ds.rb_used, n});
+  ds.rb_used += (n + 15) & ~(size_t)15;
+  return cudaGetLastError();
+}
+cudaError_t rb_sync(cudaStream_t s) {
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess || !g_arena_plan) return e;
+  DeviceScratch& ds = g_scratch[g_arena_plan->device];
+  for (const auto& q : ds.rb_pending) memcpy(q.dst, ds.rb_host + q.off, q.n);
+  ds.rb_pending.clear();
+  ds.rb_used = 0;
+  return cudaSuccess;
 }
 
 struct Csr {  // one batch's rows
@@ -4078,9 +4146,9 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
   if (coo) {
     long long lsid;
     int lhead;
-    CK(cudaMemcpyAsync(&lsid, sid.as<long long>() + coo - 1, sizeof lsid, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lhead, head.as<int>() + coo - 1, sizeof lhead, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(rb_read(&lsid, sid.as<long long>() + coo - 1, sizeof lsid, s));
+    CK(rb_read(&lhead, head.as<int>() + coo - 1, sizeof lhead, s));
+    CK(rb_sync(s));
     TRACE("sync 1775");
     nseg = lsid + lhead;
   }
@@ -4106,9 +4174,9 @@ nlg_status merge_csr(cudaStream_t s, const Params& P, unsigned long long* keys64
     CK(cub::DeviceScan::ExclusiveScan(tmp.p, tb, present.as<int>(), pos.as<long long>(), cub::Sum(), 0LL, (int)nseg, s));
     long long lpos;
     int lpres;
-    CK(cudaMemcpyAsync(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lpres, present.as<int>() + nseg - 1, sizeof lpres, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(rb_read(&lpos, pos.as<long long>() + nseg - 1, sizeof lpos, s));
+    CK(rb_read(&lpres, present.as<int>() + nseg - 1, sizeof lpres, s));
+    CK(rb_sync(s));
     TRACE("sync 1803");
     nnz = lpos + lpres;
     CK(cudaMallocAsync(&piece.indices, sizeof(int) * std::max(nnz, 1LL), s));
@@ -4282,8 +4350,8 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
     O.ovf = lists[pass & 1];
     CK(launch_rows_cap(P, RI, W, O, nblk, cap, s));
     unsigned long long hst[2] = {0, 0};  // entries used, overflowed dofs
-    CK(cudaMemcpyAsync(hst, st.p, sizeof hst, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(rb_read(hst, st.p, sizeof hst, s));
+    CK(rb_sync(s));
     TRACE("row pass");
     const unsigned hov = (unsigned)hst[1];
     used = hst[0];
@@ -4301,8 +4369,8 @@ nlg_status merge_rows(nlg_plan* pl, const Params& P, const RootIn& RI, void* ske
         CK(cudaMemsetAsync(O.novf, 0, sizeof(unsigned), s));
         CK(launch_rows_split(P, RI, W, O, hov, s));
         unsigned long long h2[2] = {0, 0};
-        CK(cudaMemcpyAsync(h2, st.p, sizeof h2, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        CK(rb_read(h2, st.p, sizeof h2, s));
+        CK(rb_sync(s));
         used = h2[0];
         if (h2[1]) { *fallback = true; return NLG_OK; }
       }
@@ -4403,8 +4471,8 @@ nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long
     g_launches += 1;
   }
   int nR = 0;
-  CK(cudaMemcpyAsync(&nR, nroots.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(rb_read(&nR, nroots.p, sizeof(int), s));
+  CK(rb_sync(s));
   TRACE("sync 1881");
   DevBuf inR;  // element -> rank in the batch's root list, -1 if not a root
   CK(inR.alloc(sizeof(int) * K, s));
@@ -4450,12 +4518,10 @@ count_pass:
     long long lastoff[6];
     int lastcnt[6];
     for (int q = 0; q < 6; ++q) {
-      CK(cudaMemcpyAsync(&lastoff[q], off.as<long long>() + (size_t)q * (nR + 1) + nR - 1, sizeof(long long),
-                         cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(&lastcnt[q], cnt.as<int>() + (size_t)q * nR + nR - 1, sizeof(int),
-                         cudaMemcpyDeviceToHost, s));
+      CK(rb_read(&lastoff[q], off.as<long long>() + (size_t)q * (nR + 1) + nR - 1, sizeof(long long), s));
+      CK(rb_read(&lastcnt[q], cnt.as<int>() + (size_t)q * nR + nR - 1, sizeof(int), s));
     }
-    CK(cudaStreamSynchronize(s));
+    CK(rb_sync(s));
     TRACE("sync 1925");
     for (int q = 0; q < 6; ++q) {
       tot[q] = lastoff[q] + lastcnt[q];
@@ -4513,8 +4579,8 @@ count_pass:
                                                       rows_plan ? kEntPerEpi * 0.5 * NC * 12.0 : 0.0);
       LAUNCHED();
       std::vector<unsigned long long> hcost((size_t)3 * nrows);
-      CK(cudaMemcpyAsync(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      CK(rb_read(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, s));
+      CK(rb_sync(s));
       // cut fraction of each limit (the halo roots a batch adds are not in
       // the per-row costs)
       static const double pf = getenv("NLG_PLAN_FRAC") ? atof(getenv("NLG_PLAN_FRAC")) : 0.55;
@@ -4572,11 +4638,11 @@ fits:
     g_launches += 2;
     long long lo[2];
     int lc[2];
-    CK(cudaMemcpyAsync(&lo[0], offF + nR - 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lo[1], offP + nR - 1, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lc[0], cnt.as<int>() + (size_t)C_FULL * nR + nR - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&lc[1], cnt.as<int>() + (size_t)C_PART * nR + nR - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(rb_read(&lo[0], offF + nR - 1, sizeof(long long), s));
+    CK(rb_read(&lo[1], offP + nR - 1, sizeof(long long), s));
+    CK(rb_read(&lc[0], cnt.as<int>() + (size_t)C_FULL * nR + nR - 1, sizeof(int), s));
+    CK(rb_read(&lc[1], cnt.as<int>() + (size_t)C_PART * nR + nR - 1, sizeof(int), s));
+    CK(rb_sync(s));
     TRACE("sync list totals");
     nF = lo[0] + lc[0];
     nPt = lo[1] + lc[1];
@@ -4812,8 +4878,8 @@ fits:
     }
     LAUNCHED();
     unsigned long long hst[3];
-    CK(cudaMemcpyAsync(hst, st64, sizeof hst, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(rb_read(hst, st64, sizeof hst, s));
+    CK(rb_sync(s));
     TRACE("stage R done");
     if (hst[1] & 0xffffffffull) {  // the runs exceed the estimate: split the rows
       if (row_hi - row_lo > 1) { *need_split = true; return NLG_OK; }
@@ -4838,8 +4904,8 @@ fits:
   out.push_back(piece);
   CK(cudaEventRecord(ev[5], s));
   unsigned long long hepi[2] = {0, 0};
-  CK(cudaMemcpyAsync(hepi, epib.p, sizeof hepi, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(rb_read(hepi, epib.p, sizeof hepi, s));
+  CK(rb_sync(s));
   TRACE("sync 2089");
   st->epi += (long long)hepi[0];
   st->n_roots += (long long)hepi[1];
@@ -4859,36 +4925,61 @@ fits:
   return NLG_OK;
 }
 
-// Host outputs: pinned staging of [data | indices | indptr] with room for
-// `nnz_cap` entries; a batch's piece is copied there on the plan's copy
-// stream as soon as the batch is merged, while the next batch computes.
+// Host outputs: a page-locked block laid out as [data | indices | indptr]
+// with room for `nnz_cap` entries; a batch's piece is copied there on the
+// plan's copy stream as soon as the batch is merged, while the next batch
+// computes.  The block is either the caller's (nlg_assemble_pinned: the CSR
+// is left there, no host copy at all) or the library's staging (nlg_assemble
+// with out_on_host: a threaded copy into the caller's pageable buffers ends
+// the call).
+struct HostArena {  // nlg_assemble_pinned: where the caller's block comes from, and the result
+  nlg_alloc_fn alloc = nullptr;
+  void* user = nullptr;
+  nlg_host_csr* out = nullptr;
+};
 struct Stager {
   nlg_plan* pl = nullptr;
   DeviceScratch* ds = nullptr;
-  long long nnz_cap = 0, used = 0;
+  char* base = nullptr;
+  long long nnz_cap = 0, used = 0, nrows = 0;
   bool on = false;
-  double* dat() const { return (double*)ds->pinned; }
-  int* idx() const { return (int*)(ds->pinned + 8 * nnz_cap); }
-  long long* ptr() const { return (long long*)(ds->pinned + ((12 * nnz_cap + 15) & ~15LL)); }
-  static size_t bytes(long long nnz, long long nrows) { return ((12 * (size_t)nnz + 15) & ~(size_t)15) + 8 * (nrows + 1); }
-  void begin(nlg_plan* p, DeviceScratch* d, long long nrows) {
-    pl = p;
-    ds = d;
-    nnz_cap = 0;
-    used = 0;
-    on = false;
-    if (!p->cstream || !d->pin_nnz) return;
-    // the staging of the largest output seen so far (grown at the end of a call)
-    if (d->pinned_cap < bytes(d->pin_nnz, nrows)) {
+  double* dat() const { return (double*)base; }
+  int* idx() const { return (int*)(base + off_idx(nnz_cap)); }
+  long long* ptr() const { return (long long*)(base + off_ptr(nnz_cap)); }
+  static size_t off_idx(long long nnz) { return 8 * (size_t)nnz; }
+  static size_t off_ptr(long long nnz) { return (12 * (size_t)nnz + 15) & ~(size_t)15; }
+  static size_t bytes(long long nnz, long long nrows) { return off_ptr(nnz) + 8 * (nrows + 1); }
+  // the library's own staging, grown to hold nnz entries
+  static char* own(DeviceScratch* d, long long nnz, long long nrows) {
+    if (d->pinned_cap < bytes(nnz, nrows)) {
       if (d->pinned) cudaFreeHost(d->pinned);
       d->pinned = nullptr;
       d->pinned_cap = 0;
-      if (cudaHostAlloc((void**)&d->pinned, bytes(d->pin_nnz, nrows), cudaHostAllocPortable) == cudaSuccess)
-        d->pinned_cap = bytes(d->pin_nnz, nrows);
+      if (cudaHostAlloc((void**)&d->pinned, bytes(nnz, nrows), cudaHostAllocPortable) == cudaSuccess)
+        d->pinned_cap = bytes(nnz, nrows);
       else
         cudaGetLastError();
     }
-    if (!d->pinned) return;
+    return d->pinned;
+  }
+  void begin(nlg_plan* p, DeviceScratch* d, long long nrows_, const HostArena* ha, unsigned long long sig) {
+    pl = p;
+    ds = d;
+    nrows = nrows_;
+    base = nullptr;
+    nnz_cap = 0;
+    used = 0;
+    on = false;
+    // the size hint is the largest output seen so far (of this problem and
+    // row range, for a caller's block); without one, everything is copied at the end
+    if (!p->cstream || !d->pin_nnz || getenv("NLG_NO_STAGE")) return;
+    if (ha) {
+      if (d->pin_sig != sig) return;
+      base = (char*)ha->alloc(ha->user, (int64_t)bytes(d->pin_nnz, nrows), 5);
+    } else {
+      base = own(d, d->pin_nnz, nrows);
+    }
+    if (!base) return;
     nnz_cap = d->pin_nnz;
     on = true;
   }
@@ -4914,21 +5005,26 @@ struct Stager {
 };
 
 // Concatenate row-ordered CSR pieces into the caller's buffers (alloc which
-// = 0 indptr, 1 indices, 2 data), on the host through pinned staging and a
-// threaded copy when out_on_host; frees the pieces.
+// = 0 indptr, 1 indices, 2 data; or the caller's page-locked block, `ha`);
+// frees the pieces.
 nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces, long long row_lo, long long row_hi,
                        int out_on_host, nlg_alloc_fn alloc, void* user, cudaEvent_t e_done, long long* nnz_out,
-                       Stager& stg) {
+                       Stager& stg, const HostArena* ha, unsigned long long sig) {
   cudaStream_t s = pl->stream;
   long long nnz = 0;
   for (auto& p : pieces) nnz += p.nnz;
   const long long nrows = row_hi - row_lo;
-  long long* u_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
-  int* u_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
-  double* u_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
-  if (!u_ptr || !u_idx || !u_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
-  // host outputs: D2H into pinned staging (full PCIe/C2C speed), then a
-  // threaded copy into the caller's pageable buffers
+  long long* u_ptr = nullptr;
+  int* u_idx = nullptr;
+  double* u_dat = nullptr;
+  if (!ha) {
+    u_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
+    u_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
+    u_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
+    if (!u_ptr || !u_idx || !u_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
+  }
+  // where the D2H copies land: the caller's buffers (device outputs; or host
+  // outputs when no page-locked block is available) or the block
   long long* o_ptr = u_ptr;
   int* o_idx = u_idx;
   double* o_dat = u_dat;
@@ -4939,24 +5035,24 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
     all_staged = stg.on;
     for (auto& p : pieces) all_staged = all_staged && p.staged >= 0;
     if (!all_staged) {
-      // (first call, or the output outgrew the staging): one staging of this size
+      // (first call, or the output outgrew the hint): one block of this size
       if (pl->cstream) CK(cudaStreamSynchronize(pl->cstream));
-      if (ds.pinned_cap < Stager::bytes(nnz, nrows)) {
-        if (ds.pinned) cudaFreeHost(ds.pinned);
-        ds.pinned = nullptr;
-        ds.pinned_cap = 0;
-        const size_t want = Stager::bytes(nnz + nnz / 8, nrows);
-        if (cudaHostAlloc((void**)&ds.pinned, want, cudaHostAllocPortable) == cudaSuccess) ds.pinned_cap = want;
-        else cudaGetLastError();
+      // (the same 1/8 headroom as the hint of later calls, so a pooled block fits them too)
+      stg.nnz_cap = std::max(nnz + nnz / 8, 1LL);
+      if (ha) {
+        stg.base = (char*)ha->alloc(ha->user, (int64_t)Stager::bytes(stg.nnz_cap, nrows), 5);
+        if (!stg.base) { set_err("output allocation failed (page-locked block)"); return NLG_ERR_CUDA; }
+      } else {
+        stg.base = Stager::own(&ds, stg.nnz_cap, nrows);
       }
-      stg.nnz_cap = nnz;
     }
-    if (ds.pinned) {
+    if (stg.base) {
       o_dat = stg.dat();
       o_idx = stg.idx();
       o_ptr = stg.ptr();
     }
-    ds.pin_nnz = std::max(ds.pin_nnz, nnz + nnz / 8);  // the next call stages batch by batch
+    ds.pin_nnz = ds.pin_sig == sig ? std::max(ds.pin_nnz, nnz + nnz / 8) : nnz + nnz / 8;  // the next call stages batch by batch
+    ds.pin_sig = sig;
   }
   DevBuf ptrbuf;
   CK(ptrbuf.alloc(sizeof(long long) * (nrows + 1), s));
@@ -4969,7 +5065,7 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
     }
     CK(cudaMemcpyAsync(ptrbuf.as<long long>() + (p.row_lo - row_lo), p.indptr, sizeof(long long) * (nr + 1),
                        cudaMemcpyDeviceToDevice, s));
-    if (p.nnz && !(all_staged && ds.pinned && o_dat == stg.dat())) {
+    if (p.nnz && !(out_on_host && all_staged)) {
       CK(cudaMemcpyAsync(o_idx + run, p.indices, sizeof(int) * p.nnz, cudaMemcpyDefault, s));
       CK(cudaMemcpyAsync(o_dat + run, p.data, sizeof(double) * p.nnz, cudaMemcpyDefault, s));
     }
@@ -4984,7 +5080,13 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
   TRACE("outputs synced");
   const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
                b_ptr = sizeof(long long) * (nrows + 1);
-  if (out_on_host && o_dat != u_dat) {  // pinned staging -> caller buffers
+  if (ha) {
+    ha->out->arena = stg.base;
+    ha->out->nnz = nnz;
+    ha->out->off_data = 0;
+    ha->out->off_indices = (int64_t)Stager::off_idx(stg.nnz_cap);
+    ha->out->off_indptr = (int64_t)Stager::off_ptr(stg.nnz_cap);
+  } else if (out_on_host && o_dat != u_dat) {  // library staging -> caller buffers
     struct Part { void* dst; const void* src; size_t n; };
     const Part parts[3] = {{u_dat, o_dat, b_dat}, {u_idx, o_idx, b_idx}, {u_ptr, o_ptr, b_ptr}};
     const int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
@@ -5226,8 +5328,9 @@ void nlg_plan_destroy(nlg_plan* pl) {
   delete pl;
 }
 
-nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t out_on_host,
-                        nlg_alloc_fn alloc, void* user, int64_t budget, nlg_stats* stats) {
+static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t out_on_host,
+                                nlg_alloc_fn alloc, void* user, int64_t budget, nlg_stats* stats,
+                                const HostArena* ha) {
   if (!pl || !alloc) { set_err("null plan or allocator"); return NLG_ERR_CONFIG; }
   if (row_lo < 0 || row_hi > pl->P.J || row_lo > row_hi) { set_err("row range out of bounds"); return NLG_ERR_CONFIG; }
   CK(cudaSetDevice(pl->device));
@@ -5246,6 +5349,8 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     else cudaGetLastError();
   }
   pl->arena_used = 0;
+  ds.rb_pending.clear();  // (reads queued by a call that failed midway)
+  ds.rb_used = 0;
   struct ArenaActivate {
     ArenaActivate(nlg_plan* p) { g_arena_plan = p; }
     ~ArenaActivate() { g_arena_plan = nullptr; }
@@ -5280,7 +5385,13 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   CK(cudaMemsetAsync(derr.p, 0xff, 2 * sizeof(unsigned long long), s));
   std::vector<Csr> pieces;
   Stager stg;
-  if (out_on_host) stg.begin(pl, &ds, row_hi - row_lo);
+  // (the size hint of a caller's block belongs to one problem and row range)
+  unsigned long long sig = 1469598103934665603ull;
+  for (unsigned long long v : {(unsigned long long)pl->P.K, (unsigned long long)pl->P.J, (unsigned long long)row_lo,
+                               (unsigned long long)row_hi, (unsigned long long)pl->P.kid,
+                               (unsigned long long)__builtin_bit_cast(long long, pl->P.delta)})
+    sig = (sig ^ v) * 1099511628211ull;
+  if (out_on_host) stg.begin(pl, &ds, row_hi - row_lo, ha, sig);
   Counters ctr{};
   Timing tm;
   // row batches: a work list of ranges, split in halves when over budget
@@ -5336,7 +5447,7 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
   }
   // pieces are produced in ascending row order (ranges are popped low-first)
   long long nnz = 0;
-  rc = emit_pieces(pl, ds, pieces, row_lo, row_hi, out_on_host, alloc, user, e2, &nnz, stg);
+  rc = emit_pieces(pl, ds, pieces, row_lo, row_hi, out_on_host, alloc, user, e2, &nnz, stg, ha, sig);
   if (rc) return rc;
   unsigned long long hc[K_NCOUNTERS], herr, herr2[2];
   CK(cudaMemcpyAsync(hc, dctr.p, sizeof hc, cudaMemcpyDeviceToHost, s));
@@ -5385,6 +5496,34 @@ nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t ou
     return NLG_ERR_NUMERICAL;
   }
   return NLG_OK;
+}
+
+nlg_status nlg_assemble(nlg_plan* pl, int64_t row_lo, int64_t row_hi, int32_t out_on_host,
+                        nlg_alloc_fn alloc, void* user, int64_t budget, nlg_stats* stats) {
+  return assemble_impl(pl, row_lo, row_hi, out_on_host, alloc, user, budget, stats, nullptr);
+}
+
+nlg_status nlg_assemble_pinned(nlg_plan* pl, int64_t row_lo, int64_t row_hi, nlg_alloc_fn block_alloc, void* user,
+                               int64_t budget, nlg_stats* stats, nlg_host_csr* out) {
+  if (!out) { set_err("null result"); return NLG_ERR_CONFIG; }
+  memset(out, 0, sizeof *out);
+  HostArena ha;
+  ha.alloc = block_alloc;
+  ha.user = user;
+  ha.out = out;
+  return assemble_impl(pl, row_lo, row_hi, 1, block_alloc, user, budget, stats, &ha);
+}
+
+void* nlg_pinned_alloc(int64_t nbytes) {
+  void* p = nullptr;
+  if (nbytes <= 0 || cudaHostAlloc(&p, (size_t)nbytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+void nlg_pinned_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 static nlg_status ensure_active(nlg_plan* pl) {
@@ -5548,7 +5687,7 @@ nlg_status nlg_mass(nlg_plan* pl, int32_t out_on_host, nlg_alloc_fn alloc, void*
   }
   long long nnz = 0;
   Stager none;
-  return emit_pieces(pl, ds, pieces, 0, P.J, out_on_host, alloc, user, nullptr, &nnz, none);
+  return emit_pieces(pl, ds, pieces, 0, P.J, out_on_host, alloc, user, nullptr, &nnz, none, nullptr, 0ull);
 }
 
 nlg_status nlg_row_work(nlg_plan* pl, int64_t* work) {

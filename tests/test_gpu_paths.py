@@ -109,3 +109,28 @@ def test_stage_w_deterministic_across_table_sizes():
     b = _assemble(c, {"NLG_ROW_FILL_DIV": "32"})
     assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
     assert np.array_equal(a.data, b.data)
+
+
+def test_pinned_host_output_pool():
+    """Host CSR through nlg_assemble_pinned (views of a pooled page-locked
+    block) equals the staged nlg_assemble path bit for bit; a live result is
+    never overwritten by a later assembly, and a dropped one is recycled."""
+    import gc
+    from paper_2207_03921_b200 import _native
+    c = Case("lshape16_affine")
+    staged = _assemble(c, {"NLG_NO_PINNED_OUTPUT": "1"})
+    a1 = _assemble(c)
+    snap = (a1.indptr.copy(), a1.indices.copy(), a1.data.copy())
+    a2 = _assemble(c)  # a1 still alive: another block
+    assert a2.data.ctypes.data != a1.data.ctypes.data
+    for m in (a1, a2):
+        assert np.array_equal(m.indptr, staged.indptr) and np.array_equal(m.indices, staged.indices)
+        assert np.array_equal(m.data, staged.data)
+    assert np.array_equal(a1.indptr, snap[0]) and np.array_equal(a1.indices, snap[1]) and np.array_equal(a1.data, snap[2])
+    assert same_pattern(a1, c.matrix) and rel_fro(a1, c.matrix) <= TOL
+    del a1, a2, m
+    gc.collect()
+    n0 = _native.PINNED.n_alloc
+    a3 = _assemble(c)  # steady state: a pooled block, no new pinning
+    assert _native.PINNED.n_alloc == n0
+    assert np.array_equal(a3.data, staged.data)

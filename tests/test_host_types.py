@@ -123,4 +123,4 @@ def test_c_abi_exports_every_declared_symbol():
     for n in sorted(names):
         assert hasattr(lib, n), f"{n} declared in include/nlg.h but not exported"
     assert set(_native.SIGNATURES) <= names
-    assert lib.nlg_abi_version() == 4
+    assert lib.nlg_abi_version() == 5
