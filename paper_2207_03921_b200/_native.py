@@ -204,8 +204,8 @@ class PinnedPool:
 
     Pinning memory costs ~0.2 s per GB, so blocks are recycled: a block goes
     back to the pool when the last numpy view of it is collected, and the
-    next assembly of a similar size takes it again.  At most ``keep`` free
-    blocks (NLG_PINNED_KEEP, default 2) stay pinned; the rest are released.
+    next assembly of a similar size takes it again.  The ``keep`` most recently
+    returned blocks (NLG_PINNED_KEEP, default 2) stay pinned; older ones are released.
     """
 
     _GRAIN = 1 << 26  # 64 MiB: similar sizes share a block
@@ -241,9 +241,9 @@ class PinnedPool:
         self.trim(self.keep)
 
     def trim(self, keep):
-        with self._mu:
-            self._free.sort()
-            drop, self._free = self._free[:max(len(self._free) - keep, 0)], self._free[max(len(self._free) - keep, 0):]
+        with self._mu:  # (least recently returned first)
+            cut = max(len(self._free) - keep, 0)
+            drop, self._free = self._free[:cut], self._free[cut:]
         lib = _lib
         for _, addr in drop:
             if lib is not None:

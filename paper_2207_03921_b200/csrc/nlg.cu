@@ -2019,7 +2019,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
     __syncwarp();
     // ---- the queued clips on consecutive lanes
 #pragma unroll 1
-    for (int qi = lane; qi < qn; qi += 32) {
+    for (int qi = lane; qi < ((P.dbg & 64) ? 0 : qn); qi += 32) {  // (NLG_DEBUG & 64 / 128 / 256: timing experiments)
       const int sl = S.q[qi];
       const int mj = (S.pm[sl] >> 4) & 3;
       const double* tv = S.tv[sl >> 4][mj == 1];
@@ -2030,7 +2030,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
     __syncwarp();
     // ---- per slot: closed-form fan sums, then fold and reduce two records
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < ((P.dbg & 128) ? 0 : 2); ++h) {
       const int rec = vs + 2 * h, sl = lane + 32 * h;
       const long long v = rd * 4 + rec;
       const bool vok = v < O.nlist;
@@ -2043,7 +2043,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
 #pragma unroll
       for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
       const int nv = S.nv[sl];
-      if (ivalid && nv >= 3) {
+      if (ivalid && nv >= 3 && !(P.dbg & 256)) {
         n_out0 += mi == 0 ? mult : 0;
         n_out1 += mi == 1 ? mult : 0;
         n_out2 += mi == 2;

@@ -54,24 +54,49 @@ __device__ __forceinline__ void push_dedup(double* ox, double* oy, unsigned& fla
   }
 }
 
+// The rows of a clip in progress: the last (and first) row stay in
+// registers, so the dedup test of a push reads no memory.
+struct ClipRows {
+  double* ox;
+  double* oy;
+  double dtol, lx, ly, fx, fy;
+  unsigned flags;
+  int n;
+  __device__ __forceinline__ void push(bool on, double px, double py, bool crossing, bool first_ok) {
+    if (on && ((first_ok && n == 0) || fabs(lx - px) > dtol || fabs(ly - py) > dtol)) {
+      ox[n] = px;
+      oy[n] = py;
+      if (n == 0) { fx = px; fy = py; }
+      lx = px;
+      ly = py;
+      if (crossing) flags |= 1u << n;
+      ++n;
+    }
+  }
+};
+
 // clip_circle: vertices of the convex CCW triangle T inside the closed disk
 // around (cx, cy) plus edge/circle crossings; bit i of *flags_out marks row i
 // as a crossing.  Returns the row count (< 3: empty/degenerate).
+// The reference's three cases per edge (leaving / entering / through the
+// disk, _geom_scalar.py:75-108) run as one predicated sequence -- lanes of a
+// warp clip different triangles, and a branch per case would run every case
+// in turn: one square root, the first root's division for every crossing
+// edge, the second root's only for "through" edges.  Same operations on the
+// same operands as the reference; rows pushed in the same order.
 __device__ __forceinline__ int clip_circle(Tri T, double cx, double cy, double delta, double* ox, double* oy,
                                         unsigned* flags_out) {
   const double rad = mul(delta, 1.0 + kBallTieRel);
   const double r2 = mul(rad, rad);
-  const double dtol = mul(kDedupRel, delta);
   const double q0 = __dsub_rn(sumsq(T.x0 - cx, T.y0 - cy), r2);
   const double q1 = __dsub_rn(sumsq(T.x1 - cx, T.y1 - cy), r2);
   const double q2 = __dsub_rn(sumsq(T.x2 - cx, T.y2 - cy), r2);
-  int n = 0;
-  unsigned flags = 0;
+  ClipRows R{ox, oy, mul(kDedupRel, delta), 0.0, 0.0, 0.0, 0.0, 0u, 0};
   if (q0 <= 0.0 && q1 <= 0.0 && q2 <= 0.0) {
     // every edge runs inside: the general loop would only append the vertices
-    push_dedup(ox, oy, flags, n, T.x0, T.y0, false, dtol, true);
-    push_dedup(ox, oy, flags, n, T.x1, T.y1, false, dtol, true);
-    push_dedup(ox, oy, flags, n, T.x2, T.y2, false, dtol, true);
+    R.push(true, T.x0, T.y0, false, true);
+    R.push(true, T.x1, T.y1, false, true);
+    R.push(true, T.x2, T.y2, false, true);
   } else {
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
@@ -79,42 +104,38 @@ __device__ __forceinline__ int clip_circle(Tri T, double cx, double cy, double d
       const double ax = T.x(i), ay = T.y(i), bx = T.x(j), by = T.y(j);
       const double qa = i == 0 ? q0 : (i == 1 ? q1 : q2);
       const double qb = j == 0 ? q0 : (j == 1 ? q1 : q2);
+      const bool ina = qa <= 0.0, inb = qb <= 0.0;
       const double dax = ax - cx, day = ay - cy;
-      if (qa <= 0.0) push_dedup(ox, oy, flags, n, ax, ay, false, dtol, true);
+      R.push(ina, ax, ay, false, true);
       const double ex = bx - ax, ey = by - ay;
       const double aa = sumsq(ex, ey);
-      if (aa <= 0.0) continue;
-      if (qa <= 0.0 && qb <= 0.0) continue;
       const double bb = mul(2.0, __dadd_rn(mul(ex, dax), mul(ey, day)));
       const double disc = __dsub_rn(mul(bb, bb), mul(mul(4.0, aa), qa));
-      if (disc <= 0.0) continue;
+      const bool cross = !(aa <= 0.0) && !(ina && inb) && !(disc <= 0.0);
+      if (!cross) continue;
       const double sq = sqrt(disc);
       const double den = mul(2.0, aa);
-      if (qa <= 0.0) {  // leaving the disk: exit root
-        const double t2 = (-bb + sq) / den;
-        if (0.0 < t2 && t2 < 1.0)
-          push_dedup(ox, oy, flags, n, __dadd_rn(ax, mul(t2, ex)), __dadd_rn(ay, mul(t2, ey)), true, dtol, true);
-      } else if (qb <= 0.0) {  // entering: entry root
-        const double t1 = (-bb - sq) / den;
-        if (0.0 < t1 && t1 < 1.0)
-          push_dedup(ox, oy, flags, n, __dadd_rn(ax, mul(t1, ex)), __dadd_rn(ay, mul(t1, ey)), true, dtol, true);
-      } else {  // outside to outside through the disk
-        const double t1 = (-bb - sq) / den;
-        const double t2 = (-bb + sq) / den;
-        if (0.0 < t1 && t2 < 1.0 && t1 < t2) {
-          push_dedup(ox, oy, flags, n, __dadd_rn(ax, mul(t1, ex)), __dadd_rn(ay, mul(t1, ey)), true, dtol, true);
-          push_dedup(ox, oy, flags, n, __dadd_rn(ax, mul(t2, ex)), __dadd_rn(ay, mul(t2, ey)), true, dtol, false);
-        }
-      }
+      // first root of the edge: the exit root when leaving, else the entry root
+      const double ta = (ina ? -bb + sq : -bb - sq) / den;
+      const bool through = !ina && !inb;
+      double tb = 0.0;
+      if (through) tb = (-bb + sq) / den;
+      const bool ok = through ? (0.0 < ta && tb < 1.0 && ta < tb) : (0.0 < ta && ta < 1.0);
+      R.push(ok, __dadd_rn(ax, mul(ta, ex)), __dadd_rn(ay, mul(ta, ey)), true, true);
+      R.push(ok && through, __dadd_rn(ax, mul(tb, ex)), __dadd_rn(ay, mul(tb, ey)), true, false);
     }
   }
-  if (n >= 2 && fabs(ox[0] - ox[n - 1]) <= dtol && fabs(oy[0] - oy[n - 1]) <= dtol) --n;
-  *flags_out = flags & ((1u << n) - 1u);
+  int n = R.n;
+  if (n >= 2 && fabs(R.fx - R.lx) <= R.dtol && fabs(R.fy - R.ly) <= R.dtol) --n;
+  *flags_out = R.flags & ((1u << n) - 1u);
   return n;
 }
 
 // insert_caps: copy the clip rows to (px, py), adding the arc midpoint behind
 // every chord between consecutive crossings when it lies inside the triangle.
+// The (<= 3) chords are evaluated first, one per trip of a short loop -- so
+// lanes clipping different triangles do their square roots and divisions
+// together -- and the rows are copied afterwards.
 __device__ __forceinline__ int insert_caps(Tri T, const double* bx, const double* by, unsigned bflag, int nb,
                                         double cx, double cy, double delta, double* px, double* py) {
   if (nb < 2) {
@@ -122,42 +143,61 @@ __device__ __forceinline__ int insert_caps(Tri T, const double* bx, const double
     return nb;
   }
   const double rad = mul(delta, 1.0 + kBallTieRel);
-  const double b0x = bx[0], b0y = by[0];  // (px, py) may overwrite it (in-place use below)
   // a cap needs a crossing followed (cyclically) by a crossing
   const unsigned next = (bflag >> 1) | ((bflag & 1u) << (nb - 1));
-  double el0 = 0.0, el1 = 0.0, el2 = 0.0, href = 0.0;
-  if (bflag & next) {
-    el0 = sqrt(sumsq(T.x1 - T.x0, T.y1 - T.y0));
-    el1 = sqrt(sumsq(T.x2 - T.x1, T.y2 - T.y1));
-    el2 = sqrt(sumsq(T.x0 - T.x2, T.y0 - T.y2));
-    href = el0;
+  unsigned cand = bflag & next, capmask = 0;
+  double capx0 = 0.0, capy0 = 0.0, capx1 = 0.0, capy1 = 0.0, capx2 = 0.0, capy2 = 0.0;
+  if (cand) {
+    const double el0 = sqrt(sumsq(T.x1 - T.x0, T.y1 - T.y0));
+    const double el1 = sqrt(sumsq(T.x2 - T.x1, T.y2 - T.y1));
+    const double el2 = sqrt(sumsq(T.x0 - T.x2, T.y0 - T.y2));
+    double href = el0;
     if (el1 > href) href = el1;
     if (el2 > href) href = el2;
+    const double tol = mul(-kCapMemberRel, href);
+    int c = 0;
+#pragma unroll 1
+    while (cand) {
+      const int i = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const int j = i + 1 == nb ? 0 : i + 1;
+      const double bix = bx[i], biy = by[i], bjx = bx[j], bjy = by[j];
+      const double chx = bjx - bix, chy = bjy - biy;
+      const double chord = sqrt(sumsq(chx, chy));
+      const double mx = __dsub_rn(mul(0.5, __dadd_rn(bix, bjx)), cx);
+      const double my = __dsub_rn(mul(0.5, __dadd_rn(biy, bjy)), cy);
+      const double nd = sqrt(sumsq(mx, my));
+      if (chord < mul(kChordSkipRel, delta) || nd < mul(1e-14, delta)) continue;
+      const double capx = __dadd_rn(cx, mul(rad, mx) / nd);
+      const double capy = __dadd_rn(cy, mul(rad, my) / nd);
+      // membership against the three edges (the reference stops at the first miss)
+      const bool inside = cross2(T.x1 - T.x0, capy - T.y0, T.y1 - T.y0, capx - T.x0) >= mul(tol, el0) &&
+                          cross2(T.x2 - T.x1, capy - T.y1, T.y2 - T.y1, capx - T.x1) >= mul(tol, el1) &&
+                          cross2(T.x0 - T.x2, capy - T.y2, T.y0 - T.y2, capx - T.x2) >= mul(tol, el2);
+      if (inside) {
+        capmask |= 1u << i;
+        if (c == 0) { capx0 = capx; capy0 = capy; }
+        else if (c == 1) { capx1 = capx; capy1 = capy; }
+        else { capx2 = capx; capy2 = capy; }
+        ++c;
+      }
+    }
   }
-  int n = 0;
+  // rows in order, each followed by its cap ((px, py) may alias (bx - 3, by - 3):
+  // row i lands at i + caps so far <= 3 + i, never ahead of an unread row)
+  int n = 0, c = 0;
 #pragma unroll 1
   for (int i = 0; i < nb; ++i) {
-    const int j = i + 1 == nb ? 0 : i + 1;
-    px[n] = bx[i];
-    py[n] = by[i];
+    const double rx = bx[i], ry = by[i];
+    px[n] = rx;
+    py[n] = ry;
     ++n;
-    if (!((bflag >> i) & 1u) || !((bflag >> j) & 1u)) continue;
-    const double bjx = j ? bx[j] : b0x, bjy = j ? by[j] : b0y;
-    const double chx = bjx - bx[i], chy = bjy - by[i];
-    const double chord = sqrt(sumsq(chx, chy));
-    if (chord < mul(kChordSkipRel, delta)) continue;
-    const double mx = __dsub_rn(mul(0.5, __dadd_rn(bx[i], bjx)), cx);
-    const double my = __dsub_rn(mul(0.5, __dadd_rn(by[i], bjy)), cy);
-    const double nd = sqrt(sumsq(mx, my));
-    if (nd < mul(1e-14, delta)) continue;
-    const double capx = __dadd_rn(cx, mul(rad, mx) / nd);
-    const double capy = __dadd_rn(cy, mul(rad, my) / nd);
-    const double tol = mul(-kCapMemberRel, href);
-    // membership against the three edges, in order, stopping at the first miss
-    bool inside = cross2(T.x1 - T.x0, capy - T.y0, T.y1 - T.y0, capx - T.x0) >= mul(tol, el0);
-    if (inside) inside = cross2(T.x2 - T.x1, capy - T.y1, T.y2 - T.y1, capx - T.x1) >= mul(tol, el1);
-    if (inside) inside = cross2(T.x0 - T.x2, capy - T.y2, T.y0 - T.y2, capx - T.x2) >= mul(tol, el2);
-    if (inside) { px[n] = capx; py[n] = capy; ++n; }
+    if ((capmask >> i) & 1u) {
+      px[n] = c == 0 ? capx0 : (c == 1 ? capx1 : capx2);
+      py[n] = c == 0 ? capy0 : (c == 1 ? capy1 : capy2);
+      ++n;
+      ++c;
+    }
   }
   return n;
 }
