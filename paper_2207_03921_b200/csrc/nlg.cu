@@ -182,6 +182,7 @@ struct Grid {
   const double* __restrict__ grad;
   const double4* __restrict__ gft;  // analytic: (A2 psi_0, A2 psi_1, A2 psi_2, A2) in scan order
   const int4* __restrict__ gdof;    // analytic: dof bases in scan order
+  const double* __restrict__ gcsum; // analytic: per cell, the sum of its elements' A2 (scan order)
   // analytic: the dof bases (columns) on the same cells, by their position
   const int* __restrict__ cstart;   // [ncell + 1]
   const int* __restrict__ cid;      // dof base of each slot
@@ -201,6 +202,15 @@ __global__ void k_grid_gather(Params P, const int* __restrict__ items, int n, in
     gft[j] = P.ftab[l];
     gdof[j] = P.dofs[l];
   }
+}
+
+// analytic: the summed A2 of each cell's elements, in scan order (one thread per cell)
+__global__ void k_cell_sums(const int* __restrict__ start, int ncell, const double4* __restrict__ gft, double* csum) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  double sacc = 0.0;
+  for (int j = start[c]; j < start[c + 1]; ++j) sacc += gft[j].w;
+  csum[c] = sacc;
 }
 
 __global__ void k_cell(Params P, Grid G, unsigned* key, int* val) {
@@ -645,6 +655,10 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
     // reach-sized cells)
     int iy = (int)floor((ck.y - G.oy) / G.cs);
     iy = min(max(iy, 0), G.ny - 1);
+    int ix = (int)floor((ck.x - G.ox) / G.cs);
+    ix = min(max(ix, 0), G.nx - 1);
+    // surely-full radius: dist <= rho  =>  (dist + r_k) + r_l <= delta for every r_l <= r_max
+    const double rho = P.delta - rk - G.rmax - 1e-9 * (P.delta + G.rmax) - 2.0 * G.cs * 1e-9;
     int c[7] = {0, 0, 0, 0, 0, 0, 0};
     long long base[4];
     int2* lists[4] = {comb, ls0, ls1, ls2};
@@ -666,7 +680,49 @@ __global__ void __launch_bounds__(256, 3) k_candidates(Params P, Grid G, const i
       if (x0 > x1) continue;
       const int c0 = G.start[yy * G.nx + x0];
       const int c1 = G.start[yy * G.nx + x1 + 1];
-      for (int j0 = c0; j0 < c1; j0 += 32) {
+      // analytic: cells that lie wholly within rho of the barycentre hold
+      // only full partners (dist + r_k + r_l <= delta with room to spare):
+      // they are counted, and their areas summed, cell by cell -- no
+      // candidate test.  The root's own cell is scanned (the pair (k, k)).
+      int seg_lo[3] = {c0, c1, c1}, seg_hi[3] = {c1, c1, c1};
+      if (P.analytic && rho > 0.0) {
+        const double dym = fmax(fabs(ylo - ck.y), fabs(yhi - ck.y));
+        if (dym < rho) {
+          const double hwd = sqrt(rho * rho - dym * dym);
+          const int xa = max((int)ceil((ck.x - hwd - G.ox) / G.cs), x0);
+          const int xb = min((int)floor((ck.x + hwd - G.ox) / G.cs) - 1, x1);
+          if (xa <= xb) {
+            // deep cells [xa, xb], minus the root's own cell
+            int ra[2] = {xa, 0}, rb[2] = {xb, -1};
+            if (yy == iy && ix >= xa && ix <= xb) {
+              rb[0] = ix - 1;
+              ra[1] = ix + 1;
+              rb[1] = xb;
+            }
+            int ns = 0, cur = c0;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              if (ra[q] > rb[q]) continue;
+              const int da = G.start[yy * G.nx + ra[q]], db = G.start[yy * G.nx + rb[q] + 1];
+              seg_lo[ns] = cur;
+              seg_hi[ns] = da;
+              ++ns;
+              cur = db;
+              if (!FILL) {
+                if (lane == 0) c[C_EPI] += db - da;
+              } else {
+                for (int cx = ra[q] + lane; cx <= rb[q]; cx += 32) own += G.gcsum[yy * G.nx + cx];
+              }
+            }
+            seg_lo[ns] = cur;
+            seg_hi[ns] = c1;
+          }
+        }
+      }
+#pragma unroll 1
+      for (int sg = 0; sg < 3; ++sg)
+      for (int j0 = seg_lo[sg]; j0 < seg_hi[sg]; j0 += 32) {
+        const int c1 = seg_hi[sg];
         const int j = j0 + lane;
         int cat = -1, fl = 0;
         bool vis = false, an = false;
@@ -3688,6 +3744,7 @@ struct nlg_plan {
   double* grid_rad = nullptr;
   double4* grid_ft = nullptr;
   int4* grid_dof = nullptr;
+  double* grid_csum = nullptr;
   int* col_start = nullptr;   // analytic: column grid
   int* col_id = nullptr;
   double4* col_pos = nullptr;
@@ -3828,9 +3885,10 @@ nlg_status prep(nlg_plan* pl) {
   double ox = ord2d(h[0]), oy = ord2d(h[1]), mx = ord2d(h[2]), my = ord2d(h[3]), rmax = ord2d(h[4]);
   if (h[2] == 0ull) { ox = oy = mx = my = 0.0; rmax = 0.0; }  // no active element
   const double reach = (P.prer + 2.0 * rmax) * (1.0 + 1e-9) + 1e-300;
-  // pitch: reach / 6 (the scanned cell rows hug the disk: ~1.5x its area; reach / 2 scanned ~2.4x);
+  // pitch: reach / 8 (the scanned cell rows hug the disk, and the cells wholly inside the analytic
+  // kernels' surely-full radius cover most of it; reach / 2 scanned ~2.4x the disk's area);
   // NLG_GRID_DIV: A/B (the row merge holds <= kMaxRowsG cell rows)
-  static const int grid_div = getenv("NLG_GRID_DIV") ? std::min(16, std::max(1, atoi(getenv("NLG_GRID_DIV")))) : 6;
+  static const int grid_div = getenv("NLG_GRID_DIV") ? std::min(16, std::max(1, atoi(getenv("NLG_GRID_DIV")))) : 8;
   double cs = reach / grid_div;
   // keep the cell count bounded (tiny horizons on huge meshes)
   const double ext_x = mx - ox, ext_y = my - oy;
@@ -3887,6 +3945,14 @@ nlg_status prep(nlg_plan* pl) {
   G.grad = pl->grid_rad;
   G.gft = P.analytic ? pl->grid_ft : nullptr;
   G.gdof = P.analytic ? pl->grid_dof : nullptr;
+  G.gcsum = nullptr;
+  if (P.analytic && K) {
+    if (pl->grid_csum) cudaFreeAsync(pl->grid_csum, st);
+    CK(cudaMallocAsync(&pl->grid_csum, sizeof(double) * ncell, st));
+    k_cell_sums<<<grid_for(ncell, 256), 256, 0, st>>>(pl->grid_start, ncell, pl->grid_ft, pl->grid_csum);
+    LAUNCHED();
+    G.gcsum = pl->grid_csum;
+  }
   G.cstart = nullptr;
   G.cid = nullptr;
   G.cpos = nullptr;
@@ -5317,7 +5383,7 @@ void nlg_plan_destroy(nlg_plan* pl) {
   void* ptrs[] = {pl->vtx,        pl->elem,       pl->dofs,     pl->ctr,      pl->rad,     pl->ftab,
                   pl->fmax,       pl->de_start,   pl->de_items, pl->grid_start, pl->grid_items, pl->act,
                   pl->grid_el,    pl->grid_ctr,   pl->grid_rad, pl->grid_ft, pl->grid_dof,
-                  pl->col_start,  pl->col_id,     pl->col_pos};
+                  pl->col_start,  pl->col_id,     pl->col_pos,  pl->grid_csum};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   for (auto& f : pl->sing_tab)
