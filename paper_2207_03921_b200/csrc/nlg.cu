@@ -375,14 +375,20 @@ __device__ __forceinline__ void fix_atomic(unsigned* c, fix_t x) {
   }
   if (x2) atomicAdd(&c[2], x2);
 }
+// Sum over the warp of 96-bit two's complement values (exact, so mod 2^96):
+// four 24-bit limbs, each summed by one warp reduction (32 x 2^24 < 2^32),
+// recombined with their carries.  Every lane gets the total.
 __device__ __forceinline__ fix_t fix_warp_sum(fix_t a) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)a, o);
-    const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(a >> 64), o);
-    a += ((fix_t)hi << 64) | (fix_t)lo;
-  }
-  return a;
+  const unsigned long long lo = (unsigned long long)a;
+  const unsigned hi = (unsigned)(a >> 64);
+  const unsigned s0 = __reduce_add_sync(0xffffffffu, (unsigned)lo & 0xffffffu);
+  const unsigned s1 = __reduce_add_sync(0xffffffffu, (unsigned)(lo >> 24) & 0xffffffu);
+  const unsigned s2 = __reduce_add_sync(0xffffffffu, ((unsigned)(lo >> 48) | (hi << 16)) & 0xffffffu);
+  const unsigned s3 = __reduce_add_sync(0xffffffffu, hi >> 8);
+  unsigned __int128 r = (unsigned __int128)s0 + ((unsigned __int128)s1 << 24) + ((unsigned __int128)s2 << 48) +
+                        ((unsigned __int128)s3 << 72);
+  r <<= 32;  // drop the bits above 96, then sign-extend
+  return (fix_t)r >> 32;
 }
 
 // The 7 rule points of a triangle (reference arithmetic, as rule_points).
