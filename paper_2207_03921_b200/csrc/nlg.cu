@@ -375,22 +375,21 @@ __device__ __forceinline__ void fix_atomic(unsigned* c, fix_t x) {
   }
   if (x2) atomicAdd(&c[2], x2);
 }
-// Sum over the warp of 96-bit two's complement values (exact, so mod 2^96):
-// four 24-bit limbs, each summed by one warp reduction (32 x 2^24 < 2^32),
-// recombined with their carries.  Every lane gets the total.
-__device__ __forceinline__ fix_t fix_warp_sum(fix_t a) {
+// Sum over a group of lanes of 96-bit two's complement values (exact, so mod
+// 2^96): four 24-bit limbs, each summed by one warp reduction (32 x 2^24 <
+// 2^32), recombined with their carries.  Every lane of the group gets the total.
+__device__ __forceinline__ fix_t fix_group_sum(unsigned mask, fix_t a) {  // (called by exactly the lanes of mask)
   const unsigned long long lo = (unsigned long long)a;
   const unsigned hi = (unsigned)(a >> 64);
-  const unsigned s0 = __reduce_add_sync(0xffffffffu, (unsigned)lo & 0xffffffu);
-  const unsigned s1 = __reduce_add_sync(0xffffffffu, (unsigned)(lo >> 24) & 0xffffffu);
-  const unsigned s2 = __reduce_add_sync(0xffffffffu, ((unsigned)(lo >> 48) | (hi << 16)) & 0xffffffu);
-  const unsigned s3 = __reduce_add_sync(0xffffffffu, hi >> 8);
+  const unsigned s0 = __reduce_add_sync(mask, (unsigned)lo & 0xffffffu);
+  const unsigned s1 = __reduce_add_sync(mask, (unsigned)(lo >> 24) & 0xffffffu);
+  const unsigned s2 = __reduce_add_sync(mask, ((unsigned)(lo >> 48) | (hi << 16)) & 0xffffffu);
+  const unsigned s3 = __reduce_add_sync(mask, hi >> 8);
   unsigned __int128 r = (unsigned __int128)s0 + ((unsigned __int128)s1 << 24) + ((unsigned __int128)s2 << 48) +
                         ((unsigned __int128)s3 << 72);
   r <<= 32;  // drop the bits above 96, then sign-extend
   return (fix_t)r >> 32;
 }
-
 // The 7 rule points of a triangle (reference arithmetic, as rule_points).
 __device__ __forceinline__ void tri_points(const double* tx, const double* ty, double* px, double* py) {
   const double e1x = tx[1] - tx[0], e2x = tx[2] - tx[0], e1y = ty[1] - ty[0], e2y = ty[2] - ty[0];
@@ -2811,6 +2810,12 @@ struct IncRoot {
   int k;          // element, -1: not a root of the batch
 };
 
+struct IncSide {  // an incident root of the row: its record sides, dofs, corner
+  RootSides R;
+  unsigned dk[3];
+  int k, a, rank, on;  // on: its own block is emitted by this batch
+};
+
 template <int NC, int CAP, int TH>
 struct RowSmem {
   using Sort = cub::BlockRadixSort<unsigned, TH, CAP / TH, unsigned>;
@@ -2823,6 +2828,10 @@ struct RowSmem {
     typename Scan::TempStorage scan;
   } u;
   IncRoot inc[kMaxInc];
+  IncSide isd[kMaxInc];                       // stored sides: the group's incident roots
+  long long spre[kMaxInc + 1];                // ... and the prefix of their side counts
+  unsigned ownacc[kMaxInc][3][NC * NC][3];    // ... and their own-block sums (96-bit fixed point)
+  unsigned ownpres[kMaxInc];
   int gr0[kMaxRowsG], gr1[kMaxRowsG], gpre[kMaxRowsG + 1];  // column ranges of the enumeration
   int er0[kMaxRowsG], epre[kMaxRowsG + 1];                  // element ranges of the same cell rows
   int ngr;
@@ -2945,73 +2954,135 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
   };
   if (inr) {
     // ---- the stored record sides of the batch roots incident to d
-    // (analytic mode: the clipped sides only; category-0 visits follow below)
+    // (analytic mode: the clipped sides only; category-0 visits follow below).
+    // The sides of up to kMaxInc incident roots form one flat index space,
+    // so every thread of the CTA has work until the last few sides.  Own-block
+    // values are summed in fixed point (exact: neither the CTA size nor the
+    // order of the sides, which depends on the batch, matters): per warp and
+    // root with one reduction, then into the group's accumulators.
     const int e0 = W.de_start[d], e1 = W.de_start[d + 1];
-    for (int ei = e0; ei < ((P.dbg & 4) ? e0 : e1); ++ei) {  // (NLG_DEBUG & 4: timing experiments)
-      const int it = __ldg(&W.de_items[ei]);
-      const int k = it >> 2, a = it & 3;
-      const int rank = __ldg(&W.inR[k]);
-      if (rank < 0) continue;  // block-uniform
-      const RootSides R = root_sides(I, rank);
-      const long long n_rs = R.n();
-      const int4 dk4 = __ldg(&P.dofs[k]);
-      const unsigned dk[3] = {(unsigned)dk4.x, (unsigned)dk4.y, (unsigned)dk4.z};
-      const bool own_on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
-      // own-block partials in fixed point: exact, so neither the CTA size
-      // nor the order of the sides (which depends on the batch) matters
-      fix_t own[3][NC2];
-      unsigned opres = 0;  // bit b * NC2 + comp
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int e = 0; e < NC2; ++e) own[b][e] = 0;
-      for (long long rs = t; rs < n_rs; rs += TH) {
-        if (*(volatile int*)&S.ovf) break;  // this table is too small: retried with a larger one
-        const int n = R.partner(I, rs);
-        const int4 dn4 = __ldg(&P.dofs[n]);
-        const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
-        const long long slot = R.slot(I, rs);
-        const double* kk = I.kkv + slot * Blk<NC>::NKK;
-        const double* kl = I.klv + slot * Blk<NC>::KLS;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          if (!((inr >> c) & 1u)) continue;
-          const int Ir = a * NC + c;
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-#pragma unroll
-            for (int dd = 0; dd < NC; ++dd) {
-              const int Jc = b * NC + dd;
-              const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
-              const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
-              if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
-                own[b][c * NC + dd] += fix_of(vo, scale);
-                opres |= 1u << (b * NC2 + c * NC + dd);
-              }
-              add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
-            }
+    for (int g0 = e0; g0 < ((P.dbg & 4) ? e0 : e1); g0 += kMaxInc) {  // (NLG_DEBUG & 4: timing experiments)
+      const int ng = min(e1 - g0, kMaxInc);
+      __syncthreads();
+      if (t < ng) {
+        IncSide& Q = S.isd[t];
+        const int it = __ldg(&W.de_items[g0 + t]);
+        const int k = it >> 2;
+        const int rank = __ldg(&W.inR[k]);
+        Q.k = k;
+        Q.a = it & 3;
+        Q.rank = rank;
+        Q.on = 0;
+        RootSides R;
+        R.f0 = R.fn = R.fb0 = R.fbn = R.p0 = R.pn = R.pb0 = R.pbn = 0;
+        if (rank >= 0) {
+          R = root_sides(I, rank);
+          const int4 dk4 = __ldg(&P.dofs[k]);
+          Q.dk[0] = (unsigned)dk4.x;
+          Q.dk[1] = (unsigned)dk4.y;
+          Q.dk[2] = (unsigned)dk4.z;
+          Q.on = I.cnt[(long long)C_KK * I.nR + rank] != 0;
         }
+        Q.R = R;
       }
-      // own block of (k, a): fixed-point partials -> warp sums -> table
-#pragma unroll
-      for (int o = 16; o; o >>= 1) opres |= __shfl_xor_sync(0xffffffffu, opres, o);
-      if (opres) {  // warp-uniform
+      for (int i = t; i < kMaxInc * 3 * NC2 * 3; i += TH) (&S.ownacc[0][0][0][0])[i] = 0;
+      if (t < kMaxInc) S.ownpres[t] = 0;
+      __syncthreads();
+      if (t == 0) {
+        long long run = 0;
+        for (int i = 0; i < ng; ++i) {
+          S.spre[i] = run;
+          run += S.isd[i].R.n();
+        }
+        S.spre[ng] = run;
+      }
+      __syncthreads();
+      const long long total = S.spre[ng];
+      int i = 0;
+      for (long long fb = t & ~31; fb < total; fb += TH) {  // (warp-uniform trip count)
+        if (*(volatile int*)&S.ovf) break;  // this table is too small: retried with a larger one
+        const long long f = fb + (t & 31);
+        const bool valid = f < total;
+        fix_t own[3][NC2];
+        unsigned opres = 0;  // bit b * NC2 + comp
 #pragma unroll
         for (int b = 0; b < 3; ++b)
 #pragma unroll
-          for (int e = 0; e < NC2; ++e) {
-            const fix_t f = fix_warp_sum(own[b][e]);
-            if ((t & 31) == 0 && own_on) add_fix(dk[b], e, f, (opres >> (b * NC2 + e)) & 1u);
+          for (int e = 0; e < NC2; ++e) own[b][e] = 0;
+        if (valid) {
+          while (f >= S.spre[i + 1]) ++i;
+          const IncSide& Q = S.isd[i];
+          const RootSides R = Q.R;
+          const long long rs = f - S.spre[i];
+          const int a = Q.a;
+          const int n = R.partner(I, rs);
+          const int4 dn4 = __ldg(&P.dofs[n]);
+          const unsigned dn[3] = {(unsigned)dn4.x, (unsigned)dn4.y, (unsigned)dn4.z};
+          const long long slot = R.slot(I, rs);
+          const double* kk = I.kkv + slot * Blk<NC>::NKK;
+          const double* kl = I.klv + slot * Blk<NC>::KLS;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (!((inr >> c) & 1u)) continue;
+            const int Ir = a * NC + c;
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int dd = 0; dd < NC; ++dd) {
+                const int Jc = b * NC + dd;
+                const double vo = __ldg(&kk[Blk<NC>::sym(min(Ir, Jc), max(Ir, Jc))]);
+                const double vn = __ldg(&kl[Blk<NC>::kl(Ir, Jc)]);
+                if (vo != 0.0 && vo == vo && fabs(vo) <= 1e300) {
+                  own[b][c * NC + dd] = fix_of(vo, scale);
+                  opres |= 1u << (b * NC2 + c * NC + dd);
+                }
+                add(dn[b], c * NC + dd, vn, __double_as_longlong(vn) != 0);
+              }
           }
+        }
+        // own partials: one warp reduction per root present in the warp
+        unsigned rem = __ballot_sync(0xffffffffu, valid);
+        while (rem) {
+          const int leader = __ffs(rem) - 1;
+          const int il = __shfl_sync(0xffffffffu, i, leader);
+          const unsigned grp = __ballot_sync(0xffffffffu, valid && i == il);
+          if (valid && i == il) {
+            const unsigned gp = __reduce_or_sync(grp, opres);
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int e = 0; e < NC2; ++e) {
+                if (!((gp >> (b * NC2 + e)) & 1u)) continue;  // group-uniform
+                const fix_t fs = fix_group_sum(grp, own[b][e]);
+                if ((t & 31) == leader) fix_atomic(S.ownacc[il][b][e], fs);
+              }
+            if ((t & 31) == leader && gp) atomicOr(&S.ownpres[il], gp);
+          }
+          rem &= ~grp;
+        }
       }
-      if (AN && t < 3 && own_on) {
+      __syncthreads();
+      // the group's own blocks -> table
+      for (int q = t; q < ng * 3 * NC2; q += TH) {
+        const int gi = q / (3 * NC2), b = (q / NC2) % 3, e = q % NC2;
+        const IncSide& Q = S.isd[gi];
+        if (!Q.on || !((S.ownpres[gi] >> (b * NC2 + e)) & 1u)) continue;
+        const unsigned* c = S.ownacc[gi][b][e];
+        const fix_t f = (fix_t)(((unsigned __int128)c[2] << 64 | (unsigned __int128)c[1] << 32 | c[0]) << 32) >> 32;
+        add_fix(Q.dk[b], e, f, true);
+      }
+      if (AN && t < 3 * ng) {
         // analytic own terms: 2 A2_k sw Phi_k[a][b] x (sum of the category-0
         // partners' A2, summed exactly by the candidate fill pass)
-        const double sa_d = __ldg(&I.own_a2[rank]);
-        if (sa_d != 0.0) {
-          const double fown = (2.0 * __ldg(&P.ftab[k].w) * sw) *
-                              (P.kid == 2 ? root_phi<2>(P, k, a, t) : root_phi<3>(P, k, a, t));
-          add(dk[t], 0, fown * sa_d, fown != 0.0);
+        const IncSide& Q = S.isd[t / 3];
+        const int b = t % 3;
+        if (Q.on) {
+          const double sa_d = __ldg(&I.own_a2[Q.rank]);
+          if (sa_d != 0.0) {
+            const double fown = (2.0 * __ldg(&P.ftab[Q.k].w) * sw) *
+                                (P.kid == 2 ? root_phi<2>(P, Q.k, Q.a, b) : root_phi<3>(P, Q.k, Q.a, b));
+            add(Q.dk[b], 0, fown * sa_d, fown != 0.0);
+          }
         }
       }
     }
