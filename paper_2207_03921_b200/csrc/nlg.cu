@@ -2833,7 +2833,7 @@ struct RowSmem {
   unsigned ownacc[kMaxInc][3][NC * NC][3];    // ... and their own-block sums (96-bit fixed point)
   unsigned ownpres[kMaxInc];
   int gr0[kMaxRowsG], gr1[kMaxRowsG], gpre[kMaxRowsG + 1];  // column ranges of the enumeration
-  int er0[kMaxRowsG], epre[kMaxRowsG + 1];                  // element ranges of the same cell rows
+  int er0[2 * kMaxRowsG], epre[2 * kMaxRowsG + 1];          // element ranges of the same cell rows (two per row)
   int ngr;
   unsigned long long bnd;  // the row's bound (incident elements' emitted values)
   double gvx, gvy, grmax, gsum_all;  // the dof's vertex, largest incident radius, sum of all row factors
@@ -3131,34 +3131,73 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
             S.gsum_all = gs;
             S.gpres_all = gp;
           }
-          // column-grid cell rows within the reach of any contribution:
-          // |x_c - v| <= delta (1 + 1e-9) + r_max(group) + 2 r_max
+          S.nrim = 0;
+        }
+        __syncthreads();
+        {
+          // cell rows within the reach of any contribution,
+          // |x_c - v| <= delta (1 + 1e-9) + r_max(group) + 2 r_max: thread y
+          // takes row y -- its column range and (phase B) its element ranges.
+          // Cells wholly inside the radius where every corner of every
+          // element is a deep column (and clear of the near zone around v)
+          // hold nothing for phase B: they split the row's elements in two.
           const double cx = S.gvx, cy = S.gvy, R = P.delta * (1.0 + 1e-9) + S.grmax + 2.0 * W.G.rmax;
           int iy = (int)floor((cy - W.G.oy) / W.G.cs);
           iy = min(max(iy, 0), W.G.ny - 1);
           const int span = (int)ceil(R / W.G.cs);
-          int n = 0, tot = 0, etot = 0;
-          for (int yy = max(iy - span, 0); yy <= min(iy + span, W.G.ny - 1) && n < kMaxRowsG; ++yy) {
+          const int y0 = max(iy - span, 0), nrow = min(min(iy + span, W.G.ny - 1) - y0 + 1, kMaxRowsG);
+          if (t < nrow) {
+            const int yy = y0 + t;
+            int c0 = 0, c1 = 0, ea0 = 0, ea1 = 0, eb0 = 0, eb1 = 0;
             const double ylo = W.G.oy + yy * W.G.cs, yhi = ylo + W.G.cs;
             const double dy = cy < ylo ? ylo - cy : (cy > yhi ? cy - yhi : 0.0);
-            if (dy > R) continue;
-            const double hw = sqrt(R * R - dy * dy);
-            const int x0 = max((int)floor((cx - hw - W.G.ox) / W.G.cs), 0);
-            const int x1 = min((int)floor((cx + hw - W.G.ox) / W.G.cs), W.G.nx - 1);
-            if (x0 > x1) continue;
-            S.gr0[n] = W.G.cstart[yy * W.G.nx + x0];
-            S.gr1[n] = W.G.cstart[yy * W.G.nx + x1 + 1];
-            S.gpre[n] = tot;
-            tot += S.gr1[n] - S.gr0[n];
-            S.er0[n] = W.G.start[yy * W.G.nx + x0];
-            S.epre[n] = etot;
-            etot += W.G.start[yy * W.G.nx + x1 + 1] - S.er0[n];
-            ++n;
+            if (dy <= R) {
+              const double hw = sqrt(R * R - dy * dy);
+              const int x0 = max((int)floor((cx - hw - W.G.ox) / W.G.cs), 0);
+              const int x1 = min((int)floor((cx + hw - W.G.ox) / W.G.cs), W.G.nx - 1);
+              if (x0 <= x1) {
+                c0 = W.G.cstart[yy * W.G.nx + x0];
+                c1 = W.G.cstart[yy * W.G.nx + x1 + 1];
+                ea0 = W.G.start[yy * W.G.nx + x0];
+                ea1 = eb0 = eb1 = W.G.start[yy * W.G.nx + x1 + 1];
+                const double mrg = W.G.rmax * (1.0 + 1e-9) + 1e-9 * P.delta;
+                const double rin = P.delta - 2.0 * S.grmax - 2.0 * W.G.rmax - 1e-12 * (P.delta + 4.0 * W.G.rmax) - mrg;
+                const double rn = 2.0 * W.G.rmax * (1.0 + 1e-9) + mrg;
+                const double dym = fmax(fabs(ylo - cy), fabs(yhi - cy));
+                if (rin > 0.0 && dym < rin && dy > rn) {
+                  const double hwd = sqrt(rin * rin - dym * dym);
+                  const int xa = max((int)ceil((cx - hwd - W.G.ox) / W.G.cs), x0);
+                  const int xb = min((int)floor((cx + hwd - W.G.ox) / W.G.cs) - 1, x1);
+                  if (xa <= xb) {
+                    ea1 = W.G.start[yy * W.G.nx + xa];
+                    eb0 = W.G.start[yy * W.G.nx + xb + 1];
+                  }
+                }
+              }
+            }
+            S.gr0[t] = c0;
+            S.gr1[t] = c1;
+            S.er0[2 * t] = ea0;
+            S.er0[2 * t + 1] = eb0;
+            S.epre[2 * t] = ea1 - ea0;      // (counts; prefixed below)
+            S.epre[2 * t + 1] = eb1 - eb0;
           }
-          S.gpre[n] = tot;
-          S.epre[n] = etot;
-          S.ngr = n;
-          S.nrim = 0;
+          __syncthreads();
+          if (t == 0) {
+            int tot = 0, etot = 0;
+            for (int r = 0; r < nrow; ++r) {
+              S.gpre[r] = tot;
+              tot += S.gr1[r] - S.gr0[r];
+            }
+            S.gpre[nrow] = tot;
+            for (int r = 0; r < 2 * nrow; ++r) {
+              const int c = S.epre[r];
+              S.epre[r] = etot;
+              etot += c;
+            }
+            S.epre[2 * nrow] = etot;
+            S.ngr = nrow;
+          }
         }
         __syncthreads();
         const int ngr = S.ngr, tot = S.gpre[ngr];
@@ -3240,7 +3279,7 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
         // their pair tests run densely.  An element whose corners (within r_n
         // of its barycentre) all lie strictly between the two radii has only
         // deep columns; one beyond eout has no category-0 visit.
-        const int etot = S.epre[ngr];
+        const int etot = S.epre[2 * ngr];
         for (int q = t; q < etot; q += TH) {
           if (*(volatile int*)&S.ovf) break;
           int r = 0;
