@@ -70,6 +70,12 @@ typedef struct nlg_problem {
   int32_t n_sing[3];                    /* identical, edge, vertex rule sizes */
   const double *sxs[3], *sys[3], *sw[3], *shx[3], *shy[3]; /* host tables */
   int32_t inputs_on_device;             /* mesh arrays are device pointers */
+  /* Label-dependent kernels (KernelSpec.value's label_x, label_y arguments,
+   * kernels.py:21-35; _pyengine._pq :38-45 forwards the element labels):
+   * value = label_scale[label_x][label_y] x the built-in kernel's value,
+   * row-major over labels 0..2.  Must be symmetric. */
+  int32_t has_label_scale;
+  double label_scale[9];
 } nlg_problem;
 
 typedef struct nlg_plan nlg_plan;

@@ -62,6 +62,7 @@ class _Prob(ctypes.Structure):
         ("n_sing", ctypes.c_int64 * 3),
         ("sxs", ctypes.c_void_p * 3), ("sys", ctypes.c_void_p * 3), ("sw", ctypes.c_void_p * 3),
         ("shx", ctypes.c_void_p * 3), ("shy", ctypes.c_void_p * 3),
+        ("has_lab", ctypes.c_int64), ("lab", ctypes.c_double * 9),
     ]
 
 
@@ -140,6 +141,9 @@ class OracleProblem:
         pb.ball_id, pb.path_touch = inp.ball_id, inp.path_touch
         pb.rskip2, pb.drop2, pb.kp0, pb.kp1 = inp.rskip2, inp.drop2, inp.kp0, inp.kp1
         pb.symmetric = inp.symmetric
+        pb.has_lab = 1 if len(getattr(inp, "label_scale", ())) else 0
+        for i, v in enumerate(getattr(inp, "label_scale", ())):
+            pb.lab[i] = v
         pb.dof_map = _p(inp.dof_map)
         pb.n_op, pb.n_ip = inp.op.shape[0], inp.ip.shape[0]
         pb.op, pb.ow, pb.oh, pb.ip, pb.iw = (_p(t) for t in tabs)

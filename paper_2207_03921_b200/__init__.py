@@ -6,7 +6,7 @@ from .assembly import (AnsatzSpace, DevicePlan, LocalStiffness, SparseSystem, as
 from .errors import ConfigurationError, DeviceError, MeshFormatError, NumericalError
 from .geometry import BALL_IDS, BALL_KINDS, PairClass, classify_pair
 from .kernels import (KernelSpec, affine_kernel, constant_kernel, constant_kernel_infinity,
-                      fractional_kernel, peridynamic_kernel)
+                      fractional_kernel, label_scaled_kernel, peridynamic_kernel)
 from .mesh import (AdjacencyGraph, Label, Mesh, build_adjacency_graph, generate_structured_mesh,
                    grid_mesh, lshape_mesh, perturb)
 from .nlio import read_mesh, read_nlcsr, write_mesh, write_nlcsr, write_nlcsr_blocks
@@ -18,7 +18,7 @@ __all__ = [
     "ConfigurationError", "DeviceError", "MeshFormatError", "NumericalError",
     "BALL_IDS", "BALL_KINDS", "PairClass", "classify_pair",
     "KernelSpec", "affine_kernel", "constant_kernel", "constant_kernel_infinity",
-    "fractional_kernel", "peridynamic_kernel",
+    "fractional_kernel", "label_scaled_kernel", "peridynamic_kernel",
     "AdjacencyGraph", "Label", "Mesh", "build_adjacency_graph", "generate_structured_mesh",
     "grid_mesh", "lshape_mesh", "perturb",
     "read_mesh", "read_nlcsr", "write_mesh", "write_nlcsr", "write_nlcsr_blocks",

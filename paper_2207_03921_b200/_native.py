@@ -40,6 +40,7 @@ class Problem(ctypes.Structure):
         ("sxs", ctypes.c_void_p * 3), ("sys", ctypes.c_void_p * 3), ("sw", ctypes.c_void_p * 3),
         ("shx", ctypes.c_void_p * 3), ("shy", ctypes.c_void_p * 3),
         ("inputs_on_device", ctypes.c_int32),
+        ("has_label_scale", ctypes.c_int32), ("label_scale", ctypes.c_double * 9),
     ]
 
 

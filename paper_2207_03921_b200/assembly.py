@@ -149,6 +149,9 @@ class DevicePlan:
             pb.n_sing[f] = rule.w.shape[0]
             pb.sxs[f], pb.sys[f], pb.sw[f], pb.shx[f], pb.shy[f] = (_ptr(a).value for a in t)
         pb.inputs_on_device = 1 if on_device else 0
+        pb.has_label_scale = 1 if len(inp.label_scale) else 0
+        for i, v in enumerate(inp.label_scale):
+            pb.label_scale[i] = v
         self._pb = pb
         handle = ctypes.c_void_p()
         s = ctypes.c_void_p(stream) if stream else None

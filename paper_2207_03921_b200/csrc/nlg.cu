@@ -1187,7 +1187,7 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
         load_tri(P, l, lx, ly);
         long long ne = 0;
         full_pair_sym1(P, kx, ky, lx, ly, K, K2, G, ne, &s_tab);
-        const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+        const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly) * lab_scale(P, ek.w, el.w);
         const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
         ev0 += ne * mult;
         out0 += 14 * mult;
@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
         load_tri(P, l, lx, ly);
         long long ne = 0;
         full_pair_peri(P, kx, ky, lx, ly, rs2, K, K2, G, ne);
-        const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly);
+        const double c2 = 2.0 * twice_area(kx, ky) * twice_area(lx, ly) * lab_scale(P, ek.w, el.w);
         const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
         ev0 += ne * mult;
         out0 += 14 * mult;
@@ -1230,6 +1230,13 @@ __global__ void __launch_bounds__(128) k_full(Params P, const int2* __restrict__
       const int mult = (emitA ? 1 : 0) + (emitB ? 1 : 0);
       ev0 += ne * mult;
       out0 += 14 * mult;
+    }
+    if (P.has_lab) {
+      const double ls = lab_scale(P, ek.w, el.w);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        kkA[e] *= ls; klA[e] *= ls; kkB[e] *= ls; klB[e] *= ls;
+      }
     }
     emit_side<NC>(P, O, O.a_base + v, emitA, k, l, kkA, klA, vm);
     emit_side<NC>(P, O, O.b_base + __ldg(&O.revpos[v]), emitB && k != l, l, k, kkB, klB, vm);
@@ -1856,7 +1863,8 @@ __global__ void __launch_bounds__(32 * clip_warps<KID>(), KID == 0 ? 6 : (KID ==
     const int pmy = S.pm[lane];
     const bool ivalid = !(pmy & 0x80);
     const int mi = (pmy >> 4) & 3, pi = pmy & 15;
-    const double Wi = ivalid ? S.W[lane] : 0.0;
+    const double Wi = ivalid ? S.W[lane] * (P.has_lab ? lab_scale(P, __ldg(&P.elem[S.vk[vs]]).w, __ldg(&P.elem[S.vl[vs]]).w) : 1.0)
+                             : 0.0;  // (label factor of the pair: every entry is linear in W)
     if (next_ok && r == 0) {
       S.ek[vs] = __ldg(&P.elem[prn.x]);
       S.el[vs] = __ldg(&P.elem[prn.y & kIdMask]);
@@ -2059,7 +2067,8 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
         }
         S.xo[sl][0] = x0;
         S.xo[sl][1] = x1;
-        S.W[sl] = c_rule.ow[p] * twice_area(ox, oy);
+        // (the pair's label factor rides on the weight: every entry is linear in W)
+        S.W[sl] = c_rule.ow[p] * twice_area(ox, oy) * lab_scale(P, ek.w, el.w);
         if (p == 0) {  // the record's inner triangle of this sweep, for the hat functions
           double* tr = S.tri[rec][m == 1];
           tr[0] = ix[0]; tr[1] = iy[0];
@@ -2309,6 +2318,7 @@ __global__ void k_pair_local(Params P, const int2* __restrict__ pairs, int n, do
     // sum the items in order and lay out the dense block: rows / columns are
     // (k's 3 nc dofs, l's 3 nc dofs); F0 -> the k rows, F1 -> the l rows
     double* B = out + (long long)pi * NB * NB;
+    const double ls = lab_scale(P, __ldg(&P.elem[k]).w, __ldg(&P.elem[l]).w);
     for (int e = lane; e < NB * NB; e += 32) {
       const int R = e / NB, Cc = e % NB;
       const bool rk = R < N3, ck = Cc < N3;
@@ -2324,6 +2334,7 @@ __global__ void k_pair_local(Params P, const int2* __restrict__ pairs, int n, do
       const int off = rk ? 0 : C::NSIDE;
 #pragma unroll 1
       for (int p = 0; p < 7; ++p) v += sF[p][off + g];
+      v *= ls;
       B[e] = v;
       report_nonfinite(nonfinite(v), k, l, P.K, errpair);
     }
@@ -3516,7 +3527,7 @@ __global__ void __launch_bounds__(kSingThreads) k_singular(Params P, const int2*
       const double cl = cross2(sTB[1][0] - sTB[0][0], sTB[2][1] - sTB[0][1], sTB[1][1] - sTB[0][1], sTB[2][0] - sTB[0][0]);
       double sc = fabs(ck) * fabs(cl);
       if (k != l) sc *= 2.0;
-      sScale = sc;
+      sScale = sc * lab_scale(P, __ldg(&P.elem[k]).w, __ldg(&P.elem[l]).w);
     }
     __syncthreads();
     double acc[A::N];
@@ -5340,6 +5351,13 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
     set_err("mesh size out of range"); return NLG_ERR_CONFIG;
   }
   if (pb->n_dofs <= 0 || pb->n_dofs >= (1LL << 31)) { set_err("dof count out of range"); return NLG_ERR_CONFIG; }
+  if (pb->has_label_scale)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < a; ++b)
+        if (!(pb->label_scale[a * 3 + b] == pb->label_scale[b * 3 + a])) {
+          set_err("label_scale must be symmetric (one factor per element pair)");
+          return NLG_ERR_CONFIG;
+        }
   CK(cudaSetDevice(device));
   nlg_plan* pl = new nlg_plan();
   pl->device = device;
@@ -5374,6 +5392,8 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   P.drop2 = pb->drop2;
   P.kp0 = pb->kp0;
   P.kp1 = pb->kp1;
+  P.has_lab = pb->has_label_scale != 0;
+  for (int i = 0; i < 9; ++i) P.lab[i] = P.has_lab ? pb->label_scale[i] : 1.0;
   P.J = pb->n_dofs;
   P.dbg = getenv("NLG_DEBUG") ? atoi(getenv("NLG_DEBUG")) : 0;
   // NLG_NO_ANALYTIC: integrate the full pairs of kid 2 / 3 per record (A/B and tests)
@@ -5383,7 +5403,8 @@ nlg_status nlg_plan_create(int32_t device, const nlg_problem* pb, void* stream, 
   // (the analytic visits are enumerated by the stage-W row merge: stage R
   // integrates every pair per record)
   P.analytic = (P.kid == 2 || P.kid == 3) && P.path == 0 && P.nc == 1 && !getenv("NLG_NO_ANALYTIC") &&
-               std::isfinite(P.cst) && std::isfinite(P.kp0) && std::isfinite(P.kp1) && pl->use_rows;
+               std::isfinite(P.cst) && std::isfinite(P.kp0) && std::isfinite(P.kp1) && pl->use_rows &&
+               !P.has_lab;  // (the analytic column factors carry one kernel constant)
   Rule7 hr;
   for (int p = 0; p < 7; ++p) {
     hr.op[p][0] = pb->op[2 * p]; hr.op[p][1] = pb->op[2 * p + 1];

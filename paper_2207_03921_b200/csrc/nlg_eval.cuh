@@ -50,7 +50,18 @@ struct Params {
   int analytic;
   const double4* __restrict__ ftab;  // [K] (A2 psi_0, A2 psi_1, A2 psi_2, A2)
   int dbg;  // NLG_DEBUG bit mask (experiments only; 0 in production)
+  // label-dependent kernels (KernelSpec.value's label_x, label_y arguments,
+  // kernels.py:21-35): value = lab[label_x][label_y] x the built-in's value,
+  // with a symmetric table -- so both visits of a pair, and its P and Q
+  // terms, carry the same factor and a record is scaled once when emitted
+  int has_lab;
+  double lab[9];
 };
+
+// label factor of the pair of elements with records' w fields wk, wl
+__device__ __forceinline__ double lab_scale(const Params& P, int wk, int wl) {
+  return P.has_lab ? P.lab[(wk & 15) * 3 + (wl & 15)] : 1.0;
+}
 
 // the 7-point rule and its weighted hat products (identical for every plan:
 // QuadratureConfig only accepts "7point", quadrature.py:20)

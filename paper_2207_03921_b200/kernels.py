@@ -16,6 +16,11 @@ id    value(x, y)                              reference
                                                 BASELINE config 5's kernel
 ====  =======================================  ==========================
 
+Label-dependent kernels (``value``'s ``label_x, label_y`` arguments,
+reference kernels.py:21-35) run on the device as a built-in times a symmetric
+3 x 3 table over the element labels (:func:`label_scaled_kernel`): interface
+problems with one coefficient per pair of subdomains.
+
 Id 3 is new: the reference reaches nonsymmetric kernels only through a
 Python callable on its interpreted engine, which cannot run on a GPU.
 Kernels with ``builtin_id < 0`` (arbitrary callables) are rejected by the
@@ -49,6 +54,7 @@ class KernelSpec:
     builtin_id: int = -1
     scale: float = math.nan
     params: tuple = ()
+    label_scale: tuple = ()  # 3 x 3 factors over the element labels (label_scaled_kernel)
 
     def __post_init__(self):
         if self.delta <= 0.0:
@@ -137,3 +143,37 @@ def affine_kernel(delta, alpha=0.5, scale=None, ball="approxcaps"):
 
     return KernelSpec(delta=delta, s=-1.0, n=1, symmetric=False, ball=ball, value=value,
                       builtin_id=3, scale=c, params=(a, c))
+
+
+def label_scaled_kernel(base, table):
+    """``table[label_x][label_y] * base.value(x, y)``: a built-in kernel whose
+    strength depends on the labels of the two host elements (interface
+    problems; the reference reaches these only through a Python callable on
+    its interpreted engine, kernels.py:21-35, _pyengine.py:38-45).
+
+    ``table`` is indexed by :class:`~.mesh.Label` (a 3 x 3 array over labels
+    0..2, or a 2 x 2 array over DOMAIN, DIRICHLET) and must be symmetric: the
+    device integrates each unordered element pair once and scales it when it
+    is emitted.  The returned spec's ``value`` is the same formula on the
+    host, so the reference's engines evaluate it identically.
+    """
+    t = np.asarray(table, dtype=np.float64)
+    if t.shape == (2, 2):
+        full = np.zeros((3, 3))
+        full[1:, 1:] = t
+        t = full
+    if t.shape != (3, 3):
+        raise ConfigurationError("label table must be 2 x 2 (DOMAIN, DIRICHLET) or 3 x 3 (labels 0..2)")
+    if not np.array_equal(t, t.T):
+        raise ConfigurationError("label table must be symmetric")
+    if base.builtin_id < 0:
+        raise ConfigurationError("label_scaled_kernel needs a built-in base kernel")
+    tab = tuple(tuple(float(v) for v in row) for row in t)
+    bval = base.value
+
+    def value(x, y, label_x=Label.DOMAIN, label_y=Label.DOMAIN):
+        return tab[int(label_x)][int(label_y)] * bval(x, y)
+
+    return KernelSpec(delta=base.delta, s=base.s, n=base.n, symmetric=base.symmetric, ball=base.ball,
+                      value=value, builtin_id=base.builtin_id, scale=base.scale,
+                      params=tuple(getattr(base, "params", ()) or ()), label_scale=tab)

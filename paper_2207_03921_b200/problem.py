@@ -50,6 +50,7 @@ class AssemblyInputs:
     ip: np.ndarray
     iw: np.ndarray
     rules: tuple  # (identical, edge, vertex) TensorizedSingularRule
+    label_scale: tuple = ()  # 9 factors over labels 0..2 (row-major), or () for none
 
 
 def touch_path(kernel, ansatz, quad):
@@ -78,6 +79,21 @@ def is_kernel_spec(kernel):
     ``nlfem.kernels.KernelSpec`` (kernels.py:21-54) both qualify, so a caller
     that swaps only the assembly import keeps its kernel objects."""
     return all(hasattr(kernel, f) for f in KERNEL_FIELDS)
+
+
+def kernel_label_scale(kernel):
+    """The 3 x 3 label table of a label-dependent kernel
+    (:func:`~.kernels.label_scaled_kernel`) as 9 floats, or ()."""
+    tab = getattr(kernel, "label_scale", ()) or ()
+    if not len(tab):
+        return ()
+    t = np.asarray(tab, dtype=np.float64)
+    if t.shape != (3, 3):
+        raise ConfigurationError("label_scale must be a 3 x 3 table over the labels 0..2")
+    if not np.array_equal(t, t.T):
+        raise ConfigurationError(
+            "label_scale must be symmetric: the device scales each element pair once")
+    return tuple(float(v) for v in t.ravel())
 
 
 def kernel_params(kernel):
@@ -138,4 +154,5 @@ def marshal(mesh, adjacency, kernel, ansatz, quad=None, n_threads=1, rows="all",
         op=np.ascontiguousarray(op), ow=np.ascontiguousarray(ow), oh=np.ascontiguousarray(oh),
         ip=np.ascontiguousarray(ip), iw=np.ascontiguousarray(iw),
         rules=tuple(singular_rule(kind, quad.gauss_points_1d) for kind in SINGULAR_KINDS),
+        label_scale=kernel_label_scale(kernel),
     )

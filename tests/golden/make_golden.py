@@ -53,6 +53,17 @@ def affine_kernel(delta, alpha, c, ball):
                          value=lambda x, y, lx=1, ly=1: np.array([[(1.0 + alpha * x[0]) * c]]))
 
 
+def labeled(base, tab2):
+    """Label-dependent kernel as the reference takes it: a Python callable
+    (builtin_id -1, interpreted engine) value = T[label_x][label_y] * base."""
+    T = np.zeros((3, 3))
+    T[1:, 1:] = np.asarray(tab2, dtype=float)
+    T = [[float(v) for v in row] for row in T]
+    bval = base.value
+    return KR.KernelSpec(delta=base.delta, s=base.s, n=base.n, symmetric=True, ball=base.ball,
+                         value=lambda x, y, lx=1, ly=1: T[int(lx)][int(ly)] * bval(x, y))
+
+
 def cases():
     d = 0.1
     c1 = 4.0 / (math.pi * d ** 4)
@@ -86,6 +97,16 @@ def cases():
                               "cg", 1, {}, "all", "one")
     out["lshape16_const"] = (lm, const_kernel(0.1, "approxcaps", c1),
                              {"id": 2, "ball": "approxcaps", "delta": 0.1, "scale": c1}, "cg", 1, {}, "all", "one")
+    # label-dependent kernels (interface coefficients per pair of subdomains)
+    t1, t2, t3 = [[1.0, 0.5], [0.5, 2.0]], [[1.0, 0.25], [0.25, 3.0]], [[1.0, 2.0], [2.0, 0.5]]
+    out["frac_s04_labels"] = (small, labeled(KR.fractional_kernel(0.4, 0.2, "approxcaps"), t1),
+                              {"id": 0, "s": 0.4, "ball": "approxcaps", "delta": 0.2, "labels": t1},
+                              "cg", 1, {}, "all", "x")
+    out["lshape16_const_labels"] = (lm, labeled(const_kernel(0.1, "approxcaps", c1), t2),
+                                    {"id": 2, "ball": "approxcaps", "delta": 0.1, "scale": c1, "labels": t2},
+                                    "cg", 1, {}, "all", "one")
+    out["peri_nocaps_labels"] = (small, labeled(KR.peridynamic_kernel(0.2, "nocaps"), t3),
+                                 {"id": 1, "ball": "nocaps", "delta": 0.2, "labels": t3}, "cg", 2, {}, "all", "body")
     return out
 
 

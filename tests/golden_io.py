@@ -31,12 +31,14 @@ def names():
 def kernel_from_spec(k):
     kid, ball, delta = k["id"], k["ball"], k["delta"]
     if kid == 0:
-        return KR.fractional_kernel(k["s"], delta, ball)
-    if kid == 1:
-        return KR.peridynamic_kernel(delta, ball)
-    if kid == 2:
-        return KR.constant_kernel(delta, ball, scale=k["scale"])
-    return KR.affine_kernel(delta, k["alpha"], k["scale"], ball)
+        base = KR.fractional_kernel(k["s"], delta, ball)
+    elif kid == 1:
+        base = KR.peridynamic_kernel(delta, ball)
+    elif kid == 2:
+        base = KR.constant_kernel(delta, ball, scale=k["scale"])
+    else:
+        base = KR.affine_kernel(delta, k["alpha"], k["scale"], ball)
+    return KR.label_scaled_kernel(base, k["labels"]) if "labels" in k else base
 
 
 class Case:

@@ -124,3 +124,25 @@ def test_c_abi_exports_every_declared_symbol():
         assert hasattr(lib, n), f"{n} declared in include/nlg.h but not exported"
     assert set(_native.SIGNATURES) <= names
     assert lib.nlg_abi_version() == 5
+
+
+def test_label_scaled_kernel_boundary():
+    """Label-dependent kernels: a symmetric table over the element labels on a
+    built-in base; the host value is table[lx][ly] * base (what a reference
+    callable computes, kernels.py:21-35); a nonsymmetric table is refused."""
+    from paper_2207_03921_b200 import Label, label_scaled_kernel
+    m = generate_structured_mesh(1.0, 0.25, 4)
+    adj = build_adjacency_graph(m)
+    ans = build_ansatz(m, "cg", 1)
+    base = fractional_kernel(0.4, 0.25)
+    k = label_scaled_kernel(base, [[1.0, 0.5], [0.5, 2.0]])
+    x, y = np.array([0.1, 0.2]), np.array([0.3, 0.25])
+    assert k.value(x, y, Label.DOMAIN, Label.DIRICHLET)[0, 0] == 0.5 * base.value(x, y)[0, 0]
+    assert k.value(x, y, Label.DIRICHLET, Label.DIRICHLET)[0, 0] == 2.0 * base.value(x, y)[0, 0]
+    inp = marshal(m, adj, k, ans)
+    assert inp.kernel_id == 0 and inp.label_scale == (0.0, 0.0, 0.0, 0.0, 1.0, 0.5, 0.0, 0.5, 2.0)
+    assert marshal(m, adj, base, ans).label_scale == ()
+    with pytest.raises(ConfigurationError, match="symmetric"):
+        label_scaled_kernel(base, [[1.0, 0.5], [0.25, 2.0]])
+    with pytest.raises(ConfigurationError, match="2 x 2"):
+        label_scaled_kernel(base, [1.0, 2.0])
