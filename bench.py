@@ -212,24 +212,36 @@ def merge_alg_bytes(cfg, inp, st):
 
 
 def _ncu_traffic(kernel, config):
-    """DRAM bytes (read + write) per launch of ``kernel`` from the newest
-    committed `ncu --set full` summary of this config (profiles/
-    r*_<kernel>_cfg<C>_ncu_summary.txt); (None, None) when none exists."""
+    """(DRAM bytes read + written, source file, extras) of ONE launch of
+    ``kernel`` from the newest committed `ncu --set full` summary of this
+    config under profiles/ (r*_cfg<C>_<kernel>_ncu_summary.txt); a step runs
+    one launch per row batch.  (None, None, {}) when no capture exists."""
     import glob
     import re
     here = os.path.dirname(os.path.abspath(__file__))
-    files = sorted(glob.glob(os.path.join(here, "profiles", f"r*_{kernel}_cfg{config}_ncu_summary.txt")))
+    files = sorted(glob.glob(os.path.join(here, "profiles", f"r*_cfg{config}_{kernel}_ncu_summary.txt")) +
+                   glob.glob(os.path.join(here, "profiles", f"r*_{kernel}_cfg{config}_ncu_summary.txt")),
+                   key=lambda f: os.path.basename(f).split("_")[0])
     if not files:
-        return None, None
+        return None, None, {}
     txt = open(files[-1]).read()
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     total = 0.0
     for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         m = re.search(rf"^{re.escape(key)}\s+([0-9.]+) (\w+)", txt, re.M)
         if not m:
-            return None, None
+            return None, None, {}
         total += float(m.group(1)) * scale.get(m.group(2), 1)
-    return total, os.path.relpath(files[-1], here)
+    extra = {}
+    for key, name in (("gpu__time_duration.sum", "launch_ms"),
+                      ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_active_pct"),
+                      ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue_active_pct"),
+                      ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_pct"),
+                      ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads_per_instruction")):
+        m = re.search(rf"^{re.escape(key)}\s+([0-9.]+)", txt, re.M)
+        if m:
+            extra[name] = float(m.group(1))
+    return total, os.path.relpath(files[-1], here), extra
 
 
 def cpu_model():
@@ -417,10 +429,15 @@ def main():
     dom = max(phases, key=lambda k: phases[k]["ms"])
     top = phases[dom] if phases[dom].get("frac") is not None else phases["k_clipped"]
     dom_name = dom if phases[dom].get("frac") is not None else "k_clipped"
-    traffic, traffic_src = _ncu_traffic(dom_name, args.config)
+    # (the clipped pairs of the constant / affine kernels run in k_clipped_cf)
+    closed_form = inp.kernel_id in (2, 3) and inp.path_touch == 0 and inp.ball_id != 2
+    kern_name = "k_clipped_cf" if dom_name == "k_clipped" and closed_form else dom_name
+    traffic, traffic_src, ncu_extra = _ncu_traffic(kern_name, args.config)
     roofline = {
-        "bound": top["bound"], "kernel": dom_name, "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
+        "bound": top["bound"], "kernel": kern_name, "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
         "frac": top["frac"], "traffic": traffic, "traffic_source": traffic_src,
+        "traffic_note": "DRAM bytes of ONE launch (ncu --set full); a step runs one launch per row batch",
+        "ncu": ncu_extra,
         "peak_source": ("measured DFMA microbenchmark (nlg_fp64_peak) on this GPU, this run" if top["bound"] == "fp64"
                         else "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"),
         "kernel_ms": top["ms"], "share_of_step": top["ms"] / ms_per_step if ms_per_step else None,
