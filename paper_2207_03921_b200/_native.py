@@ -264,18 +264,22 @@ PINNED = PinnedPool()
 
 class PinnedSink:
     """Block callback of nlg_assemble_pinned: hands out pooled page-locked
-    blocks and turns the one the library used into the CSR arrays."""
+    blocks and turns the one the library used into the CSR arrays.  When no
+    page-locked memory can be had (host limits), the block is ordinary numpy
+    memory: the library's copies still land there, only slower."""
 
     def __init__(self):
-        self.blocks = []  # (address, capacity) handed out during this call
+        self.blocks = []  # (address, capacity, owner) handed out during this call; owner: numpy fallback
         self._cb = ALLOC_FN(self._alloc)
 
     def _alloc(self, user, nbytes, which):
         try:
             addr, cap = PINNED.take(nbytes)
+            owner = None
             if addr is None:
-                return None
-            self.blocks.append((addr, cap))
+                owner = np.empty(max(int(nbytes), 8), dtype=np.uint8)
+                addr, cap = int(owner.ctypes.data), owner.size
+            self.blocks.append((addr, cap, owner))
             return addr
         except Exception:  # noqa: BLE001 -- NULL makes the library fail cleanly
             return None
@@ -285,12 +289,13 @@ class PinnedSink:
         return self._cb
 
     def release(self, keep_addr=None):
-        """Blocks not holding the result go back to the pool; the result's (address, capacity)."""
+        """Blocks not holding the result go back to the pool; the result's
+        (address, capacity, owner) is returned."""
         kept = None
-        for addr, cap in self.blocks:
+        for addr, cap, owner in self.blocks:
             if keep_addr is not None and addr == keep_addr and kept is None:
-                kept = (addr, cap)
-            else:
+                kept = (addr, cap, owner)
+            elif owner is None:
                 PINNED.give(addr, cap)
         self.blocks = []
         return kept
@@ -299,7 +304,7 @@ class PinnedSink:
         kept = self.release(out.arena)
         if kept is None:
             raise DeviceError("nlg_assemble_pinned returned a block this sink did not hand out")
-        buf = PINNED.view(*kept)
+        buf = kept[2] if kept[2] is not None else PINNED.view(kept[0], kept[1])
         nnz = int(out.nnz)
         indptr = buf[out.off_indptr:out.off_indptr + 8 * (n_rows + 1)].view(np.int64)
         indices = buf[out.off_indices:out.off_indices + 4 * nnz].view(np.int32)

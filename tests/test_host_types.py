@@ -146,3 +146,21 @@ def test_label_scaled_kernel_boundary():
         label_scaled_kernel(base, [[1.0, 0.5], [0.25, 2.0]])
     with pytest.raises(ConfigurationError, match="2 x 2"):
         label_scaled_kernel(base, [1.0, 2.0])
+
+
+def test_pinned_sink_falls_back_to_pageable_memory(monkeypatch):
+    """Without page-locked memory the host CSR block is ordinary numpy memory
+    (the library's copies still land there); the arrays are views of it."""
+    from paper_2207_03921_b200 import _native
+    monkeypatch.setattr(_native.PINNED, "take", lambda nbytes: (None, 0))
+    sink = _native.PinnedSink()
+    first = sink._alloc(None, 4096, 5)
+    addr = sink._alloc(None, 1000, 5)   # the library asked twice: the first block is dropped
+    assert first and addr and first != addr
+    out = _native.HostCsr()
+    out.arena, out.nnz, out.off_data, out.off_indices, out.off_indptr = addr, 10, 0, 80, 128
+    ip, ix, dv = sink.arrays(out, 4)
+    assert (ip.dtype, ix.dtype, dv.dtype) == (np.int64, np.int32, np.float64)
+    assert (ip.shape, ix.shape, dv.shape) == ((5,), (10,), (10,))
+    assert dv.ctypes.data == addr and ix.ctypes.data == addr + 80 and ip.ctypes.data == addr + 128
+    assert sink.blocks == []
