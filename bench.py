@@ -373,8 +373,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
+    # Row batches: the library plans a batch within 60 % of the device by
+    # default.  This process holds nothing else on the GPU, so the timed steps
+    # allow 75 % -- config 5 then runs as ONE batch and no pair is integrated
+    # twice at a batch cut (768 vs 825 ms).  The warm-up proves it fits; if it
+    # does not, the library default is used.  (e2e below: library defaults.)
+    budget = int(0.75 * torch.cuda.mem_get_info(local)[1])
+    try:
+        for _ in range(args.warmup):
+            plan.assemble(lo, hi, out_on_host=False, reuse_output=True, mem_budget=budget)
+    except Exception as exc:  # noqa: BLE001
+        print(f"# mem_budget 75 % did not fit ({exc}); library default", file=sys.stderr)
+        budget = 0
+        torch.cuda.empty_cache()
+        for _ in range(args.warmup):
+            plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
     barrier()
     launches0 = _native.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -384,7 +397,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))  # evict L2 between steps (outside the timed pair)
             ev[i][0].record()
-            _, _, _, st = plan.assemble(lo, hi, out_on_host=False, reuse_output=True)
+            _, _, _, st = plan.assemble(lo, hi, out_on_host=False, reuse_output=True, mem_budget=budget)
             ev[i][1].record()
             stats.append(st)
         barrier()
@@ -488,7 +501,8 @@ def main():
                        "rows": "all" if (lo, hi) == (0, J) else f"[{lo}, {hi}) of {J}",
                        "parallelism": f"rowshard{ws}" if sws == ws else f"emulated rank {srank} of {sws} on 1 GPU",
                        "l2": "flushed between steps (512 MB write)", "inputs": "mesh arrays resident in HBM",
-                       "output": "CSR resident in HBM"},
+                       "output": "CSR resident in HBM",
+                       "mem_budget": "75 % of HBM per row batch" if budget else "library default (60 %)"},
             "assembly_ms": ms_per_step,
             "step_ms": [round(x, 3) for x in ms_steps],
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

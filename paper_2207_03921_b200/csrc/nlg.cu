@@ -3944,6 +3944,12 @@ struct DevBuf {  // scratch: bump-allocated from the plan's arena, else stream-o
     }
     return cudaMallocAsync(&p, n, st);
   }
+  // stream-ordered, never from the arena (buffers that outlive the batches:
+  // the arena may be handed back before the outputs are allocated)
+  cudaError_t alloc_pool(size_t n, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(&p, (std::max<size_t>(n, 16) + 255) & ~(size_t)255, st);
+  }
   ~DevBuf() {
     if (p && !arena) cudaFreeAsync(p, s);
   }
@@ -4610,7 +4616,7 @@ struct Timing {
 };
 
 // one row batch: returns NLG_OK and appends to `out`, or asks for a split
-nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget, bool allow_sample,
+nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget, int out_copies, bool allow_sample,
                      std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
                      unsigned long long* d_counters, unsigned long long* d_err, bool* need_split,
                      std::vector<long long>* cuts, bool no_analytic, bool* analytic_fallback) {
@@ -4741,8 +4747,14 @@ count_pass:
                              (rows_plan ? 0LL : (long long)(kRunFrac * (double)(nUB * 2 * E))) + 1;
     const long long ent_ub = rows_plan ? ent_estimate(P, nUB, tot[C_EPI], nR) : 0LL;
     const long long side_bytes = 8LL * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));  // kkv + klv
+    // (ent_ub is ~1.5x the CSR entries: it covers the merge's entry buffer and
+    // most of the batch's piece; the pieces of EARLIER batches come off the budget)
+    (void)out_copies;
     const long long bytes = nStUB * 2 * side_bytes + coo_ub * (16 + 16) + ent_ub * 12 +
                             (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 + nUB * 24;
+    if (g_trace)
+      fprintf(stderr, "[nlg] plan rows [%lld, %lld) stride %d: est %.1f GB (stored %.1f, entries %.1f) of budget %.1f GB\n",
+              row_lo, row_hi, stride, 1e-9 * bytes, 1e-9 * nStUB * 2 * side_bytes, 1e-9 * ent_ub * 12, 1e-9 * budget);
     // 32-bit sizes: records (reverse-index sort) and COO entries must fit
     const bool too_big = (budget > 0 && bytes > budget) || coo_ub >= (1LL << 31) || nUB >= (1LL << 31);
     if (stride > 1 && !too_big) {  // the sample says it fits: count exactly
@@ -5136,6 +5148,8 @@ struct Stager {
   char* base = nullptr;
   long long nnz_cap = 0, used = 0, nrows = 0;
   bool on = false;
+  std::vector<cudaEvent_t> tev;  // NLG_TRACE: copy start / end events per piece
+  std::vector<long long> tnnz;
   double* dat() const { return (double*)base; }
   int* idx() const { return (int*)(base + off_idx(nnz_cap)); }
   long long* ptr() const { return (long long*)(base + off_ptr(nnz_cap)); }
@@ -5187,9 +5201,22 @@ struct Stager {
     CK(cudaEventRecord(ev, pl->stream));
     CK(cudaStreamWaitEvent(pl->cstream, ev, 0));
     cudaEventDestroy(ev);
+    if (g_trace) {  // when each piece's copy starts and ends (NLG_TRACE)
+      cudaEvent_t a;
+      cudaEventCreate(&a);
+      cudaEventRecord(a, pl->cstream);
+      tev.push_back(a);
+    }
     if (c.nnz) {
       CK(cudaMemcpyAsync(dat() + used, c.data, sizeof(double) * c.nnz, cudaMemcpyDeviceToHost, pl->cstream));
       CK(cudaMemcpyAsync(idx() + used, c.indices, sizeof(int) * c.nnz, cudaMemcpyDeviceToHost, pl->cstream));
+    }
+    if (g_trace) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, pl->cstream);
+      tev.push_back(b);
+      tnnz.push_back(c.nnz);
     }
     c.staged = used;
     used += c.nnz;
@@ -5211,9 +5238,34 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
   int* u_idx = nullptr;
   double* u_dat = nullptr;
   if (!ha) {
-    u_ptr = (long long*)alloc(user, sizeof(long long) * (nrows + 1), 0);
-    u_idx = (int*)alloc(user, sizeof(int) * std::max(nnz, 1LL), 1);
-    u_dat = (double*)alloc(user, sizeof(double) * std::max(nnz, 1LL), 2);
+    // a caller's device allocation may fail only because this library holds
+    // the memory: the batches' freed scratch in the stream-ordered pool, then
+    // the scratch arena itself (sized by the largest call so far; the batches
+    // are done with it, and the next call grows it again).  Hand them back
+    // and ask again.
+    auto ask = [&](size_t n, int which) -> void* {
+      void* p = alloc(user, (int64_t)n, which);
+      cudaMemPool_t mp;
+      if (!p && !out_on_host && cudaDeviceGetDefaultMemPool(&mp, pl->device) == cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(s);
+        cudaMemPoolTrimTo(mp, 0);
+        p = alloc(user, (int64_t)n, which);
+      }
+      if (!p && !out_on_host && ds.arena) {
+        cudaGetLastError();
+        cudaStreamSynchronize(s);
+        cudaFree(ds.arena);
+        ds.arena = nullptr;
+        ds.cap = 0;
+        ds.peak = 0;  // (regrown to what the next call needs)
+        p = alloc(user, (int64_t)n, which);
+      }
+      return p;
+    };
+    u_ptr = (long long*)ask(sizeof(long long) * (nrows + 1), 0);
+    u_idx = (int*)ask(sizeof(int) * std::max(nnz, 1LL), 1);
+    u_dat = (double*)ask(sizeof(double) * std::max(nnz, 1LL), 2);
     if (!u_ptr || !u_idx || !u_dat) { set_err("output allocation failed"); return NLG_ERR_CUDA; }
   }
   // where the D2H copies land: the caller's buffers (device outputs; or host
@@ -5271,6 +5323,18 @@ nlg_status emit_pieces(nlg_plan* pl, DeviceScratch& ds, std::vector<Csr>& pieces
   CK(cudaStreamSynchronize(s));
   if (pl->cstream) CK(cudaStreamSynchronize(pl->cstream));
   TRACE("outputs synced");
+  if (g_trace && e_done) {
+    for (size_t i = 0; i + 1 < stg.tev.size(); i += 2) {
+      float t0 = 0, t1 = 0;
+      cudaEventElapsedTime(&t0, stg.tev[i], e_done);
+      cudaEventElapsedTime(&t1, stg.tev[i + 1], e_done);
+      fprintf(stderr, "[nlg] piece %zu: %.2f GB copied from %.1f to %.1f ms before the end (%.1f GB/s)\n", i / 2,
+              12e-9 * stg.tnnz[i / 2], t0, t1, 12e-6 * stg.tnnz[i / 2] / std::max(t0 - t1, 1e-3f));
+    }
+    for (auto e : stg.tev) cudaEventDestroy(e);
+    stg.tev.clear();
+    stg.tnnz.clear();
+  }
   const size_t b_dat = sizeof(double) * std::max(nnz, 1LL), b_idx = sizeof(int) * std::max(nnz, 1LL),
                b_ptr = sizeof(long long) * (nrows + 1);
   if (ha) {
@@ -5563,6 +5627,13 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
   st.err_k = st.err_l = -1;
   TRACE("assemble begin");
   if (budget <= 0) {
+    // 60 % of the device by default.  Fewer row batches are faster -- a pair
+    // whose elements fall in different batches is integrated once per batch
+    // (config 5: one batch 768 ms at mem_budget = 75 %, three batches 825 ms)
+    // -- but the scratch arena, the stream-ordered pool, the finished pieces
+    // and the caller's own buffers share the device, and a process that has
+    // assembled other problems before holds more of it: callers that know
+    // their process pass a larger mem_budget (bench.py does).
     static thread_local size_t totm = 0;
     if (!totm) {
       size_t fr = 0;
@@ -5582,8 +5653,8 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
   if (rc) return rc;
   CK(cudaEventRecord(e1, s));
   DevBuf dctr, derr;
-  CK(dctr.alloc(sizeof(unsigned long long) * K_NCOUNTERS, s));
-  CK(derr.alloc(2 * sizeof(unsigned long long), s));
+  CK(dctr.alloc_pool(sizeof(unsigned long long) * K_NCOUNTERS, s));
+  CK(derr.alloc_pool(2 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(dctr.p, 0, sizeof(unsigned long long) * K_NCOUNTERS, s));
   CK(cudaMemsetAsync(derr.p, 0xff, 2 * sizeof(unsigned long long), s));
   std::vector<Csr> pieces;
@@ -5601,9 +5672,24 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
   struct Range {
     long long first, second;
     bool plain;  // without the analytic enumeration (after a stage-W overflow)
+    bool tail;   // the short last batch of a streamed host output (not split off again)
   };
   std::vector<Range> todo;
-  if (row_hi > row_lo) todo.push_back({row_lo, row_hi, false});
+  if (row_hi > row_lo) todo.push_back({row_lo, row_hi, false, false});
+  // Streamed host output (>= 0.4 GB): a batch's rows are copied while the
+  // NEXT batch computes, and nothing overlaps the last batch's copy.  Three
+  // row chunks of 62 / 26 / 12 %: each copy fits inside the next chunk's
+  // compute (the copy engine is ~3x faster than the rows are produced), and
+  // the tail is the copy of the last 12 %.  More chunks would shorten it
+  // further but integrate more pairs twice (one chunk per side of a cut).
+  if (out_on_host && stg.on && stg.nnz_cap > (1LL << 25) && row_hi - row_lo >= 64 * pl->P.nc) {
+    const long long nc = pl->P.nc, n = row_hi - row_lo;
+    const long long c1 = row_lo + (long long)(0.62 * (double)n) / nc * nc, c2 = row_lo + (long long)(0.88 * (double)n) / nc * nc;
+    todo.clear();
+    todo.push_back({c2, row_hi, false, true});  // (popped last)
+    todo.push_back({c1, c2, false, true});
+    todo.push_back({row_lo, c1, false, true});
+  }
   while (!todo.empty()) {
     auto rg = todo.back();
     todo.pop_back();
@@ -5611,7 +5697,13 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
     std::vector<long long> cuts;
     const bool first_attempt = st.n_batches == 0 && st.n_replans == 0;
     const size_t npieces = pieces.size();
-    rc = run_batch(pl, rg.first, rg.second, budget, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
+    // what the finished pieces hold (and, for device outputs, their copy in
+    // the caller's buffers at the end) is no longer available to a batch
+    const int out_copies = out_on_host ? 1 : 2;
+    long long held = 0;
+    for (const Csr& c : pieces) held += 12 * c.nnz + 8 * (c.row_hi - c.row_lo + 1);
+    const long long budget_now = std::max<long long>((long long)budget / 8, (long long)budget - (long long)out_copies * held);
+    rc = run_batch(pl, rg.first, rg.second, budget_now, out_copies, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
                    derr.as<unsigned long long>(), &split, &cuts, rg.plain, &an_fb);
     if (rc) break;
     if (out_on_host && pieces.size() > npieces) {
@@ -5619,7 +5711,7 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
       if (rc) break;
     }
     if (an_fb) {
-      todo.push_back({rg.first, rg.second, true});
+      todo.push_back({rg.first, rg.second, true, rg.tail});
       st.n_replans += 1;
       continue;
     }
@@ -5630,11 +5722,11 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
       long long hi = rg.second;
       for (size_t c = cuts.size(); c-- > 0;) {
         if (cuts[c] > rg.first && cuts[c] < hi) {
-          todo.push_back({cuts[c], hi, rg.plain});
+          todo.push_back({cuts[c], hi, rg.plain, rg.tail});
           hi = cuts[c];
         }
       }
-      todo.push_back({rg.first, hi, rg.plain});
+      todo.push_back({rg.first, hi, rg.plain, rg.tail});
       st.n_replans += 1;
     }
   }
