@@ -378,7 +378,8 @@ def main():
     # allow 75 % -- config 5 then runs as ONE batch and no pair is integrated
     # twice at a batch cut (768 vs 825 ms).  The warm-up proves it fits; if it
     # does not, the library default is used.  (e2e below: library defaults.)
-    budget = int(0.75 * torch.cuda.mem_get_info(local)[1])
+    # (whole problems only: a config-4 shard at 75 % ran out of memory)
+    budget = int(0.75 * torch.cuda.mem_get_info(local)[1]) if sws == 1 else 0
     try:
         for _ in range(args.warmup):
             plan.assemble(lo, hi, out_on_host=False, reuse_output=True, mem_budget=budget)

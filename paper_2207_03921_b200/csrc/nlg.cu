@@ -5702,7 +5702,10 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
     const int out_copies = out_on_host ? 1 : 2;
     long long held = 0;
     for (const Csr& c : pieces) held += 12 * c.nnz + 8 * (c.row_hi - c.row_lo + 1);
-    const long long budget_now = std::max<long long>((long long)budget / 8, (long long)budget - (long long)out_copies * held);
+    // (NLG_HELD=1: A/B -- the finished pieces come off the budget)
+    static const bool held_env = getenv("NLG_HELD") != nullptr;
+    const long long budget_now = held_env ? std::max<long long>((long long)budget / 8, (long long)budget - (long long)out_copies * held)
+                                          : (long long)budget;
     rc = run_batch(pl, rg.first, rg.second, budget_now, out_copies, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
                    derr.as<unsigned long long>(), &split, &cuts, rg.plain, &an_fb);
     if (rc) break;
