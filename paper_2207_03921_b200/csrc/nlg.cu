@@ -4616,7 +4616,7 @@ struct Timing {
 };
 
 // one row batch: returns NLG_OK and appends to `out`, or asks for a split
-nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget, int out_copies, bool allow_sample,
+nlg_status run_batch(nlg_plan* pl, long long row_lo, long long row_hi, long long budget, bool allow_sample,
                      std::vector<Csr>& out, nlg_stats* st, Counters& ctr, Timing& tm,
                      unsigned long long* d_counters, unsigned long long* d_err, bool* need_split,
                      std::vector<long long>* cuts, bool no_analytic, bool* analytic_fallback) {
@@ -4748,8 +4748,7 @@ count_pass:
     const long long ent_ub = rows_plan ? ent_estimate(P, nUB, tot[C_EPI], nR) : 0LL;
     const long long side_bytes = 8LL * (3 * NC * (3 * NC + 1) / 2 + (NC == 1 ? 12 : 36));  // kkv + klv
     // (ent_ub is ~1.5x the CSR entries: it covers the merge's entry buffer and
-    // most of the batch's piece; the pieces of EARLIER batches come off the budget)
-    (void)out_copies;
+    // most of the batch's piece)
     const long long bytes = nStUB * 2 * side_bytes + coo_ub * (16 + 16) + ent_ub * 12 +
                             (2 * nUB + nS[0] + nS[1] + nS[2]) * 8 + nUB * 24;
     if (g_trace)
@@ -5672,10 +5671,9 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
   struct Range {
     long long first, second;
     bool plain;  // without the analytic enumeration (after a stage-W overflow)
-    bool tail;   // the short last batch of a streamed host output (not split off again)
   };
   std::vector<Range> todo;
-  if (row_hi > row_lo) todo.push_back({row_lo, row_hi, false, false});
+  if (row_hi > row_lo) todo.push_back({row_lo, row_hi, false});
   // Streamed host output (>= 0.4 GB): a batch's rows are copied while the
   // NEXT batch computes, and nothing overlaps the last batch's copy.  Three
   // row chunks of 62 / 26 / 12 %: each copy fits inside the next chunk's
@@ -5686,9 +5684,9 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
     const long long nc = pl->P.nc, n = row_hi - row_lo;
     const long long c1 = row_lo + (long long)(0.62 * (double)n) / nc * nc, c2 = row_lo + (long long)(0.88 * (double)n) / nc * nc;
     todo.clear();
-    todo.push_back({c2, row_hi, false, true});  // (popped last)
-    todo.push_back({c1, c2, false, true});
-    todo.push_back({row_lo, c1, false, true});
+    todo.push_back({c2, row_hi, false});  // (popped last)
+    todo.push_back({c1, c2, false});
+    todo.push_back({row_lo, c1, false});
   }
   while (!todo.empty()) {
     auto rg = todo.back();
@@ -5697,16 +5695,10 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
     std::vector<long long> cuts;
     const bool first_attempt = st.n_batches == 0 && st.n_replans == 0;
     const size_t npieces = pieces.size();
-    // what the finished pieces hold (and, for device outputs, their copy in
-    // the caller's buffers at the end) is no longer available to a batch
-    const int out_copies = out_on_host ? 1 : 2;
-    long long held = 0;
-    for (const Csr& c : pieces) held += 12 * c.nnz + 8 * (c.row_hi - c.row_lo + 1);
-    // (NLG_HELD=1: A/B -- the finished pieces come off the budget)
-    static const bool held_env = getenv("NLG_HELD") != nullptr;
-    const long long budget_now = held_env ? std::max<long long>((long long)budget / 8, (long long)budget - (long long)out_copies * held)
-                                          : (long long)budget;
-    rc = run_batch(pl, rg.first, rg.second, budget_now, out_copies, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
+    // (the budget does not shrink with the finished pieces: taking them off
+    // cut config 4's shards into 9 batches instead of 6 and cost 8 % -- more
+    // cuts, more pairs integrated twice; emit_pieces hands memory back instead)
+    rc = run_batch(pl, rg.first, rg.second, budget, first_attempt, pieces, &st, ctr, tm, dctr.as<unsigned long long>(),
                    derr.as<unsigned long long>(), &split, &cuts, rg.plain, &an_fb);
     if (rc) break;
     if (out_on_host && pieces.size() > npieces) {
@@ -5714,7 +5706,7 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
       if (rc) break;
     }
     if (an_fb) {
-      todo.push_back({rg.first, rg.second, true, rg.tail});
+      todo.push_back({rg.first, rg.second, true});
       st.n_replans += 1;
       continue;
     }
@@ -5725,11 +5717,11 @@ static nlg_status assemble_impl(nlg_plan* pl, int64_t row_lo, int64_t row_hi, in
       long long hi = rg.second;
       for (size_t c = cuts.size(); c-- > 0;) {
         if (cuts[c] > rg.first && cuts[c] < hi) {
-          todo.push_back({cuts[c], hi, rg.plain, rg.tail});
+          todo.push_back({cuts[c], hi, rg.plain});
           hi = cuts[c];
         }
       }
-      todo.push_back({rg.first, hi, rg.plain, rg.tail});
+      todo.push_back({rg.first, hi, rg.plain});
       st.n_replans += 1;
     }
   }

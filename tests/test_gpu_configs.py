@@ -46,6 +46,24 @@ def test_cfg3_peridynamic_nc2(transform):
     assert abs(A - A.T).max() <= 1e-12 * abs(A).max()
 
 
+def test_cfg3_streamed_host_output_equals_one_batch():
+    """A host CSR of >= 0.4 GB is produced in three row chunks once the
+    output size is known (the copy of each chunk overlaps the next chunk's
+    compute): bit for bit the matrix of the first call, which ran as one
+    batch and copied everything at the end."""
+    from paper_2207_03921_b200 import bfs_assemble
+    cfg = _cfg(3)
+    args = (cfg.mesh, cfg.adjacency, cfg.kernel, cfg.ansatz, cfg.quad)
+    st1, st2 = {}, {}
+    # (a different row range than any other test: this call has no size hint yet)
+    J = cfg.ansatz.dof_count
+    A1 = bfs_assemble(*args, row_range=(2, J), stats=st1).matrix
+    A2 = bfs_assemble(*args, row_range=(2, J), stats=st2).matrix
+    assert st1["n_batches"] == 1 and st2["n_batches"] >= 3
+    assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
+    assert np.array_equal(A1.data, A2.data)
+
+
 def test_cfg4_row_strip():
     """N=2048 (8.4M triangles): an owner-computed strip of rows around sampled vertices."""
     from paper_2207_03921_b200 import bfs_assemble
