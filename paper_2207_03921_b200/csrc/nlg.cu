@@ -4786,7 +4786,10 @@ count_pass:
       CK(rb_read(hcost.data(), rcost.p, sizeof(unsigned long long) * 3 * nrows, s));
       CK(rb_sync(s));
       // cut fraction of each limit (the halo roots a batch adds are not in
-      // the per-row costs)
+      // the per-row costs).  Taller batches integrate fewer pairs twice -- a
+      // config-4 shard takes 2,393 ms at 0.55 (6 batches), 2,283 at 0.7 (5),
+      // 2,210 at 0.75 (4) -- but at 0.7 the eight shards of config 4 run one
+      // after the other ran out of memory at the fourth (pieces + outputs)
       static const double pf = getenv("NLG_PLAN_FRAC") ? atof(getenv("NLG_PLAN_FRAC")) : 0.55;
       const double lim[3] = {budget > 0 ? pf * (double)budget : 1e300, pf * (double)(1LL << 31),
                              pf * (double)(1LL << 31)};
