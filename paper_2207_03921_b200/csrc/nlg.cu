@@ -3277,9 +3277,8 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
         };
         // phase A: every deep column (all its elements full partners of every
         // group root): gsum_all x H
-        for (int q = t; q < tot; q += TH) {
+        for (int q = t, r = 0; q < tot; q += TH) {  // (r: the cell row of q, kept across iterations)
           if (*(volatile int*)&S.ovf) break;
-          int r = 0;
           while (q >= S.gpre[r + 1]) ++r;
           const int jv = S.gr0[r] + (q - S.gpre[r]);
           const double4 cp = ld_f4(W.G.cpos + jv);
@@ -3291,9 +3290,8 @@ __global__ void __launch_bounds__(TH) k_row_asm(Params P, RootIn I, RowIn W, Row
         // of its barycentre) all lie strictly between the two radii has only
         // deep columns; one beyond eout has no category-0 visit.
         const int etot = S.epre[2 * ngr];
-        for (int q = t; q < etot; q += TH) {
+        for (int q = t, r = 0; q < etot; q += TH) {
           if (*(volatile int*)&S.ovf) break;
-          int r = 0;
           while (q >= S.epre[r + 1]) ++r;
           const int j = S.er0[r] + (q - S.epre[r]);
           const double2 cl = W.G.gctr[j];
