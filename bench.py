@@ -443,9 +443,9 @@ def main():
     dom = max(phases, key=lambda k: phases[k]["ms"])
     top = phases[dom] if phases[dom].get("frac") is not None else phases["k_clipped"]
     dom_name = dom if phases[dom].get("frac") is not None else "k_clipped"
-    # (the clipped pairs of the constant / affine kernels run in k_clipped_cf)
+    # (the clipped pairs of the constant / affine kernels run in k_clipped_cfr)
     closed_form = inp.kernel_id in (2, 3) and inp.path_touch == 0 and inp.ball_id != 2
-    kern_name = "k_clipped_cf" if dom_name == "k_clipped" and closed_form else dom_name
+    kern_name = "k_clipped_cfr" if dom_name == "k_clipped" and closed_form else dom_name
     traffic, traffic_src, ncu_extra = _ncu_traffic(kern_name, args.config)
     roofline = {
         "bound": top["bound"], "kernel": kern_name, "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],

@@ -2226,6 +2226,322 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cf(Params P, const i
   warp_add_ll((unsigned long long)n_out2, &O.counters[K_OUT_M2]);
 }
 
+// k_clipped_cf with a clip queue that runs across rounds.  A round of four
+// records queues ~21 items that need a clip, so a clip pass of k_clipped_cf
+// runs on ~21 of 32 lanes.  Here the queue is a ring: a round is classified
+// one round ahead of its sums, and a clip pass runs when 32 items are queued
+// (or when the previous round still waits for some of its own), on full
+// lanes.  Clip results live in a ring of kCfCap polygons indexed by queue
+// position; items wholly inside the ball keep no polygon (it is the inner
+// triangle, read from tv).  The per-round state is double buffered.  Items
+// are computed exactly as in k_clipped_cf and folded by the same shuffles:
+// the values are the same bits, only the schedule differs.
+constexpr int kCfCap = 64;
+template <int KID>
+struct CfMeta {
+  double xo[64][2];
+  double tri[4][2][7];  // [record][inner side]: o.x o.y e1x e1y e2x e2y idet
+  double tv[4][2][6];   // [record][inner side]: the inner triangle's vertices x0 x1 x2 y0 y1 y2
+  double ta[4][2];      // [record][outer side is l]: twice the outer triangle's area
+  double ls[4];         // the record's label factor
+  unsigned char pm[64];  // p | m << 4 | 0x40 (inside: polygon = tv) | 0x80 (no item)
+  unsigned char nv[64];
+  unsigned char st[64];  // clipped items: polygon ring index
+  int vk[4], vl[4], fl[4];
+};
+template <int KID>
+struct CfRing {
+  CfMeta<KID> M[2];
+  double px[kCfCap][kMaxPoly], py[kCfCap][kMaxPoly];
+  int4 ek[4], el[4];
+  unsigned char q[128];  // queued items: slot | round parity << 6
+};
+template <int KID, int NWB, int MINB>
+__global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const int2* __restrict__ list, VisitOut O) {
+  static_assert(KID == 2 || KID == 3, "closed-form path: constant / affine kernels");
+  using C = ClipCfg<KID>;
+  constexpr int NC = 1, N3 = 3;
+  extern __shared__ __align__(16) unsigned char cf_smem[];
+  CfRing<KID>& S = reinterpret_cast<CfRing<KID>*>(cf_smem)[threadIdx.x >> 5];
+  const int lane = lane_id();
+  const long long nround = (O.nlist + 3) / 4;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  unsigned n_eval0 = 0, n_eval1 = 0, n_eval2 = 0, n_out0 = 0, n_out1 = 0, n_out2 = 0;
+  double vmx = 0.0;
+  const int r = lane & 15, vs = lane >> 4;
+  int2 pnext = make_int2(0, 0);
+  int4 eknext = make_int4(0, 0, 0, 0), elnext = eknext;
+  auto fetch = [&](long long rdn) {
+    if (lane < 4) {
+      const long long v = rdn * 4 + lane;
+      if (rdn < nround && v < O.nlist) {
+        pnext = list[v];
+        eknext = __ldg(&P.elem[pnext.x & kIdMask]);
+        elnext = __ldg(&P.elem[pnext.y & kIdMask]);
+      }
+    }
+  };
+  fetch(w0);
+  int head = 0, tail = 0;  // clip items processed / queued so far by this warp
+  int prev_start = 0, prev_end = 0, par = 0;
+  long long prev = -1;
+  for (long long rd = w0;; rd += nw) {
+    const bool have = rd < nround;
+    const int cur_start = tail;
+    if (have) {
+      CfMeta<KID>& M = S.M[par];
+      if (lane < 4 && rd * 4 + lane < O.nlist) {
+        M.vk[lane] = pnext.x & kIdMask;
+        M.vl[lane] = pnext.y & kIdMask;
+        M.fl[lane] = pnext.y & ~kIdMask;
+        S.ek[lane] = eknext;
+        S.el[lane] = elnext;
+      }
+      __syncwarp();
+      fetch(rd + nw);
+      // ---- classify both slots of the lane; queue the ones that need a clip
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rec = vs + 2 * h, sl = lane + 32 * h;
+        const long long v = rd * 4 + rec;
+        bool valid = v < O.nlist && r < 14;
+        const int k = valid ? M.vk[rec] : 0, l = valid ? M.vl[rec] : 0;
+        int m = r >= 7 ? 1 : 0;
+        const int p = r % 7;
+        if (valid && k == l) {
+          if (m == 1) valid = false;
+          m = 2;
+        }
+        bool need_clip = false, inside_item = false;
+        int nv = 0;
+        if (valid) {
+          const int4 ek = S.ek[rec], el = S.el[rec];
+          double ox[3], oy[3], ix[3], iy[3];
+          {
+            const int4 eo = m == 1 ? el : ek, ei = m == 1 ? ek : el;
+            const double2 a0 = __ldg(&P.vtx[eo.x]), a1 = __ldg(&P.vtx[eo.y]), a2 = __ldg(&P.vtx[eo.z]);
+            const double2 b0 = __ldg(&P.vtx[ei.x]), b1 = __ldg(&P.vtx[ei.y]), b2 = __ldg(&P.vtx[ei.z]);
+            ox[0] = a0.x; oy[0] = a0.y; ox[1] = a1.x; oy[1] = a1.y; ox[2] = a2.x; oy[2] = a2.y;
+            ix[0] = b0.x; iy[0] = b0.y; ix[1] = b1.x; iy[1] = b1.y; ix[2] = b2.x; iy[2] = b2.y;
+          }
+          const double e1x = ox[1] - ox[0], e2x = ox[2] - ox[0], e1y = oy[1] - oy[0], e2y = oy[2] - oy[0];
+          const double x0 = __dadd_rn(__dadd_rn(ox[0], mul(e1x, c_rule.op[p][0])), mul(e2x, c_rule.op[p][1]));
+          const double x1 = __dadd_rn(__dadd_rn(oy[0], mul(e1y, c_rule.op[p][0])), mul(e2y, c_rule.op[p][1]));
+          const int inner_el = m == 1 ? k : l;
+          const double2 ci = __ldg(&P.ctr[inner_el]);
+          const double reach = P.delta * (1.0 + 1e-6) + __ldg(&P.rad[inner_el]);
+          const double dcx = ci.x - x0, dcy = ci.y - x1;
+          const bool far = P.ball != 2 && dcx * dcx + dcy * dcy > reach * reach;
+          if (!far) {
+            bool inside = P.ball != 2;
+            if (inside) {
+              const double rad = mul(P.delta, 1.0 + kBallTieRel), r2b = mul(rad, rad);
+#pragma unroll
+              for (int i = 0; i < 3; ++i) inside = inside && __dsub_rn(sumsq(ix[i] - x0, iy[i] - x1), r2b) <= 0.0;
+            }
+            if (inside) {
+              // the deduplicated inner triangle: three rows unless two vertices coincide within dtol
+              const double dtol = mul(kDedupRel, P.delta);
+              double lx = ix[0], ly = iy[0];
+              nv = 1;
+#pragma unroll
+              for (int i = 1; i < 3; ++i)
+                if (fabs(lx - ix[i]) > dtol || fabs(ly - iy[i]) > dtol) {
+                  lx = ix[i];
+                  ly = iy[i];
+                  ++nv;
+                }
+              if (nv >= 2 && fabs(ix[0] - lx) <= dtol && fabs(iy[0] - ly) <= dtol) --nv;
+              inside_item = true;
+            } else {
+              need_clip = true;
+            }
+          }
+          M.xo[sl][0] = x0;
+          M.xo[sl][1] = x1;
+          if (p == 0) {  // the record's triangles of this sweep
+            M.ta[rec][m == 1] = twice_area(ox, oy);
+            if (m != 1) M.ls[rec] = lab_scale(P, ek.w, el.w);
+            double* tr = M.tri[rec][m == 1];
+            tr[0] = ix[0]; tr[1] = iy[0];
+            tr[2] = ix[1] - ix[0]; tr[3] = iy[1] - iy[0];
+            tr[4] = ix[2] - ix[0]; tr[5] = iy[2] - iy[0];
+            tr[6] = 1.0 / cross2(tr[2], tr[5], tr[3], tr[4]);
+            double* tv = M.tv[rec][m == 1];
+            tv[0] = ix[0]; tv[1] = ix[1]; tv[2] = ix[2];
+            tv[3] = iy[0]; tv[4] = iy[1]; tv[5] = iy[2];
+          }
+        }
+        M.pm[sl] = (unsigned char)(p | (m << 4) | (inside_item ? 0x40 : 0) | (valid ? 0 : 0x80));
+        M.nv[sl] = (unsigned char)nv;
+        const unsigned qm = __ballot_sync(0xffffffffu, need_clip);
+        if (need_clip) S.q[(tail + __popc(qm & ((1u << lane) - 1u))) & 127] = (unsigned char)(sl | (par << 6));
+        tail += __popc(qm);
+      }
+    }
+    __syncwarp();
+    // ---- clip passes: full lanes, or whatever the previous round still waits for
+    {
+      const int live0 = prev >= 0 ? prev_start : cur_start;  // oldest polygon still needed
+      for (;;) {
+        const int n = min(min(32, tail - head), kCfCap - (head - live0));
+        const bool forced = prev >= 0 && head < prev_end;
+        if (n <= 0 || (n < 32 && !forced)) break;
+        if (lane < n) {
+          const int qi = head + lane, e = S.q[qi & 127];
+          const int sl = e & 63, si = qi & (kCfCap - 1);
+          CfMeta<KID>& Mq = S.M[e >> 6];
+          const int mj = (Mq.pm[sl] >> 4) & 3;
+          const double* tv = Mq.tv[sl >> 4][mj == 1];
+          const Tri Tq{tv[0], tv[1], tv[2], tv[3], tv[4], tv[5]};
+          Mq.nv[sl] = (unsigned char)truncate_inner_inplace(Tq, Mq.xo[sl][0], Mq.xo[sl][1], P.delta, P.ball,
+                                                            S.px[si], S.py[si]);
+          Mq.st[sl] = (unsigned char)si;
+        }
+        head += n;
+      }
+    }
+    __syncwarp();
+    // ---- the previous round: closed-form fan sums per slot, then fold and reduce two records
+    if (prev >= 0) {
+      const CfMeta<KID>& M = S.M[par ^ 1];
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int rec = vs + 2 * h, sl = lane + 32 * h;
+        const long long v = prev * 4 + rec;
+        const bool vok = v < O.nlist;
+        const int pmy = M.pm[sl];
+        const bool ivalid = !(pmy & 0x80);
+        const int mi = (pmy >> 4) & 3, pi = pmy & 15;
+        const int rf = vok ? M.fl[rec] : 0, rk = vok ? M.vk[rec] : 0, rl = vok ? M.vl[rec] : 0;
+        const int mult = ((rf & kEmitA) ? 1 : 0) + ((rf & kEmitB) ? 1 : 0);
+        double si[C::NSUM];
+#pragma unroll
+        for (int i = 0; i < C::NSUM; ++i) si[i] = 0.0;
+        const int nv = M.nv[sl];
+        if (ivalid && nv >= 3) {
+          n_out0 += mi == 0 ? mult : 0;
+          n_out1 += mi == 1 ? mult : 0;
+          n_out2 += mi == 2;
+          const double* tvi = M.tv[rec][mi == 1];
+          const int st = M.st[sl];
+          const double* qx = (pmy & 0x40) ? tvi : S.px[st];
+          const double* qy = (pmy & 0x40) ? tvi + 3 : S.py[st];
+          const double* tr = M.tri[rec][mi == 1];
+          const double o0 = tr[0], o1 = tr[1], e1x = tr[2], e1y = tr[3], e2x = tr[4], e2y = tr[5], idet = tr[6];
+          const double q0x = qx[0], q0y = qy[0];
+          const double v0 = q0x - o0, v1 = q0y - o1;
+          const double z1 = (v0 * e2y - v1 * e2x) * idet, z2 = (e1x * v1 - e1y * v0) * idet;
+          const double x0 = M.xo[sl][0];
+          int ne = 0;
+#pragma unroll 1
+          for (int t = 1; t < nv - 1; ++t) {
+            const double ax = qx[t] - q0x, ay = qy[t] - q0y;
+            const double bx = qx[t + 1] - q0x, by = qy[t + 1] - q0y;
+            const double jac2 = cross2(ax, by, ay, bx);
+            if (!(jac2 > P.drop2)) continue;
+            const double z1a = (ax * e2y - ay * e2x) * idet, z2a = (e1x * ay - e1y * ax) * idet;
+            const double z1b = (bx * e2y - by * e2x) * idet, z2b = (e1x * by - e1y * bx) * idet;
+            double sm[C::NSUM];
+            closed_moments<KID>(P, q0x, ax, bx, jac2, x0, z1, z2, z1a, z2a, z1b, z2b, sm);
+#pragma unroll
+            for (int i = 0; i < C::NSUM; ++i) si[i] += sm[i];
+            ne += 7;
+          }
+          n_eval0 += mi == 0 ? ne * mult : 0;
+          n_eval1 += mi == 1 ? ne * mult : 0;
+          n_eval2 += mi == 2 ? ne : 0;
+        }
+        // fold into both visits, reduce-scatter over the record's 16 lanes
+        // (the pair's label factor rides on the weight: every entry is linear in W)
+        const double Wi = ivalid ? mul(mul(c_rule.ow[pi], M.ta[rec][mi == 1]), M.ls[rec]) : 0.0;
+        const double* ohi = c_rule.oh[pi];
+        const FoldSrc<KID> fs(Wi, ohi, si);
+        const bool m1 = mi == 1, m2 = ivalid && mi == 2;
+        constexpr int NBATCH = (C::NVAL + 31) / 32;
+        double smA = 0.0, smB = 0.0;  // the sides' largest |value| (the roots' merge bounds)
+#pragma unroll
+        for (int bt = 0; bt < NBATCH; ++bt) {
+          double vals[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int g = bt * 32 + i;
+            double val = 0.0;
+            if (g < C::NVAL) {
+              double f0, f1;
+              fs.entry(g < C::NSIDE ? g : g - C::NSIDE, f0, f1);
+              if (g < C::NSIDE) {
+                const double a0 = ivalid ? (m1 ? f1 : f0) : 0.0;
+                val = m2 ? a0 + f1 : a0;
+              } else {
+                val = ivalid && !m2 ? (m1 ? f0 : f1) : 0.0;
+              }
+            }
+            vals[i] = val;
+          }
+#pragma unroll
+          for (int off = 8, half = 16; off >= 1; off >>= 1, half >>= 1) {
+            const bool upper = lane & off;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const double send = upper ? vals[i] : vals[i + half];
+              const double keep = upper ? vals[i + half] : vals[i];
+              vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int g = bt * 32 + r * 2 + h2;
+            if (!vok || g >= C::NVAL) continue;
+            const double val = vals[h2];
+            const int side = g / C::NSIDE, w = g % C::NSIDE;
+            const bool on = side == 0 ? (rf & kEmitA) != 0 : ((rf & kEmitB) != 0 && rk != rl);
+            const int root = side == 0 ? rk : rl, nb = side == 0 ? rl : rk;
+            const long long slot = side ? O.b_base + __ldg(&O.revpos[v]) : O.a_base + v;
+            if (on) {
+              report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
+              vmx = fmax(vmx, fabs(val));
+              if (side == 0) smA = fmax(smA, fabs(val));
+              else smB = fmax(smB, fabs(val));
+            }
+            if (w < C::NKK) {
+              O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;
+            } else {
+              const int e = w - C::NKK, I = e / N3, J = e % N3;
+              O.klv[slot * Blk<NC>::KLS + Blk<NC>::kl(I, J)] = on ? emit_val(val) : 0.0;
+            }
+          }
+        }
+        if (!P.analytic) {  // (analytic rows: a plan bound covers the clipped values)
+#pragma unroll
+          for (int o = 8; o; o >>= 1) {  // within the record's 16 lanes
+            smA = fmax(smA, __shfl_xor_sync(0xffffffffu, smA, o));
+            smB = fmax(smB, __shfl_xor_sync(0xffffffffu, smB, o));
+          }
+          if (r == 0 && vok) {
+            elem_bound(O.emax, rk, smA);
+            elem_bound(O.emax, rl, smB);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!have) break;
+    prev = rd;
+    prev_start = cur_start;
+    prev_end = tail;
+    par ^= 1;
+  }
+  warp_max_abs(vmx, O.vmax);
+  warp_add_ll((unsigned long long)n_eval0, &O.counters[K_EVAL_M0]);
+  warp_add_ll((unsigned long long)n_out0, &O.counters[K_OUT_M0]);
+  warp_add_ll((unsigned long long)n_eval1, &O.counters[K_EVAL_M1]);
+  warp_add_ll((unsigned long long)n_out1, &O.counters[K_OUT_M1]);
+  warp_add_ll((unsigned long long)n_eval2, &O.counters[K_EVAL_M2]);
+  warp_add_ll((unsigned long long)n_out2, &O.counters[K_OUT_M2]);
+}
+
 // ---------------------------------------------------------------------
 // local_contribution (assembly.py:327-448): the 4-term block of the ORDERED
 // pair (k, l) -- outer points on k, the inner element l retriangulated
@@ -4231,8 +4547,8 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
     } else if (wl) {
       if constexpr (KID == 2 || KID == 3) {
         // four records per warp round, warp-local clip queue (k_clipped_cf);
-        // NLG_CLIP_WL = 1..4 picks the block shape (A/B experiments)
-        static const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 3;
+        // NLG_CLIP_WL = 1..4 picks k_clipped_cf's block shape (A/B experiments); 5 (default): k_clipped_cfr
+        static const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 5;
         const long long rounds = (nP + 3) / 4;
         auto launch = [&](auto kern, int nwb) -> cudaError_t {
           const int smem = nwb * (int)sizeof(CfWarp<KID>);
@@ -4242,6 +4558,13 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
           kern<<<gcf, 32 * nwb, smem, pl->stream>>>(P, lp, O);
           return cudaGetLastError();
         };
+        if (var >= 5) {  // ring clip queue across rounds (k_clipped_cfr)
+          const int smem = 8 * (int)sizeof(CfRing<KID>);
+          const unsigned gcf = (unsigned)std::min<long long>((rounds + 7) / 8, 148LL * 64);
+          CK(cudaFuncSetAttribute(k_clipped_cfr<KID, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          k_clipped_cfr<KID, 8, 2><<<gcf, 256, smem, pl->stream>>>(P, lp, O);
+          CK(cudaGetLastError());
+        } else
         switch (var) {
           case 1: CK(launch(k_clipped_cf<KID, 4, 4>, 4)); break;
           case 2: CK(launch(k_clipped_cf<KID, 4, 5>, 4)); break;
