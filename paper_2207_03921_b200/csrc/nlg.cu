@@ -2256,7 +2256,7 @@ struct CfRing {
   int4 ek[4], el[4];
   unsigned char q[128];  // queued items: slot | round parity << 6
 };
-template <int KID, int NWB, int MINB>
+template <int KID, int NWB, int MINB, int CU = 2>
 __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const int2* __restrict__ list, VisitOut O) {
   static_assert(KID == 2 || KID == 3, "closed-form path: constant / affine kernels");
   using C = ClipCfg<KID>;
@@ -2301,7 +2301,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
       __syncwarp();
       fetch(rd + nw);
       // ---- classify both slots of the lane; queue the ones that need a clip
-#pragma unroll
+#pragma unroll CU
       for (int h = 0; h < 2; ++h) {
         const int rec = vs + 2 * h, sl = lane + 32 * h;
         const long long v = rd * 4 + rec;
@@ -4558,12 +4558,21 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
           kern<<<gcf, 32 * nwb, smem, pl->stream>>>(P, lp, O);
           return cudaGetLastError();
         };
-        if (var >= 5) {  // ring clip queue across rounds (k_clipped_cfr)
-          const int smem = 8 * (int)sizeof(CfRing<KID>);
-          const unsigned gcf = (unsigned)std::min<long long>((rounds + 7) / 8, 148LL * 64);
-          CK(cudaFuncSetAttribute(k_clipped_cfr<KID, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-          k_clipped_cfr<KID, 8, 2><<<gcf, 256, smem, pl->stream>>>(P, lp, O);
-          CK(cudaGetLastError());
+        if (var >= 5) {  // ring clip queue across rounds (k_clipped_cfr); 6..8: A/B shapes
+          auto launch_r = [&](auto kern, int nwb) -> cudaError_t {
+            const int smem = nwb * (int)sizeof(CfRing<KID>);
+            const unsigned gcf = (unsigned)std::min<long long>((rounds + nwb - 1) / nwb, 148LL * 512 / nwb);
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            kern<<<gcf, 32 * nwb, smem, pl->stream>>>(P, lp, O);
+            return cudaGetLastError();
+          };
+          switch (var) {
+            case 6: CK(launch_r(k_clipped_cfr<KID, 8, 2, 1>, 8)); break;
+            case 7: CK(launch_r(k_clipped_cfr<KID, 4, 4, 2>, 4)); break;
+            case 8: CK(launch_r(k_clipped_cfr<KID, 16, 1, 2>, 16)); break;
+            default: CK(launch_r(k_clipped_cfr<KID, 8, 2, 2>, 8)); break;
+          }
         } else
         switch (var) {
           case 1: CK(launch(k_clipped_cf<KID, 4, 4>, 4)); break;
