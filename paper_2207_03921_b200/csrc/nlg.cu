@@ -2256,7 +2256,7 @@ struct CfRing {
   int4 ek[4], el[4];
   unsigned char q[128];  // queued items: slot | round parity << 6
 };
-template <int KID, int NWB, int MINB, int CU = 2>
+template <int KID, int NWB, int MINB, int CU = 2, int SY = 0>
 __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const int2* __restrict__ list, VisitOut O) {
   static_assert(KID == 2 || KID == 3, "closed-form path: constant / affine kernels");
   using C = ClipCfg<KID>;
@@ -2286,7 +2286,16 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
   int head = 0, tail = 0;  // clip items processed / queued so far by this warp
   int prev_start = 0, prev_end = 0, par = 0;
   long long prev = -1;
-  for (long long rd = w0;; rd += nw) {
+  // every warp of a block runs the block's iteration count (its first warp's
+  // rounds + the flush), so that the block can re-align its warps' phases
+  // every SY rounds: warps in the same phase share the instruction cache
+  const long long wb0 = (blockIdx.x * (long long)blockDim.x) >> 5;
+  const long long niter = wb0 < nround ? (nround - wb0 + nw - 1) / nw + 1 : 0;
+  long long rd = w0;
+  for (long long it = 0; it < niter; ++it, rd += nw) {
+    if (SY > 0 && it % SY == 0) __syncthreads();
+    if (SY < 0 && it % (-SY) == 0)  // the four warps of a scheduler (warp % 4) only
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + ((threadIdx.x >> 5) & 3)) : "memory");
     const bool have = rd < nround;
     const int cur_start = tail;
     if (have) {
@@ -2527,8 +2536,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
       }
       __syncwarp();
     }
-    if (!have) break;
-    prev = rd;
+    prev = have ? rd : -1;
     prev_start = cur_start;
     prev_end = tail;
     par ^= 1;
@@ -4546,39 +4554,38 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
       k_clipped<KID, true><<<g, 32 * NWB, smem, pl->stream>>>(P, lp, O);
     } else if (wl) {
       if constexpr (KID == 2 || KID == 3) {
-        // four records per warp round, warp-local clip queue (k_clipped_cf);
-        // NLG_CLIP_WL = 1..4 picks k_clipped_cf's block shape (A/B experiments); 5 (default): k_clipped_cfr
-        static const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 5;
+        // four records per warp round, warp-local clip queue.  Default:
+        // k_clipped_cfr (ring queue), one 16-warp block per SM, classify loop
+        // rolled, the four warps of a scheduler re-aligned every 2 rounds
+        // (config 5, ms: 375; without the barrier 385-394, block barrier
+        // every 4 rounds 380, 8-warp blocks 396, classify unrolled 393-412).
+        // NLG_CLIP_WL picks the A/B variants: 3 k_clipped_cf (no ring, 439),
+        // 5 ring 8 x 2 unrolled, 9 no barrier, 11 block barrier every 4 rounds.
+        static const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 14;
         const long long rounds = (nP + 3) / 4;
-        auto launch = [&](auto kern, int nwb) -> cudaError_t {
-          const int smem = nwb * (int)sizeof(CfWarp<KID>);
-          const unsigned gcf = (unsigned)std::min<long long>((rounds + nwb - 1) / nwb, 148LL * 64);
-          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-          if (e != cudaSuccess) return e;
-          kern<<<gcf, 32 * nwb, smem, pl->stream>>>(P, lp, O);
-          return cudaGetLastError();
-        };
-        if (var >= 5) {  // ring clip queue across rounds (k_clipped_cfr); 6..8: A/B shapes
+        if (var >= 5) {
           auto launch_r = [&](auto kern, int nwb) -> cudaError_t {
             const int smem = nwb * (int)sizeof(CfRing<KID>);
-            const unsigned gcf = (unsigned)std::min<long long>((rounds + nwb - 1) / nwb, 148LL * 512 / nwb);
+            // (blocks for 512 warps per SM: fewer, longer-lived blocks measured slower, 385 -> 397 at 16)
+            static const int gmul = getenv("NLG_CF_GRID") ? atoi(getenv("NLG_CF_GRID")) : 512;
+            const unsigned gcf = (unsigned)std::min<long long>((rounds + nwb - 1) / nwb, 148LL * gmul / nwb);
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return e;
             kern<<<gcf, 32 * nwb, smem, pl->stream>>>(P, lp, O);
             return cudaGetLastError();
           };
           switch (var) {
-            case 6: CK(launch_r(k_clipped_cfr<KID, 8, 2, 1>, 8)); break;
-            case 7: CK(launch_r(k_clipped_cfr<KID, 4, 4, 2>, 4)); break;
-            case 8: CK(launch_r(k_clipped_cfr<KID, 16, 1, 2>, 16)); break;
-            default: CK(launch_r(k_clipped_cfr<KID, 8, 2, 2>, 8)); break;
+            case 5: CK(launch_r(k_clipped_cfr<KID, 8, 2, 2>, 8)); break;
+            case 9: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1>, 16)); break;
+            case 11: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, 4>, 16)); break;
+            default: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2>, 16)); break;
           }
-        } else
-        switch (var) {
-          case 1: CK(launch(k_clipped_cf<KID, 4, 4>, 4)); break;
-          case 2: CK(launch(k_clipped_cf<KID, 4, 5>, 4)); break;
-          case 4: CK(launch(k_clipped_cf<KID, 8, 3>, 8)); break;
-          default: CK(launch(k_clipped_cf<KID, 8, 2>, 8)); break;  // measured best on config 5
+        } else {
+          const int smem = 8 * (int)sizeof(CfWarp<KID>);
+          const unsigned gcf = (unsigned)std::min<long long>((rounds + 7) / 8, 148LL * 64);
+          CK(cudaFuncSetAttribute(k_clipped_cf<KID, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          k_clipped_cf<KID, 8, 2><<<gcf, 256, smem, pl->stream>>>(P, lp, O);
+          CK(cudaGetLastError());
         }
       }
     } else {
