@@ -2256,13 +2256,14 @@ struct CfRing {
   int4 ek[4], el[4];
   unsigned char q[128];  // queued items: slot | round parity << 6
 };
-template <int KID, int NWB, int MINB, int CU = 2, int SY = 0>
+template <int KID, int NWB, int MINB, int CU = 2, int SY = 0, int BALL = -1>
 __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const int2* __restrict__ list, VisitOut O) {
   static_assert(KID == 2 || KID == 3, "closed-form path: constant / affine kernels");
   using C = ClipCfg<KID>;
   constexpr int NC = 1, N3 = 3;
   extern __shared__ __align__(16) unsigned char cf_smem[];
   CfRing<KID>& S = reinterpret_cast<CfRing<KID>*>(cf_smem)[threadIdx.x >> 5];
+  const int ball = BALL >= 0 ? BALL : P.ball;  // (BALL: the ball's code alone, a denser instruction stream)
   const int lane = lane_id();
   const long long nround = (O.nlist + 3) / 4;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -2341,9 +2342,9 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
           const double2 ci = __ldg(&P.ctr[inner_el]);
           const double reach = P.delta * (1.0 + 1e-6) + __ldg(&P.rad[inner_el]);
           const double dcx = ci.x - x0, dcy = ci.y - x1;
-          const bool far = P.ball != 2 && dcx * dcx + dcy * dcy > reach * reach;
+          const bool far = ball != 2 && dcx * dcx + dcy * dcy > reach * reach;
           if (!far) {
-            bool inside = P.ball != 2;
+            bool inside = ball != 2;
             if (inside) {
               const double rad = mul(P.delta, 1.0 + kBallTieRel), r2b = mul(rad, rad);
 #pragma unroll
@@ -2404,7 +2405,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
           const int mj = (Mq.pm[sl] >> 4) & 3;
           const double* tv = Mq.tv[sl >> 4][mj == 1];
           const Tri Tq{tv[0], tv[1], tv[2], tv[3], tv[4], tv[5]};
-          Mq.nv[sl] = (unsigned char)truncate_inner_inplace(Tq, Mq.xo[sl][0], Mq.xo[sl][1], P.delta, P.ball,
+          Mq.nv[sl] = (unsigned char)truncate_inner_inplace(Tq, Mq.xo[sl][0], Mq.xo[sl][1], P.delta, ball,
                                                             S.px[si], S.py[si]);
           Mq.st[sl] = (unsigned char)si;
         }
@@ -4578,7 +4579,11 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
             case 5: CK(launch_r(k_clipped_cfr<KID, 8, 2, 2>, 8)); break;
             case 9: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1>, 16)); break;
             case 11: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, 4>, 16)); break;
-            default: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2>, 16)); break;
+            case 18: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2>, 16)); break;
+            default:
+              if (P.ball == 0) CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2, 0>, 16));
+              else CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2, 1>, 16));
+              break;
           }
         } else {
           const int smem = 8 * (int)sizeof(CfWarp<KID>);
