@@ -4547,7 +4547,7 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
     constexpr int NWB = clip_warps<KID>();
     const unsigned g = (unsigned)std::min<long long>((chunks + NWB - 1) / NWB, 148LL * 256 / NWB);
     // warp-local clipping for the closed-form kernels (NLG_CLIP_WL=0: block queue)
-    static const bool wl_env = !(getenv("NLG_CLIP_WL") && atoi(getenv("NLG_CLIP_WL")) == 0);
+    const bool wl_env = !(getenv("NLG_CLIP_WL") && atoi(getenv("NLG_CLIP_WL")) == 0);  // (read per launch: tests switch it)
     const bool wl = (KID == 2 || KID == 3) && P.path == 0 && wl_env;
     if (P.ball == 2) {
       const int smem = NWB * (int)sizeof(ClipWarp<KID, true>) + (int)sizeof(ClipBlock<KID>);
@@ -4558,11 +4558,13 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
         // four records per warp round, warp-local clip queue.  Default:
         // k_clipped_cfr (ring queue), one 16-warp block per SM, classify loop
         // rolled, the four warps of a scheduler re-aligned every 2 rounds
-        // (config 5, ms: 375; without the barrier 385-394, block barrier
-        // every 4 rounds 380, 8-warp blocks 396, classify unrolled 393-412).
+        // (config 5, ms: 375, 367 instantiated per ball; without the barrier
+        // 376-394, every 3 / 4 / 8 rounds 366 / 366 / 369, block barrier every
+        // 4 rounds 380, 8-warp blocks 396, classify unrolled 393-412).
         // NLG_CLIP_WL picks the A/B variants: 3 k_clipped_cf (no ring, 439),
-        // 5 ring 8 x 2 unrolled, 9 no barrier, 11 block barrier every 4 rounds.
-        static const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 14;
+        // 5 ring 8 x 2 unrolled, 9 no barrier, 11 block barrier every 4 rounds,
+        // 18 the ball read at run time.
+        const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 14;
         const long long rounds = (nP + 3) / 4;
         if (var >= 5) {
           auto launch_r = [&](auto kern, int nwb) -> cudaError_t {

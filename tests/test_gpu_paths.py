@@ -5,7 +5,8 @@
 * stage W table retries and the fallback itself, forced on small fixtures
   by lowering the table fill limit (NLG_ROW_FILL_DIV);
 * analytic full pairs of the constant / affine kernels vs integrating them
-  per record (NLG_NO_ANALYTIC).
+  per record (NLG_NO_ANALYTIC);
+* the clipped-pair kernel's schedules (NLG_CLIP_WL): bitwise equal.
 
 The switches are read when a plan is created, so each call sets its own
 environment.  Same pattern bit for bit; values within 1e-13 relative
@@ -99,6 +100,20 @@ def test_stage_w_column_split_rows(name):
     b = _assemble(c, {"NLG_ROW_FILL_DIV": div}, stats=st)
     assert st["n_merge_fallbacks"] == 0 and st["n_row_retries"] > 0
     _agree(a, b, c.matrix)
+
+
+@pytest.mark.parametrize("name", [n for n in names() if n.startswith(("cfg1", "const", "lshape16"))])
+@pytest.mark.parametrize("variant", ["3", "5", "9", "11", "18"])
+def test_clip_ring_schedules_same_bits(name, variant):
+    """k_clipped_cfr (clip queue as a ring across rounds, block shapes and
+    barriers of NLG_CLIP_WL = 5 / 9 / 11 / 18 / default) computes every item
+    as k_clipped_cf (3: no ring) does and folds it by the same shuffles:
+    another schedule, the same bits."""
+    c = Case(name)
+    a = _assemble(c)
+    b = _assemble(c, {"NLG_CLIP_WL": variant})
+    assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.data, b.data)
 
 
 def test_stage_w_deterministic_across_table_sizes():
