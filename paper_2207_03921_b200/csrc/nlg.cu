@@ -2256,7 +2256,7 @@ struct CfRing {
   int4 ek[4], el[4];
   unsigned char q[128];  // queued items: slot | round parity << 6
 };
-template <int KID, int NWB, int MINB, int CU = 2, int SY = 0, int BALL = -1>
+template <int KID, int NWB, int MINB, int CU = 2, int SY = 0, int BALL = -1, int AN = -1>
 __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const int2* __restrict__ list, VisitOut O) {
   static_assert(KID == 2 || KID == 3, "closed-form path: constant / affine kernels");
   using C = ClipCfg<KID>;
@@ -2264,6 +2264,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
   extern __shared__ __align__(16) unsigned char cf_smem[];
   CfRing<KID>& S = reinterpret_cast<CfRing<KID>*>(cf_smem)[threadIdx.x >> 5];
   const int ball = BALL >= 0 ? BALL : P.ball;  // (BALL: the ball's code alone, a denser instruction stream)
+  const bool analytic = AN >= 0 ? AN != 0 : P.analytic != 0;  // (AN: likewise for the per-element bounds)
   const int lane = lane_id();
   const long long nround = (O.nlist + 3) / 4;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -2512,8 +2513,10 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
             if (on) {
               report_nonfinite(nonfinite(val), root, nb, P.K, O.errpair);
               vmx = fmax(vmx, fabs(val));
-              if (side == 0) smA = fmax(smA, fabs(val));
-              else smB = fmax(smB, fabs(val));
+              if (!analytic) {
+                if (side == 0) smA = fmax(smA, fabs(val));
+                else smB = fmax(smB, fabs(val));
+              }
             }
             if (w < C::NKK) {
               O.kkv[slot * Blk<NC>::NKK + w] = on ? val : 0.0;
@@ -2523,7 +2526,7 @@ __global__ void __launch_bounds__(32 * NWB, MINB) k_clipped_cfr(Params P, const 
             }
           }
         }
-        if (!P.analytic) {  // (analytic rows: a plan bound covers the clipped values)
+        if (!analytic) {  // (analytic rows: a plan bound covers the clipped values)
 #pragma unroll
           for (int o = 8; o; o >>= 1) {  // within the record's 16 lanes
             smA = fmax(smA, __shfl_xor_sync(0xffffffffu, smA, o));
@@ -4563,7 +4566,7 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
         // 4 rounds 380, 8-warp blocks 396, classify unrolled 393-412).
         // NLG_CLIP_WL picks the A/B variants: 3 k_clipped_cf (no ring, 439),
         // 5 ring 8 x 2 unrolled, 9 no barrier, 11 block barrier every 4 rounds,
-        // 18 the ball read at run time.
+        // 18 the ball read at run time, 23 approxcaps without the analytic instantiation.
         const int var = getenv("NLG_CLIP_WL") ? atoi(getenv("NLG_CLIP_WL")) : 14;
         const long long rounds = (nP + 3) / 4;
         if (var >= 5) {
@@ -4582,8 +4585,10 @@ nlg_status run_visits(nlg_plan* pl, const Params& P, const int2* lf, const int2*
             case 9: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1>, 16)); break;
             case 11: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, 4>, 16)); break;
             case 18: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2>, 16)); break;
+            case 23: CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2, 1>, 16)); break;
             default:
               if (P.ball == 0) CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2, 0>, 16));
+              else if (P.analytic) CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2, 1, 1>, 16));
               else CK(launch_r(k_clipped_cfr<KID, 16, 1, 1, -2, 1>, 16));
               break;
           }
